@@ -1,0 +1,449 @@
+/*
+ * exmy_oracle.c -- plain, slow, scalar CPU oracle for the eXmY tensor codec.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Nothing on the product path may link, load or
+ * call this file: only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs use it.  It shares no code, header,
+ * table or constant with paper_2405_13938_b200/csrc (the CUDA path).
+ *
+ * Every function follows the plain definition in the paper (P:n = line n of
+ * PAPER.md, S:n = line n of SPEC.md) or, where the paper is silent, the
+ * reading numbered Dn in DESIGN.md "Readings".  No blocking, no bit tricks:
+ *
+ *   quantize  = the grid point nearest to the exact input value, ties to the
+ *               code whose LSB is 0, saturating at the largest magnitude
+ *               (D5-D8).  Implemented as: enumerate all
+ *               2^(k-1) magnitude codes, compute their exact values in fp64,
+ *               sort them (qsort, a library primitive), binary-search the two
+ *               neighbours of |v| and compare |v| with their exact midpoint.
+ *   code value = (-1)^s (2^y+m) 2^(e-bias-y) for e>=1, (-1)^s m 2^(1-bias-y)
+ *               for e=0 or x=0 (Table 1, subnormals P:172-175; D3),
+ *               with bias = 2^x + 126 - e_max (metadata = maximum biased
+ *               exponent; D1).
+ *   pack      = power-of-2 decomposition of k, widest segment takes the most
+ *               significant code bits, element i of a group at bits
+ *               [w*i, w*i+w) of a little-endian 8w-bit container
+ *               (Fig. 3; D12-D16).
+ *
+ * Exactness of the fp64 arithmetic used here: every fp32 value and every grid
+ * value of a format with x<=8, y<=23, e_max in [0,254] is a normal fp64
+ * number (smallest grid quantum 2^(1-382-23) > 2^-1022), the sum of two
+ * adjacent grid values has at most y+3 significant bits, and /2 is exact; so
+ * every comparison below is exact.  Values are built with ldexp from
+ * integers, never by reinterpreting host floats, so host FTZ/DAZ modes cannot
+ * matter.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <math.h>
+
+#include "exmy_oracle.h"
+
+/* ---------------------------------------------------------------- formats */
+
+int oracle_format_valid(int x, int y, int e_max)
+{
+    if (x < 0 || x > 8 || y < 0 || y > 23) return 0;
+    if (1 + x + y > ORACLE_MAX_K) return 0;
+    if (e_max < 0 || e_max > 254) return 0;           /* D4 */
+    return 1;
+}
+
+/* bias from metadata, D1: the top exponent code 2^x-1 sits at fp32 biased
+ * exponent e_max, i.e. (2^x - 1) - bias + 127 = e_max. */
+int oracle_bias(int x, int e_max) { return (1 << x) + 126 - e_max; }
+
+/* Exact value of a magnitude code (sign bit excluded), Table 1 + P:172-175. */
+double oracle_code_magnitude(uint32_t mag, int x, int y, int e_max)
+{
+    int bias = oracle_bias(x, e_max);
+    uint32_t e = (x == 0) ? 0u : (mag >> y);
+    uint32_t m = mag & ((1u << y) - 1u);
+    if (e == 0)                                   /* subnormal / x=0 (D3) */
+        return ldexp((double)m, 1 - bias - y);
+    return ldexp((double)((1u << y) + m), (int)e - bias - y);
+}
+
+double oracle_code_value(uint32_t code, int x, int y, int e_max)
+{
+    int k = 1 + x + y;
+    uint32_t s = (code >> (k - 1)) & 1u;
+    double a = oracle_code_magnitude(code & ((1u << (k - 1)) - 1u), x, y, e_max);
+    return s ? -a : a;   /* -0.0 for the negative zero code (D10) */
+}
+
+/* ------------------------------------------------------------- the grid */
+
+typedef struct { double v; uint32_t mag; } grid_pt;
+
+static int cmp_grid(const void *a, const void *b)
+{
+    double va = ((const grid_pt *)a)->v, vb = ((const grid_pt *)b)->v;
+    return (va > vb) - (va < vb);
+}
+
+typedef struct { grid_pt *pts; uint32_t n; int x, y, e_max; } grid;
+
+static int grid_build(grid *g, int x, int y, int e_max)
+{
+    g->n = 1u << (x + y);
+    g->x = x; g->y = y; g->e_max = e_max;
+    g->pts = (grid_pt *)malloc(sizeof(grid_pt) * g->n);
+    if (!g->pts) return -1;
+    for (uint32_t c = 0; c < g->n; ++c) {
+        g->pts[c].v = oracle_code_magnitude(c, x, y, e_max);
+        g->pts[c].mag = c;
+    }
+    qsort(g->pts, g->n, sizeof(grid_pt), cmp_grid);
+    return 0;
+}
+
+static void grid_free(grid *g) { free(g->pts); g->pts = NULL; }
+
+/* exact real value of an fp32 bit pattern (finite only) */
+static double f32_value(uint32_t u)
+{
+    uint32_t E = (u >> 23) & 0xFFu, f = u & 0x7FFFFFu;
+    double a = (E == 0) ? ldexp((double)f, -149)
+                        : ldexp((double)(f | 0x800000u), (int)E - 150);
+    return (u >> 31) ? -a : a;
+}
+
+/* nearest magnitude code to |v| (v finite), D5-D8 */
+static uint32_t grid_nearest(const grid *g, double a)
+{
+    /* i = number of grid points with value <= a  (a >= 0 and grid[0] = 0) */
+    uint32_t lo = 0, hi = g->n;
+    while (lo < hi) {
+        uint32_t mid = lo + (hi - lo) / 2;
+        if (g->pts[mid].v <= a) lo = mid + 1; else hi = mid;
+    }
+    uint32_t i = lo;                 /* >= 1 */
+    const grid_pt *below = &g->pts[i - 1];
+    if (below->v == a) return below->mag;
+    if (i == g->n) return below->mag;             /* above max: saturate (D7) */
+    const grid_pt *above = &g->pts[i];
+    double midpoint = (below->v + above->v) / 2.0;   /* exact, see header */
+    if (a < midpoint) return below->mag;
+    if (a > midpoint) return above->mag;
+    /* tie: the code with LSB 0 (D6) */
+    return (below->mag & 1u) ? above->mag : below->mag;
+}
+
+/* ------------------------------------------- exact value -> fp32 / bf16 */
+
+/* RTNE of an exact fp64 value to a binary format with p significand bits
+ * (incl. the implicit bit) and 8 exponent bits, bias 127 (fp32: p=24, bf16:
+ * p=8).  Returns the bit pattern in the low 1+8+(p-1) bits.  Plain
+ * round-to-nearest-even on the quantum 2^(max(E,-126) - (p-1)). */
+static uint32_t round_to_ieee8(double v, int p)
+{
+    uint32_t sign = signbit(v) ? 1u : 0u;
+    double a = fabs(v);
+    uint32_t sbit = sign << (p - 1 + 8);
+    if (a == 0.0) return sbit;
+    int e;
+    (void)frexp(a, &e);               /* a = f * 2^e, f in [0.5,1) => E = e-1 */
+    int E = e - 1;
+    if (E < -126) E = -126;
+    int qe = E - (p - 1);             /* exponent of the output quantum */
+    double s = ldexp(a, -qe);         /* exact scaling: s < 2^p */
+    double fl = floor(s);
+    double frac = s - fl;             /* exact */
+    uint64_t r = (uint64_t)fl;
+    if (frac > 0.5 || (frac == 0.5 && (r & 1u))) r += 1;
+    if (r == 0) return sbit;
+    if (r == (1ull << p)) { r >>= 1; qe += 1; }   /* carry into next binade */
+    uint32_t bits;
+    if (r < (1ull << (p - 1))) {
+        bits = (uint32_t)r;           /* subnormal output (qe == -126-(p-1)) */
+    } else {
+        int ef = qe + (p - 1) + 127;
+        if (ef >= 255) bits = 0xFFu << (p - 1);   /* overflow -> Inf (never hit for k<=9) */
+        else bits = ((uint32_t)ef << (p - 1)) | (uint32_t)(r - (1ull << (p - 1)));
+    }
+    return sbit | bits;
+}
+
+uint32_t oracle_round_f32(double v) { return round_to_ieee8(v, 24); }
+uint16_t oracle_round_bf16(double v) { return (uint16_t)round_to_ieee8(v, 8); }
+
+/* ------------------------------------------------------ element codecs */
+
+static int is_special(uint32_t u) { return ((u >> 23) & 0xFFu) == 0xFFu; }
+
+/* k-bit code of the finite fp32 pattern u: sign bit always from u (D10). */
+static uint32_t encode_finite(const grid *g, uint32_t u)
+{
+    int k = 1 + g->x + g->y;
+    uint32_t s = u >> 31;
+    double a = fabs(f32_value(u));
+    return (s << (k - 1)) | grid_nearest(g, a);
+}
+
+/* per-element codes without packing (specials -> code 0, flagged) */
+int oracle_encode_codes(const void *in, int dtype, int64_t n, int x, int y, int e_max,
+                        uint16_t *codes, uint8_t *special)
+{
+    if (!oracle_format_valid(x, y, e_max)) return -1;
+    grid g;
+    if (grid_build(&g, x, y, e_max)) return -1;
+    for (int64_t i = 0; i < n; ++i) {
+        uint32_t u = (dtype == ORACLE_BF16) ? ((uint32_t)((const uint16_t *)in)[i] << 16)
+                                            : ((const uint32_t *)in)[i];
+        special[i] = (uint8_t)is_special(u);
+        codes[i] = special[i] ? 0 : (uint16_t)encode_finite(&g, u);
+    }
+    grid_free(&g);
+    return 0;
+}
+
+int oracle_encode_element(uint32_t u, int x, int y, int e_max, uint32_t *code)
+{
+    if (!oracle_format_valid(x, y, e_max)) return -1;
+    if (is_special(u)) { *code = 0; return 1; }
+    grid g;
+    if (grid_build(&g, x, y, e_max)) return -1;
+    *code = encode_finite(&g, u);
+    grid_free(&g);
+    return 0;
+}
+
+/* ------------------------------------------------------------ histogram */
+
+/* histogram of the 8-bit biased exponent field; bin 255 holds
+ * NaN/Inf (D18), bin 0 holds zeros and input subnormals (D11). */
+void oracle_histogram(const void *in, int dtype, int64_t n, uint64_t hist[256])
+{
+    for (int64_t i = 0; i < n; ++i) {
+        uint32_t u = (dtype == ORACLE_BF16) ? ((uint32_t)((const uint16_t *)in)[i] << 16)
+                                            : ((const uint32_t *)in)[i];
+        hist[(u >> 23) & 0xFFu] += 1;
+    }
+}
+
+/* metadata = maximum biased exponent before rounding. */
+int oracle_emax(const uint64_t hist[256])
+{
+    for (int b = 254; b >= 0; --b)
+        if (hist[b]) return b;
+    return 0;
+}
+
+/* P:473-478 (D19): the smallest x whose 2^x-1 normal exponent codes, placed
+ * at the top of the populated range, cover at least (1-budget) of the
+ * non-zero finite values. */
+int oracle_choose_x(const uint64_t hist[256], double budget)
+{
+    int e_max = oracle_emax(hist);
+    uint64_t total = 0;
+    for (int b = 1; b <= 254; ++b) total += hist[b];
+    for (int x = 0; x <= 8; ++x) {
+        uint64_t covered = 0;
+        for (int b = e_max - (1 << x) + 2; b <= e_max; ++b)
+            if (b >= 1) covered += hist[b];
+        if ((double)covered >= (1.0 - budget) * (double)total) return x;
+    }
+    return 8;
+}
+
+/* ------------------------------------------------------------- quantize */
+
+static uint32_t load_u32(const void *in, int dtype, int64_t i)
+{
+    return (dtype == ORACLE_BF16) ? ((uint32_t)((const uint16_t *)in)[i] << 16)
+                                  : ((const uint32_t *)in)[i];
+}
+
+static void store_value(void *out, int dtype, int64_t i, double v)
+{
+    if (dtype == ORACLE_BF16) ((uint16_t *)out)[i] = oracle_round_bf16(v);
+    else ((uint32_t *)out)[i] = oracle_round_f32(v);
+}
+
+/* Emulation: fp -> nearest grid value -> same container dtype,
+ * NaN/Inf passed through bit-exactly (D9, D21). */
+int oracle_quantize(const void *in, void *out, int dtype, int64_t n, int x, int y, int e_max)
+{
+    if (!oracle_format_valid(x, y, e_max)) return -1;
+    grid g;
+    if (grid_build(&g, x, y, e_max)) return -1;
+    for (int64_t i = 0; i < n; ++i) {
+        uint32_t u = load_u32(in, dtype, i);
+        if (is_special(u)) {
+            if (dtype == ORACLE_BF16) ((uint16_t *)out)[i] = ((const uint16_t *)in)[i];
+            else ((uint32_t *)out)[i] = u;
+            continue;
+        }
+        uint32_t code = encode_finite(&g, u);
+        store_value(out, dtype, i, oracle_code_value(code, x, y, e_max));
+    }
+    grid_free(&g);
+    return 0;
+}
+
+/* --------------------------------------------------------- bit packing */
+
+int oracle_segments(int k, int widths[4], int64_t n, int64_t offsets[4])
+{
+    int ns = 0;
+    int64_t off = 0;
+    for (int w = 8; w >= 1; w >>= 1) {
+        if (k & w) {
+            widths[ns] = w;
+            if (offsets) offsets[ns] = off;
+            off += n * w / 8;
+            ++ns;
+        }
+    }
+    return ns;
+}
+
+/* element index (row-major) of lane i of container idx */
+static int64_t lane_element(int64_t idx, int i, int64_t rows, int64_t cols, int axis)
+{
+    (void)rows;
+    if (axis == ORACLE_ROWS) {          /* container (g,c): elements (8g+i, c) */
+        int64_t g = idx / cols, c = idx % cols;
+        return (8 * g + i) * cols + c;
+    } else {                            /* container (r,g): elements (r, 8g+i) */
+        int64_t gpr = cols / 8;
+        int64_t r = idx / gpr, g = idx % gpr;
+        return r * cols + 8 * g + i;
+    }
+}
+
+int oracle_shape_ok(int64_t rows, int64_t cols, int axis)
+{
+    if (rows < 0 || cols < 0) return 0;
+    if (axis == ORACLE_ROWS) return rows % 8 == 0;
+    if (axis == ORACLE_COLS) return cols % 8 == 0;
+    return 0;
+}
+
+/* P:311-353, Fig. 3; D12-D16.  codes are uint16 k-bit codes, row-major. */
+int oracle_pack(const uint16_t *codes, int64_t rows, int64_t cols, int axis, int k, uint8_t *packed)
+{
+    if (k < 1 || k > ORACLE_MAX_PACK_K || !oracle_shape_ok(rows, cols, axis)) return -1;
+    int64_t n = rows * cols;
+    int widths[4]; int64_t offs[4];
+    int ns = oracle_segments(k, widths, n, offs);
+    int hi = k;
+    for (int j = 0; j < ns; ++j) {
+        int w = widths[j], lo = hi - w;
+        uint32_t fmask = (1u << w) - 1u;
+        uint8_t *seg = packed + offs[j];
+        if (w == 8) {                   /* D15: byte passthrough, element order */
+            for (int64_t e = 0; e < n; ++e) seg[e] = (uint8_t)((codes[e] >> lo) & 0xFFu);
+        } else {
+            int64_t ncont = n / 8;
+            for (int64_t idx = 0; idx < ncont; ++idx) {
+                uint32_t cont = 0;
+                for (int i = 0; i < 8; ++i) {
+                    uint32_t field = ((uint32_t)codes[lane_element(idx, i, rows, cols, axis)] >> lo) & fmask;
+                    cont |= field << (w * i);
+                }
+                for (int b = 0; b < w; ++b)          /* little-endian container */
+                    seg[idx * w + b] = (uint8_t)(cont >> (8 * b));
+            }
+        }
+        hi = lo;
+    }
+    return 0;
+}
+
+int oracle_unpack(const uint8_t *packed, int64_t rows, int64_t cols, int axis, int k, uint16_t *codes)
+{
+    if (k < 1 || k > ORACLE_MAX_PACK_K || !oracle_shape_ok(rows, cols, axis)) return -1;
+    int64_t n = rows * cols;
+    int widths[4]; int64_t offs[4];
+    int ns = oracle_segments(k, widths, n, offs);
+    for (int64_t e = 0; e < n; ++e) codes[e] = 0;
+    int hi = k;
+    for (int j = 0; j < ns; ++j) {
+        int w = widths[j], lo = hi - w;
+        uint32_t fmask = (1u << w) - 1u;
+        const uint8_t *seg = packed + offs[j];
+        if (w == 8) {
+            for (int64_t e = 0; e < n; ++e) codes[e] |= (uint16_t)((uint32_t)seg[e] << lo);
+        } else {
+            int64_t ncont = n / 8;
+            for (int64_t idx = 0; idx < ncont; ++idx) {
+                uint32_t cont = 0;
+                for (int b = 0; b < w; ++b) cont |= (uint32_t)seg[idx * w + b] << (8 * b);
+                for (int i = 0; i < 8; ++i) {
+                    uint32_t field = (cont >> (w * i)) & fmask;
+                    codes[lane_element(idx, i, rows, cols, axis)] |= (uint16_t)(field << lo);
+                }
+            }
+        }
+        hi = lo;
+    }
+    return 0;
+}
+
+/* --------------------------------------------------------- encode/decode */
+
+/* Type conversion then bit packing.  NaN/Inf are kept out of
+ * band (D9): code 0 in the packed stream plus (index, fp32 bits)
+ * in ascending index order.  Returns the number of specials (all of them,
+ * even beyond capacity), or -1 on invalid arguments. */
+int64_t oracle_encode(const void *in, int dtype, int64_t rows, int64_t cols, int axis,
+                      int x, int y, int e_max, uint8_t *packed,
+                      int64_t *sp_index, uint32_t *sp_bits, int64_t sp_capacity)
+{
+    if (!oracle_format_valid(x, y, e_max) || !oracle_shape_ok(rows, cols, axis)) return -1;
+    if (1 + x + y > ORACLE_MAX_PACK_K) return -1;
+    int64_t n = rows * cols;
+    uint16_t *codes = (uint16_t *)malloc(sizeof(uint16_t) * (size_t)(n ? n : 1));
+    if (!codes) return -1;
+    grid g;
+    if (grid_build(&g, x, y, e_max)) { free(codes); return -1; }
+    int64_t ns = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        uint32_t u = load_u32(in, dtype, i);
+        if (is_special(u)) {
+            codes[i] = 0;
+            if (ns < sp_capacity) { sp_index[ns] = i; sp_bits[ns] = u; }
+            ++ns;
+        } else {
+            codes[i] = (uint16_t)encode_finite(&g, u);
+        }
+    }
+    grid_free(&g);
+    oracle_pack(codes, rows, cols, axis, 1 + x + y, packed);
+    free(codes);
+    return ns;
+}
+
+/* Unpack then code -> exact value -> RTNE to out dtype (D21); specials are
+ * written back from their original fp32 bits (bf16 out: top 16 bits, quiet
+ * bit forced if a NaN payload would vanish, D9). */
+int oracle_decode(const uint8_t *packed, int64_t rows, int64_t cols, int axis,
+                  int x, int y, int e_max,
+                  const int64_t *sp_index, const uint32_t *sp_bits, int64_t sp_count,
+                  void *out, int out_dtype)
+{
+    if (!oracle_format_valid(x, y, e_max) || !oracle_shape_ok(rows, cols, axis)) return -1;
+    if (1 + x + y > ORACLE_MAX_PACK_K) return -1;
+    int64_t n = rows * cols;
+    uint16_t *codes = (uint16_t *)malloc(sizeof(uint16_t) * (size_t)(n ? n : 1));
+    if (!codes) return -1;
+    oracle_unpack(packed, rows, cols, axis, 1 + x + y, codes);
+    for (int64_t i = 0; i < n; ++i)
+        store_value(out, out_dtype, i, oracle_code_value(codes[i], x, y, e_max));
+    free(codes);
+    for (int64_t j = 0; j < sp_count; ++j) {
+        int64_t i = sp_index[j];
+        uint32_t u = sp_bits[j];
+        if (out_dtype == ORACLE_BF16) {
+            uint16_t b = (uint16_t)(u >> 16);
+            if ((u & 0x7FFFFFu) != 0 && (b & 0x7Fu) == 0) b |= 0x40u;   /* keep it a NaN */
+            ((uint16_t *)out)[i] = b;
+        } else {
+            ((uint32_t *)out)[i] = u;
+        }
+    }
+    return 0;
+}
