@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""bench.py -- eXmY codec throughput on B200 (driver contract: one JSON line).
+
+Workload (BASELINE.json configs[1], "config 2"): a 16384 x 16384 bf16 tensor
+~ N(0, 0.02^2) (LLM-weight-like, seed 1), packed along rows, through every
+7-bit format e0m6 .. e6m0.  One STEP is one pass of the whole hot path
+(SURVEY 8(a)):  exponent histogram (A1) -> e_max (A2) -> for each of the 7
+formats: quantize (A3), encode (A4+A5), decode (A6+A7); at N > 1 also the
+histogram all-reduce and the all-gather of packed shards (A8).
+
+value = input GB/s of the step: sum over the codec calls of the bytes of each
+call's input buffer (histogram 2n, quantize 2n, encode 2n, decode n*k/8 per
+format), divided by the device time of the step; at N>1 summed over ranks
+(weak scaling: every rank owns one 16384^2 shard) over the max rank time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+METRIC = "encode/decode input-GB/s per B200 and at 8 GPUs; % of HBM roofline"
+R = C = 16384
+FORMATS = [(x, 6 - x) for x in range(0, 7)]           # e0m6 .. e6m0 (k = 7)
+K_BITS = 7
+SEED = 1
+FALLBACK_HBM_GBS = 6650.0
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ------------------------------------------------------------ clock sampling
+REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting", 0x10: "sync_boost"}
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 3:
+                try:
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                except ValueError:
+                    pass
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [s[0] for s in self.samples]
+        reasons = set()
+        for s in self.samples:
+            for bit, name in REASON_BITS.items():
+                if s[2] & bit and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------- dist
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def init_dist(ws, local, backend="nccl"):
+    if ws > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend, device_id=torch.device("cuda", local) if backend == "nccl" else None)
+        return dist
+    return None
+
+
+# --------------------------------------------------------------- our arm
+def run_ours(args):
+    import paper_2405_13938_b200 as exmy
+    from paper_2405_13938_b200 import dist as xdist
+    import workloads as W
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = init_dist(ws, local)
+    group = None
+
+    n = R * C
+    t = W.bf16_weights((R, C), seed=SEED + rank, device=dev)            # weak scaling: one shard per rank
+    hist = torch.zeros(256, dtype=torch.int64, device=dev)
+    meta = torch.zeros(1, dtype=torch.uint8, device=dev)
+    packed = [torch.empty(n * K_BITS // 8, dtype=torch.uint8, device=dev) for _ in FORMATS]
+    qout = torch.empty_like(t)
+    dout = torch.empty_like(t)
+    cap = 4096
+    spi = torch.empty(cap, dtype=torch.int64, device=dev)
+    spb = torch.empty(cap, dtype=torch.int32, device=dev)
+    spc = torch.zeros(1, dtype=torch.int64, device=dev)
+    gathered = torch.empty(ws * n * K_BITS // 8, dtype=torch.uint8, device=dev) if ws > 1 else None
+    L = exmy.lib()
+    st = torch.cuda.current_stream(dev)
+    sp = exmy._stream(dev)
+    P = exmy._ptr
+    ops = ["hist", "emax", "allreduce", "quantize", "encode", "allgather", "decode"]
+    ev = {o: [] for o in ops}
+
+    def rec(name, fn):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        fn()
+        b.record(st)
+        ev[name].append((a, b))
+
+    def chk(s):
+        if s != 0:
+            raise exmy.ExmyError(s, "bench")
+
+    def step(timed):
+        hist.zero_()
+        f = rec if timed else (lambda name, fn: fn())
+        f("hist", lambda: chk(L.exmy_exponent_histogram(P(t), exmy.BF16, n, P(hist), sp)))
+        if ws > 1:
+            f("allreduce", lambda: xdist.allreduce_histogram(hist, group))
+        f("emax", lambda: chk(L.exmy_emax_from_histogram(P(hist), P(meta), sp)))
+        for i, (x, y) in enumerate(FORMATS):
+            f("quantize", lambda: chk(L.exmy_quantize(P(t), P(qout), exmy.BF16, n, x, y, P(meta), sp)))
+            f("encode", lambda: chk(L.exmy_encode(P(t), exmy.BF16, R, C, exmy.ROWS, x, y, P(meta), P(packed[i]),
+                                                  P(spi), P(spb), P(spc), cap, sp)))
+            if ws > 1:
+                f("allgather", lambda: xdist.allgather_bytes(packed[i], gathered, group))
+            f("decode", lambda: chk(L.exmy_decode(P(packed[i]), R, C, exmy.ROWS, x, y, P(meta), P(spi), P(spb),
+                                                  P(spc), cap, P(dout), exmy.BF16, sp)))
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize(dev)
+    for k in ev:
+        ev[k].clear()
+
+    with ClockSampler(local) as clk:
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(st)
+        for _ in range(args.steps):
+            step(True)
+        t1.record(st)
+        torch.cuda.synchronize(dev)
+        if dist:
+            dist.barrier()
+    ms_total = t0.elapsed_time(t1)
+    if dist:
+        tt = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_total = float(tt.item())
+    ms_step = ms_total / args.steps
+    per_op_ms = {k: sum(a.elapsed_time(b) for a, b in v) / args.steps for k, v in ev.items() if v}
+    launches = {k: len(v) / args.steps for k, v in ev.items() if v}
+
+    # bytes per step (one rank)
+    nf = len(FORMATS)
+    packed_b = n * K_BITS // 8
+    in_bytes = {"hist": 2 * n, "quantize": nf * 2 * n, "encode": nf * 2 * n, "decode": nf * packed_b}
+    alg_bytes = {"hist": 2 * n, "emax": 2048, "quantize": nf * 4 * n, "encode": nf * (2 * n + packed_b),
+                 "decode": nf * (packed_b + 2 * n)}
+    step_in = sum(in_bytes.values())
+    value = ws * step_in / (ms_step * 1e-3) / 1e9
+
+    peak, peak_src = peaks()
+    per_op = {}
+    for k in ("hist", "quantize", "encode", "decode"):
+        ms = per_op_ms[k]
+        nl = launches[k]
+        per_op[k] = {"ms_per_launch": ms / nl, "input_gbs": in_bytes[k] / (ms * 1e-3) / 1e9,
+                     "hbm_gbs": alg_bytes[k] / (ms * 1e-3) / 1e9,
+                     "frac_of_measured": alg_bytes[k] / (ms * 1e-3) / 1e9 / peak,
+                     "frac_of_8tbs": alg_bytes[k] / (ms * 1e-3) / 1e9 / 8000.0}
+    dom = max(("quantize", "encode", "decode", "hist"), key=lambda k: per_op_ms[k])
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(dom)
+        except Exception:
+            traffic = None
+    achieved = per_op[dom]["hbm_gbs"]
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": dom,
+                "algorithmic_bytes_per_launch": alg_bytes[dom] / launches[dom], "peak_source": peak_src}
+
+    # gpu launches of OUR kernels per step: hist 1, emax 1; per format quantize 1,
+    # encode 2 (encode + specials sort), decode 2 (decode + specials scatter)
+    gpu_launches = args.steps * (2 + nf * 5)
+
+    result = {
+        "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": "config2: 16384x16384 bf16 ~N(0,0.02^2) seed 1 (+rank), ROWS packing, "
+                               "7-bit formats e0m6..e6m0; step = histogram, e_max, 7x(quantize, encode, decode)"
+                               + (", + hist all-reduce and packed all-gather (NCCL)" if ws > 1 else ""),
+                   "elements_per_gpu": n, "formats": [f"e{x}m{y}" for x, y in FORMATS], "axis": "rows",
+                   "l2": "inputs (512 MiB) larger than L2 (126 MB); no flush needed",
+                   "parallelism": f"shard-per-rank x{ws}" if ws > 1 else "single GPU",
+                   "value_definition": "sum of codec-call input bytes per step / device step time"},
+        "per_op": per_op, "per_op_ms_per_step": {k: round(v, 4) for k, v in per_op_ms.items()},
+        "roofline": roofline, "gpu_launches": gpu_launches,
+    }
+    result["clocks"] = clk.summary()
+
+    # ---------------- e2e through the C ABI with host buffers (rank-local)
+    e2e_steps = max(1, min(args.steps, 3))
+    hc = {}
+    t_host = t.cpu().pin_memory()
+    host_packed = torch.empty(packed_b, dtype=torch.uint8).pin_memory()
+    host_meta = torch.empty(1, dtype=torch.uint8).pin_memory()
+    host_out = torch.empty_like(t_host).pin_memory()
+    for x, y in FORMATS:
+        hc[(x, y)] = exmy.HostCodec((R, C), torch.bfloat16, (x, y), device=dev, specials_capacity=cap)
+    del qout, packed
+    torch.cuda.empty_cache()
+
+    def e2e_step():
+        for x, y in FORMATS:
+            c = hc[(x, y)]
+            c.encode(t_host, host_packed, host_meta)
+            c.decode(host_packed, host_out)
+        torch.cuda.synchronize(dev)
+        _ = float(host_out[0, 0])
+
+    e2e_step()
+    if dist:
+        dist.barrier()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    for _ in range(e2e_steps):
+        e2e_step()
+    b.record(st)
+    torch.cuda.synchronize(dev)
+    e2e_ms = a.elapsed_time(b) / e2e_steps
+    if dist:
+        tt = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_in = nf * (2 * n + 2 * n + packed_b)     # histogram + encode inputs, decode input per format
+    result["e2e"] = {"value": round(ws * e2e_in / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+                     "h2d_bytes_per_step": nf * (2 * n + packed_b), "d2h_bytes_per_step": nf * (packed_b + 1 + 2 * n),
+                     "ms_per_step": round(e2e_ms, 3), "steps": e2e_steps,
+                     "path": "exmy_encode_host + exmy_decode_host (pinned host buffers) per format"}
+
+    if rank == 0 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(t[:args.cpu_rows].cpu())
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------ the oracle arm
+def oracle_step(bits, orc):
+    """One hot-path pass of the CPU oracle over a (rows, C) bf16 sample."""
+    h = orc.histogram(bits)
+    e = orc.emax(h)
+    nbytes = bits.size * 2
+    in_bytes = nbytes
+    for x, y in FORMATS:
+        orc.quantize(bits, (x, y), e)
+        p, idx, sb, ns = orc.encode(bits, (x, y), e, orc.ROWS)
+        orc.decode(p, bits.shape, (x, y), e, orc.ROWS, idx, sb, bits.dtype)
+        in_bytes += nbytes + nbytes + p.size
+    return in_bytes
+
+
+def cpu_baseline(sample: torch.Tensor):
+    import oracle as orc
+    import workloads as W
+    bits = W.to_bits(sample)
+    orc.lib()
+    t0 = time.perf_counter()
+    in_bytes = oracle_step(bits, orc)
+    dt = time.perf_counter() - t0
+    return {"value": round(in_bytes / dt / 1e9, 5), "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"rows 0..{bits.shape[0]} of the same 16384x16384 bf16 tensor ({bits.size} elements, "
+                      f"{bits.shape[0] / R * 100:.3g}% of it): histogram + 7 x (quantize, encode, decode), "
+                      f"single-threaded scalar C oracle, {dt:.2f} s"}
+
+
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    import oracle as orc
+    import workloads as W
+    t = W.bf16_weights((R, C), seed=SEED, device="cuda" if torch.cuda.is_available() else "cpu")
+    rows = args.cpu_rows
+    bits = W.to_bits(t[:rows])
+    orc.lib()
+    for _ in range(args.warmup):
+        oracle_step(bits, orc)
+    t0 = time.perf_counter()
+    in_bytes = 0
+    for _ in range(args.steps):
+        in_bytes += oracle_step(bits, orc)
+    dt = time.perf_counter() - t0
+    v = in_bytes / dt / 1e9
+    print(json.dumps({
+        "metric": METRIC, "value": round(v, 5), "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "impl": "reference",
+        "config": {"workload": "config2 sample: rows of the 16384x16384 bf16 ~N(0,0.02^2) tensor, ROWS, "
+                               "7-bit formats; step = histogram, e_max, 7x(quantize, encode, decode)",
+                   "rows": rows, "elements": int(bits.size)},
+        "cpu_baseline": {"value": round(v, 5), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{rows} of {R} rows per step (bounded sample), scalar C oracle"},
+        "e2e": {"value": round(v, 5), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-rows", type=int, default=256)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

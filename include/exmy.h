@@ -1,0 +1,199 @@
+/*
+ * exmy.h -- C ABI of the B200 (sm_100a) eXmY tensor codec  (libexmy.so)
+ *
+ * eXmY (arXiv 2405.13938) is a floating-point format with 1 sign bit, X
+ * exponent bits and Y mantissa bits, k = 1+X+Y bits in total, a software
+ * defined exponent bias and subnormals (Table 1,
+ * P:139-175).  Citations: P:n = PAPER.md line n; Dn = reading n in DESIGN.md.
+ *
+ * Format descriptor:
+ *   x in [0,8], y >= 0, k = 1+x+y in [3,9] on the GPU path (every format of
+ *   total width 3..9 bits, 42 formats).
+ *   Metadata ("meta") is the per-tensor MAXIMUM BIASED EXPONENT,
+ *   one uint8 in DEVICE memory, e_max in [0,254] (D4).  It fixes the bias:
+ *   bias = 2^x + 126 - e_max (D1), i.e. the top exponent code 2^x-1 lands on
+ *   fp32 biased exponent e_max.  Kernels clamp a device value of 255 to 254.
+ *
+ * Code layout (D2): [sign(1) | exponent(x) | mantissa(y)], MSB -> LSB.
+ *   e >= 1: value = (-1)^s (1 + m/2^y) 2^(e - bias)
+ *   e == 0 (and every code when x == 0, D3): value = (-1)^s m 2^(1 - bias - y)
+ * Rounding (D5-D8): round to nearest, ties to the code whose LSB
+ *   is 0; values beyond the largest magnitude saturate; values
+ *   that round to zero keep their sign (D10); fp32 subnormal inputs are exact
+ *   (D11).  NaN/Inf are kept out of band (D9).
+ *
+ * Packed layout (Fig. 3; D12-D16):
+ *   a (R,C) row-major tensor with R % 8 == 0 (ROWS) or C % 8 == 0 (COLS) is
+ *   split into groups of 8 elements:
+ *     ROWS: group (g,c) = elements (8g+i, c), container index g*C + c
+ *     COLS: group (r,g) = elements (r, 8g+i), container index r*(C/8) + g
+ *   k is decomposed into its set bits, descending (7 = 4+2+1, 9 = 8+1).
+ *   Segment j (width w_j) takes code bits [hi_j - w_j, hi_j), hi_0 = k: the
+ *   widest segment holds the most significant bits (D13).  For w in {1,2,4}
+ *   container = sum_i field_i << (w*i), stored little-endian in w bytes (D14);
+ *   for w = 8 the segment is the byte array in row-major element order (D15).
+ *   Segments are concatenated in decomposition order; segment j starts at
+ *   byte sum_{j'<j} n*w_j'/8; the total is exactly n*k/8 bytes.
+ *   A row shard [r0,r1) of segment j is the byte range
+ *   off_j + [r0*C*w_j/8, r1*C*w_j/8) (ROWS: r0, r1 multiples of 8) and
+ *   decodes on its own.
+ *
+ * Conventions for every call below:
+ *   - Tensor pointers are CUDA DEVICE pointers owned by the caller; the
+ *     library never allocates, frees or synchronises.  Every device op is
+ *     enqueued on `stream` (a cudaStream_t passed as void*, NULL = legacy
+ *     default stream) and returns after the launches.
+ *   - Inputs are fp32 (EXMY_F32) or bf16 (EXMY_BF16) bit patterns, row-major
+ *     contiguous.  Any alignment is accepted: 16-byte aligned tensors and
+ *     segment bases take the vectorised kernels, others a scalar kernel with
+ *     identical results.
+ *   - n = 0 is a no-op returning EXMY_OK.
+ *   - Errors are returned, never aborted on: EXMY_E_FORMAT (x,y out of range,
+ *     k not in [3,9]), EXMY_E_SHAPE (ROWS with R%8, COLS with C%8, negative
+ *     sizes), EXMY_E_DTYPE, EXMY_E_ARG (NULL pointer where one is required),
+ *     EXMY_E_CAPACITY (capacity < 0), EXMY_E_META (host helpers: e_max or
+ *     bias out of range), EXMY_E_CUDA (launch error from cudaGetLastError).
+ */
+#ifndef EXMY_H
+#define EXMY_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    EXMY_OK = 0,
+    EXMY_E_FORMAT = 1,
+    EXMY_E_META = 2,
+    EXMY_E_SHAPE = 3,
+    EXMY_E_DTYPE = 4,
+    EXMY_E_ALIGN = 5,     /* reserved: misaligned tensors take the scalar kernels */
+    EXMY_E_CAPACITY = 6,
+    EXMY_E_CUDA = 7,
+    EXMY_E_ARG = 8
+} exmy_status;
+
+typedef enum { EXMY_F32 = 0, EXMY_BF16 = 1 } exmy_dtype;
+typedef enum { EXMY_AXIS_ROWS = 0, EXMY_AXIS_COLS = 1 } exmy_axis;
+
+/* ------------------------------------------------------------ host helpers */
+
+/* Library version string. */
+const char *exmy_version(void);
+
+/* Human-readable name of a status code (static storage). */
+const char *exmy_status_string(int status);
+
+/* 1 if (x, y) is a GPU-supported format (x in [0,8], k=1+x+y in [3,9]). */
+int exmy_format_valid(int x, int y);
+
+/* Packed size in bytes, n*k/8; -1 if the format is invalid or
+ * n is negative or not a multiple of 8. */
+int64_t exmy_packed_bytes(int64_t n, int x, int y);
+
+/* Segment plan of width k for n elements: writes the widths
+ * (descending set bits of k) and byte offsets; returns the segment count,
+ * or -1 for k outside [1,15] or bad n.  widths/offsets: host arrays of 4. */
+int exmy_segments(int k, int64_t n, int *widths, int64_t *offsets);
+
+/* bias <-> metadata (D1): bias = 2^x + 126 - e_max.  Return EXMY_E_META if
+ * the result would leave e_max in [0,254]. */
+exmy_status exmy_bias_from_emax(int x, int e_max, int *bias_out);
+exmy_status exmy_emax_from_bias(int x, int bias, int *emax_out);
+
+/* e_max of a HOST histogram: the top populated bin in [0,254], 0 if none
+ * (max exponent before rounding). */
+int exmy_emax_from_histogram_host(const uint64_t *hist_host);
+
+/* Choose X (D19): the smallest x in [0,8] whose 2^x-1 normal
+ * exponent codes, placed at the top of the populated range (bins
+ * e_max-2^x+2 .. e_max), hold at least (1 - flush_budget) of the non-zero
+ * finite values (bins 1..254).  hist_host: 256 host counters. */
+exmy_status exmy_choose_x(const uint64_t *hist_host, double flush_budget, int *x_out);
+
+/* -------------------------------------------------------------- device ops */
+
+/* Exponent histogram (A1): hist[b] += number of elements whose
+ * 8-bit biased exponent field is b.  Bin 0 = zeros and input subnormals,
+ * bin 255 = NaN/Inf (D18).  `hist`: device uint64[256], ACCUMULATED into
+ * (zero it first for a fresh histogram).  Reads n elements once. */
+exmy_status exmy_exponent_histogram(const void *in, int dtype, int64_t n,
+                                    uint64_t *hist, void *stream);
+
+/* Per-tensor metadata from a device histogram (A2): *meta =
+ * top populated bin in [0,254] (0 if none).  One tiny launch; graph-safe. */
+exmy_status exmy_emax_from_histogram(const uint64_t *hist, uint8_t *meta, void *stream);
+
+/* Emulation / quantize (A3): out[i] = the eXmY grid value nearest
+ * to in[i] (RTNE, saturating, subnormals, signed zero), converted RTNE to
+ * the same container dtype (D21); NaN/Inf bit patterns pass through
+ * unchanged.  in/out: n elements of `dtype`; out may alias in. */
+exmy_status exmy_quantize(const void *in, void *out, int dtype, int64_t n,
+                          int x, int y, const uint8_t *meta, void *stream);
+
+/* Encode = type conversion (A4) + power-of-2 bit packing
+ * (A5), fused: codes never touch HBM.
+ *   in: (rows, cols) row-major fp32/bf16; packed: n*k/8 bytes (layout above).
+ *   NaN/Inf (D9): code 0 in the packed stream; (index, fp32 bits) appended to
+ *   sp_index[]/sp_bits[] (device, capacity entries) in ascending index order;
+ *   *sp_count (device uint64) is SET to the total number of specials, even
+ *   when it exceeds capacity (extra entries are dropped; check after the
+ *   stream syncs).  The histogram's bin 255 is that count.  sp_index/sp_bits
+ *   may be NULL iff sp_capacity == 0; sp_count may be NULL only if the input
+ *   is known to hold no NaN/Inf. */
+exmy_status exmy_encode(const void *in, int dtype, int64_t rows, int64_t cols, int axis,
+                        int x, int y, const uint8_t *meta, uint8_t *packed,
+                        int64_t *sp_index, uint32_t *sp_bits, uint64_t *sp_count,
+                        int64_t sp_capacity, void *stream);
+
+/* Decode = unpack (A6) + dequantize (A7), fused: out[i] = value of code i
+ * rounded RTNE to out_dtype (D21); then min(*sp_count, sp_capacity) specials
+ * are written back from their fp32 bits (bf16 out: the top 16 bits, quiet
+ * bit forced if a NaN payload would vanish, D9).  sp_* may all be NULL/0
+ * when the tensor holds no specials.  Decode of a row shard: pass the
+ * shard's own segment bytes (see the layout note) and its row count. */
+exmy_status exmy_decode(const uint8_t *packed, int64_t rows, int64_t cols, int axis,
+                        int x, int y, const uint8_t *meta,
+                        const int64_t *sp_index, const uint32_t *sp_bits,
+                        const uint64_t *sp_count, int64_t sp_capacity,
+                        void *out, int out_dtype, void *stream);
+
+/* Test/diagnostic knobs (process-global, not thread-safe; default 0).
+ * exmy_debug_force_generic(1) routes every element through the integer
+ * generic encode/decode paths instead of the fast paths, so both can be
+ * checked against the oracle; exmy_debug_hist_mode selects the histogram
+ * counter-update variant (0: lane-private read-modify-write, 1: lane-private
+ * shared-memory atomics).  Pass -1 to query.  Return the previous value. */
+int exmy_debug_force_generic(int on);
+int exmy_debug_hist_mode(int mode);
+
+/* ------------------------------------------------ host-buffer conveniences */
+
+/* End-to-end encode of a HOST tensor (pinned memory recommended): H2D copy
+ * into `dev_in` (caller-owned device scratch of n*esize bytes), histogram ->
+ * e_max -> encode into `dev_packed` (device, n*k/8 bytes), D2H copy of the
+ * packed bytes into `host_packed` and of the metadata byte into
+ * `host_meta`.  `dev_hist` (uint64[256]) and `dev_meta` (uint8) are device
+ * scratch; specials as in exmy_encode (device arrays).  Asynchronous on
+ * `stream`: host buffers are valid after the stream syncs. */
+exmy_status exmy_encode_host(const void *host_in, int dtype, int64_t rows, int64_t cols,
+                             int axis, int x, int y,
+                             void *dev_in, uint64_t *dev_hist, uint8_t *dev_meta,
+                             uint8_t *dev_packed, int64_t *sp_index, uint32_t *sp_bits,
+                             uint64_t *sp_count, int64_t sp_capacity,
+                             uint8_t *host_packed, uint8_t *host_meta, void *stream);
+
+/* End-to-end decode of HOST packed bytes: H2D copy into `dev_packed`, decode
+ * into `dev_out`, D2H copy into `host_out`.  meta is a device byte. */
+exmy_status exmy_decode_host(const uint8_t *host_packed, int64_t rows, int64_t cols, int axis,
+                             int x, int y, const uint8_t *meta,
+                             const int64_t *sp_index, const uint32_t *sp_bits,
+                             const uint64_t *sp_count, int64_t sp_capacity,
+                             uint8_t *dev_packed, void *dev_out, int out_dtype,
+                             void *host_out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EXMY_H */

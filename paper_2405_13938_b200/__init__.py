@@ -1,0 +1,380 @@
+"""eXmY tensor codec on B200 (arXiv 2405.13938) -- thin Python binding.
+
+Argument marshalling only: every step of the codec runs in the sm_100a
+kernels of ``libexmy.so`` through its C ABI (``include/exmy.h``).  PyTorch is
+used for device memory, streams and process groups.  There is no CPU
+fallback: importing without the built library raises.
+
+    import paper_2405_13938_b200 as exmy
+    h = exmy.histogram(t)                  # uint64[256] on t.device
+    meta = exmy.emax(h)                    # uint8[1] device metadata
+    q = exmy.quantize(t, "e3m2", meta)     # emulation
+    p = exmy.encode(t, "e3m3", axis="rows")  # Packed
+    t2 = exmy.decode(p)                    # == quantize(t, "e3m3", p.meta)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_PKG, "libexmy.so")
+
+F32, BF16 = 0, 1
+ROWS, COLS = 0, 1
+_AXES = {"rows": ROWS, "cols": COLS, ROWS: ROWS, COLS: COLS}
+
+STATUS = {0: "ok", 1: "E_FORMAT", 2: "E_META", 3: "E_SHAPE", 4: "E_DTYPE", 5: "E_ALIGN",
+          6: "E_CAPACITY", 7: "E_CUDA", 8: "E_ARG"}
+
+
+class ExmyError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(f"{what}: {STATUS.get(status, status)} ({_lib.exmy_status_string(status).decode()})")
+
+
+def _load():
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(
+            f"{_LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the codec has no CPU fallback)")
+    L = ctypes.CDLL(_LIB_PATH)
+    i64, i32, vp, dbl = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_double
+    sig = {
+        "exmy_version": ([], ctypes.c_char_p),
+        "exmy_status_string": ([i32], ctypes.c_char_p),
+        "exmy_format_valid": ([i32, i32], i32),
+        "exmy_packed_bytes": ([i64, i32, i32], i64),
+        "exmy_segments": ([i32, i64, vp, vp], i32),
+        "exmy_bias_from_emax": ([i32, i32, vp], i32),
+        "exmy_emax_from_bias": ([i32, i32, vp], i32),
+        "exmy_emax_from_histogram_host": ([vp], i32),
+        "exmy_choose_x": ([vp, dbl, vp], i32),
+        "exmy_debug_force_generic": ([i32], i32),
+        "exmy_debug_hist_mode": ([i32], i32),
+        "exmy_exponent_histogram": ([vp, i32, i64, vp, vp], i32),
+        "exmy_emax_from_histogram": ([vp, vp, vp], i32),
+        "exmy_quantize": ([vp, vp, i32, i64, i32, i32, vp, vp], i32),
+        "exmy_encode": ([vp, i32, i64, i64, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp], i32),
+        "exmy_decode": ([vp, i64, i64, i32, i32, i32, vp, vp, vp, vp, i64, vp, i32, vp], i32),
+        "exmy_encode_host": ([vp, i32, i64, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, i64, vp, vp, vp], i32),
+        "exmy_decode_host": ([vp, i64, i64, i32, i32, i32, vp, vp, vp, vp, i64, vp, vp, i32, vp, vp], i32),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    return L
+
+
+_lib = _load()
+LIB_PATH = _LIB_PATH
+EXPORTED = ["exmy_version", "exmy_status_string", "exmy_format_valid", "exmy_packed_bytes", "exmy_segments",
+            "exmy_bias_from_emax", "exmy_emax_from_bias", "exmy_emax_from_histogram_host", "exmy_choose_x",
+            "exmy_debug_force_generic", "exmy_debug_hist_mode", "exmy_exponent_histogram",
+            "exmy_emax_from_histogram", "exmy_quantize", "exmy_encode", "exmy_decode", "exmy_encode_host",
+            "exmy_decode_host"]
+
+
+def lib():
+    return _lib
+
+
+def version() -> str:
+    return _lib.exmy_version().decode()
+
+
+# ----------------------------------------------------------------- helpers
+def parse_format(fmt) -> tuple[int, int]:
+    """'e3m2' -> (3, 2); case-insensitive."""
+    if isinstance(fmt, str):
+        f = fmt.strip().lower()
+        if not f.startswith("e") or "m" not in f:
+            raise ValueError(f"bad format {fmt!r}")
+        x, y = f[1:].split("m")
+        x, y = int(x), int(y)
+    else:
+        x, y = int(fmt[0]), int(fmt[1])
+    if not _lib.exmy_format_valid(x, y):
+        raise ValueError(f"unsupported format e{x}m{y} (x in [0,8], 3 <= 1+x+y <= 9)")
+    return x, y
+
+
+def format_name(x: int, y: int) -> str:
+    return f"e{x}m{y}"
+
+
+def all_formats(kmin: int = 3, kmax: int = 9):
+    """Every GPU format of total width kmin..kmax (42 formats for 3..9)."""
+    return [(x, k - 1 - x) for k in range(kmin, kmax + 1) for x in range(0, min(8, k - 1) + 1)]
+
+
+def packed_bytes(n: int, fmt) -> int:
+    x, y = parse_format(fmt)
+    r = _lib.exmy_packed_bytes(n, x, y)
+    if r < 0:
+        raise ValueError("n must be a non-negative multiple of 8")
+    return r
+
+
+def segments(k: int, n: int):
+    w = (ctypes.c_int * 4)()
+    o = (ctypes.c_int64 * 4)()
+    ns = _lib.exmy_segments(k, n, w, o)
+    if ns < 0:
+        raise ValueError("bad k or n")
+    return list(w)[:ns], list(o)[:ns]
+
+
+def bias_from_emax(x: int, e_max: int) -> int:
+    b = ctypes.c_int()
+    _check(_lib.exmy_bias_from_emax(x, e_max, ctypes.byref(b)), "bias_from_emax")
+    return b.value
+
+
+def emax_from_bias(x: int, bias: int) -> int:
+    e = ctypes.c_int()
+    _check(_lib.exmy_emax_from_bias(x, bias, ctypes.byref(e)), "emax_from_bias")
+    return e.value
+
+
+def choose_x(hist, flush_budget: float = 0.0011) -> int:
+    """X from a histogram; hist: 256 counts (any device)."""
+    h = torch.as_tensor(hist).detach().to("cpu", torch.int64).contiguous()
+    xo = ctypes.c_int()
+    _check(_lib.exmy_choose_x(ctypes.c_void_p(h.data_ptr()), float(flush_budget), ctypes.byref(xo)), "choose_x")
+    return xo.value
+
+
+def force_generic(on: bool | None = None) -> bool:
+    """Test knob: route everything through the integer generic paths."""
+    return bool(_lib.exmy_debug_force_generic(-1 if on is None else int(on)))
+
+
+def hist_mode(mode: int | None = None) -> int:
+    return _lib.exmy_debug_hist_mode(-1 if mode is None else int(mode))
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        raise ExmyError(status, what)
+
+
+def _stream(device) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _dtype_code(dt) -> int:
+    if dt == torch.float32:
+        return F32
+    if dt == torch.bfloat16:
+        return BF16
+    raise TypeError(f"eXmY codec takes float32 or bfloat16 tensors, got {dt}")
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("tensor must live on a CUDA device (no CPU fallback)")
+
+
+def _meta_tensor(meta, device) -> torch.Tensor:
+    if isinstance(meta, torch.Tensor):
+        if meta.dtype != torch.uint8 or meta.numel() != 1:
+            raise TypeError("meta must be a uint8 tensor with one element")
+        return meta.to(device) if meta.device != torch.device(device) else meta
+    e = int(meta)
+    if not 0 <= e <= 254:
+        raise ValueError("e_max must be in [0, 254] (D4)")
+    return torch.tensor([e], dtype=torch.uint8, device=device)
+
+
+def _as_2d(t: torch.Tensor):
+    if t.dim() == 0:
+        raise ValueError("scalar tensor")
+    if t.dim() == 1:
+        return 1, t.shape[0]
+    return t.numel() // t.shape[-1], t.shape[-1]
+
+
+# ---------------------------------------------------------------- device ops
+def histogram(t: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Exponent histogram: int64[256] (uint64 semantics) on t.device.
+    ``out`` is accumulated into when given."""
+    _require_cuda(t)
+    t = t.contiguous()
+    if out is None:
+        out = torch.zeros(256, dtype=torch.int64, device=t.device)
+    _check(_lib.exmy_exponent_histogram(_ptr(t), _dtype_code(t.dtype), t.numel(), _ptr(out), _stream(t.device)),
+           "exponent_histogram")
+    return out
+
+
+def emax(hist: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Device metadata byte: top populated histogram bin in [0,254]."""
+    _require_cuda(hist)
+    if out is None:
+        out = torch.empty(1, dtype=torch.uint8, device=hist.device)
+    _check(_lib.exmy_emax_from_histogram(_ptr(hist), _ptr(out), _stream(hist.device)), "emax_from_histogram")
+    return out
+
+
+def max_exponent(t: torch.Tensor) -> torch.Tensor:
+    """Histogram + e_max in one call: the per-tensor metadata of t."""
+    return emax(histogram(t))
+
+
+def quantize(t: torch.Tensor, fmt, meta=None, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Emulation: nearest eXmY grid value in t's dtype; NaN/Inf kept."""
+    _require_cuda(t)
+    x, y = parse_format(fmt)
+    t = t.contiguous()
+    m = max_exponent(t) if meta is None else _meta_tensor(meta, t.device)
+    if out is None:
+        out = torch.empty_like(t)
+    _check(_lib.exmy_quantize(_ptr(t), _ptr(out), _dtype_code(t.dtype), t.numel(), x, y, _ptr(m), _stream(t.device)),
+           "quantize")
+    return out
+
+
+@dataclass
+class Packed:
+    """Packed eXmY tensor: segments of the power-of-2 decomposition."""
+    data: torch.Tensor        # uint8[n*k/8]
+    meta: torch.Tensor        # uint8[1] device: max biased exponent
+    sp_index: torch.Tensor    # int64[capacity]
+    sp_bits: torch.Tensor     # int32[capacity] (fp32 bit patterns)
+    sp_count: torch.Tensor    # int64[1] device (uint64 semantics)
+    shape: tuple
+    x: int
+    y: int
+    axis: int
+    dtype: torch.dtype        # source dtype
+
+    @property
+    def k(self) -> int:
+        return 1 + self.x + self.y
+
+    @property
+    def rows(self) -> int:
+        return _as_2d_shape(self.shape)[0]
+
+    @property
+    def cols(self) -> int:
+        return _as_2d_shape(self.shape)[1]
+
+    def segments(self):
+        """[(width, uint8 view)] in decomposition order."""
+        n = self.rows * self.cols
+        ws, offs = segments(self.k, n)
+        return [(w, self.data[o:o + n * w // 8]) for w, o in zip(ws, offs)]
+
+    def specials(self):
+        cnt = int(self.sp_count.item())
+        c = min(cnt, self.sp_index.numel())
+        return self.sp_index[:c], self.sp_bits[:c], cnt
+
+
+def _as_2d_shape(shape):
+    if len(shape) == 1:
+        return 1, shape[0]
+    r = 1
+    for s in shape[:-1]:
+        r *= s
+    return r, shape[-1]
+
+
+def encode(t: torch.Tensor, fmt, meta=None, axis="rows", specials_capacity: int = 4096,
+           out: torch.Tensor | None = None) -> Packed:
+    """Type conversion + power-of-2 bit packing.  meta=None derives
+    the per-tensor max biased exponent from the histogram."""
+    _require_cuda(t)
+    x, y = parse_format(fmt)
+    ax = _AXES[axis]
+    t = t.contiguous()
+    R, C = _as_2d(t)
+    dev = t.device
+    m = max_exponent(t) if meta is None else _meta_tensor(meta, dev)
+    n = R * C
+    k = 1 + x + y
+    if out is None:
+        out = torch.empty(n * k // 8 if n % 8 == 0 else 0, dtype=torch.uint8, device=dev)
+    cap = int(specials_capacity)
+    spi = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
+    spb = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    spc = torch.zeros(1, dtype=torch.int64, device=dev)
+    _check(_lib.exmy_encode(_ptr(t), _dtype_code(t.dtype), R, C, ax, x, y, _ptr(m), _ptr(out), _ptr(spi), _ptr(spb),
+                            _ptr(spc), cap, _stream(dev)), "encode")
+    return Packed(out, m, spi, spb, spc, tuple(t.shape), x, y, ax, t.dtype)
+
+
+def decode(p: Packed, dtype: torch.dtype | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Unpack + dequantize; RTNE to ``dtype`` (default: source dtype)."""
+    dtype = p.dtype if dtype is None else dtype
+    dev = p.data.device
+    R, C = p.rows, p.cols
+    if out is None:
+        out = torch.empty(p.shape, dtype=dtype, device=dev)
+    cap = p.sp_index.numel() if p.sp_count is not None else 0
+    _check(_lib.exmy_decode(_ptr(p.data), R, C, p.axis, p.x, p.y, _ptr(p.meta), _ptr(p.sp_index), _ptr(p.sp_bits),
+                            _ptr(p.sp_count), cap, _ptr(out), _dtype_code(dtype), _stream(dev)), "decode")
+    return out
+
+
+def decode_raw(data: torch.Tensor, rows: int, cols: int, fmt, meta, axis="rows", dtype=torch.bfloat16,
+               out: torch.Tensor | None = None) -> torch.Tensor:
+    """Decode bare packed bytes (e.g. one row shard) without specials."""
+    x, y = parse_format(fmt)
+    dev = data.device
+    m = _meta_tensor(meta, dev)
+    if out is None:
+        out = torch.empty((rows, cols), dtype=dtype, device=dev)
+    _check(_lib.exmy_decode(_ptr(data), rows, cols, _AXES[axis], x, y, _ptr(m), None, None, None, 0, _ptr(out),
+                            _dtype_code(dtype), _stream(dev)), "decode")
+    return out
+
+
+# ------------------------------------------------------- host-buffer path
+class HostCodec:
+    """End-to-end codec for host tensors (pinned): H2D -> histogram -> e_max ->
+    encode -> D2H, all inside the C ABI (exmy_encode_host / exmy_decode_host).
+    Device scratch is allocated once here (the library itself never allocates)."""
+
+    def __init__(self, shape, dtype, fmt, axis="rows", device="cuda", specials_capacity: int = 4096):
+        self.x, self.y = parse_format(fmt)
+        self.R, self.C = _as_2d_shape(tuple(shape))
+        self.shape = tuple(shape)
+        self.dtype = dtype
+        self.axis = _AXES[axis]
+        self.device = torch.device(device)
+        n = self.R * self.C
+        self.nbytes_packed = n * (1 + self.x + self.y) // 8
+        self.dev_in = torch.empty(self.shape, dtype=dtype, device=device)
+        self.dev_hist = torch.zeros(256, dtype=torch.int64, device=device)
+        self.dev_meta = torch.zeros(1, dtype=torch.uint8, device=device)
+        self.dev_packed = torch.empty(self.nbytes_packed, dtype=torch.uint8, device=device)
+        self.dev_out = torch.empty(self.shape, dtype=dtype, device=device)
+        self.cap = specials_capacity
+        self.spi = torch.empty(max(self.cap, 1), dtype=torch.int64, device=device)
+        self.spb = torch.empty(max(self.cap, 1), dtype=torch.int32, device=device)
+        self.spc = torch.zeros(1, dtype=torch.int64, device=device)
+
+    def encode(self, host_in: torch.Tensor, host_packed: torch.Tensor, host_meta: torch.Tensor | None = None):
+        _check(_lib.exmy_encode_host(_ptr(host_in), _dtype_code(self.dtype), self.R, self.C, self.axis, self.x,
+                                     self.y, _ptr(self.dev_in), _ptr(self.dev_hist), _ptr(self.dev_meta),
+                                     _ptr(self.dev_packed), _ptr(self.spi), _ptr(self.spb), _ptr(self.spc), self.cap,
+                                     _ptr(host_packed), _ptr(host_meta), _stream(self.device)), "encode_host")
+
+    def decode(self, host_packed: torch.Tensor, host_out: torch.Tensor):
+        _check(_lib.exmy_decode_host(_ptr(host_packed), self.R, self.C, self.axis, self.x, self.y, _ptr(self.dev_meta),
+                                     _ptr(self.spi), _ptr(self.spb), _ptr(self.spc), self.cap, _ptr(self.dev_packed),
+                                     _ptr(self.dev_out), _dtype_code(self.dtype), _ptr(host_out),
+                                     _stream(self.device)), "decode_host")

@@ -1,0 +1,94 @@
+// exmy_tu_encode.cu -- K3 encode launchers (+ K5 specials sort).
+#include "exmy_launch.cuh"
+
+namespace exmy {
+
+namespace {
+template <int K, bool BF16>
+exmy_status launch_encode_k(const uint8_t *in, int64_t R, int64_t C, int axis, int x, int y, const uint8_t *meta,
+                            uint8_t *packed, const Plan &p, int64_t *spi, uint32_t *spb,
+                            unsigned long long *spc, int64_t cap, cudaStream_t st) {
+    constexpr int V = Elem<BF16>::V;
+    const int64_t n = R * C;
+    bool vec = aligned(in, 16);
+    if (axis == EXMY_AXIS_ROWS) {
+        vec = vec && (C % V == 0);
+        for (int s = 0; s < p.nseg; ++s) {
+            size_t a = p.w[s] == 8 ? (size_t)V : (size_t)((V * p.w[s]) < 16 ? V * p.w[s] : 16);
+            vec = vec && aligned(packed + p.so.off[s], a);
+        }
+        if (vec) {
+            const int threads = 256;
+            static int occ = 0;
+            if (!occ) occ = occupancy(k_encode_rows<K, BF16>, threads, 0);
+            const int64_t CV = C / V, G = R / 8;
+            int64_t gx = cdiv(CV, threads);
+            int64_t target = (int64_t)num_sms() * occ;
+            int64_t gy = target / gx;
+            if (gy < 1) gy = 1;
+            if (gy > G) gy = G;
+            if (gy > 65535) gy = 65535;
+            if (gx > INT_MAX) return EXMY_E_SHAPE;
+            k_encode_rows<K, BF16><<<dim3((unsigned)gx, (unsigned)gy), threads, 0, st>>>(
+                in, R, C, x, y, meta, packed, p.so, spi, spb, spc, cap);
+            return launch_status();
+        }
+    } else {
+        for (int s = 0; s < p.nseg; ++s) vec = vec && aligned(packed + p.so.off[s], p.w[s]);
+        if (vec) {
+            const int threads = 256;
+            static int occ = 0;
+            if (!occ) occ = occupancy(k_encode_cols<K, BF16>, threads, 0);
+            int64_t tiles = cdiv(n / 8, 128);
+            int64_t blocks = cdiv(tiles, threads / 32);
+            int64_t maxb = (int64_t)num_sms() * occ;
+            if (blocks > maxb) blocks = maxb;
+            k_encode_cols<K, BF16><<<(unsigned)blocks, threads, 0, st>>>(in, n, x, y, meta, packed, p.so, spi, spb,
+                                                                         spc, cap);
+            return launch_status();
+        }
+    }
+    const int64_t ncont = n / 8;
+    int64_t blocks = cdiv(ncont, 256);
+    int64_t maxb = (int64_t)num_sms() * 8;
+    if (blocks > maxb) blocks = maxb;
+    k_encode_generic<BF16><<<(unsigned)blocks, 256, 0, st>>>(in, C, ncont, axis, x, y, meta, packed, p.so, p.nseg,
+                                                             make_int4(p.w[0], p.w[1], p.w[2], p.w[3]), spi, spb,
+                                                             spc, cap);
+    return launch_status();
+}
+
+template <bool BF16>
+exmy_status encode_dispatch(int k, const uint8_t *in, int64_t R, int64_t C, int axis, int x, int y,
+                            const uint8_t *meta, uint8_t *packed, const Plan &p, int64_t *spi, uint32_t *spb,
+                            unsigned long long *spc, int64_t cap, cudaStream_t st) {
+    switch (k) {
+        case 3: return launch_encode_k<3, BF16>(in, R, C, axis, x, y, meta, packed, p, spi, spb, spc, cap, st);
+        case 4: return launch_encode_k<4, BF16>(in, R, C, axis, x, y, meta, packed, p, spi, spb, spc, cap, st);
+        case 5: return launch_encode_k<5, BF16>(in, R, C, axis, x, y, meta, packed, p, spi, spb, spc, cap, st);
+        case 6: return launch_encode_k<6, BF16>(in, R, C, axis, x, y, meta, packed, p, spi, spb, spc, cap, st);
+        case 7: return launch_encode_k<7, BF16>(in, R, C, axis, x, y, meta, packed, p, spi, spb, spc, cap, st);
+        case 8: return launch_encode_k<8, BF16>(in, R, C, axis, x, y, meta, packed, p, spi, spb, spc, cap, st);
+        case 9: return launch_encode_k<9, BF16>(in, R, C, axis, x, y, meta, packed, p, spi, spb, spc, cap, st);
+    }
+    return EXMY_E_FORMAT;
+}
+
+}  // namespace
+
+exmy_status launch_encode(const uint8_t *in, bool bf16, int64_t R, int64_t C, int axis, int x, int y,
+                          const uint8_t *meta, uint8_t *packed, int64_t *spi, uint32_t *spb,
+                          unsigned long long *spc, int64_t cap, cudaStream_t st) {
+    const int k = 1 + x + y;
+    Plan p = make_plan(k, R * C);
+    return bf16 ? encode_dispatch<true>(k, in, R, C, axis, x, y, meta, packed, p, spi, spb, spc, cap, st)
+                : encode_dispatch<false>(k, in, R, C, axis, x, y, meta, packed, p, spi, spb, spc, cap, st);
+}
+
+exmy_status launch_specials_sort(int64_t *spi, uint32_t *spb, const unsigned long long *spc, int64_t cap,
+                                 cudaStream_t st) {
+    k_specials_sort<<<1, 1024, 0, st>>>(spi, spb, spc, cap);
+    return launch_status();
+}
+
+}  // namespace exmy

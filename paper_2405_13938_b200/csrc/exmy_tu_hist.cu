@@ -1,0 +1,41 @@
+// exmy_tu_hist.cu -- K1 exponent histogram + K1b e_max launchers.
+#include "exmy_launch.cuh"
+
+namespace exmy {
+
+namespace {
+template <bool BF16, int MODE>
+exmy_status launch_hist_vec(const uint8_t *in, int64_t n, unsigned long long *hist, cudaStream_t st) {
+    static int occ = 0;
+    if (!occ) {
+        cudaFuncSetAttribute(k_hist<BF16, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM);
+        occ = occupancy(k_hist<BF16, MODE>, HIST_THREADS, HIST_SMEM);
+    }
+    const int64_t nvec = n / Elem<BF16>::V;
+    int64_t blocks = cdiv(cdiv(nvec, 128), HIST_WARPS);
+    if (blocks < 1) blocks = 1;
+    int64_t maxb = (int64_t)num_sms() * occ;
+    if (blocks > maxb) blocks = maxb;
+    k_hist<BF16, MODE><<<(unsigned)blocks, HIST_THREADS, HIST_SMEM, st>>>(in, n, hist);
+    return launch_status();
+}
+}  // namespace
+
+exmy_status launch_histogram(const uint8_t *in, bool bf16, int64_t n, unsigned long long *hist, cudaStream_t st) {
+    if (!aligned(in, 16)) {
+        int64_t blocks = cdiv(n, 256);
+        if (blocks > (int64_t)num_sms() * 4) blocks = (int64_t)num_sms() * 4;
+        if (bf16) k_hist_scalar<true><<<(unsigned)blocks, 256, 0, st>>>(in, n, hist);
+        else k_hist_scalar<false><<<(unsigned)blocks, 256, 0, st>>>(in, n, hist);
+        return launch_status();
+    }
+    if (bf16) return g_hist_mode ? launch_hist_vec<true, 1>(in, n, hist, st) : launch_hist_vec<true, 0>(in, n, hist, st);
+    return g_hist_mode ? launch_hist_vec<false, 1>(in, n, hist, st) : launch_hist_vec<false, 0>(in, n, hist, st);
+}
+
+exmy_status launch_emax(const unsigned long long *hist, uint8_t *meta, cudaStream_t st) {
+    k_emax<<<1, 256, 0, st>>>(hist, meta);
+    return launch_status();
+}
+
+}  // namespace exmy

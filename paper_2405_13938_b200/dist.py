@@ -1,0 +1,97 @@
+"""Sharded eXmY driver (A8): one process per GPU, torch.distributed (NCCL over
+NVLink 5 / NVSwitch on B200; gloo in the CPU tests).
+
+The paper's layout is shard-friendly: "the array can be sharded along rows or
+columns, before or after packing, and each shard can be independently
+reconstructed".  Rank r owns rows [r*R/G, (r+1)*R/G); a row
+shard's packed bytes are, per segment j, the contiguous byte range
+off_j + [r0*C*w_j/8, r1*C*w_j/8) of the single-GPU packed buffer.  So:
+
+  1. each rank histograms its shard; one 2 KiB all-reduce (sum) gives the
+     global per-tensor histogram -> global e_max (metadata);
+  2. encode / decode are embarrassingly parallel (no communication);
+  3. the exchange of compressed shards ("network
+     communication") is one all-gather of each rank's packed bytes;
+     `to_global_layout` re-arranges the gathered shard buffers into exactly
+     the bytes a single-GPU encode of the whole tensor produces.
+
+The codec calls go through ``codec`` (default: this package's CUDA binding)
+so the host logic can be exercised with any implementation of the same four
+calls; the product path has no CPU fallback.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def _default_codec():
+    import paper_2405_13938_b200 as exmy
+    return exmy
+
+
+def shard_rows(R: int, G: int, r: int, axis_rows: bool = True) -> tuple[int, int]:
+    """Row range of rank r (ROWS packing needs multiples of 8)."""
+    if R % G:
+        raise ValueError(f"rows {R} not divisible by world size {G}")
+    per = R // G
+    if axis_rows and per % 8:
+        raise ValueError("ROWS packing needs R/G to be a multiple of 8 (P:351-353)")
+    return r * per, (r + 1) * per
+
+
+def allreduce_histogram(hist: torch.Tensor, group=None) -> torch.Tensor:
+    """C1: sum of the per-rank exponent histograms (int64[256], in place)."""
+    dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=group)
+    return hist
+
+
+def allgather_bytes(local: torch.Tensor, out: torch.Tensor, group=None) -> torch.Tensor:
+    """C2: all-gather of equal-size packed shards into out[G * nbytes]."""
+    dist.all_gather_into_tensor(out, local, group=group)
+    return out
+
+
+def to_global_layout(gathered: torch.Tensor, G: int, rows_per_rank: int, C: int, k: int, codec=None) -> torch.Tensor:
+    """Rearrange G concatenated shard buffers (rank order) into the byte layout
+    of a single encode of the full (G*rows_per_rank, C) tensor."""
+    codec = codec or _default_codec()
+    n_local = rows_per_rank * C
+    nb = n_local * k // 8
+    ws, offs = codec.segments(k, n_local)
+    parts = []
+    for w, o in zip(ws, offs):
+        seg_len = n_local * w // 8
+        for r in range(G):
+            parts.append(gathered[r * nb + o: r * nb + o + seg_len])
+    return torch.cat(parts)
+
+
+def sharded_encode(shard: torch.Tensor, fmt, axis="rows", group=None, codec=None):
+    """Encode this rank's row shard with the GLOBAL per-tensor e_max.
+    Returns (packed, meta); byte-identical to the corresponding ranges of a
+    single-GPU encode of the full tensor."""
+    codec = codec or _default_codec()
+    hist = codec.histogram(shard)
+    allreduce_histogram(hist, group)
+    meta = codec.emax(hist)
+    return codec.encode(shard, fmt, meta, axis=axis), meta
+
+
+def sharded_roundtrip(shard: torch.Tensor, fmt, axis="rows", group=None, codec=None, gather=True):
+    """Encode own shard -> all-gather packed shards -> decode every shard.
+    Returns (global packed bytes in single-GPU layout, decoded full tensor)."""
+    codec = codec or _default_codec()
+    G = dist.get_world_size(group)
+    p, meta = sharded_encode(shard, fmt, axis, group, codec)
+    R_local, C = (1, shard.shape[0]) if shard.dim() == 1 else (shard.numel() // shard.shape[-1], shard.shape[-1])
+    nb = p.data.numel()
+    out = torch.empty(G * nb, dtype=torch.uint8, device=p.data.device)
+    allgather_bytes(p.data, out, group)
+    k = 1 + p.x + p.y
+    glob = to_global_layout(out, G, R_local, C, k, codec)
+    if not gather:
+        return glob, None
+    dec = [codec.decode_raw(out[r * nb:(r + 1) * nb], R_local, C, (p.x, p.y), meta, axis=axis, dtype=shard.dtype)
+           for r in range(G)]
+    return glob, torch.cat(dec, 0)

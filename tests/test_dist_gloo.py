@@ -1,0 +1,114 @@
+"""N>1 host logic of the sharded driver (paper_2405_13938_b200.dist) on CPU:
+world_size 2 and 4 over gloo, with the oracle standing in for the kernels
+(the product path itself has no CPU fallback).  Checks the two properties
+the exchange step must give: all-gathered packed bytes == a single encode of
+the whole tensor (global e_max via the histogram all-reduce), and
+decode of every gathered shard == quantize of the whole tensor."""
+import os
+import socket
+import types
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+class OracleCodec:
+    """The four codec calls of the binding, computed by the CPU oracle."""
+
+    def __init__(self):
+        import oracle
+        self.o = oracle
+        oracle.lib()
+
+    def segments(self, k, n):
+        return self.o.segments(k, n)
+
+    def histogram(self, t):
+        import workloads as W
+        return torch.from_numpy(self.o.histogram(W.to_bits(t)).astype(np.int64))
+
+    def emax(self, hist):
+        return torch.tensor([self.o.emax(hist.numpy().astype(np.uint64))], dtype=torch.uint8)
+
+    def encode(self, t, fmt, meta, axis="rows"):
+        import workloads as W
+        x, y = self.o.parse_format(fmt)
+        bits = W.to_bits(t)
+        ax = self.o.ROWS if axis == "rows" else self.o.COLS
+        packed, _, _, _ = self.o.encode(bits, (x, y), int(meta.item()), ax)
+        return types.SimpleNamespace(data=torch.from_numpy(packed), x=x, y=y)
+
+    def decode_raw(self, data, rows, cols, fmt, meta, axis="rows", dtype=torch.bfloat16):
+        import workloads as W
+        ax = self.o.ROWS if axis == "rows" else self.o.COLS
+        out = self.o.decode(data.numpy(), (rows, cols), fmt, int(meta.item()) if torch.is_tensor(meta) else meta,
+                            ax, out_dtype=np.uint16 if dtype == torch.bfloat16 else np.uint32)
+        return W.from_bits(out)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, ws, port, fmt, axis, results):
+    import sys
+    sys.path.insert(0, ROOT)
+    import workloads as W
+    from paper_2405_13938_b200 import dist as xdist
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=ws)
+    try:
+        full = W.bf16_weights((64, 48), seed=11, std=0.05)
+        full.view(-1)[5] = float("inf")  # specials don't disturb the byte layout
+        r0, r1 = xdist.shard_rows(64, ws, rank, axis == "rows")
+        codec = OracleCodec()
+        glob, dec = xdist.sharded_roundtrip(full[r0:r1].contiguous(), fmt, axis=axis, codec=codec)
+        results[rank] = (glob.numpy().tobytes(), W.to_bits(dec).tobytes())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ws", [2, 4])
+@pytest.mark.parametrize("fmt,axis", [("e3m3", "rows"), ("e2m2", "cols"), ("e5m3", "rows"), ("e1m1", "cols")])
+def test_sharded_roundtrip_gloo(orc, ws, fmt, axis):
+    import workloads as W
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    results = mgr.dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, ws, port, fmt, axis, results)) for r in range(ws)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    full = W.bf16_weights((64, 48), seed=11, std=0.05)
+    full.view(-1)[5] = float("inf")
+    bits = W.to_bits(full)
+    e = orc.emax(orc.histogram(bits))
+    ax = orc.ROWS if axis == "rows" else orc.COLS
+    ref_packed = orc.encode(bits, fmt, e, ax)[0]
+    q = orc.quantize(bits, fmt, e)
+    q.reshape(-1)[5] = 0  # decode_raw carries no specials list: code 0 -> +0
+    for r in range(ws):
+        glob, dec = results[r]
+        assert np.frombuffer(glob, np.uint8).tolist() == ref_packed.tolist()
+        np.testing.assert_array_equal(np.frombuffer(dec, np.uint16).reshape(64, 48), q)
+
+
+def test_shard_rows_validation():
+    from paper_2405_13938_b200 import dist as xdist
+    assert xdist.shard_rows(64, 4, 1) == (16, 32)
+    with pytest.raises(ValueError):
+        xdist.shard_rows(60, 8, 0)
+    with pytest.raises(ValueError):
+        xdist.shard_rows(64, 4, 0, True) if False else xdist.shard_rows(48, 4, 0, True)
+    assert xdist.shard_rows(48, 4, 0, False) == (0, 12)
