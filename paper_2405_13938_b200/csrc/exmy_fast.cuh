@@ -1,0 +1,782 @@
+// exmy_fast.cuh -- the fast (vectorised, SWAR) encode / decode / quantize
+// kernels.  Same results as the integer generic path (exmy_device.cuh) bit
+// for bit; every kernel checks the fast-path preconditions on the device
+// (warp-uniform, from the metadata byte) and falls back per tile.
+//
+// Encode: one addition does the rounding.  For |v| in binade Ecl (clamped
+// to [o+1, e_max+1]) the grid quantum is q = 2^(Ecl-127-y) (subnormal
+// region: Ecl = o+1).  With C = 2^7 q as a bf16 (or 2^23 q as an fp32),
+// ulp(C) = q and |v| < 2^(y+1) q <= C, so RN(|v| + C) = C + RTNE_q(|v|)
+// exactly (ties to an even significand = even code, y >= 1), and the
+// count of quanta is bits(RN(|v|+C)) - bits(C).  The code is that count
+// plus (Ecl-o-1) << y (the implicit bit is in the count).  A carry out of
+// the binade lands on the next exponent code; saturation is one min.
+// For y = 0 the tie parity of the count and of the code differ when
+// Ecl-o-1 is odd; C is then moved by one quantum so the hardware's "even
+// significand" is the even code.  bf16 inputs run two elements per 32-bit
+// register (16-bit SIMD lanes, HADD2.BF16) for y <= 6.
+//
+// Decode: the magnitude code shifted into a bf16/fp32 bit pattern is the
+// value scaled by 2^-o (code exponent 0 lands on subnormals); one
+// multiply by 2^o (RN, subnormals kept) gives RTNE(exact value) (D21).
+//
+// Packing: codes are moved into byte-lane registers (4 containers x one
+// element each) and the power-of-2 segments are built with shift/LOP3
+// masks and PRMT byte transposes (SWAR) -- about 2 ops per element for
+// k = 7 instead of 3 ops per element per segment.
+#pragma once
+#include "exmy_kernels.cuh"
+
+namespace exmy {
+
+// ---------------------------------------------------------- SIMD helpers
+__device__ __forceinline__ uint32_t vmax_u16x2(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("max.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+__device__ __forceinline__ uint32_t vmin_u16x2(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("min.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+__device__ __forceinline__ uint32_t hadd2_bf16(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+__device__ __forceinline__ uint32_t hsub2_bf16(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("sub.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+__device__ __forceinline__ uint32_t hmul2_bf16(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) { return __byte_perm(a, b, s); }
+
+template <int S>
+__device__ __forceinline__ uint32_t shl_s(uint32_t v) {   // shift left by S (right if S < 0)
+    if constexpr (S >= 0) return v << S;
+    else return v >> (-S);
+}
+
+// ------------------------------------------------------- fast parameters
+struct FastP {
+    // encode / quantize
+    bool enc_simd;      // bf16 16-bit-lane path usable (bf16 input, y <= 6)
+    bool enc_f32;       // per-element fp32 path usable
+    bool y0;            // parity fix needed
+    uint32_t lo2, hi2;  // clamp bounds on the exponent field (bf16 lanes)
+    uint32_t k2, k3;    // (7-y)<<7, (o+1)<<y per lane (bf16 lanes)
+    uint32_t m2;        // M per lane
+    uint32_t par2;      // parity constant per lane (y = 0)
+    uint32_t lo, hi, k2f, k3f, parf;   // fp32 variants
+    int sh_b, sh_f;     // 7-y, 23-y
+    // decode
+    bool dec_fast;      // fp32 out: x <= 7
+    bool dec_fast_bf;   // bf16 out: x <= 7, y <= 7
+    bool two_mul;       // o > 127
+    uint32_t s1_bf2, s2_bf2;   // 2^min(o,127), 2^(o-127) as bf16 pairs
+    float s1_f, s2_f;
+    uint32_t maxv2;     // largest grid magnitude as bf16 lanes (quantize)
+    uint32_t maxvf;     // ... as fp32 bits
+};
+
+__device__ __forceinline__ uint32_t bf16_pow2(int e) {   // e in [-133, 127]
+    return e >= -126 ? (uint32_t)(e + 127) << 7 : (1u << (e + 133));
+}
+
+__device__ __forceinline__ FastP make_fast(const Fmt &F, bool bf16_in, int force_generic) {
+    FastP P;
+    const int x = F.x, y = F.y, o = F.o, e = F.e_max;
+    const bool base = !force_generic && o >= 0;
+    P.enc_simd = base && bf16_in && y <= 6 && e <= 246 + y;
+    P.enc_f32 = base && y <= 22 && e <= 230 + y;
+    P.y0 = (y == 0);
+    P.lo2 = ((uint32_t)(o + 1) << 7) * 0x00010001u;
+    P.hi2 = ((uint32_t)(e + 1) << 7) * 0x00010001u;
+    P.k2 = ((uint32_t)(7 - (y > 7 ? 7 : y)) << 7) * 0x00010001u;
+    P.k3 = ((uint32_t)(o + 1) << y) * 0x00010001u;
+    P.m2 = F.M * 0x00010001u;
+    P.par2 = ((uint32_t)((o + 1) & 1)) * 0x00010001u;
+    P.lo = (uint32_t)(o + 1) << 23;
+    P.hi = (uint32_t)(e + 1) << 23;
+    P.k2f = (uint32_t)(23 - y) << 23;
+    P.k3f = (uint32_t)(o + 1) << y;
+    P.parf = (uint32_t)((o + 1) & 1);
+    P.sh_b = 7 - (y > 7 ? 7 : y);
+    P.sh_f = 23 - y;
+    P.dec_fast = !force_generic && x <= 7;
+    P.dec_fast_bf = P.dec_fast && y <= 7;
+    P.two_mul = o > 127;
+    const int e1 = o > 127 ? 127 : o, e2 = o > 127 ? o - 127 : 0;
+    P.s1_bf2 = (e1 >= -133 ? bf16_pow2(e1) : 0u) * 0x00010001u;
+    P.s2_bf2 = bf16_pow2(e2) * 0x00010001u;
+    P.s1_f = pow2f_exact(e1 < -149 ? -149 : e1);
+    P.s2_f = pow2f_exact(e2);
+    // largest grid magnitude as bf16 / fp32 bits (quantize saturation); only
+    // used when the fast encode preconditions hold (o >= 0, y <= 22)
+    uint32_t mv, mvf;
+    const uint32_t yb = (uint32_t)(y > 7 ? 7 : y);
+    if (x == 0) {   // (2^y - 1) 2^(e_max-126-y) = (2 - 2^(1-y)) 2^(e_max-128) ... normalised below
+        if (e >= 1) {
+            mv = ((uint32_t)e << 7) | ((((1u << yb) - 1u) << (8 - yb)) & 0x7Fu);
+            mvf = ((uint32_t)e << 23) | ((((1u << y) - 1u) << (24 - y)) & 0x7FFFFFu);
+        } else {    // e_max = 0: a subnormal in both containers
+            mv = (1u << 7) - (1u << (7 - yb));
+            mvf = (1u << 23) - (1u << (23 - y));
+        }
+    } else {
+        mv = ((uint32_t)e << 7) | ((((1u << yb) - 1u) << (7 - yb)) & 0x7Fu);
+        mvf = ((uint32_t)e << 23) | ((((1u << y) - 1u) << (23 - y)) & 0x7FFFFFu);
+    }
+    P.maxvf = mvf;
+    P.maxv2 = mv * 0x00010001u;
+    return P;
+}
+
+// ------------------------------------------------------- code computation
+// two bf16 elements (one 32-bit word) -> two k-bit codes in 16-bit lanes;
+// flag accumulates lanes holding NaN/Inf (bit 15 / 31 set)
+template <int K>
+__device__ __forceinline__ uint32_t enc_pair_bf16(uint32_t w, const FastP &P, uint32_t &flag) {
+    const uint32_t a2 = w & 0x7FFF7FFFu;
+    uint32_t ecl = w & 0x7F807F80u;
+    ecl = vmax_u16x2(ecl, P.lo2);
+    ecl = vmin_u16x2(ecl, P.hi2);
+    uint32_t c = ecl + P.k2;
+    if (P.y0) c += ((ecl >> 7) ^ P.par2) & 0x00010001u;   // even code, not even count
+    const uint32_t s = hadd2_bf16(a2, c);
+    uint32_t code = s - c + (ecl >> P.sh_b) - P.k3;
+    code = vmin_u16x2(code, P.m2);
+    code |= (w >> (16 - K)) & ((1u << (K - 1)) * 0x00010001u);
+    flag |= a2 + 0x00800080u;
+    return code;
+}
+
+// one fp32 pattern -> k-bit code; flag accumulates NaN/Inf
+template <int K>
+__device__ __forceinline__ uint32_t enc_f32_fast(uint32_t u, const FastP &P, uint32_t &flag) {
+    const uint32_t a = u & 0x7FFFFFFFu;
+    uint32_t ecl = u & 0x7F800000u;
+    ecl = max(ecl, P.lo);
+    ecl = min(ecl, P.hi);
+    uint32_t c = ecl + P.k2f;
+    if (P.y0) c += ((ecl >> 23) ^ P.parf) & 1u;
+    const uint32_t s = __float_as_uint(__fadd_rn(__uint_as_float(a), __uint_as_float(c)));
+    uint32_t code = s - c + (ecl >> P.sh_f) - P.k3f;
+    code = min(code, (1u << (K - 1)) - 1u);
+    code |= (u >> (32 - K)) & (1u << (K - 1));
+    flag |= a + 0x00800000u;
+    return code;
+}
+
+// quantize two bf16 elements directly in bf16 arithmetic (value, not code)
+__device__ __forceinline__ uint32_t quant_pair_bf16(uint32_t w, const FastP &P, uint32_t &flag) {
+    const uint32_t a2 = w & 0x7FFF7FFFu;
+    uint32_t ecl = w & 0x7F807F80u;
+    ecl = vmax_u16x2(ecl, P.lo2);
+    ecl = vmin_u16x2(ecl, P.hi2);
+    uint32_t c = ecl + P.k2;
+    if (P.y0) c += ((ecl >> 7) ^ P.par2) & 0x00010001u;
+    const uint32_t s = hadd2_bf16(a2, c);
+    uint32_t q = hsub2_bf16(s, c);            // exact (Sterbenz): RTNE_q(|v|)
+    q = vmin_u16x2(q, P.maxv2);
+    flag |= a2 + 0x00800080u;
+    return q | (w & 0x80008000u);
+}
+
+// ------------------------------------------------------ decode helpers
+// code pair (16-bit lanes) -> bf16 pair
+template <int K>
+__device__ __forceinline__ uint32_t dec_pair_bf16(uint32_t cp, const FastP &P, int y) {
+    uint32_t mag = cp & (((1u << (K - 1)) - 1u) * 0x00010001u);
+    uint32_t b = mag << (7 - y);
+    uint32_t v = hmul2_bf16(b, P.s1_bf2);
+    if (P.two_mul) v = hmul2_bf16(v, P.s2_bf2);
+    return v | ((cp << (16 - K)) & 0x80008000u);
+}
+
+template <int K>
+__device__ __forceinline__ uint32_t dec_f32_fast(uint32_t code, const FastP &P, int y) {
+    uint32_t mag = code & ((1u << (K - 1)) - 1u);
+    float f = __uint_as_float(mag << (23 - y));
+    f = __fmul_rn(f, P.s1_f);
+    if (P.two_mul) f = __fmul_rn(f, P.s2_f);
+    return __float_as_uint(f) | ((code << (32 - K)) & 0x80000000u);
+}
+
+// ------------------------------------------------------------ SWAR pack
+// R[8]: byte-lane registers; byte l of R[i] = bits of element i of container
+// l (4 containers).  Produces the 4 containers of segment (W, LO) as W words.
+template <int W, int LO>
+__device__ __forceinline__ void swar_pack4(const uint32_t (&R)[8], uint32_t (&out)[W]) {
+    if constexpr (W == 1) {
+        uint32_t b = 0;
+        b |= shl_s<0 - LO>(R[0]) & (0x01010101u << 0);
+        b |= shl_s<1 - LO>(R[1]) & (0x01010101u << 1);
+        b |= shl_s<2 - LO>(R[2]) & (0x01010101u << 2);
+        b |= shl_s<3 - LO>(R[3]) & (0x01010101u << 3);
+        b |= shl_s<4 - LO>(R[4]) & (0x01010101u << 4);
+        b |= shl_s<5 - LO>(R[5]) & (0x01010101u << 5);
+        b |= shl_s<6 - LO>(R[6]) & (0x01010101u << 6);
+        b |= shl_s<7 - LO>(R[7]) & (0x01010101u << 7);
+        out[0] = b;
+    } else if constexpr (W == 2) {
+        uint32_t lo = 0, hi = 0;
+        lo |= shl_s<0 - LO>(R[0]) & (0x03030303u << 0);
+        lo |= shl_s<2 - LO>(R[1]) & (0x03030303u << 2);
+        lo |= shl_s<4 - LO>(R[2]) & (0x03030303u << 4);
+        lo |= shl_s<6 - LO>(R[3]) & (0x03030303u << 6);
+        hi |= shl_s<0 - LO>(R[4]) & (0x03030303u << 0);
+        hi |= shl_s<2 - LO>(R[5]) & (0x03030303u << 2);
+        hi |= shl_s<4 - LO>(R[6]) & (0x03030303u << 4);
+        hi |= shl_s<6 - LO>(R[7]) & (0x03030303u << 6);
+        out[0] = prmt(lo, hi, 0x5140);
+        out[1] = prmt(lo, hi, 0x7362);
+    } else {
+        static_assert(W == 4, "");
+        uint32_t N[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            N[j] = (shl_s<-LO>(R[2 * j]) & 0x0F0F0F0Fu) | (shl_s<4 - LO>(R[2 * j + 1]) & 0xF0F0F0F0u);
+        const uint32_t t0 = prmt(N[0], N[1], 0x5140), t1 = prmt(N[2], N[3], 0x5140);
+        const uint32_t t2 = prmt(N[0], N[1], 0x7362), t3 = prmt(N[2], N[3], 0x7362);
+        out[0] = prmt(t0, t1, 0x5410);
+        out[1] = prmt(t0, t1, 0x7632);
+        out[2] = prmt(t2, t3, 0x5410);
+        out[3] = prmt(t2, t3, 0x7632);
+    }
+}
+
+// inverse: OR the segment's bits back into byte-lane registers R[8]
+template <int W, int LO>
+__device__ __forceinline__ void swar_unpack4(const uint32_t (&in)[W], uint32_t (&R)[8]) {
+    if constexpr (W == 1) {
+        const uint32_t b = in[0];
+        R[0] |= shl_s<LO - 0>(b & (0x01010101u << 0));
+        R[1] |= shl_s<LO - 1>(b & (0x01010101u << 1));
+        R[2] |= shl_s<LO - 2>(b & (0x01010101u << 2));
+        R[3] |= shl_s<LO - 3>(b & (0x01010101u << 3));
+        R[4] |= shl_s<LO - 4>(b & (0x01010101u << 4));
+        R[5] |= shl_s<LO - 5>(b & (0x01010101u << 5));
+        R[6] |= shl_s<LO - 6>(b & (0x01010101u << 6));
+        R[7] |= shl_s<LO - 7>(b & (0x01010101u << 7));
+    } else if constexpr (W == 2) {
+        const uint32_t lo = prmt(in[0], in[1], 0x6420), hi = prmt(in[0], in[1], 0x7531);
+        R[0] |= shl_s<LO - 0>(lo & (0x03030303u << 0));
+        R[1] |= shl_s<LO - 2>(lo & (0x03030303u << 2));
+        R[2] |= shl_s<LO - 4>(lo & (0x03030303u << 4));
+        R[3] |= shl_s<LO - 6>(lo & (0x03030303u << 6));
+        R[4] |= shl_s<LO - 0>(hi & (0x03030303u << 0));
+        R[5] |= shl_s<LO - 2>(hi & (0x03030303u << 2));
+        R[6] |= shl_s<LO - 4>(hi & (0x03030303u << 4));
+        R[7] |= shl_s<LO - 6>(hi & (0x03030303u << 6));
+    } else {
+        static_assert(W == 4, "");
+        const uint32_t t0 = prmt(in[0], in[1], 0x5140), t1 = prmt(in[2], in[3], 0x5140);
+        const uint32_t t2 = prmt(in[0], in[1], 0x7362), t3 = prmt(in[2], in[3], 0x7362);
+        const uint32_t N[4] = {prmt(t0, t1, 0x5410), prmt(t0, t1, 0x7632), prmt(t2, t3, 0x5410),
+                               prmt(t2, t3, 0x7632)};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            R[2 * j] |= shl_s<LO>(N[j] & 0x0F0F0F0Fu);
+            R[2 * j + 1] |= shl_s<LO - 4>(N[j] & 0xF0F0F0F0u);
+        }
+    }
+}
+
+}  // namespace exmy
+
+namespace exmy {
+
+__device__ __forceinline__ uint32_t quant_f32_fast(uint32_t u, const FastP &P, uint32_t &flag) {
+    const uint32_t a = u & 0x7FFFFFFFu;
+    uint32_t ecl = u & 0x7F800000u;
+    ecl = max(ecl, P.lo);
+    ecl = min(ecl, P.hi);
+    uint32_t c = ecl + P.k2f;
+    if (P.y0) c += ((ecl >> 23) ^ P.parf) & 1u;
+    const float s = __fadd_rn(__uint_as_float(a), __uint_as_float(c));
+    uint32_t q = __float_as_uint(__fsub_rn(s, __uint_as_float(c)));   // exact
+    q = min(q, P.maxvf);
+    flag |= (a + 0x00800000u) & 0x80000000u;
+    return q | (u & 0x80000000u);
+}
+
+__device__ __forceinline__ uint32_t word_of(const uint4 &r, int t) {
+    return t == 0 ? r.x : t == 1 ? r.y : t == 2 ? r.z : r.w;
+}
+
+// codes of the 16-byte vector r (8 bf16 / 4 fp32 elements) as 16-bit-lane pairs
+// cp[t] = codes (2t, 2t+1); the fast paths accumulate a NaN/Inf flag, the
+// generic path records specials itself (idx0 = element index of element 0,
+// stride = element index step between consecutive vector elements).
+template <int K, bool BF16>
+__device__ __forceinline__ void vec_codes(const uint4 &r, uint32_t (&cp)[BF16 ? 4 : 2], const FastP &P,
+                                          const Fmt &F, uint32_t &flag, int64_t idx0, int64_t *spi, uint32_t *spb,
+                                          unsigned long long *spc, int64_t cap) {
+    constexpr int NP = BF16 ? 4 : 2;
+    if (BF16 && P.enc_simd) {
+#pragma unroll
+        for (int t = 0; t < NP; ++t) cp[t] = enc_pair_bf16<K>(word_of(r, t), P, flag);
+        flag &= 0x80008000u;
+    } else if (P.enc_f32) {
+        uint32_t f = 0;
+#pragma unroll
+        for (int t = 0; t < NP; ++t) {
+            uint32_t lo = enc_f32_fast<K>(vec_elem<BF16>(r, 2 * t), P, f);
+            uint32_t hi = enc_f32_fast<K>(vec_elem<BF16>(r, 2 * t + 1), P, f);
+            cp[t] = lo | (hi << 16);
+        }
+        flag |= f & 0x80000000u;
+    } else {
+#pragma unroll
+        for (int t = 0; t < NP; ++t) {
+            uint32_t lo = enc_elem(vec_elem<BF16>(r, 2 * t), F, idx0 + 2 * t, spi, spb, spc, cap);
+            uint32_t hi = enc_elem(vec_elem<BF16>(r, 2 * t + 1), F, idx0 + 2 * t + 1, spi, spb, spc, cap);
+            cp[t] = lo | (hi << 16);
+        }
+    }
+}
+
+template <int K, bool BF16>
+__device__ __forceinline__ void vec_codes_generic(const uint4 &r, uint32_t (&cp)[BF16 ? 4 : 2], const Fmt &F,
+                                                  int64_t idx0, int64_t *spi, uint32_t *spb,
+                                                  unsigned long long *spc, int64_t cap) {
+    constexpr int NP = BF16 ? 4 : 2;
+#pragma unroll
+    for (int t = 0; t < NP; ++t) {
+        uint32_t lo = enc_elem(vec_elem<BF16>(r, 2 * t), F, idx0 + 2 * t, spi, spb, spc, cap);
+        uint32_t hi = enc_elem(vec_elem<BF16>(r, 2 * t + 1), F, idx0 + 2 * t + 1, spi, spb, spc, cap);
+        cp[t] = lo | (hi << 16);
+    }
+}
+
+// ---------------------------------------------------------- encode ROWS
+template <int K, int NH, int S>
+__device__ __forceinline__ void rows_fast_store(const uint32_t (&RL)[NH][8], const uint32_t (&RH)[NH][8],
+                                                uint8_t *packed, const SegOffsets &so, int64_t g, int64_t C,
+                                                int64_t c0) {
+    if constexpr (S < seg_count(K)) {
+        constexpr int W = seg_width(K, S), LO = seg_lo(K, S);
+        uint8_t *seg = packed + so.off[S];
+        if constexpr (W == 8) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                uint32_t w[NH];
+#pragma unroll
+                for (int h = 0; h < NH; ++h) w[h] = (K == 9) ? RH[h][i] : RL[h][i];
+                store_words<NH>(seg + (8 * g + i) * C + c0, w);
+            }
+        } else {
+            uint32_t w[NH * W];
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+                uint32_t out[W];
+                swar_pack4<W, LO>(RL[h], out);
+#pragma unroll
+                for (int q = 0; q < W; ++q) w[h * W + q] = out[q];
+            }
+            store_words<NH * W>(seg + (g * C + c0) * W, w);
+        }
+        rows_fast_store<K, NH, S + 1>(RL, RH, packed, so, g, C, c0);
+    }
+}
+
+template <int K, bool BF16>
+__global__ void __launch_bounds__(256) k_enc_rows_fast(const uint8_t *__restrict__ in, int64_t R, int64_t C, int x,
+                                                       int y, const uint8_t *__restrict__ meta,
+                                                       uint8_t *__restrict__ packed, SegOffsets so, int64_t *spi,
+                                                       uint32_t *spb, unsigned long long *spc, int64_t cap,
+                                                       int force_generic) {
+    using EL = Elem<BF16>;
+    constexpr int V = EL::V, NP = V / 2, NH = V / 4;
+    const Fmt F = load_fmt(x, y, meta);
+    const FastP P = make_fast(F, BF16, force_generic);
+    const int64_t CV = C / V, G = R / 8;
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= CV) return;
+    const int64_t c0 = j * V;
+    for (int64_t g = blockIdx.y; g < G; g += gridDim.y) {
+        uint4 r[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r[i] = ldg_nc_v4(in + ((8 * g + i) * C + c0) * EL::ES);
+        uint32_t cp[8][NP];
+        uint32_t flag = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) vec_codes<K, BF16>(r[i], cp[i], P, F, flag, (8 * g + i) * C + c0, spi, spb, spc, cap);
+        if (flag) {
+#pragma unroll 1
+            for (int i = 0; i < 8; ++i) vec_codes_generic<K, BF16>(r[i], cp[i], F, (8 * g + i) * C + c0, spi, spb, spc, cap);
+        }
+        uint32_t RL[NH][8], RH[NH][8];
+#pragma unroll
+        for (int h = 0; h < NH; ++h)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                RL[h][i] = prmt(cp[i][2 * h], cp[i][2 * h + 1], 0x6420);
+                RH[h][i] = (K == 9) ? prmt(cp[i][2 * h] >> 1, cp[i][2 * h + 1] >> 1, 0x6420) : 0u;
+            }
+        rows_fast_store<K, NH, 0>(RL, RH, packed, so, g, C, c0);
+    }
+}
+
+// ---------------------------------------------------------- encode COLS
+template <int K, int S>
+__device__ __forceinline__ void cols_fast_store(const uint32_t (&RL)[8], const uint32_t (&RH)[8],
+                                                const uint32_t (&cp)[4][4], uint8_t *packed, const SegOffsets &so,
+                                                int64_t q0, int64_t NG) {
+    if constexpr (S < seg_count(K)) {
+        constexpr int W = seg_width(K, S), LO = seg_lo(K, S);
+        uint8_t *seg = packed + so.off[S];
+        if constexpr (W == 8) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t q = q0 + 32 * u;
+                if (q < NG) {
+                    constexpr int SH = (K == 9) ? 1 : 0;
+                    const uint32_t w0 = prmt(cp[u][0] >> SH, cp[u][1] >> SH, 0x6420);
+                    const uint32_t w1 = prmt(cp[u][2] >> SH, cp[u][3] >> SH, 0x6420);
+                    stg_v2(seg + 8 * q, w0, w1);
+                }
+            }
+        } else {
+            uint32_t out[W];
+            swar_pack4<W, LO>(RL, out);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t q = q0 + 32 * u;
+                if (q < NG) {
+                    if constexpr (W == 4) *(uint32_t *)(seg + 4 * q) = out[u];
+                    else if constexpr (W == 2) *(uint16_t *)(seg + 2 * q) = (uint16_t)(out[u >> 1] >> (16 * (u & 1)));
+                    else seg[q] = (uint8_t)(out[0] >> (8 * u));
+                }
+            }
+        }
+        cols_fast_store<K, S + 1>(RL, RH, cp, packed, so, q0, NG);
+    }
+}
+
+template <int K, bool BF16>
+__global__ void __launch_bounds__(256) k_enc_cols_fast(const uint8_t *__restrict__ in, int64_t n, int x, int y,
+                                                       const uint8_t *__restrict__ meta, uint8_t *__restrict__ packed,
+                                                       SegOffsets so, int64_t *spi, uint32_t *spb,
+                                                       unsigned long long *spc, int64_t cap, int force_generic) {
+    using EL = Elem<BF16>;
+    constexpr int NV = BF16 ? 1 : 2;   // 16-byte vectors per group of 8
+    constexpr int NP = EL::V / 2;      // pairs per vector
+    const Fmt F = load_fmt(x, y, meta);
+    const FastP P = make_fast(F, BF16, force_generic);
+    const int64_t NG = n / 8;
+    const int lane = threadIdx.x & 31;
+    const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    for (int64_t base = gw * 128; base < NG; base += warps_total * 128) {
+        uint4 r[4][NV];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t q = base + 32 * u + lane;
+#pragma unroll
+            for (int t = 0; t < NV; ++t)
+                r[u][t] = q < NG ? ldg_nc_v4(in + q * 8 * EL::ES + 16 * t) : make_uint4(0, 0, 0, 0);
+        }
+        uint32_t cp[4][4];   // group u, pair t (elements 2t, 2t+1)
+        uint32_t flag = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t q = base + 32 * u + lane;
+#pragma unroll
+            for (int t = 0; t < NV; ++t) {
+                uint32_t c2[NP];
+                vec_codes<K, BF16>(r[u][t], c2, P, F, flag, 8 * q + t * EL::V, spi, spb, spc, q < NG ? cap : 0);
+#pragma unroll
+                for (int p = 0; p < NP; ++p) cp[u][t * NP + p] = c2[p];
+            }
+        }
+        if (flag) {
+#pragma unroll 1
+            for (int u = 0; u < 4; ++u) {
+                const int64_t q = base + 32 * u + lane;
+                if (q >= NG) continue;
+                for (int t = 0; t < NV; ++t) {
+                    uint32_t c2[NP];
+                    vec_codes_generic<K, BF16>(r[u][t], c2, F, 8 * q + t * EL::V, spi, spb, spc, cap);
+                    for (int p = 0; p < NP; ++p) cp[u][t * NP + p] = c2[p];
+                }
+            }
+        }
+        uint32_t RL[8], RH[8];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const uint32_t y01 = prmt(cp[0][t], cp[1][t], 0x6420), y23 = prmt(cp[2][t], cp[3][t], 0x6420);
+            RL[2 * t] = prmt(y01, y23, 0x6420);
+            RL[2 * t + 1] = prmt(y01, y23, 0x7531);
+            if (K == 9) {
+                const uint32_t h01 = prmt(cp[0][t] >> 1, cp[1][t] >> 1, 0x6420);
+                const uint32_t h23 = prmt(cp[2][t] >> 1, cp[3][t] >> 1, 0x6420);
+                RH[2 * t] = prmt(h01, h23, 0x6420);
+                RH[2 * t + 1] = prmt(h01, h23, 0x7531);
+            }
+        }
+        cols_fast_store<K, 0>(RL, RH, cp, packed, so, base + lane, NG);
+    }
+}
+
+}  // namespace exmy
+
+namespace exmy {
+
+// ---------------------------------------------------------- decode helpers
+// pair of codes (16-bit lanes) from byte-lane registers
+template <int K>
+__device__ __forceinline__ uint32_t pair_from_lanes(uint32_t rl, uint32_t rh, uint32_t sel) {
+    uint32_t p = prmt(rl, 0u, sel);
+    if (K == 9) p |= prmt(rh, 0u, sel) << 1;
+    return p;
+}
+
+// pair of codes -> pair of output words (bf16: one word; fp32: two words)
+template <int K>
+__device__ __forceinline__ uint32_t dec_pair_to_bf16(uint32_t cp, const FastP &P, const Fmt &F) {
+    if (P.dec_fast_bf) return dec_pair_bf16<K>(cp, P, F.y);
+    return dec_code_generic<8>(cp & 0xFFFFu, F) | (dec_code_generic<8>(cp >> 16, F) << 16);
+}
+template <int K>
+__device__ __forceinline__ uint32_t dec_to_f32(uint32_t code, const FastP &P, const Fmt &F) {
+    if (P.dec_fast) return dec_f32_fast<K>(code, P, F.y);
+    return dec_code_generic<24>(code, F);
+}
+
+// ---------------------------------------------------------- decode ROWS
+template <int K, int NH, int S>
+__device__ __forceinline__ void rows_fast_load(uint32_t (&RL)[NH][8], uint32_t (&RH)[NH][8], const uint8_t *packed,
+                                               const SegOffsets &so, int64_t g, int64_t C, int64_t c0) {
+    if constexpr (S < seg_count(K)) {
+        constexpr int W = seg_width(K, S), LO = seg_lo(K, S);
+        const uint8_t *seg = packed + so.off[S];
+        if constexpr (W == 8) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                uint32_t w[NH];
+                load_words<NH>(seg + (8 * g + i) * C + c0, w);
+#pragma unroll
+                for (int h = 0; h < NH; ++h) {
+                    if (K == 9) RH[h][i] = w[h];
+                    else RL[h][i] = w[h];
+                }
+            }
+        } else {
+            uint32_t w[NH * W];
+            load_words<NH * W>(seg + (g * C + c0) * W, w);
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+                uint32_t in[W];
+#pragma unroll
+                for (int q = 0; q < W; ++q) in[q] = w[h * W + q];
+                swar_unpack4<W, LO>(in, RL[h]);
+            }
+        }
+        rows_fast_load<K, NH, S + 1>(RL, RH, packed, so, g, C, c0);
+    }
+}
+
+template <int K, bool OBF16>
+__global__ void __launch_bounds__(256) k_dec_rows_fast(const uint8_t *__restrict__ packed, int64_t R, int64_t C,
+                                                       int x, int y, const uint8_t *__restrict__ meta, SegOffsets so,
+                                                       uint8_t *__restrict__ out, int force_generic) {
+    using EL = Elem<OBF16>;
+    constexpr int V = EL::V, NH = V / 4;
+    const Fmt F = load_fmt(x, y, meta);
+    const FastP P = make_fast(F, false, force_generic);
+    const int64_t CV = C / V, G = R / 8;
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= CV) return;
+    const int64_t c0 = j * V;
+    for (int64_t g = blockIdx.y; g < G; g += gridDim.y) {
+        uint32_t RL[NH][8], RH[NH][8];
+#pragma unroll
+        for (int h = 0; h < NH; ++h)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) { RL[h][i] = 0; RH[h][i] = 0; }
+        rows_fast_load<K, NH, 0>(RL, RH, packed, so, g, C, c0);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            uint32_t o[4];
+            if (OBF16) {
+#pragma unroll
+                for (int h = 0; h < NH; ++h) {
+                    o[2 * h] = dec_pair_to_bf16<K>(pair_from_lanes<K>(RL[h][i], RH[h][i], 0x4140), P, F);
+                    o[2 * h + 1] = dec_pair_to_bf16<K>(pair_from_lanes<K>(RL[h][i], RH[h][i], 0x4342), P, F);
+                }
+            } else {
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    uint32_t code = (RL[0][i] >> (8 * v)) & 0xFFu;
+                    if (K == 9) code |= ((RH[0][i] >> (8 * v)) & 0xFFu) << 1;
+                    o[v] = dec_to_f32<K>(code, P, F);
+                }
+            }
+            stg_v4(out + ((8 * g + i) * C + c0) * EL::ES, make_uint4(o[0], o[1], o[2], o[3]));
+        }
+    }
+}
+
+// ---------------------------------------------------------- decode COLS
+template <int K, int S>
+__device__ __forceinline__ void cols_fast_load(uint32_t (&RL)[8], uint32_t (&RH)[8], const uint8_t *packed,
+                                               const SegOffsets &so, int64_t q0, int64_t NG) {
+    if constexpr (S < seg_count(K)) {
+        constexpr int W = seg_width(K, S), LO = seg_lo(K, S);
+        const uint8_t *seg = packed + so.off[S];
+        if constexpr (W == 8) {
+            uint32_t a[4], b[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t q = q0 + 32 * u;
+                uint2 t = q < NG ? __ldg((const uint2 *)(seg + 8 * q)) : make_uint2(0, 0);
+                a[u] = t.x;
+                b[u] = t.y;
+            }
+            // 4x4 byte transposes: group-major words -> element-major byte lanes
+            uint32_t *dst = (K == 9) ? RH : RL;
+            const uint32_t a0 = prmt(a[0], a[1], 0x5140), a1 = prmt(a[2], a[3], 0x5140);
+            const uint32_t a2 = prmt(a[0], a[1], 0x7362), a3 = prmt(a[2], a[3], 0x7362);
+            dst[0] = prmt(a0, a1, 0x5410); dst[1] = prmt(a0, a1, 0x7632);
+            dst[2] = prmt(a2, a3, 0x5410); dst[3] = prmt(a2, a3, 0x7632);
+            const uint32_t b0 = prmt(b[0], b[1], 0x5140), b1 = prmt(b[2], b[3], 0x5140);
+            const uint32_t b2 = prmt(b[0], b[1], 0x7362), b3 = prmt(b[2], b[3], 0x7362);
+            dst[4] = prmt(b0, b1, 0x5410); dst[5] = prmt(b0, b1, 0x7632);
+            dst[6] = prmt(b2, b3, 0x5410); dst[7] = prmt(b2, b3, 0x7632);
+        } else {
+            uint32_t in[W];
+#pragma unroll
+            for (int q = 0; q < W; ++q) in[q] = 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t q = q0 + 32 * u;
+                if (q < NG) {
+                    if constexpr (W == 4) in[u] = __ldg((const unsigned int *)(seg + 4 * q));
+                    else if constexpr (W == 2)
+                        in[u >> 1] |= (uint32_t)__ldg((const unsigned short *)(seg + 2 * q)) << (16 * (u & 1));
+                    else in[0] |= (uint32_t)__ldg((const unsigned char *)(seg + q)) << (8 * u);
+                }
+            }
+            swar_unpack4<W, LO>(in, RL);
+        }
+        cols_fast_load<K, S + 1>(RL, RH, packed, so, q0, NG);
+    }
+}
+
+template <int K, bool OBF16>
+__global__ void __launch_bounds__(256) k_dec_cols_fast(const uint8_t *__restrict__ packed, int64_t n, int x, int y,
+                                                       const uint8_t *__restrict__ meta, SegOffsets so,
+                                                       uint8_t *__restrict__ out, int force_generic) {
+    const Fmt F = load_fmt(x, y, meta);
+    const FastP P = make_fast(F, false, force_generic);
+    const int64_t NG = n / 8;
+    const int lane = threadIdx.x & 31;
+    const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    for (int64_t base = gw * 128; base < NG; base += warps_total * 128) {
+        uint32_t RL[8], RH[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { RL[i] = 0; RH[i] = 0; }
+        cols_fast_load<K, 0>(RL, RH, packed, so, base + lane, NG);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t q = base + 32 * u + lane;
+            if (q >= NG) continue;
+            if (OBF16) {
+                uint32_t o[4];
+                const uint32_t sel = (uint32_t)u | ((uint32_t)(4 + u) << 4);   // bytes 0, 1 <- lanes, masked
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    uint32_t cp = prmt(RL[2 * t], RL[2 * t + 1], sel);
+                    cp = (cp & 0xFFu) | ((cp & 0xFF00u) << 8);
+                    if (K == 9) {
+                        uint32_t ch = prmt(RH[2 * t], RH[2 * t + 1], sel);
+                        cp |= ((ch & 0xFFu) | ((ch & 0xFF00u) << 8)) << 1;
+                    }
+                    o[t] = dec_pair_to_bf16<K>(cp, P, F);
+                }
+                stg_v4(out + q * 16, make_uint4(o[0], o[1], o[2], o[3]));
+            } else {
+                uint32_t o[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    uint32_t code = (RL[i] >> (8 * u)) & 0xFFu;
+                    if (K == 9) code |= ((RH[i] >> (8 * u)) & 0xFFu) << 1;
+                    o[i] = dec_to_f32<K>(code, P, F);
+                }
+                stg_v4(out + q * 32, make_uint4(o[0], o[1], o[2], o[3]));
+                stg_v4(out + q * 32 + 16, make_uint4(o[4], o[5], o[6], o[7]));
+            }
+        }
+    }
+}
+
+// -------------------------------------------------------------- quantize
+template <bool BF16>
+__global__ void __launch_bounds__(256) k_quant_fast(const uint8_t *__restrict__ in, uint8_t *__restrict__ out,
+                                                    int64_t n, int x, int y, const uint8_t *__restrict__ meta,
+                                                    int force_generic) {
+    using EL = Elem<BF16>;
+    const Fmt F = load_fmt(x, y, meta);
+    const FastP P = make_fast(F, BF16, force_generic);
+    const DecPath DP = make_dec_path(F, force_generic);
+    const int64_t nvec = n / EL::V;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    constexpr int U = 4;
+    const bool fast = BF16 ? P.enc_simd : P.enc_f32;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; base < nvec; base += stride * U) {
+        uint4 r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t vi = base + u * stride;
+            if (vi < nvec) r[u] = ldg_nc_v4(in + vi * 16);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t vi = base + u * stride;
+            if (vi >= nvec) continue;
+            uint32_t o[4];
+            uint32_t flag = 0;
+            if (fast) {
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    o[t] = BF16 ? quant_pair_bf16(word_of(r[u], t), P, flag) : quant_f32_fast(word_of(r[u], t), P, flag);
+                flag &= 0x80008000u;
+            }
+            if (!fast || flag) {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const uint32_t w = word_of(r[u], t);
+                    if (BF16) {
+                        const uint32_t lo = quantize_elem<true>(w << 16, F, DP);
+                        const uint32_t hi = quantize_elem<true>(w & 0xFFFF0000u, F, DP);
+                        o[t] = (lo & 0xFFFFu) | (hi << 16);
+                    } else {
+                        o[t] = quantize_elem<false>(w, F, DP);
+                    }
+                }
+            }
+            stg_v4(out + vi * 16, make_uint4(o[0], o[1], o[2], o[3]));
+        }
+    }
+    if (blockIdx.x == 0) {
+        for (int64_t i = nvec * EL::V + threadIdx.x; i < n; i += blockDim.x) {
+            if (BF16) {
+                const uint32_t u = (uint32_t)((const uint16_t *)in)[i] << 16;
+                ((uint16_t *)out)[i] = (uint16_t)quantize_elem<true>(u, F, DP);
+            } else {
+                ((uint32_t *)out)[i] = quantize_elem<false>(((const uint32_t *)in)[i], F, DP);
+            }
+        }
+    }
+}
+
+}  // namespace exmy

@@ -107,13 +107,23 @@ __global__ void __launch_bounds__(HIST_THREADS) k_hist(const uint8_t *__restrict
     // each lane may count at most 65535 elements between flushes
     constexpr int64_t EPOCH_VECS = (BF16 ? 8000 : 16000) / 4;   // per lane, in units of 4 vectors
     int64_t epoch = 0;
-    // warp-uniform loop: iteration t covers vectors (gw + t*warps_total)*128 + 32*u + lane
-    for (int64_t base = gw * 128; base < nvec; base += warps_total * 128) {
+    // warp-uniform loop: iteration t covers vectors (gw + t*warps_total)*128 + 32*u + lane.
+    // Loads are double-buffered: the next iteration's 4 vectors are in flight
+    // while this iteration's 32 (bf16) elements update the counters.
+    const int64_t step = warps_total * 128;
+    uint4 nxt[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int64_t vi = gw * 128 + 32 * u + lane;
+        nxt[u] = vi < nvec ? ldg_nc_v4(in + vi * 16) : make_uint4(0, 0, 0, 0);
+    }
+    for (int64_t base = gw * 128; base < nvec; base += step) {
         uint4 r[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            int64_t vi = base + 32 * u + lane;
-            r[u] = vi < nvec ? ldg_nc_v4(in + vi * 16) : make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+            r[u] = nxt[u];
+            const int64_t vi = base + step + 32 * u + lane;
+            nxt[u] = vi < nvec ? ldg_nc_v4(in + vi * 16) : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {

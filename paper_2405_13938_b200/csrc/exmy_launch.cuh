@@ -6,7 +6,7 @@
 #include <cuda_runtime.h>
 
 #include "exmy.h"
-#include "exmy_kernels.cuh"
+#include "exmy_fast.cuh"
 
 namespace exmy {
 

@@ -19,7 +19,7 @@ exmy_status launch_decode_k(const uint8_t *packed, int64_t R, int64_t C, int axi
         if (vec) {
             const int threads = 256;
             static int occ = 0;
-            if (!occ) occ = occupancy(k_decode_rows<K, OBF16>, threads, 0);
+            if (!occ) occ = occupancy(k_dec_rows_fast<K, OBF16>, threads, 0);
             const int64_t CV = C / V, G = R / 8;
             int64_t gx = cdiv(CV, threads);
             int64_t target = (int64_t)num_sms() * occ;
@@ -28,7 +28,7 @@ exmy_status launch_decode_k(const uint8_t *packed, int64_t R, int64_t C, int axi
             if (gy > G) gy = G;
             if (gy > 65535) gy = 65535;
             if (gx > INT_MAX) return EXMY_E_SHAPE;
-            k_decode_rows<K, OBF16><<<dim3((unsigned)gx, (unsigned)gy), threads, 0, st>>>(packed, R, C, x, y, meta,
+            k_dec_rows_fast<K, OBF16><<<dim3((unsigned)gx, (unsigned)gy), threads, 0, st>>>(packed, R, C, x, y, meta,
                                                                                          p.so, out, g_force_generic);
             return launch_status();
         }
@@ -37,12 +37,12 @@ exmy_status launch_decode_k(const uint8_t *packed, int64_t R, int64_t C, int axi
         if (vec) {
             const int threads = 256;
             static int occ = 0;
-            if (!occ) occ = occupancy(k_decode_cols<K, OBF16>, threads, 0);
+            if (!occ) occ = occupancy(k_dec_cols_fast<K, OBF16>, threads, 0);
             int64_t tiles = cdiv(n / 8, 128);
             int64_t blocks = cdiv(tiles, threads / 32);
             int64_t maxb = (int64_t)num_sms() * occ;
             if (blocks > maxb) blocks = maxb;
-            k_decode_cols<K, OBF16><<<(unsigned)blocks, threads, 0, st>>>(packed, n, x, y, meta, p.so, out,
+            k_dec_cols_fast<K, OBF16><<<(unsigned)blocks, threads, 0, st>>>(packed, n, x, y, meta, p.so, out,
                                                                           g_force_generic);
             return launch_status();
         }

@@ -20,7 +20,7 @@ exmy_status launch_encode_k(const uint8_t *in, int64_t R, int64_t C, int axis, i
         if (vec) {
             const int threads = 256;
             static int occ = 0;
-            if (!occ) occ = occupancy(k_encode_rows<K, BF16>, threads, 0);
+            if (!occ) occ = occupancy(k_enc_rows_fast<K, BF16>, threads, 0);
             const int64_t CV = C / V, G = R / 8;
             int64_t gx = cdiv(CV, threads);
             int64_t target = (int64_t)num_sms() * occ;
@@ -29,8 +29,8 @@ exmy_status launch_encode_k(const uint8_t *in, int64_t R, int64_t C, int axis, i
             if (gy > G) gy = G;
             if (gy > 65535) gy = 65535;
             if (gx > INT_MAX) return EXMY_E_SHAPE;
-            k_encode_rows<K, BF16><<<dim3((unsigned)gx, (unsigned)gy), threads, 0, st>>>(
-                in, R, C, x, y, meta, packed, p.so, spi, spb, spc, cap);
+            k_enc_rows_fast<K, BF16><<<dim3((unsigned)gx, (unsigned)gy), threads, 0, st>>>(
+                in, R, C, x, y, meta, packed, p.so, spi, spb, spc, cap, g_force_generic);
             return launch_status();
         }
     } else {
@@ -38,13 +38,13 @@ exmy_status launch_encode_k(const uint8_t *in, int64_t R, int64_t C, int axis, i
         if (vec) {
             const int threads = 256;
             static int occ = 0;
-            if (!occ) occ = occupancy(k_encode_cols<K, BF16>, threads, 0);
+            if (!occ) occ = occupancy(k_enc_cols_fast<K, BF16>, threads, 0);
             int64_t tiles = cdiv(n / 8, 128);
             int64_t blocks = cdiv(tiles, threads / 32);
             int64_t maxb = (int64_t)num_sms() * occ;
             if (blocks > maxb) blocks = maxb;
-            k_encode_cols<K, BF16><<<(unsigned)blocks, threads, 0, st>>>(in, n, x, y, meta, packed, p.so, spi, spb,
-                                                                         spc, cap);
+            k_enc_cols_fast<K, BF16><<<(unsigned)blocks, threads, 0, st>>>(in, n, x, y, meta, packed, p.so, spi,
+                                                                           spb, spc, cap, g_force_generic);
             return launch_status();
         }
     }

@@ -1,0 +1,79 @@
+"""Per-op timing (CUDA events, median of reps) for kernel tuning.
+python tools/bench_ops.py [--dtype bf16|f32] [--fmts e3m3,e6m0] [--axis rows|cols] [--hist-modes 0,1]"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_2405_13938_b200 as exmy  # noqa: E402
+import workloads as W  # noqa: E402
+
+
+def timeit(fn, reps=20, warm=3):
+    for _ in range(warm):
+        fn()
+    ts = []
+    for _ in range(reps):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return statistics.median(ts)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--dtype", default="bf16")
+    ap.add_argument("--rows", type=int, default=16384)
+    ap.add_argument("--cols", type=int, default=16384)
+    ap.add_argument("--fmts", default="e0m6,e1m5,e2m4,e3m3,e4m2,e5m1,e6m0")
+    ap.add_argument("--axis", default="rows")
+    ap.add_argument("--hist-modes", default="0,1")
+    a = ap.parse_args()
+    dev = torch.device("cuda")
+    R, C = a.rows, a.cols
+    n = R * C
+    if a.dtype == "bf16":
+        t = W.bf16_weights((R, C), seed=1, device=dev)
+        es = 2
+    else:
+        t = W.f32_gradients(n, device=dev).view(R, C)
+        es = 4
+    peak = 6555.5
+    res = {}
+    h = torch.zeros(256, dtype=torch.int64, device=dev)
+    for m in [int(v) for v in a.hist_modes.split(",")]:
+        exmy.hist_mode(m)
+        ms = timeit(lambda: exmy.histogram(t, out=h))
+        res[f"hist_mode{m}"] = {"ms": ms, "gbs": n * es / ms / 1e6, "frac": n * es / ms / 1e6 / peak}
+    exmy.hist_mode(0)
+    meta = exmy.max_exponent(t)
+    q = torch.empty_like(t)
+    d = torch.empty_like(t)
+    for f in a.fmts.split(","):
+        x, y = exmy.parse_format(f)
+        k = 1 + x + y
+        ms = timeit(lambda: exmy.quantize(t, f, meta, out=q))
+        res[f"quantize_{f}"] = {"ms": ms, "gbs": 2 * n * es / ms / 1e6, "frac": 2 * n * es / ms / 1e6 / peak}
+        buf = torch.empty(n * k // 8, dtype=torch.uint8, device=dev)
+        ms = timeit(lambda: exmy.encode(t, f, meta, axis=a.axis, out=buf))
+        res[f"encode_{f}"] = {"ms": ms, "gbs": n * (es + k / 8) / ms / 1e6, "frac": n * (es + k / 8) / ms / 1e6 / peak}
+        p = exmy.encode(t, f, meta, axis=a.axis, out=buf)
+        ms = timeit(lambda: exmy.decode(p, out=d))
+        res[f"decode_{f}"] = {"ms": ms, "gbs": n * (es + k / 8) / ms / 1e6, "frac": n * (es + k / 8) / ms / 1e6 / peak}
+    for k_, v in res.items():
+        print(f"{k_:16s} {v['ms']*1e3:9.1f} us {v['gbs']:8.1f} GB/s  {v['frac']*100:5.1f}%")
+    print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()
