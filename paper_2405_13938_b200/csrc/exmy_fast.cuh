@@ -139,38 +139,46 @@ __device__ __forceinline__ FastP make_fast(const Fmt &F, bool bf16_in, int force
 }
 
 // ------------------------------------------------------- code computation
+// Encode modes (chosen on the host from (dtype, y); e_max is checked on the
+// device): bf16 SIMD pairs for y in 1..6 / y = 0, per-element fp32 FADD for
+// fp32 inputs and bf16 with y >= 7.
+enum EncMode { ENC_SIMD = 0, ENC_SIMD_Y0 = 1, ENC_F32 = 2, ENC_F32_Y0 = 3 };
+
 // two bf16 elements (one 32-bit word) -> two k-bit codes in 16-bit lanes;
-// flag accumulates lanes holding NaN/Inf (bit 15 / 31 set)
-template <int K>
-__device__ __forceinline__ uint32_t enc_pair_bf16(uint32_t w, const FastP &P, uint32_t &flag) {
+// amax accumulates the largest magnitude seen (NaN/Inf test at the end)
+template <int K, bool Y0>
+__device__ __forceinline__ uint32_t enc_pair_bf16(uint32_t w, const FastP &P, uint32_t &amax) {
     const uint32_t a2 = w & 0x7FFF7FFFu;
     uint32_t ecl = w & 0x7F807F80u;
     ecl = vmax_u16x2(ecl, P.lo2);
     ecl = vmin_u16x2(ecl, P.hi2);
     uint32_t c = ecl + P.k2;
-    if (P.y0) c += ((ecl >> 7) ^ P.par2) & 0x00010001u;   // even code, not even count
+    if (Y0) c += ((ecl >> 7) ^ P.par2) & 0x00010001u;   // even code, not even count
     const uint32_t s = hadd2_bf16(a2, c);
     uint32_t code = s - c + (ecl >> P.sh_b) - P.k3;
     code = vmin_u16x2(code, P.m2);
     code |= (w >> (16 - K)) & ((1u << (K - 1)) * 0x00010001u);
-    flag |= a2 + 0x00800080u;
+    amax = vmax_u16x2(amax, a2);
     return code;
 }
+__device__ __forceinline__ bool amax_special_bf16(uint32_t amax) {
+    return ((amax + 0x00800080u) & 0x80008000u) != 0u;
+}
 
-// one fp32 pattern -> k-bit code; flag accumulates NaN/Inf
-template <int K>
-__device__ __forceinline__ uint32_t enc_f32_fast(uint32_t u, const FastP &P, uint32_t &flag) {
+// one fp32 pattern -> k-bit code
+template <int K, bool Y0>
+__device__ __forceinline__ uint32_t enc_f32_fast(uint32_t u, const FastP &P, uint32_t &amax) {
     const uint32_t a = u & 0x7FFFFFFFu;
     uint32_t ecl = u & 0x7F800000u;
     ecl = max(ecl, P.lo);
     ecl = min(ecl, P.hi);
     uint32_t c = ecl + P.k2f;
-    if (P.y0) c += ((ecl >> 23) ^ P.parf) & 1u;
+    if (Y0) c += ((ecl >> 23) ^ P.parf) & 1u;
     const uint32_t s = __float_as_uint(__fadd_rn(__uint_as_float(a), __uint_as_float(c)));
     uint32_t code = s - c + (ecl >> P.sh_f) - P.k3f;
     code = min(code, (1u << (K - 1)) - 1u);
     code |= (u >> (32 - K)) & (1u << (K - 1));
-    flag |= a + 0x00800000u;
+    amax = max(amax, a);
     return code;
 }
 
@@ -311,48 +319,86 @@ __device__ __forceinline__ uint32_t word_of(const uint4 &r, int t) {
     return t == 0 ? r.x : t == 1 ? r.y : t == 2 ? r.z : r.w;
 }
 
-// codes of the 16-byte vector r (8 bf16 / 4 fp32 elements) as 16-bit-lane pairs
-// cp[t] = codes (2t, 2t+1); the fast paths accumulate a NaN/Inf flag, the
-// generic path records specials itself (idx0 = element index of element 0,
-// stride = element index step between consecutive vector elements).
-template <int K, bool BF16>
-__device__ __forceinline__ void vec_codes(const uint4 &r, uint32_t (&cp)[BF16 ? 4 : 2], const FastP &P,
-                                          const Fmt &F, uint32_t &flag, int64_t idx0, int64_t *spi, uint32_t *spb,
-                                          unsigned long long *spc, int64_t cap) {
-    constexpr int NP = BF16 ? 4 : 2;
-    if (BF16 && P.enc_simd) {
+// codes of NW input words (bf16: 2 elements per word, fp32: 1) as 16-bit-lane
+// pairs cp[t] = codes (2t, 2t+1).  The fast paths accumulate a NaN/Inf flag;
+// the generic path records specials itself (idx0 = index of element 0).
+template <bool BF16, int NW>
+__device__ __forceinline__ uint32_t wordvec_elem(const uint32_t (&w)[NW], int v) {
+    if (BF16) return (v & 1) ? (w[v >> 1] & 0xFFFF0000u) : (w[v >> 1] << 16);
+    return w[v];
+}
+
+template <int K, bool BF16, int MODE, int NW>
+__device__ __forceinline__ void vec_codes(const uint32_t (&w)[NW], uint32_t (&cp)[BF16 ? NW : NW / 2],
+                                          const FastP &P, uint32_t &amax) {
+    constexpr int NP = BF16 ? NW : NW / 2;
+    if constexpr (MODE == ENC_SIMD || MODE == ENC_SIMD_Y0) {
+        static_assert(BF16, "SIMD encode needs bf16 input");
 #pragma unroll
-        for (int t = 0; t < NP; ++t) cp[t] = enc_pair_bf16<K>(word_of(r, t), P, flag);
-        flag &= 0x80008000u;
-    } else if (P.enc_f32) {
-        uint32_t f = 0;
-#pragma unroll
-        for (int t = 0; t < NP; ++t) {
-            uint32_t lo = enc_f32_fast<K>(vec_elem<BF16>(r, 2 * t), P, f);
-            uint32_t hi = enc_f32_fast<K>(vec_elem<BF16>(r, 2 * t + 1), P, f);
-            cp[t] = lo | (hi << 16);
-        }
-        flag |= f & 0x80000000u;
+        for (int t = 0; t < NP; ++t) cp[t] = enc_pair_bf16<K, MODE == ENC_SIMD_Y0>(w[t], P, amax);
     } else {
 #pragma unroll
         for (int t = 0; t < NP; ++t) {
-            uint32_t lo = enc_elem(vec_elem<BF16>(r, 2 * t), F, idx0 + 2 * t, spi, spb, spc, cap);
-            uint32_t hi = enc_elem(vec_elem<BF16>(r, 2 * t + 1), F, idx0 + 2 * t + 1, spi, spb, spc, cap);
+            uint32_t lo = enc_f32_fast<K, MODE == ENC_F32_Y0>(wordvec_elem<BF16, NW>(w, 2 * t), P, amax);
+            uint32_t hi = enc_f32_fast<K, MODE == ENC_F32_Y0>(wordvec_elem<BF16, NW>(w, 2 * t + 1), P, amax);
             cp[t] = lo | (hi << 16);
         }
     }
 }
 
-template <int K, bool BF16>
-__device__ __forceinline__ void vec_codes_generic(const uint4 &r, uint32_t (&cp)[BF16 ? 4 : 2], const Fmt &F,
-                                                  int64_t idx0, int64_t *spi, uint32_t *spb,
-                                                  unsigned long long *spc, int64_t cap) {
-    constexpr int NP = BF16 ? 4 : 2;
+template <bool BF16, int MODE>
+__device__ __forceinline__ bool amax_special(uint32_t amax) {
+    if constexpr (MODE == ENC_SIMD || MODE == ENC_SIMD_Y0) return amax_special_bf16(amax);
+    else return amax >= 0x7F800000u;
+}
+
+template <bool BF16, int MODE>
+__device__ __forceinline__ bool enc_fast_ok(const Fmt &F, int force_generic) {
+    if (force_generic || F.o < 0) return false;
+    return (MODE == ENC_SIMD || MODE == ENC_SIMD_Y0) ? (F.e_max <= 246 + F.y) : (F.e_max <= 230 + F.y);
+}
+
+// 4 consecutive elements of a row: bf16 -> 2 words (8 B), fp32 -> 4 words (16 B)
+template <bool BF16>
+__device__ __forceinline__ void load4(const uint8_t *p, uint32_t (&w)[BF16 ? 2 : 4]) {
+    if constexpr (BF16) {
+        uint2 t;
+        asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(t.x), "=r"(t.y) : "l"(p));
+        w[0] = t.x; w[1] = t.y;
+    } else {
+        uint4 t = ldg_nc_v4(p);
+        w[0] = t.x; w[1] = t.y; w[2] = t.z; w[3] = t.w;
+    }
+}
+
+// One container (8 elements) on the integer generic path, stored with plain
+// byte stores; kept out of line so the fast paths' register allocation does
+// not pay for it (it runs only for tiles holding NaN/Inf, or for metadata
+// outside the fast preconditions).
+template <bool BF16, int K>
+__device__ __noinline__ void enc_container_generic(const uint8_t *__restrict__ in, int64_t C, int64_t idx, int axis,
+                                                   const Fmt F, uint8_t *packed, const SegOffsets so, int64_t *spi,
+                                                   uint32_t *spb, unsigned long long *spc, int64_t cap) {
+    uint32_t c[8];
+    int64_t e[8];
 #pragma unroll
-    for (int t = 0; t < NP; ++t) {
-        uint32_t lo = enc_elem(vec_elem<BF16>(r, 2 * t), F, idx0 + 2 * t, spi, spb, spc, cap);
-        uint32_t hi = enc_elem(vec_elem<BF16>(r, 2 * t + 1), F, idx0 + 2 * t + 1, spi, spb, spc, cap);
-        cp[t] = lo | (hi << 16);
+    for (int i = 0; i < 8; ++i) {
+        e[i] = lane_elem(idx, i, C, axis);
+        c[i] = enc_elem(load_elem_scalar<BF16>(in, e[i]), F, e[i], spi, spb, spc, cap);
+    }
+    int hi = K;
+#pragma unroll
+    for (int s = 0; s < seg_count(K); ++s) {
+        const int w = seg_width(K, s), lo = hi - w;
+        uint8_t *seg = packed + so.off[s];
+        if (w == 8) {
+            for (int i = 0; i < 8; ++i) seg[e[i]] = (uint8_t)(c[i] >> lo);
+        } else {
+            uint32_t cont = 0;
+            for (int i = 0; i < 8; ++i) cont |= ((c[i] >> lo) & ((1u << w) - 1u)) << (w * i);
+            for (int b = 0; b < w; ++b) seg[idx * w + b] = (uint8_t)(cont >> (8 * b));
+        }
+        hi = lo;
     }
 }
 
@@ -387,41 +433,67 @@ __device__ __forceinline__ void rows_fast_store(const uint32_t (&RL)[NH][8], con
     }
 }
 
-template <int K, bool BF16>
+// Thread tile: 8 rows (one row group g) x 4 adjacent columns.  Every store
+// of a segment is then one instruction per thread covering whole sectors
+// across the warp (4 containers x w bytes: 16/8/4 B); a 32-byte per-thread
+// store split in two instructions made L2 write partial sectors back twice.
+template <int K, bool BF16, int MODE>
 __global__ void __launch_bounds__(256) k_enc_rows_fast(const uint8_t *__restrict__ in, int64_t R, int64_t C, int x,
                                                        int y, const uint8_t *__restrict__ meta,
                                                        uint8_t *__restrict__ packed, SegOffsets so, int64_t *spi,
                                                        uint32_t *spb, unsigned long long *spc, int64_t cap,
                                                        int force_generic) {
     using EL = Elem<BF16>;
-    constexpr int V = EL::V, NP = V / 2, NH = V / 4;
+    constexpr int NW = BF16 ? 2 : 4;   // words per 4 elements
     const Fmt F = load_fmt(x, y, meta);
     const FastP P = make_fast(F, BF16, force_generic);
-    const int64_t CV = C / V, G = R / 8;
+    const int64_t CV = C / 4, G = R / 8;
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= CV) return;
-    const int64_t c0 = j * V;
-    for (int64_t g = blockIdx.y; g < G; g += gridDim.y) {
-        uint4 r[8];
+    const int64_t c0 = j * 4;
+    const uint8_t *src = in + c0 * EL::ES;
+    const int64_t rstride = C * EL::ES;
+    if (!enc_fast_ok<BF16, MODE>(F, force_generic)) {   // metadata outside the fast preconditions
+        for (int64_t g = blockIdx.y; g < G; g += gridDim.y)
+            for (int v = 0; v < 4; ++v)
+                enc_container_generic<BF16, K>(in, C, g * C + c0 + v, 0, F, packed, so, spi, spb, spc, cap);
+        return;
+    }
+    // software pipeline: the next tile's 8 row chunks are in flight while
+    // this tile is converted and packed
+    uint32_t nxt[8][NW];
+    int64_t g = blockIdx.y;
+    if (g < G) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) r[i] = ldg_nc_v4(in + ((8 * g + i) * C + c0) * EL::ES);
-        uint32_t cp[8][NP];
-        uint32_t flag = 0;
+        for (int i = 0; i < 8; ++i) load4<BF16>(src + (8 * g + i) * rstride, nxt[i]);
+    }
+    for (; g < G; g += gridDim.y) {
+        uint32_t w[8][NW];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) vec_codes<K, BF16>(r[i], cp[i], P, F, flag, (8 * g + i) * C + c0, spi, spb, spc, cap);
-        if (flag) {
-#pragma unroll 1
-            for (int i = 0; i < 8; ++i) vec_codes_generic<K, BF16>(r[i], cp[i], F, (8 * g + i) * C + c0, spi, spb, spc, cap);
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int q = 0; q < NW; ++q) w[i][q] = nxt[i][q];
+        const int64_t gn = g + gridDim.y;
+        if (gn < G) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) load4<BF16>(src + (8 * gn + i) * rstride, nxt[i]);
         }
-        uint32_t RL[NH][8], RH[NH][8];
+        uint32_t cp[8][2];
+        uint32_t amax = 0;
 #pragma unroll
-        for (int h = 0; h < NH; ++h)
+        for (int i = 0; i < 8; ++i) vec_codes<K, BF16, MODE, NW>(w[i], cp[i], P, amax);
+        if (!amax_special<BF16, MODE>(amax)) {
+            uint32_t RL[1][8], RH[1][8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                RL[h][i] = prmt(cp[i][2 * h], cp[i][2 * h + 1], 0x6420);
-                RH[h][i] = (K == 9) ? prmt(cp[i][2 * h] >> 1, cp[i][2 * h + 1] >> 1, 0x6420) : 0u;
+                RL[0][i] = prmt(cp[i][0], cp[i][1], 0x6420);
+                RH[0][i] = (K == 9) ? prmt(cp[i][0] >> 1, cp[i][1] >> 1, 0x6420) : 0u;
             }
-        rows_fast_store<K, NH, 0>(RL, RH, packed, so, g, C, c0);
+            rows_fast_store<K, 1, 0>(RL, RH, packed, so, g, C, c0);
+        } else {   // NaN/Inf in the tile (rare): integer path, records the specials
+            for (int v = 0; v < 4; ++v)
+                enc_container_generic<BF16, K>(in, C, g * C + c0 + v, 0, F, packed, so, spi, spb, spc, cap);
+        }
     }
 }
 
@@ -461,7 +533,7 @@ __device__ __forceinline__ void cols_fast_store(const uint32_t (&RL)[8], const u
     }
 }
 
-template <int K, bool BF16>
+template <int K, bool BF16, int MODE>
 __global__ void __launch_bounds__(256) k_enc_cols_fast(const uint8_t *__restrict__ in, int64_t n, int x, int y,
                                                        const uint8_t *__restrict__ meta, uint8_t *__restrict__ packed,
                                                        SegOffsets so, int64_t *spi, uint32_t *spb,
@@ -473,56 +545,70 @@ __global__ void __launch_bounds__(256) k_enc_cols_fast(const uint8_t *__restrict
     const FastP P = make_fast(F, BF16, force_generic);
     const int64_t NG = n / 8;
     const int lane = threadIdx.x & 31;
-    const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int64_t step = (int64_t)gridDim.x * (blockDim.x >> 5) * 128;
     const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    for (int64_t base = gw * 128; base < NG; base += warps_total * 128) {
+    if (!enc_fast_ok<BF16, MODE>(F, force_generic)) {
+        for (int64_t base = gw * 128; base < NG; base += step)
+            for (int u = 0; u < 4; ++u) {
+                const int64_t q = base + 32 * u + lane;
+                if (q < NG) enc_container_generic<BF16, K>(in, 0, q, 1, F, packed, so, spi, spb, spc, cap);
+            }
+        return;
+    }
+    uint4 nxt[4][NV];
+    int64_t base = gw * 128;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int64_t q = base + 32 * u + lane;
+#pragma unroll
+        for (int t = 0; t < NV; ++t)
+            nxt[u][t] = q < NG ? ldg_nc_v4(in + q * 8 * EL::ES + 16 * t) : make_uint4(0, 0, 0, 0);
+    }
+    for (; base < NG; base += step) {
         uint4 r[4][NV];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const int64_t q = base + 32 * u + lane;
+            const int64_t qn = base + step + 32 * u + lane;
 #pragma unroll
-            for (int t = 0; t < NV; ++t)
-                r[u][t] = q < NG ? ldg_nc_v4(in + q * 8 * EL::ES + 16 * t) : make_uint4(0, 0, 0, 0);
+            for (int t = 0; t < NV; ++t) {
+                r[u][t] = nxt[u][t];
+                nxt[u][t] = qn < NG ? ldg_nc_v4(in + qn * 8 * EL::ES + 16 * t) : make_uint4(0, 0, 0, 0);
+            }
         }
         uint32_t cp[4][4];   // group u, pair t (elements 2t, 2t+1)
-        uint32_t flag = 0;
+        uint32_t amax = 0;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const int64_t q = base + 32 * u + lane;
 #pragma unroll
             for (int t = 0; t < NV; ++t) {
                 uint32_t c2[NP];
-                vec_codes<K, BF16>(r[u][t], c2, P, F, flag, 8 * q + t * EL::V, spi, spb, spc, q < NG ? cap : 0);
+                const uint32_t ww[4] = {r[u][t].x, r[u][t].y, r[u][t].z, r[u][t].w};
+                vec_codes<K, BF16, MODE, 4>(ww, c2, P, amax);
 #pragma unroll
                 for (int p = 0; p < NP; ++p) cp[u][t * NP + p] = c2[p];
             }
         }
-        if (flag) {
-#pragma unroll 1
-            for (int u = 0; u < 4; ++u) {
-                const int64_t q = base + 32 * u + lane;
-                if (q >= NG) continue;
-                for (int t = 0; t < NV; ++t) {
-                    uint32_t c2[NP];
-                    vec_codes_generic<K, BF16>(r[u][t], c2, F, 8 * q + t * EL::V, spi, spb, spc, cap);
-                    for (int p = 0; p < NP; ++p) cp[u][t * NP + p] = c2[p];
+        if (!amax_special<BF16, MODE>(amax)) {
+            uint32_t RL[8], RH[8];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const uint32_t y01 = prmt(cp[0][t], cp[1][t], 0x6420), y23 = prmt(cp[2][t], cp[3][t], 0x6420);
+                RL[2 * t] = prmt(y01, y23, 0x6420);
+                RL[2 * t + 1] = prmt(y01, y23, 0x7531);
+                if (K == 9) {
+                    const uint32_t h01 = prmt(cp[0][t] >> 1, cp[1][t] >> 1, 0x6420);
+                    const uint32_t h23 = prmt(cp[2][t] >> 1, cp[3][t] >> 1, 0x6420);
+                    RH[2 * t] = prmt(h01, h23, 0x6420);
+                    RH[2 * t + 1] = prmt(h01, h23, 0x7531);
                 }
             }
-        }
-        uint32_t RL[8], RH[8];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const uint32_t y01 = prmt(cp[0][t], cp[1][t], 0x6420), y23 = prmt(cp[2][t], cp[3][t], 0x6420);
-            RL[2 * t] = prmt(y01, y23, 0x6420);
-            RL[2 * t + 1] = prmt(y01, y23, 0x7531);
-            if (K == 9) {
-                const uint32_t h01 = prmt(cp[0][t] >> 1, cp[1][t] >> 1, 0x6420);
-                const uint32_t h23 = prmt(cp[2][t] >> 1, cp[3][t] >> 1, 0x6420);
-                RH[2 * t] = prmt(h01, h23, 0x6420);
-                RH[2 * t + 1] = prmt(h01, h23, 0x7531);
+            cols_fast_store<K, 0>(RL, RH, cp, packed, so, base + lane, NG);
+        } else {
+            for (int u = 0; u < 4; ++u) {
+                const int64_t q = base + 32 * u + lane;
+                if (q < NG) enc_container_generic<BF16, K>(in, 0, q, 1, F, packed, so, spi, spb, spc, cap);
             }
         }
-        cols_fast_store<K, 0>(RL, RH, cp, packed, so, base + lane, NG);
     }
 }
 

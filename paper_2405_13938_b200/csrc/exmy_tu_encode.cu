@@ -4,24 +4,21 @@
 namespace exmy {
 
 namespace {
-template <int K, bool BF16>
-exmy_status launch_encode_k(const uint8_t *in, int64_t R, int64_t C, int axis, int x, int y, const uint8_t *meta,
+template <int K, bool BF16, int MODE>
+exmy_status launch_encode_km(const uint8_t *in, int64_t R, int64_t C, int axis, int x, int y, const uint8_t *meta,
                             uint8_t *packed, const Plan &p, int64_t *spi, uint32_t *spb,
                             unsigned long long *spc, int64_t cap, cudaStream_t st) {
-    constexpr int V = Elem<BF16>::V;
     const int64_t n = R * C;
     bool vec = aligned(in, 16);
     if (axis == EXMY_AXIS_ROWS) {
-        vec = vec && (C % V == 0);
-        for (int s = 0; s < p.nseg; ++s) {
-            size_t a = p.w[s] == 8 ? (size_t)V : (size_t)((V * p.w[s]) < 16 ? V * p.w[s] : 16);
-            vec = vec && aligned(packed + p.so.off[s], a);
-        }
+        // thread tile = 8 rows x 4 columns: 4-element row chunks, 4*w-byte segment stores
+        vec = aligned(in, 4 * Elem<BF16>::ES) && (C % 4 == 0);
+        for (int s = 0; s < p.nseg; ++s) vec = vec && aligned(packed + p.so.off[s], p.w[s] == 8 ? 4 : 4 * p.w[s]);
         if (vec) {
             const int threads = 256;
             static int occ = 0;
-            if (!occ) occ = occupancy(k_enc_rows_fast<K, BF16>, threads, 0);
-            const int64_t CV = C / V, G = R / 8;
+            if (!occ) occ = occupancy(k_enc_rows_fast<K, BF16, MODE>, threads, 0);
+            const int64_t CV = C / 4, G = R / 8;
             int64_t gx = cdiv(CV, threads);
             int64_t target = (int64_t)num_sms() * occ;
             int64_t gy = target / gx;
@@ -29,7 +26,7 @@ exmy_status launch_encode_k(const uint8_t *in, int64_t R, int64_t C, int axis, i
             if (gy > G) gy = G;
             if (gy > 65535) gy = 65535;
             if (gx > INT_MAX) return EXMY_E_SHAPE;
-            k_enc_rows_fast<K, BF16><<<dim3((unsigned)gx, (unsigned)gy), threads, 0, st>>>(
+            k_enc_rows_fast<K, BF16, MODE><<<dim3((unsigned)gx, (unsigned)gy), threads, 0, st>>>(
                 in, R, C, x, y, meta, packed, p.so, spi, spb, spc, cap, g_force_generic);
             return launch_status();
         }
@@ -38,12 +35,12 @@ exmy_status launch_encode_k(const uint8_t *in, int64_t R, int64_t C, int axis, i
         if (vec) {
             const int threads = 256;
             static int occ = 0;
-            if (!occ) occ = occupancy(k_enc_cols_fast<K, BF16>, threads, 0);
+            if (!occ) occ = occupancy(k_enc_cols_fast<K, BF16, MODE>, threads, 0);
             int64_t tiles = cdiv(n / 8, 128);
             int64_t blocks = cdiv(tiles, threads / 32);
             int64_t maxb = (int64_t)num_sms() * occ;
             if (blocks > maxb) blocks = maxb;
-            k_enc_cols_fast<K, BF16><<<(unsigned)blocks, threads, 0, st>>>(in, n, x, y, meta, packed, p.so, spi,
+            k_enc_cols_fast<K, BF16, MODE><<<(unsigned)blocks, threads, 0, st>>>(in, n, x, y, meta, packed, p.so, spi,
                                                                            spb, spc, cap, g_force_generic);
             return launch_status();
         }
@@ -56,6 +53,23 @@ exmy_status launch_encode_k(const uint8_t *in, int64_t R, int64_t C, int axis, i
                                                              make_int4(p.w[0], p.w[1], p.w[2], p.w[3]), spi, spb,
                                                              spc, cap);
     return launch_status();
+}
+
+// encode mode from (dtype, y): bf16 SIMD pairs for y <= 6, per-element fp32 otherwise
+template <int K, bool BF16>
+exmy_status launch_encode_k(const uint8_t *in, int64_t R, int64_t C, int axis, int x, int y, const uint8_t *meta,
+                            uint8_t *packed, const Plan &p, int64_t *spi, uint32_t *spb,
+                            unsigned long long *spc, int64_t cap, cudaStream_t st) {
+    if (BF16 && y <= 6) {
+        if (y == 0)
+            return launch_encode_km<K, BF16, (BF16 ? ENC_SIMD_Y0 : ENC_F32_Y0)>(in, R, C, axis, x, y, meta, packed, p,
+                                                                               spi, spb, spc, cap, st);
+        return launch_encode_km<K, BF16, (BF16 ? ENC_SIMD : ENC_F32)>(in, R, C, axis, x, y, meta, packed, p, spi, spb,
+                                                                     spc, cap, st);
+    }
+    if (y == 0)
+        return launch_encode_km<K, BF16, ENC_F32_Y0>(in, R, C, axis, x, y, meta, packed, p, spi, spb, spc, cap, st);
+    return launch_encode_km<K, BF16, ENC_F32>(in, R, C, axis, x, y, meta, packed, p, spi, spb, spc, cap, st);
 }
 
 template <bool BF16>

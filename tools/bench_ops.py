@@ -16,17 +16,21 @@ import workloads as W  # noqa: E402
 
 
 def timeit(fn, reps=20, warm=3):
+    """average device time per call over `reps` back-to-back calls (the
+    launch queue stays ahead of the GPU, so host overhead is hidden)"""
     for _ in range(warm):
         fn()
+    torch.cuda.synchronize()
     ts = []
-    for _ in range(reps):
+    for _ in range(3):
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record()
-        fn()
+        for _ in range(reps):
+            fn()
         b.record()
         torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b))
+        ts.append(a.elapsed_time(b) / reps)
     return statistics.median(ts)
 
 
