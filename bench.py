@@ -56,26 +56,55 @@ REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_pow
 
 
 class ClockSampler:
-    def __init__(self, index: int):
+    """Samples SM clock and clock-event (throttle) reasons through NVML every
+    ~2 ms in a background thread while the timed region runs (nvidia-smi's
+    own polling cannot start fast enough for a tens-of-ms region); falls back
+    to `nvidia-smi -lms 100` if NVML is unavailable."""
+
+    def __init__(self, index: int, period_s: float = 0.002):
         self.index = index
+        self.period = period_s
         self.samples = []
-        self.proc = None
+        self.stop = threading.Event()
         self.thread = None
+        self.proc = None
+        self.src = "nvml"
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index),
-                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+
+            def loop():
+                while not self.stop.is_set():
+                    try:
+                        sm = float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                        rs = int(pynvml.nvmlDeviceGetCurrentClocksEventReasons(h))
+                        self.samples.append((sm, self.max_mhz, rs))
+                    except Exception:
+                        pass
+                    time.sleep(self.period)
+
+            self.thread = threading.Thread(target=loop, daemon=True)
             self.thread.start()
+            time.sleep(0.01)
         except Exception:
-            self.proc = None
+            self.src = "nvidia-smi"
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.index),
+                     "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                     "--format=csv,noheader,nounits", "-lms", "100"],
+                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self.thread = threading.Thread(target=self._read_smi, daemon=True)
+                self.thread.start()
+            except Exception:
+                self.proc = None
         return self
 
-    def _read(self):
+    def _read_smi(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) >= 3:
@@ -85,6 +114,7 @@ class ClockSampler:
                     pass
 
     def __exit__(self, *a):
+        self.stop.set()
         if self.proc:
             self.proc.terminate()
             try:
@@ -96,7 +126,7 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "source": self.src}
         sm = [s[0] for s in self.samples]
         reasons = set()
         for s in self.samples:
@@ -104,7 +134,7 @@ class ClockSampler:
                 if s[2] & bit and name != "gpu_idle":
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(s[1] for s in self.samples),
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "sm_min_mhz": min(sm), "reasons": sorted(reasons), "samples": len(sm), "source": self.src}
 
 
 # ------------------------------------------------------------------- dist

@@ -438,7 +438,7 @@ __device__ __forceinline__ void rows_fast_store(const uint32_t (&RL)[NH][8], con
 // across the warp (4 containers x w bytes: 16/8/4 B); a 32-byte per-thread
 // store split in two instructions made L2 write partial sectors back twice.
 template <int K, bool BF16, int MODE>
-__global__ void __launch_bounds__(256) k_enc_rows_fast(const uint8_t *__restrict__ in, int64_t R, int64_t C, int x,
+__global__ void __launch_bounds__(256, BF16 ? 3 : 1) k_enc_rows_fast(const uint8_t *__restrict__ in, int64_t R, int64_t C, int x,
                                                        int y, const uint8_t *__restrict__ meta,
                                                        uint8_t *__restrict__ packed, SegOffsets so, int64_t *spi,
                                                        uint32_t *spb, unsigned long long *spc, int64_t cap,
@@ -638,11 +638,23 @@ __device__ __forceinline__ uint32_t dec_to_f32(uint32_t code, const FastP &P, co
 }
 
 // ---------------------------------------------------------- decode ROWS
+// Raw packed words of one 8-row x (4*NH)-column tile, all segments: loaded
+// one tile ahead (software pipeline) and unpacked into byte lanes after.
+__host__ __device__ constexpr int seg_words(int k, int s, int nh) {
+    return seg_width(k, s) == 8 ? 8 * nh : nh * seg_width(k, s);
+}
+__host__ __device__ constexpr int seg_word_off(int k, int s, int nh) {
+    int o = 0;
+    for (int t = 0; t < s; ++t) o += seg_words(k, t, nh);
+    return o;
+}
+__host__ __device__ constexpr int tile_words(int k, int nh) { return seg_word_off(k, seg_count(k), nh); }
+
 template <int K, int NH, int S>
-__device__ __forceinline__ void rows_fast_load(uint32_t (&RL)[NH][8], uint32_t (&RH)[NH][8], const uint8_t *packed,
-                                               const SegOffsets &so, int64_t g, int64_t C, int64_t c0) {
+__device__ __forceinline__ void rows_load_raw(uint32_t (&raw)[tile_words(K, NH)], const uint8_t *packed,
+                                              const SegOffsets &so, int64_t g, int64_t C, int64_t c0) {
     if constexpr (S < seg_count(K)) {
-        constexpr int W = seg_width(K, S), LO = seg_lo(K, S);
+        constexpr int W = seg_width(K, S), OFF = seg_word_off(K, S, NH);
         const uint8_t *seg = packed + so.off[S];
         if constexpr (W == 8) {
 #pragma unroll
@@ -650,60 +662,98 @@ __device__ __forceinline__ void rows_fast_load(uint32_t (&RL)[NH][8], uint32_t (
                 uint32_t w[NH];
                 load_words<NH>(seg + (8 * g + i) * C + c0, w);
 #pragma unroll
-                for (int h = 0; h < NH; ++h) {
-                    if (K == 9) RH[h][i] = w[h];
-                    else RL[h][i] = w[h];
-                }
+                for (int h = 0; h < NH; ++h) raw[OFF + i * NH + h] = w[h];
             }
         } else {
             uint32_t w[NH * W];
             load_words<NH * W>(seg + (g * C + c0) * W, w);
 #pragma unroll
-            for (int h = 0; h < NH; ++h) {
-                uint32_t in[W];
-#pragma unroll
-                for (int q = 0; q < W; ++q) in[q] = w[h * W + q];
-                swar_unpack4<W, LO>(in, RL[h]);
-            }
+            for (int q = 0; q < NH * W; ++q) raw[OFF + q] = w[q];
         }
-        rows_fast_load<K, NH, S + 1>(RL, RH, packed, so, g, C, c0);
+        rows_load_raw<K, NH, S + 1>(raw, packed, so, g, C, c0);
     }
 }
 
-template <int K, bool OBF16>
+template <int K, int NH, int S>
+__device__ __forceinline__ void rows_unpack_raw(const uint32_t (&raw)[tile_words(K, NH)], uint32_t (&RL)[NH][8],
+                                                uint32_t (&RH)[NH][8]) {
+    if constexpr (S < seg_count(K)) {
+        constexpr int W = seg_width(K, S), LO = seg_lo(K, S), OFF = seg_word_off(K, S, NH);
+        if constexpr (W == 8) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int h = 0; h < NH; ++h) {
+                    if (K == 9) RH[h][i] = raw[OFF + i * NH + h];
+                    else RL[h][i] = raw[OFF + i * NH + h];
+                }
+        } else {
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+                uint32_t in[W];
+#pragma unroll
+                for (int q = 0; q < W; ++q) in[q] = raw[OFF + h * W + q];
+                swar_unpack4<W, LO>(in, RL[h]);
+            }
+        }
+        rows_unpack_raw<K, NH, S + 1>(raw, RL, RH);
+    }
+}
+
+enum DecMode { DEC_FAST = 0, DEC_GENERIC = 1 };
+
+template <int K, bool OBF16, int MODE>
+__device__ __forceinline__ uint32_t dec_pair_bf16_m(uint32_t cp, const FastP &P, const Fmt &F) {
+    if constexpr (MODE == DEC_FAST) return dec_pair_bf16<K>(cp, P, F.y);
+    else return dec_code_generic<8>(cp & 0xFFFFu, F) | (dec_code_generic<8>(cp >> 16, F) << 16);
+}
+template <int K, int MODE>
+__device__ __forceinline__ uint32_t dec_f32_m(uint32_t code, const FastP &P, const Fmt &F) {
+    if constexpr (MODE == DEC_FAST) return dec_f32_fast<K>(code, P, F.y);
+    else return dec_code_generic<24>(code, F);
+}
+
+template <int K, bool OBF16, int MODE>
 __global__ void __launch_bounds__(256) k_dec_rows_fast(const uint8_t *__restrict__ packed, int64_t R, int64_t C,
                                                        int x, int y, const uint8_t *__restrict__ meta, SegOffsets so,
-                                                       uint8_t *__restrict__ out, int force_generic) {
+                                                       uint8_t *__restrict__ out) {
     using EL = Elem<OBF16>;
-    constexpr int V = EL::V, NH = V / 4;
+    constexpr int V = EL::V, NH = V / 4, TW = tile_words(K, NH);
     const Fmt F = load_fmt(x, y, meta);
-    const FastP P = make_fast(F, false, force_generic);
+    const FastP P = make_fast(F, false, 0);
     const int64_t CV = C / V, G = R / 8;
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= CV) return;
     const int64_t c0 = j * V;
-    for (int64_t g = blockIdx.y; g < G; g += gridDim.y) {
+    uint32_t nxt[TW];
+    int64_t g = blockIdx.y;
+    if (g < G) rows_load_raw<K, NH, 0>(nxt, packed, so, g, C, c0);
+    for (; g < G; g += gridDim.y) {
+        uint32_t raw[TW];
+#pragma unroll
+        for (int q = 0; q < TW; ++q) raw[q] = nxt[q];
+        if (g + gridDim.y < G) rows_load_raw<K, NH, 0>(nxt, packed, so, g + gridDim.y, C, c0);
         uint32_t RL[NH][8], RH[NH][8];
 #pragma unroll
         for (int h = 0; h < NH; ++h)
 #pragma unroll
             for (int i = 0; i < 8; ++i) { RL[h][i] = 0; RH[h][i] = 0; }
-        rows_fast_load<K, NH, 0>(RL, RH, packed, so, g, C, c0);
+        rows_unpack_raw<K, NH, 0>(raw, RL, RH);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             uint32_t o[4];
             if (OBF16) {
 #pragma unroll
                 for (int h = 0; h < NH; ++h) {
-                    o[2 * h] = dec_pair_to_bf16<K>(pair_from_lanes<K>(RL[h][i], RH[h][i], 0x4140), P, F);
-                    o[2 * h + 1] = dec_pair_to_bf16<K>(pair_from_lanes<K>(RL[h][i], RH[h][i], 0x4342), P, F);
+                    o[2 * h] = dec_pair_bf16_m<K, OBF16, MODE>(pair_from_lanes<K>(RL[h][i], RH[h][i], 0x4140), P, F);
+                    o[2 * h + 1] = dec_pair_bf16_m<K, OBF16, MODE>(pair_from_lanes<K>(RL[h][i], RH[h][i], 0x4342), P, F);
                 }
             } else {
 #pragma unroll
                 for (int v = 0; v < 4; ++v) {
                     uint32_t code = (RL[0][i] >> (8 * v)) & 0xFFu;
                     if (K == 9) code |= ((RH[0][i] >> (8 * v)) & 0xFFu) << 1;
-                    o[v] = dec_to_f32<K>(code, P, F);
+                    o[v] = dec_f32_m<K, MODE>(code, P, F);
                 }
             }
             stg_v4(out + ((8 * g + i) * C + c0) * EL::ES, make_uint4(o[0], o[1], o[2], o[3]));
@@ -757,12 +807,12 @@ __device__ __forceinline__ void cols_fast_load(uint32_t (&RL)[8], uint32_t (&RH)
     }
 }
 
-template <int K, bool OBF16>
+template <int K, bool OBF16, int MODE>
 __global__ void __launch_bounds__(256) k_dec_cols_fast(const uint8_t *__restrict__ packed, int64_t n, int x, int y,
                                                        const uint8_t *__restrict__ meta, SegOffsets so,
-                                                       uint8_t *__restrict__ out, int force_generic) {
+                                                       uint8_t *__restrict__ out) {
     const Fmt F = load_fmt(x, y, meta);
-    const FastP P = make_fast(F, false, force_generic);
+    const FastP P = make_fast(F, false, 0);
     const int64_t NG = n / 8;
     const int lane = threadIdx.x & 31;
     const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -787,7 +837,7 @@ __global__ void __launch_bounds__(256) k_dec_cols_fast(const uint8_t *__restrict
                         uint32_t ch = prmt(RH[2 * t], RH[2 * t + 1], sel);
                         cp |= ((ch & 0xFFu) | ((ch & 0xFF00u) << 8)) << 1;
                     }
-                    o[t] = dec_pair_to_bf16<K>(cp, P, F);
+                    o[t] = dec_pair_bf16_m<K, OBF16, MODE>(cp, P, F);
                 }
                 stg_v4(out + q * 16, make_uint4(o[0], o[1], o[2], o[3]));
             } else {
@@ -796,7 +846,7 @@ __global__ void __launch_bounds__(256) k_dec_cols_fast(const uint8_t *__restrict
                 for (int i = 0; i < 8; ++i) {
                     uint32_t code = (RL[i] >> (8 * u)) & 0xFFu;
                     if (K == 9) code |= ((RH[i] >> (8 * u)) & 0xFFu) << 1;
-                    o[i] = dec_to_f32<K>(code, P, F);
+                    o[i] = dec_f32_m<K, MODE>(code, P, F);
                 }
                 stg_v4(out + q * 32, make_uint4(o[0], o[1], o[2], o[3]));
                 stg_v4(out + q * 32 + 16, make_uint4(o[4], o[5], o[6], o[7]));

@@ -4,8 +4,8 @@
 namespace exmy {
 
 namespace {
-template <int K, bool OBF16>
-exmy_status launch_decode_k(const uint8_t *packed, int64_t R, int64_t C, int axis, int x, int y,
+template <int K, bool OBF16, int MODE>
+exmy_status launch_decode_km(const uint8_t *packed, int64_t R, int64_t C, int axis, int x, int y,
                             const uint8_t *meta, const Plan &p, uint8_t *out, cudaStream_t st) {
     constexpr int V = Elem<OBF16>::V;
     const int64_t n = R * C;
@@ -19,7 +19,7 @@ exmy_status launch_decode_k(const uint8_t *packed, int64_t R, int64_t C, int axi
         if (vec) {
             const int threads = 256;
             static int occ = 0;
-            if (!occ) occ = occupancy(k_dec_rows_fast<K, OBF16>, threads, 0);
+            if (!occ) occ = occupancy(k_dec_rows_fast<K, OBF16, MODE>, threads, 0);
             const int64_t CV = C / V, G = R / 8;
             int64_t gx = cdiv(CV, threads);
             int64_t target = (int64_t)num_sms() * occ;
@@ -28,8 +28,8 @@ exmy_status launch_decode_k(const uint8_t *packed, int64_t R, int64_t C, int axi
             if (gy > G) gy = G;
             if (gy > 65535) gy = 65535;
             if (gx > INT_MAX) return EXMY_E_SHAPE;
-            k_dec_rows_fast<K, OBF16><<<dim3((unsigned)gx, (unsigned)gy), threads, 0, st>>>(packed, R, C, x, y, meta,
-                                                                                         p.so, out, g_force_generic);
+            k_dec_rows_fast<K, OBF16, MODE><<<dim3((unsigned)gx, (unsigned)gy), threads, 0, st>>>(packed, R, C, x, y, meta,
+                                                                                               p.so, out);
             return launch_status();
         }
     } else {
@@ -37,13 +37,12 @@ exmy_status launch_decode_k(const uint8_t *packed, int64_t R, int64_t C, int axi
         if (vec) {
             const int threads = 256;
             static int occ = 0;
-            if (!occ) occ = occupancy(k_dec_cols_fast<K, OBF16>, threads, 0);
+            if (!occ) occ = occupancy(k_dec_cols_fast<K, OBF16, MODE>, threads, 0);
             int64_t tiles = cdiv(n / 8, 128);
             int64_t blocks = cdiv(tiles, threads / 32);
             int64_t maxb = (int64_t)num_sms() * occ;
             if (blocks > maxb) blocks = maxb;
-            k_dec_cols_fast<K, OBF16><<<(unsigned)blocks, threads, 0, st>>>(packed, n, x, y, meta, p.so, out,
-                                                                          g_force_generic);
+            k_dec_cols_fast<K, OBF16, MODE><<<(unsigned)blocks, threads, 0, st>>>(packed, n, x, y, meta, p.so, out);
             return launch_status();
         }
     }
@@ -55,6 +54,16 @@ exmy_status launch_decode_k(const uint8_t *packed, int64_t R, int64_t C, int axi
                                                               make_int4(p.w[0], p.w[1], p.w[2], p.w[3]), out,
                                                               g_force_generic);
     return launch_status();
+}
+
+// decode mode from the format (no metadata dependence): the multiply path
+// needs x <= 7 (and y <= 7 for bf16 output); the debug knob forces generic
+template <int K, bool OBF16>
+exmy_status launch_decode_k(const uint8_t *packed, int64_t R, int64_t C, int axis, int x, int y,
+                            const uint8_t *meta, const Plan &p, uint8_t *out, cudaStream_t st) {
+    const bool fast = !g_force_generic && x <= 7 && (!OBF16 || y <= 7);
+    return fast ? launch_decode_km<K, OBF16, DEC_FAST>(packed, R, C, axis, x, y, meta, p, out, st)
+                : launch_decode_km<K, OBF16, DEC_GENERIC>(packed, R, C, axis, x, y, meta, p, out, st);
 }
 
 template <bool OBF16>

@@ -68,7 +68,7 @@ def test_histogram_parity(exmy, orc, dt, n, mode):
         h = exmy.histogram(dev_bits(bits)).cpu().numpy().astype(np.uint64)
         np.testing.assert_array_equal(h, orc.histogram(bits))
     finally:
-        exmy.hist_mode(0)
+        exmy.hist_mode(1)
 
 
 @pytest.mark.parametrize("dt", ["bf16", "f32"])

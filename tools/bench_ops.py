@@ -59,7 +59,7 @@ def main():
         exmy.hist_mode(m)
         ms = timeit(lambda: exmy.histogram(t, out=h))
         res[f"hist_mode{m}"] = {"ms": ms, "gbs": n * es / ms / 1e6, "frac": n * es / ms / 1e6 / peak}
-    exmy.hist_mode(0)
+    exmy.hist_mode(1)
     meta = exmy.max_exponent(t)
     q = torch.empty_like(t)
     d = torch.empty_like(t)
