@@ -21,7 +21,8 @@ from dataclasses import dataclass
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_PKG, "libexmy.so")
+# EXMY_LIB_PATH: A/B experiments with an alternative build of the same ABI
+_LIB_PATH = os.environ.get("EXMY_LIB_PATH") or os.path.join(_PKG, "libexmy.so")
 
 F32, BF16 = 0, 1
 ROWS, COLS = 0, 1

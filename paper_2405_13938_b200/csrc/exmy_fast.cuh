@@ -152,10 +152,16 @@ __device__ __forceinline__ uint32_t enc_pair_bf16(uint32_t w, const FastP &P, ui
     uint32_t ecl = w & 0x7F807F80u;
     ecl = vmax_u16x2(ecl, P.lo2);
     ecl = vmin_u16x2(ecl, P.hi2);
-    uint32_t c = ecl + P.k2;
-    if (Y0) c += ((ecl >> 7) ^ P.par2) & 0x00010001u;   // even code, not even count
+    uint32_t c, t;
+    if (Y0) {   // y = 0: shift is 7; move C by one quantum where Ecl-o-1 is odd (even code, not even count)
+        t = ecl >> 7;
+        c = ecl + P.k2 + ((t ^ P.par2) & 0x00010001u);
+    } else {
+        t = ecl >> P.sh_b;
+        c = ecl + P.k2;
+    }
     const uint32_t s = hadd2_bf16(a2, c);
-    uint32_t code = s - c + (ecl >> P.sh_b) - P.k3;
+    uint32_t code = s - c + t - P.k3;
     code = vmin_u16x2(code, P.m2);
     code |= (w >> (16 - K)) & ((1u << (K - 1)) * 0x00010001u);
     amax = vmax_u16x2(amax, a2);
@@ -438,7 +444,7 @@ __device__ __forceinline__ void rows_fast_store(const uint32_t (&RL)[NH][8], con
 // across the warp (4 containers x w bytes: 16/8/4 B); a 32-byte per-thread
 // store split in two instructions made L2 write partial sectors back twice.
 template <int K, bool BF16, int MODE>
-__global__ void __launch_bounds__(256, BF16 ? 3 : 1) k_enc_rows_fast(const uint8_t *__restrict__ in, int64_t R, int64_t C, int x,
+__global__ void __launch_bounds__(256, BF16 ? 3 : 2) k_enc_rows_fast(const uint8_t *__restrict__ in, int64_t R, int64_t C, int x,
                                                        int y, const uint8_t *__restrict__ meta,
                                                        uint8_t *__restrict__ packed, SegOffsets so, int64_t *spi,
                                                        uint32_t *spb, unsigned long long *spc, int64_t cap,
@@ -825,8 +831,36 @@ __global__ void __launch_bounds__(256) k_dec_cols_fast(const uint8_t *__restrict
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int64_t q = base + 32 * u + lane;
+            if (!OBF16) {
+                // fp32 out: 32 B per group.  Lanes swap halves through shuffles
+                // so each store instruction writes 512 contiguous bytes (whole
+                // sectors); a per-lane 32 B store split in two instructions
+                // leaves half-written sectors that L2 writes back twice.
+                uint32_t o[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    uint32_t code = (RL[i] >> (8 * u)) & 0xFFu;
+                    if (K == 9) code |= ((RH[i] >> (8 * u)) & 0xFFu) << 1;
+                    o[i] = dec_f32_m<K, MODE>(code, P, F);
+                }
+                const int64_t g0 = base + 32 * u;            // first group of this warp row
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int src = 16 * h + (lane >> 1);
+                    const bool hi = lane & 1;
+                    uint32_t v[4];
+#pragma unroll
+                    for (int k2 = 0; k2 < 4; ++k2) {
+                        const uint32_t a = __shfl_sync(0xFFFFFFFFu, o[k2], src);
+                        const uint32_t b = __shfl_sync(0xFFFFFFFFu, o[4 + k2], src);
+                        v[k2] = hi ? b : a;
+                    }
+                    if (g0 + src < NG) stg_v4(out + (g0 * 32) + (32 * h + lane) * 16, make_uint4(v[0], v[1], v[2], v[3]));
+                }
+                continue;
+            }
             if (q >= NG) continue;
-            if (OBF16) {
+            {
                 uint32_t o[4];
                 const uint32_t sel = (uint32_t)u | ((uint32_t)(4 + u) << 4);   // bytes 0, 1 <- lanes, masked
 #pragma unroll
@@ -840,16 +874,6 @@ __global__ void __launch_bounds__(256) k_dec_cols_fast(const uint8_t *__restrict
                     o[t] = dec_pair_bf16_m<K, OBF16, MODE>(cp, P, F);
                 }
                 stg_v4(out + q * 16, make_uint4(o[0], o[1], o[2], o[3]));
-            } else {
-                uint32_t o[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    uint32_t code = (RL[i] >> (8 * u)) & 0xFFu;
-                    if (K == 9) code |= ((RH[i] >> (8 * u)) & 0xFFu) << 1;
-                    o[i] = dec_f32_m<K, MODE>(code, P, F);
-                }
-                stg_v4(out + q * 32, make_uint4(o[0], o[1], o[2], o[3]));
-                stg_v4(out + q * 32 + 16, make_uint4(o[4], o[5], o[6], o[7]));
             }
         }
     }
@@ -868,12 +892,21 @@ __global__ void __launch_bounds__(256) k_quant_fast(const uint8_t *__restrict__ 
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     constexpr int U = 4;
     const bool fast = BF16 ? P.enc_simd : P.enc_f32;
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; base < nvec; base += stride * U) {
+    // software pipeline: the next U vectors are in flight while these are processed
+    uint4 nxt[U];
+    const int64_t base0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int64_t vi = base0 + u * stride;
+        if (vi < nvec) nxt[u] = ldg_nc_v4(in + vi * 16);
+    }
+    for (int64_t base = base0; base < nvec; base += stride * U) {
         uint4 r[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int64_t vi = base + u * stride;
-            if (vi < nvec) r[u] = ldg_nc_v4(in + vi * 16);
+            r[u] = nxt[u];
+            const int64_t vn = base + (U + u) * stride;
+            if (vn < nvec) nxt[u] = ldg_nc_v4(in + vn * 16);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
