@@ -154,6 +154,14 @@ def init_dist(ws, local, backend="nccl"):
     return None
 
 
+def device_index(local):
+    """One process per GPU.  (--dist-backend gloo exists only to smoke-test the
+    N>1 host logic on a 1-GPU box; ranks then share the device, and their
+    collectives run on the CPU, so no kernel waits on another rank.)"""
+    n = torch.cuda.device_count()
+    return local % n if n else local
+
+
 # --------------------------------------------------------------- our arm
 def run_ours(args):
     import paper_2405_13938_b200 as exmy
@@ -161,9 +169,10 @@ def run_ours(args):
     import workloads as W
 
     ws, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    dist = init_dist(ws, local)
+    di = device_index(local)
+    torch.cuda.set_device(di)
+    dev = torch.device("cuda", di)
+    dist = init_dist(ws, di, args.dist_backend)
     group = None
 
     n = R * C
@@ -219,7 +228,7 @@ def run_ours(args):
     for k in ev:
         ev[k].clear()
 
-    with ClockSampler(local) as clk:
+    with ClockSampler(di) as clk:
         if dist:
             dist.barrier()
         torch.cuda.synchronize(dev)
@@ -410,6 +419,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-rows", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

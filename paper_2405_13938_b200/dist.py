@@ -40,14 +40,30 @@ def shard_rows(R: int, G: int, r: int, axis_rows: bool = True) -> tuple[int, int
     return r * per, (r + 1) * per
 
 
+def _host_staged(t: torch.Tensor, group) -> bool:
+    """gloo (CPU tests / 1-GPU smoke runs) moves device tensors through host."""
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
 def allreduce_histogram(hist: torch.Tensor, group=None) -> torch.Tensor:
     """C1: sum of the per-rank exponent histograms (int64[256], in place)."""
+    if _host_staged(hist, group):
+        h = hist.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+        hist.copy_(h)
+        return hist
     dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=group)
     return hist
 
 
 def allgather_bytes(local: torch.Tensor, out: torch.Tensor, group=None) -> torch.Tensor:
     """C2: all-gather of equal-size packed shards into out[G * nbytes]."""
+    if _host_staged(local, group) or dist.get_backend(group) == "gloo":
+        G = dist.get_world_size(group)
+        parts = [torch.empty_like(local, device="cpu") for _ in range(G)]
+        dist.all_gather(parts, local.cpu(), group=group)
+        out.copy_(torch.cat(parts))
+        return out
     dist.all_gather_into_tensor(out, local, group=group)
     return out
 

@@ -323,3 +323,32 @@ def test_host_codec_roundtrip(exmy, orc):
     assert int(hm.item()) == e
     np.testing.assert_array_equal(hp.numpy(), orc.encode(bits, "e2m4", e, orc.ROWS)[0])
     np.testing.assert_array_equal(W.to_bits(hout), orc.quantize(bits, "e2m4", e))
+
+
+@pytest.mark.parametrize("axis", ["rows", "cols"])
+def test_beyond_2e32_elements(exmy, orc, axis):
+    """Maximum-size edge case: n > 2^32 elements (64-bit indexing everywhere).
+    Parity on windows past the 2^32 boundary (rows are contiguous byte ranges
+    per segment) + decode == quantize on sampled rows."""
+    if torch.cuda.get_device_properties(0).total_memory < 60e9:
+        pytest.skip("needs a large-memory GPU")
+    R, C = 65536 + 64, 65536
+    t = W.bf16_weights((R, C), seed=21, device=DEV)
+    meta = exmy.max_exponent(t)
+    e = int(meta.item())
+    p = exmy.encode(t, "e3m3", meta, axis=axis)
+    ws, offs = exmy.segments(7, R * C)
+    for r0 in (0, 65536 - 8, 65536 + 8, R - 8):
+        rows = W.to_bits(t[r0:r0 + 8])
+        ref = orc.encode(rows, "e3m3", e, orc.ROWS if axis == "rows" else orc.COLS)[0]
+        got = torch.cat([p.data[o + r0 * C * w // 8: o + (r0 + 8) * C * w // 8] for w, o in zip(ws, offs)])
+        np.testing.assert_array_equal(got.cpu().numpy(), ref, err_msg=f"window {r0}")
+    d = exmy.decode(p)
+    del p
+    torch.cuda.empty_cache()
+    q = exmy.quantize(t, "e3m3", meta)
+    for r0 in (0, 65536 - 8, 65536 + 8, R - 8):
+        assert torch.equal(d[r0:r0 + 8].view(torch.int16), q[r0:r0 + 8].view(torch.int16))
+        np.testing.assert_array_equal(W.to_bits(q[r0:r0 + 8]), orc.quantize(W.to_bits(t[r0:r0 + 8]), "e3m3", e))
+    h = exmy.histogram(t).cpu().numpy().astype(np.uint64)
+    assert int(h.sum()) == R * C
