@@ -11,6 +11,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 
 namespace exmy {
 

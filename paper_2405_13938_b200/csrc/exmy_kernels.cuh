@@ -164,86 +164,6 @@ __global__ void __launch_bounds__(HIST_THREADS) k_hist(const uint8_t *__restrict
     }
 }
 
-// Variants for measurement (exmy_debug_hist_mode):
-//  mode 2: lane-private 32-bit counters, one bin per shared word (bank =
-//          lane), updated with shared-memory atomics; bin<<7 is read straight
-//          off the bit pattern (w & 0x7F80), so ~2.5 ALU ops per element.
-//  mode 3: warp-aggregated: __match_any_sync groups equal bins of a warp
-//          instruction, the leader adds popc(mask) to a per-warp histogram.
-constexpr int HIST2_WARPS = 6;                        // mode 2: 6 x 32 KB = 192 KB
-constexpr int HIST2_SMEM = HIST2_WARPS * 256 * 32 * 4;
-constexpr int HIST3_THREADS = 256;
-constexpr int HIST3_SMEM = (HIST3_THREADS / 32) * 256 * 4;
-
-template <bool BF16, int MODE>
-__global__ void k_hist_v2(const uint8_t *__restrict__ in, int64_t n, unsigned long long *__restrict__ hist) {
-    extern __shared__ uint32_t hs[];
-    using EL = Elem<BF16>;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int words = (MODE == 2) ? 256 * 32 : 256;
-    for (int i = threadIdx.x; i < nw * words; i += blockDim.x) hs[i] = 0;
-    __syncthreads();
-    uint32_t *wb = hs + warp * words;
-    // mode 2 counters: byte address of (bin, lane) = bin*128 + lane*4
-    char *lb = reinterpret_cast<char *>(wb) + lane * 4;
-    const int64_t nvec = n / EL::V;
-    const int64_t step = (int64_t)gridDim.x * nw * 128;
-    const int64_t gw = (int64_t)blockIdx.x * nw + warp;
-    uint4 nxt[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const int64_t vi = gw * 128 + 32 * u + lane;
-        nxt[u] = vi < nvec ? ldg_nc_v4(in + vi * 16) : make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-    }
-    for (int64_t base = gw * 128; base < nvec; base += step) {
-        uint4 r[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            r[u] = nxt[u];
-            const int64_t vi = base + step + 32 * u + lane;
-            nxt[u] = vi < nvec ? ldg_nc_v4(in + vi * 16) : make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const bool ok = base + 32 * u + lane < nvec;
-            const uint32_t w[4] = {r[u].x, r[u].y, r[u].z, r[u].w};
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-#pragma unroll
-                for (int h = 0; h < (BF16 ? 2 : 1); ++h) {
-                    const uint32_t v = BF16 ? (h ? (w[q] >> 16) : w[q]) : (w[q] >> 16);
-                    if (MODE == 2) {
-                        if (ok) atomicAdd(reinterpret_cast<uint32_t *>(lb + (v & 0x7F80u)), 1u);
-                    } else {
-                        const uint32_t b = ok ? ((v >> 7) & 0xFFu) : 0x100u;   // 0x100: no bin
-                        const uint32_t m = __match_any_sync(0xFFFFFFFFu, b);
-                        if (b < 0x100u && lane == __ffs(m) - 1) atomicAdd(&wb[b], (uint32_t)__popc(m));
-                    }
-                }
-            }
-        }
-    }
-    if (blockIdx.x == 0 && warp == 0) {   // scalar tail
-        for (int64_t i = nvec * EL::V + lane; i < n; i += 32) {
-            const uint32_t u = BF16 ? ((uint32_t)((const uint16_t *)in)[i] << 16) : ((const uint32_t *)in)[i];
-            const uint32_t b = (u >> 23) & 0xFFu;
-            if (MODE == 2) atomicAdd(&wb[b * 32 + lane], 1u);
-            else atomicAdd(&wb[b], 1u);
-        }
-    }
-    __syncthreads();
-    for (int b = threadIdx.x; b < 256; b += blockDim.x) {
-        unsigned long long s = 0;
-        for (int w2 = 0; w2 < nw; ++w2) {
-            if (MODE == 2)
-                for (int l = 0; l < 32; ++l) s += hs[w2 * words + b * 32 + l];
-            else
-                s += hs[w2 * words + b];
-        }
-        if (s) atomicAdd(hist + b, s);
-    }
-}
-
 // misaligned input: plain grid-stride loop with global atomics per warp bin
 template <bool BF16>
 __global__ void k_hist_scalar(const uint8_t *__restrict__ in, int64_t n, unsigned long long *__restrict__ hist) {

@@ -19,23 +19,6 @@ exmy_status launch_hist_vec(const uint8_t *in, int64_t n, unsigned long long *hi
     k_hist<BF16, MODE><<<(unsigned)blocks, HIST_THREADS, HIST_SMEM, st>>>(in, n, hist);
     return launch_status();
 }
-template <bool BF16, int MODE>
-exmy_status launch_hist_v2(const uint8_t *in, int64_t n, unsigned long long *hist, cudaStream_t st) {
-    const int threads = MODE == 2 ? HIST2_WARPS * 32 : HIST3_THREADS;
-    const int smem = MODE == 2 ? HIST2_SMEM : HIST3_SMEM;
-    static int occ = 0;
-    if (!occ) {
-        cudaFuncSetAttribute(k_hist_v2<BF16, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        occ = occupancy(k_hist_v2<BF16, MODE>, threads, smem);
-    }
-    const int64_t nvec = n / Elem<BF16>::V;
-    int64_t blocks = cdiv(cdiv(nvec, 128), threads / 32);
-    if (blocks < 1) blocks = 1;
-    int64_t maxb = (int64_t)num_sms() * occ;
-    if (blocks > maxb) blocks = maxb;
-    k_hist_v2<BF16, MODE><<<(unsigned)blocks, threads, smem, st>>>(in, n, hist);
-    return launch_status();
-}
 }  // namespace
 
 exmy_status launch_histogram(const uint8_t *in, bool bf16, int64_t n, unsigned long long *hist, cudaStream_t st) {
@@ -48,8 +31,6 @@ exmy_status launch_histogram(const uint8_t *in, bool bf16, int64_t n, unsigned l
     }
     switch (g_hist_mode) {
         case 0: return bf16 ? launch_hist_vec<true, 0>(in, n, hist, st) : launch_hist_vec<false, 0>(in, n, hist, st);
-        case 2: return bf16 ? launch_hist_v2<true, 2>(in, n, hist, st) : launch_hist_v2<false, 2>(in, n, hist, st);
-        case 3: return bf16 ? launch_hist_v2<true, 3>(in, n, hist, st) : launch_hist_v2<false, 3>(in, n, hist, st);
         default: return bf16 ? launch_hist_vec<true, 1>(in, n, hist, st) : launch_hist_vec<false, 1>(in, n, hist, st);
     }
 }

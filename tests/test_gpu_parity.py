@@ -58,7 +58,7 @@ def oracle_boundary_f32(orc, fmt, e_max):
 
 
 # ----------------------------------------------------------------- K1 / K1b
-@pytest.mark.parametrize("mode", [0, 1, 2, 3])
+@pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("dt", ["bf16", "f32"])
 @pytest.mark.parametrize("n", [0, 1, 7, 8 * 1000 + 5, 1 << 20, (1 << 22) + 3])
 def test_histogram_parity(exmy, orc, dt, n, mode):
