@@ -81,6 +81,8 @@ struct FastP {
     bool two_mul;       // o > 127
     uint32_t s1_bf2, s2_bf2;   // 2^min(o,127), 2^(o-127) as bf16 pairs
     float s1_f, s2_f;
+    uint32_t big2;      // bf16 lanes: 0x8000 - (248+y)<<7, tile fallback threshold bias
+    uint32_t bigf;      // fp32: (232+y)<<23
     uint32_t maxv2;     // largest grid magnitude as bf16 lanes (quantize)
     uint32_t maxvf;     // ... as fp32 bits
 };
@@ -108,6 +110,12 @@ __device__ __forceinline__ FastP make_fast(const Fmt &F, bool bf16_in, int force
     P.k3f = (uint32_t)(o + 1) << y;
     P.parf = (uint32_t)((o + 1) & 1);
     P.sh_b = 7 - (y > 7 ? 7 : y);
+    // Without an upper clamp on the exponent, C = 2^(E-127+7-y) overflows only
+    // for E > 247+y (bf16) / 231+y (fp32); tiles holding such magnitudes (or
+    // NaN/Inf) take the generic path.  Below that, magnitudes above the grid
+    // saturate through min(code, M).
+    P.big2 = (0x8000u - ((uint32_t)(248 + (y > 7 ? 7 : y)) << 7)) * 0x00010001u;
+    P.bigf = (uint32_t)(232 + y) << 23;
     P.sh_f = 23 - y;
     P.dec_fast = !force_generic && x <= 7;
     P.dec_fast_bf = P.dec_fast && y <= 7;
@@ -149,9 +157,7 @@ enum EncMode { ENC_SIMD = 0, ENC_SIMD_Y0 = 1, ENC_F32 = 2, ENC_F32_Y0 = 3 };
 template <int K, bool Y0>
 __device__ __forceinline__ uint32_t enc_pair_bf16(uint32_t w, const FastP &P, uint32_t &amax) {
     const uint32_t a2 = w & 0x7FFF7FFFu;
-    uint32_t ecl = w & 0x7F807F80u;
-    ecl = vmax_u16x2(ecl, P.lo2);
-    ecl = vmin_u16x2(ecl, P.hi2);
+    uint32_t ecl = vmax_u16x2(w & 0x7F807F80u, P.lo2);   // subnormal region -> binade o+1
     uint32_t c, t;
     if (Y0) {   // y = 0: shift is 7; move C by one quantum where Ecl-o-1 is odd (even code, not even count)
         t = ecl >> 7;
@@ -167,17 +173,16 @@ __device__ __forceinline__ uint32_t enc_pair_bf16(uint32_t w, const FastP &P, ui
     amax = vmax_u16x2(amax, a2);
     return code;
 }
-__device__ __forceinline__ bool amax_special_bf16(uint32_t amax) {
-    return ((amax + 0x00800080u) & 0x80008000u) != 0u;
+// any lane at or above the fallback threshold (NaN/Inf, or huge values)
+__device__ __forceinline__ bool amax_special_bf16(uint32_t amax, const FastP &P) {
+    return ((amax + P.big2) & 0x80008000u) != 0u;
 }
 
 // one fp32 pattern -> k-bit code
 template <int K, bool Y0>
 __device__ __forceinline__ uint32_t enc_f32_fast(uint32_t u, const FastP &P, uint32_t &amax) {
     const uint32_t a = u & 0x7FFFFFFFu;
-    uint32_t ecl = u & 0x7F800000u;
-    ecl = max(ecl, P.lo);
-    ecl = min(ecl, P.hi);
+    const uint32_t ecl = max(u & 0x7F800000u, P.lo);
     uint32_t c = ecl + P.k2f;
     if (Y0) c += ((ecl >> 23) ^ P.parf) & 1u;
     const uint32_t s = __float_as_uint(__fadd_rn(__uint_as_float(a), __uint_as_float(c)));
@@ -191,15 +196,13 @@ __device__ __forceinline__ uint32_t enc_f32_fast(uint32_t u, const FastP &P, uin
 // quantize two bf16 elements directly in bf16 arithmetic (value, not code)
 __device__ __forceinline__ uint32_t quant_pair_bf16(uint32_t w, const FastP &P, uint32_t &flag) {
     const uint32_t a2 = w & 0x7FFF7FFFu;
-    uint32_t ecl = w & 0x7F807F80u;
-    ecl = vmax_u16x2(ecl, P.lo2);
-    ecl = vmin_u16x2(ecl, P.hi2);
+    const uint32_t ecl = vmax_u16x2(w & 0x7F807F80u, P.lo2);
     uint32_t c = ecl + P.k2;
     if (P.y0) c += ((ecl >> 7) ^ P.par2) & 0x00010001u;
     const uint32_t s = hadd2_bf16(a2, c);
     uint32_t q = hsub2_bf16(s, c);            // exact (Sterbenz): RTNE_q(|v|)
     q = vmin_u16x2(q, P.maxv2);
-    flag |= a2 + 0x00800080u;
+    flag |= a2 + P.big2;                      // NaN/Inf or C-overflow range -> generic
     return q | (w & 0x80008000u);
 }
 
@@ -309,15 +312,13 @@ namespace exmy {
 
 __device__ __forceinline__ uint32_t quant_f32_fast(uint32_t u, const FastP &P, uint32_t &flag) {
     const uint32_t a = u & 0x7FFFFFFFu;
-    uint32_t ecl = u & 0x7F800000u;
-    ecl = max(ecl, P.lo);
-    ecl = min(ecl, P.hi);
+    const uint32_t ecl = max(u & 0x7F800000u, P.lo);
     uint32_t c = ecl + P.k2f;
     if (P.y0) c += ((ecl >> 23) ^ P.parf) & 1u;
     const float s = __fadd_rn(__uint_as_float(a), __uint_as_float(c));
     uint32_t q = __float_as_uint(__fsub_rn(s, __uint_as_float(c)));   // exact
     q = min(q, P.maxvf);
-    flag |= (a + 0x00800000u) & 0x80000000u;
+    flag |= (a >= P.bigf) ? 0x80000000u : 0u;
     return q | (u & 0x80000000u);
 }
 
@@ -353,9 +354,9 @@ __device__ __forceinline__ void vec_codes(const uint32_t (&w)[NW], uint32_t (&cp
 }
 
 template <bool BF16, int MODE>
-__device__ __forceinline__ bool amax_special(uint32_t amax) {
-    if constexpr (MODE == ENC_SIMD || MODE == ENC_SIMD_Y0) return amax_special_bf16(amax);
-    else return amax >= 0x7F800000u;
+__device__ __forceinline__ bool amax_special(uint32_t amax, const FastP &P) {
+    if constexpr (MODE == ENC_SIMD || MODE == ENC_SIMD_Y0) return amax_special_bf16(amax, P);
+    else return amax >= P.bigf;
 }
 
 template <bool BF16, int MODE>
@@ -488,7 +489,7 @@ __global__ void __launch_bounds__(256, BF16 ? 3 : 2) k_enc_rows_fast(const uint8
         uint32_t amax = 0;
 #pragma unroll
         for (int i = 0; i < 8; ++i) vec_codes<K, BF16, MODE, NW>(w[i], cp[i], P, amax);
-        if (!amax_special<BF16, MODE>(amax)) {
+        if (!amax_special<BF16, MODE>(amax, P)) {
             uint32_t RL[1][8], RH[1][8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -594,7 +595,7 @@ __global__ void __launch_bounds__(256) k_enc_cols_fast(const uint8_t *__restrict
                 for (int p = 0; p < NP; ++p) cp[u][t * NP + p] = c2[p];
             }
         }
-        if (!amax_special<BF16, MODE>(amax)) {
+        if (!amax_special<BF16, MODE>(amax, P)) {
             uint32_t RL[8], RH[8];
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
