@@ -6,10 +6,15 @@ namespace exmy {
 namespace {
 template <bool BF16, int MODE>
 exmy_status launch_hist_vec(const uint8_t *in, int64_t n, unsigned long long *hist, cudaStream_t st) {
+    // the opt-in shared-memory size is a per-device function attribute
+    static unsigned long long configured = 0;
     static int occ = 0;
-    if (!occ) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64 || !(configured & (1ull << dev))) {
         cudaFuncSetAttribute(k_hist<BF16, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM);
         occ = occupancy(k_hist<BF16, MODE>, HIST_THREADS, HIST_SMEM);
+        if (dev >= 0 && dev < 64) configured |= 1ull << dev;
     }
     const int64_t nvec = n / Elem<BF16>::V;
     int64_t blocks = cdiv(cdiv(nvec, 128), HIST_WARPS);
