@@ -67,6 +67,12 @@ def lib():
         L.oracle_encode.argtypes = [vp, i32, i64, i64, i32, i32, i32, i32, vp, vp, vp, i64]
         L.oracle_encode.restype = i64
         L.oracle_decode.argtypes = [vp, i64, i64, i32, i32, i32, i32, vp, vp, i64, vp, i32]
+        L.oracle_block_shape_ok.argtypes = [i64, i64, i64, i64]
+        L.oracle_block_max_exponent.argtypes = [vp, i32, i64, i64, i64, i64, i32, i32, vp]
+        L.oracle_quantize_blocked.argtypes = [vp, vp, i32, i64, i64, i64, i64, i32, i32, vp]
+        L.oracle_encode_blocked.argtypes = [vp, i32, i64, i64, i32, i64, i64, i32, i32, vp, vp, vp, vp, i64]
+        L.oracle_encode_blocked.restype = i64
+        L.oracle_decode_blocked.argtypes = [vp, i64, i64, i32, i64, i64, i32, i32, vp, vp, vp, i64, vp, i32]
     return _lib
 
 
@@ -216,4 +222,67 @@ def decode(packed: np.ndarray, shape, fmt, e_max: int, axis: int = ROWS,
     rc = lib().oracle_decode(_p(packed), rows, cols, axis, x, y, e_max, _p(sp_index), _p(sp_bits), cnt, _p(out), odt)
     if rc:
         raise ValueError("invalid format/e_max/shape")
+    return out
+
+
+# ------------------------------------------------------------ block metadata
+SCHEME_MAX_BEFORE, SCHEME_MAX_AFTER = 0, 1
+
+
+def block_max_exponent(bits: np.ndarray, block, y: int = 0, scheme: int = SCHEME_MAX_BEFORE) -> np.ndarray:
+    """Per-block metadata; bits (rows, cols); block = (br, bc)."""
+    bits = np.ascontiguousarray(bits)
+    rows, cols = bits.shape
+    br, bc = block
+    meta = np.zeros((rows // br) * (cols // bc), np.uint8)
+    if lib().oracle_block_max_exponent(_p(bits), _dtype_code(bits), rows, cols, br, bc, y, scheme, _p(meta)):
+        raise ValueError("bad block shape / scheme")
+    return meta.reshape(rows // br, cols // bc)
+
+
+def quantize_blocked(bits: np.ndarray, fmt, meta: np.ndarray, block) -> np.ndarray:
+    x, y = parse_format(fmt)
+    bits = np.ascontiguousarray(bits)
+    rows, cols = bits.shape
+    m = np.ascontiguousarray(meta, np.uint8)
+    out = np.empty_like(bits)
+    if lib().oracle_quantize_blocked(_p(bits), _p(out), _dtype_code(bits), rows, cols, block[0], block[1], x, y, _p(m)):
+        raise ValueError("invalid arguments")
+    return out
+
+
+def encode_blocked(bits: np.ndarray, fmt, meta: np.ndarray, block, axis: int = ROWS):
+    x, y = parse_format(fmt)
+    bits = np.ascontiguousarray(bits)
+    rows, cols = bits.shape
+    m = np.ascontiguousarray(meta, np.uint8)
+    k = 1 + x + y
+    packed = np.empty(rows * cols * k // 8, np.uint8)
+    cap = rows * cols
+    idx = np.empty(max(cap, 1), np.int64)
+    sb = np.empty(max(cap, 1), np.uint32)
+    ns = lib().oracle_encode_blocked(_p(bits), _dtype_code(bits), rows, cols, axis, block[0], block[1], x, y, _p(m),
+                                     _p(packed), _p(idx), _p(sb), cap)
+    if ns < 0:
+        raise ValueError("invalid arguments")
+    return packed, idx[:ns].copy(), sb[:ns].copy(), int(ns)
+
+
+def decode_blocked(packed, shape, fmt, meta, block, axis: int = ROWS, sp_index=None, sp_bits=None,
+                   out_dtype=np.uint16) -> np.ndarray:
+    x, y = parse_format(fmt)
+    rows, cols = shape
+    packed = np.ascontiguousarray(packed, dtype=np.uint8)
+    m = np.ascontiguousarray(meta, np.uint8)
+    if sp_index is None:
+        sp_index, sp_bits, cnt = np.zeros(1, np.int64), np.zeros(1, np.uint32), 0
+    else:
+        sp_index = np.ascontiguousarray(sp_index, np.int64)
+        sp_bits = np.ascontiguousarray(sp_bits, np.uint32)
+        cnt = sp_index.size
+    out = np.empty((rows, cols), dtype=out_dtype)
+    odt = BF16 if out.dtype == np.uint16 else F32
+    if lib().oracle_decode_blocked(_p(packed), rows, cols, axis, block[0], block[1], x, y, _p(m), _p(sp_index),
+                                   _p(sp_bits), cnt, _p(out), odt):
+        raise ValueError("invalid arguments")
     return out

@@ -447,3 +447,168 @@ int oracle_decode(const uint8_t *packed, int64_t rows, int64_t cols, int axis,
     }
     return 0;
 }
+
+/* ====================================================== block metadata */
+/* Blocks ("a tensor, a row, a column, a sub row or even a 2D
+ * tile") are block_rows x block_cols tiles of the row-major (rows, cols)
+ * tensor, block_rows | rows and block_cols | cols.  Block (i, j) owns
+ * metadata byte meta[i * (cols / block_cols) + j]. */
+int oracle_block_shape_ok(int64_t rows, int64_t cols, int64_t br, int64_t bc)
+{
+    if (rows < 0 || cols < 0 || br < 1 || bc < 1) return 0;
+    if (rows % br || cols % bc) return 0;
+    return 1;
+}
+
+static int64_t block_of(int64_t e, int64_t cols, int64_t br, int64_t bc)
+{
+    int64_t r = e / cols, c = e % cols;
+    return (r / br) * (cols / bc) + c / bc;
+}
+
+/* biased exponent (fp32 convention) of |v| rounded RTNE to y mantissa bits in
+ * its own binade, exponent range unbounded; <= 0 reported as 0 */
+static int exponent_after_rounding(uint32_t u, int y)
+{
+    double a = fabs(f32_value(u));
+    if (a == 0.0) return 0;
+    int e;
+    (void)frexp(a, &e);               /* a in [2^(e-1), 2^e) */
+    int E = e - 1;
+    double s = ldexp(a, y - E);       /* in [2^y, 2^(y+1)), exact */
+    double fl = floor(s), frac = s - fl;
+    double r = fl;
+    if (frac > 0.5 || (frac == 0.5 && fmod(fl, 2.0) != 0.0)) r += 1.0;
+    if (r >= ldexp(1.0, y + 1)) E += 1;   /* carry into the next binade */
+    int be = E + 127;
+    return be < 0 ? 0 : be;
+}
+
+/* Per-block metadata.  scheme 0 = maximum exponent before rounding (the
+ * largest 8-bit biased exponent field of a finite element);
+ * scheme 1 = after rounding to y mantissa bits.
+ * NaN/Inf are ignored; a block without finite elements gets 0; results are
+ * clamped to [0,254] (D4). */
+int oracle_block_max_exponent(const void *in, int dtype, int64_t rows, int64_t cols,
+                              int64_t br, int64_t bc, int y, int scheme, uint8_t *meta)
+{
+    if (!oracle_block_shape_ok(rows, cols, br, bc) || y < 0 || y > 23 || (scheme != 0 && scheme != 1)) return -1;
+    int64_t nb = (rows / br) * (cols / bc);
+    for (int64_t b = 0; b < nb; ++b) meta[b] = 0;
+    for (int64_t e = 0; e < rows * cols; ++e) {
+        uint32_t u = load_u32(in, dtype, e);
+        if (is_special(u)) continue;
+        int be = scheme == 0 ? (int)((u >> 23) & 0xFFu) : exponent_after_rounding(u, y);
+        if (be > 254) be = 254;
+        int64_t b = block_of(e, cols, br, bc);
+        if (be > meta[b]) meta[b] = (uint8_t)be;
+    }
+    return 0;
+}
+
+/* grids for every metadata value, built on first use */
+typedef struct { grid g[255]; int built[255]; int x, y; } grid_cache;
+
+static const grid *cache_get(grid_cache *gc, int e_max)
+{
+    if (!gc->built[e_max]) {
+        if (grid_build(&gc->g[e_max], gc->x, gc->y, e_max)) return NULL;
+        gc->built[e_max] = 1;
+    }
+    return &gc->g[e_max];
+}
+
+static void cache_free(grid_cache *gc)
+{
+    for (int i = 0; i < 255; ++i)
+        if (gc->built[i]) grid_free(&gc->g[i]);
+}
+
+static int meta_at(const uint8_t *meta, int64_t e, int64_t cols, int64_t br, int64_t bc)
+{
+    int m = meta[block_of(e, cols, br, bc)];
+    return m > 254 ? 254 : m;
+}
+
+/* Emulation with block metadata: element e is quantized on the grid of its
+ * block's e_max. */
+int oracle_quantize_blocked(const void *in, void *out, int dtype, int64_t rows, int64_t cols,
+                            int64_t br, int64_t bc, int x, int y, const uint8_t *meta)
+{
+    if (!oracle_format_valid(x, y, 0) || !oracle_block_shape_ok(rows, cols, br, bc)) return -1;
+    grid_cache *gc = (grid_cache *)calloc(1, sizeof(grid_cache));
+    if (!gc) return -1;
+    gc->x = x; gc->y = y;
+    for (int64_t e = 0; e < rows * cols; ++e) {
+        uint32_t u = load_u32(in, dtype, e);
+        if (is_special(u)) {
+            if (dtype == ORACLE_BF16) ((uint16_t *)out)[e] = ((const uint16_t *)in)[e];
+            else ((uint32_t *)out)[e] = u;
+            continue;
+        }
+        int em = meta_at(meta, e, cols, br, bc);
+        const grid *g = cache_get(gc, em);
+        uint32_t code = encode_finite(g, u);
+        store_value(out, dtype, e, oracle_code_value(code, x, y, em));
+    }
+    cache_free(gc);
+    free(gc);
+    return 0;
+}
+
+int64_t oracle_encode_blocked(const void *in, int dtype, int64_t rows, int64_t cols, int axis,
+                              int64_t br, int64_t bc, int x, int y, const uint8_t *meta, uint8_t *packed,
+                              int64_t *sp_index, uint32_t *sp_bits, int64_t sp_capacity)
+{
+    if (!oracle_format_valid(x, y, 0) || !oracle_shape_ok(rows, cols, axis) ||
+        !oracle_block_shape_ok(rows, cols, br, bc) || 1 + x + y > ORACLE_MAX_PACK_K) return -1;
+    int64_t n = rows * cols;
+    uint16_t *codes = (uint16_t *)malloc(sizeof(uint16_t) * (size_t)(n ? n : 1));
+    grid_cache *gc = (grid_cache *)calloc(1, sizeof(grid_cache));
+    if (!codes || !gc) { free(codes); free(gc); return -1; }
+    gc->x = x; gc->y = y;
+    int64_t ns = 0;
+    for (int64_t e = 0; e < n; ++e) {
+        uint32_t u = load_u32(in, dtype, e);
+        if (is_special(u)) {
+            codes[e] = 0;
+            if (ns < sp_capacity) { sp_index[ns] = e; sp_bits[ns] = u; }
+            ++ns;
+        } else {
+            codes[e] = (uint16_t)encode_finite(cache_get(gc, meta_at(meta, e, cols, br, bc)), u);
+        }
+    }
+    cache_free(gc);
+    free(gc);
+    oracle_pack(codes, rows, cols, axis, 1 + x + y, packed);
+    free(codes);
+    return ns;
+}
+
+int oracle_decode_blocked(const uint8_t *packed, int64_t rows, int64_t cols, int axis,
+                          int64_t br, int64_t bc, int x, int y, const uint8_t *meta,
+                          const int64_t *sp_index, const uint32_t *sp_bits, int64_t sp_count,
+                          void *out, int out_dtype)
+{
+    if (!oracle_format_valid(x, y, 0) || !oracle_shape_ok(rows, cols, axis) ||
+        !oracle_block_shape_ok(rows, cols, br, bc) || 1 + x + y > ORACLE_MAX_PACK_K) return -1;
+    int64_t n = rows * cols;
+    uint16_t *codes = (uint16_t *)malloc(sizeof(uint16_t) * (size_t)(n ? n : 1));
+    if (!codes) return -1;
+    oracle_unpack(packed, rows, cols, axis, 1 + x + y, codes);
+    for (int64_t e = 0; e < n; ++e)
+        store_value(out, out_dtype, e, oracle_code_value(codes[e], x, y, meta_at(meta, e, cols, br, bc)));
+    free(codes);
+    for (int64_t j = 0; j < sp_count; ++j) {
+        int64_t i = sp_index[j];
+        uint32_t u = sp_bits[j];
+        if (out_dtype == ORACLE_BF16) {
+            uint16_t b = (uint16_t)(u >> 16);
+            if ((u & 0x7FFFFFu) != 0 && (b & 0x7Fu) == 0) b |= 0x40u;
+            ((uint16_t *)out)[i] = b;
+        } else {
+            ((uint32_t *)out)[i] = u;
+        }
+    }
+    return 0;
+}

@@ -38,6 +38,18 @@ int oracle_decode(const uint8_t *packed, int64_t rows, int64_t cols, int axis,
                   int x, int y, int e_max,
                   const int64_t *sp_index, const uint32_t *sp_bits, int64_t sp_count,
                   void *out, int out_dtype);
+int oracle_block_shape_ok(int64_t rows, int64_t cols, int64_t br, int64_t bc);
+int oracle_block_max_exponent(const void *in, int dtype, int64_t rows, int64_t cols,
+                              int64_t br, int64_t bc, int y, int scheme, uint8_t *meta);
+int oracle_quantize_blocked(const void *in, void *out, int dtype, int64_t rows, int64_t cols,
+                            int64_t br, int64_t bc, int x, int y, const uint8_t *meta);
+int64_t oracle_encode_blocked(const void *in, int dtype, int64_t rows, int64_t cols, int axis,
+                              int64_t br, int64_t bc, int x, int y, const uint8_t *meta, uint8_t *packed,
+                              int64_t *sp_index, uint32_t *sp_bits, int64_t sp_capacity);
+int oracle_decode_blocked(const uint8_t *packed, int64_t rows, int64_t cols, int axis,
+                          int64_t br, int64_t bc, int x, int y, const uint8_t *meta,
+                          const int64_t *sp_index, const uint32_t *sp_bits, int64_t sp_count,
+                          void *out, int out_dtype);
 #ifdef __cplusplus
 }
 #endif
