@@ -168,6 +168,48 @@ exmy_status exmy_decode(const uint8_t *packed, int64_t rows, int64_t cols, int a
 int exmy_debug_force_generic(int on);
 int exmy_debug_hist_mode(int mode);
 
+/* ------------------------------------------------------- block metadata */
+/* Blocks ("a tensor, a row, a column, a sub row or even a 2D
+ * tile"; per-row metadata is the paper's quality recipe): the
+ * (rows, cols) row-major tensor is tiled by block_rows x block_cols blocks,
+ * block_rows | rows and block_cols | cols (else EXMY_E_SHAPE).  Block (i, j)
+ * owns metadata byte meta[i * (cols / block_cols) + j] (device memory).
+ *   tensor: (rows, cols)   row: (1, cols)   column: (rows, 1)
+ *   sub-row of length L: (1, L)   2-D tile: (r, c)
+ * Every element is coded exactly as the per-tensor calls would code it with
+ * its block's e_max.  The fast kernels need block_cols % 4 == 0 (ROWS
+ * encode), % 8 (COLS, and ROWS decode to bf16) and block_rows == 1 or
+ * % 8 == 0; other shapes take a scalar kernel with identical results. */
+typedef enum { EXMY_SCHEME_MAX_BEFORE = 0, EXMY_SCHEME_MAX_AFTER = 1 } exmy_scheme;
+
+/* Per-block metadata.  MAX_BEFORE: the largest 8-bit
+ * biased exponent field of a finite element of the block (the maximum
+ * exponent before rounding).  MAX_AFTER: the biased exponent of the block's
+ * largest magnitude after rounding it RTNE to y mantissa bits in its own
+ * binade (so 3.9 with y=1 gives 129, "it always rounds up to 4.0").  NaN/Inf
+ * are ignored; a block with no finite non-zero element gets 0; results are
+ * clamped to 254.  One warp per block: use exmy_exponent_histogram for
+ * whole-tensor metadata. */
+exmy_status exmy_block_max_exponent(const void *in, int dtype, int64_t rows, int64_t cols,
+                                    int64_t block_rows, int64_t block_cols, int y, int scheme,
+                                    uint8_t *meta, void *stream);
+
+/* exmy_quantize / exmy_encode / exmy_decode with block metadata; arguments
+ * as the per-tensor calls plus the block shape. */
+exmy_status exmy_quantize_blocked(const void *in, void *out, int dtype, int64_t rows, int64_t cols,
+                                  int64_t block_rows, int64_t block_cols, int x, int y,
+                                  const uint8_t *meta, void *stream);
+exmy_status exmy_encode_blocked(const void *in, int dtype, int64_t rows, int64_t cols, int axis,
+                                int64_t block_rows, int64_t block_cols, int x, int y,
+                                const uint8_t *meta, uint8_t *packed, int64_t *sp_index,
+                                uint32_t *sp_bits, uint64_t *sp_count, int64_t sp_capacity,
+                                void *stream);
+exmy_status exmy_decode_blocked(const uint8_t *packed, int64_t rows, int64_t cols, int axis,
+                                int64_t block_rows, int64_t block_cols, int x, int y,
+                                const uint8_t *meta, const int64_t *sp_index,
+                                const uint32_t *sp_bits, const uint64_t *sp_count,
+                                int64_t sp_capacity, void *out, int out_dtype, void *stream);
+
 /* ------------------------------------------------ host-buffer conveniences */
 
 /* End-to-end encode of a HOST tensor (pinned memory recommended): H2D copy

@@ -466,8 +466,11 @@ static int64_t block_of(int64_t e, int64_t cols, int64_t br, int64_t bc)
     return (r / br) * (cols / bc) + c / bc;
 }
 
-/* biased exponent (fp32 convention) of |v| rounded RTNE to y mantissa bits in
- * its own binade, exponent range unbounded; <= 0 reported as 0 */
+/* biased exponent (fp32 convention) of |v| rounded to nearest with y mantissa
+ * bits in its own binade, exponent range unbounded; <= 0 reported as 0
+ * (P:225-226).  Ties go to the representation whose last kept bit is 0
+ * (RTNE "extended ... to arbitrary number of mantissa bits"): the
+ * mantissa LSB for y >= 1, the exponent LSB for y = 0 (reading D22). */
 static int exponent_after_rounding(uint32_t u, int y)
 {
     double a = fabs(f32_value(u));
@@ -478,7 +481,8 @@ static int exponent_after_rounding(uint32_t u, int y)
     double s = ldexp(a, y - E);       /* in [2^y, 2^(y+1)), exact */
     double fl = floor(s), frac = s - fl;
     double r = fl;
-    if (frac > 0.5 || (frac == 0.5 && fmod(fl, 2.0) != 0.0)) r += 1.0;
+    int lsb_odd = (y >= 1) ? (fmod(fl, 2.0) != 0.0) : (((E + 127) & 1) != 0);
+    if (frac > 0.5 || (frac == 0.5 && lsb_odd)) r += 1.0;
     if (r >= ldexp(1.0, y + 1)) E += 1;   /* carry into the next binade */
     int be = E + 127;
     return be < 0 ? 0 : be;

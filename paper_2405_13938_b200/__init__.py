@@ -62,6 +62,10 @@ def _load():
         "exmy_quantize": ([vp, vp, i32, i64, i32, i32, vp, vp], i32),
         "exmy_encode": ([vp, i32, i64, i64, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp], i32),
         "exmy_decode": ([vp, i64, i64, i32, i32, i32, vp, vp, vp, vp, i64, vp, i32, vp], i32),
+        "exmy_block_max_exponent": ([vp, i32, i64, i64, i64, i64, i32, i32, vp, vp], i32),
+        "exmy_quantize_blocked": ([vp, vp, i32, i64, i64, i64, i64, i32, i32, vp, vp], i32),
+        "exmy_encode_blocked": ([vp, i32, i64, i64, i32, i64, i64, i32, i32, vp, vp, vp, vp, vp, i64, vp], i32),
+        "exmy_decode_blocked": ([vp, i64, i64, i32, i64, i64, i32, i32, vp, vp, vp, vp, i64, vp, i32, vp], i32),
         "exmy_encode_host": ([vp, i32, i64, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, i64, vp, vp, vp], i32),
         "exmy_decode_host": ([vp, i64, i64, i32, i32, i32, vp, vp, vp, vp, i64, vp, vp, i32, vp, vp], i32),
     }
@@ -78,7 +82,8 @@ EXPORTED = ["exmy_version", "exmy_status_string", "exmy_format_valid", "exmy_pac
             "exmy_bias_from_emax", "exmy_emax_from_bias", "exmy_emax_from_histogram_host", "exmy_choose_x",
             "exmy_debug_force_generic", "exmy_debug_hist_mode", "exmy_exponent_histogram",
             "exmy_emax_from_histogram", "exmy_quantize", "exmy_encode", "exmy_decode", "exmy_encode_host",
-            "exmy_decode_host"]
+            "exmy_decode_host", "exmy_block_max_exponent", "exmy_quantize_blocked", "exmy_encode_blocked",
+            "exmy_decode_blocked"]
 
 
 def lib():
@@ -259,6 +264,7 @@ class Packed:
     y: int
     axis: int
     dtype: torch.dtype        # source dtype
+    block: tuple | None = None   # (block_rows, block_cols) when meta is per block
 
     @property
     def k(self) -> int:
@@ -325,9 +331,86 @@ def decode(p: Packed, dtype: torch.dtype | None = None, out: torch.Tensor | None
     if out is None:
         out = torch.empty(p.shape, dtype=dtype, device=dev)
     cap = p.sp_index.numel() if p.sp_count is not None else 0
+    if p.block is not None:
+        _check(_lib.exmy_decode_blocked(_ptr(p.data), R, C, p.axis, p.block[0], p.block[1], p.x, p.y, _ptr(p.meta),
+                                        _ptr(p.sp_index), _ptr(p.sp_bits), _ptr(p.sp_count), cap, _ptr(out),
+                                        _dtype_code(dtype), _stream(dev)), "decode_blocked")
+        return out
     _check(_lib.exmy_decode(_ptr(p.data), R, C, p.axis, p.x, p.y, _ptr(p.meta), _ptr(p.sp_index), _ptr(p.sp_bits),
                             _ptr(p.sp_count), cap, _ptr(out), _dtype_code(dtype), _stream(dev)), "decode")
     return out
+
+
+# ------------------------------------------------------------ block metadata
+SCHEMES = {"before": 0, "max-before": 0, "after": 1, "max-after": 1, 0: 0, 1: 1}
+
+
+def block_shape(shape, block):
+    """'tensor' | 'row' | 'col' | ('subrow', L) | (br, bc) -> (br, bc) (P:230-241)."""
+    R, C = _as_2d_shape(tuple(shape))
+    if block == "tensor":
+        return R, C
+    if block == "row":
+        return 1, C
+    if block in ("col", "column"):
+        return R, 1
+    if isinstance(block, tuple) and len(block) == 2 and block[0] == "subrow":
+        return 1, int(block[1])
+    return int(block[0]), int(block[1])
+
+
+def block_max_exponent(t: torch.Tensor, block, y: int = 0, scheme="before", out: torch.Tensor | None = None):
+    """Per-block metadata: max biased exponent before / after rounding to y
+    mantissa bits.  Returns uint8 (R/br, C/bc)."""
+    _require_cuda(t)
+    t = t.contiguous()
+    R, C = _as_2d(t)
+    br, bc = block_shape(t.shape, block)
+    if out is None:
+        out = torch.empty((R // br if br else 0, C // bc if bc else 0), dtype=torch.uint8, device=t.device)
+    _check(_lib.exmy_block_max_exponent(_ptr(t), _dtype_code(t.dtype), R, C, br, bc, int(y), SCHEMES[scheme],
+                                        _ptr(out), _stream(t.device)), "block_max_exponent")
+    return out
+
+
+def quantize_blocked(t: torch.Tensor, fmt, meta: torch.Tensor, block, out: torch.Tensor | None = None):
+    _require_cuda(t)
+    x, y = parse_format(fmt)
+    t = t.contiguous()
+    R, C = _as_2d(t)
+    br, bc = block_shape(t.shape, block)
+    if out is None:
+        out = torch.empty_like(t)
+    _check(_lib.exmy_quantize_blocked(_ptr(t), _ptr(out), _dtype_code(t.dtype), R, C, br, bc, x, y,
+                                      _ptr(meta.contiguous()), _stream(t.device)), "quantize_blocked")
+    return out
+
+
+def encode_blocked(t: torch.Tensor, fmt, meta: torch.Tensor | None, block, axis="rows", scheme="before",
+                   specials_capacity: int = 4096, out: torch.Tensor | None = None) -> Packed:
+    """Encode with one metadata byte per block; meta=None computes it with
+    the given scheme."""
+    _require_cuda(t)
+    x, y = parse_format(fmt)
+    ax = _AXES[axis]
+    t = t.contiguous()
+    R, C = _as_2d(t)
+    br, bc = block_shape(t.shape, block)
+    dev = t.device
+    if meta is None:
+        meta = block_max_exponent(t, (br, bc), y, scheme)
+    meta = meta.contiguous()
+    n = R * C
+    k = 1 + x + y
+    if out is None:
+        out = torch.empty(n * k // 8 if n % 8 == 0 else 0, dtype=torch.uint8, device=dev)
+    cap = int(specials_capacity)
+    spi = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
+    spb = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    spc = torch.zeros(1, dtype=torch.int64, device=dev)
+    _check(_lib.exmy_encode_blocked(_ptr(t), _dtype_code(t.dtype), R, C, ax, br, bc, x, y, _ptr(meta), _ptr(out),
+                                    _ptr(spi), _ptr(spb), _ptr(spc), cap, _stream(dev)), "encode_blocked")
+    return Packed(out, meta, spi, spb, spc, tuple(t.shape), x, y, ax, t.dtype, (br, bc))
 
 
 def decode_raw(data: torch.Tensor, rows: int, cols: int, fmt, meta, axis="rows", dtype=torch.bfloat16,

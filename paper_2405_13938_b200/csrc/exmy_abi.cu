@@ -34,6 +34,10 @@ exmy_status check_layout(int64_t rows, int64_t cols, int axis, int64_t *n) {
     return EXMY_OK;
 }
 
+bool block_ok(int64_t rows, int64_t cols, int64_t br, int64_t bc) {
+    return br >= 1 && bc >= 1 && rows % br == 0 && cols % bc == 0;
+}
+
 }  // namespace
 
 // ====================================================================== ABI
@@ -187,6 +191,77 @@ exmy_status exmy_decode(const uint8_t *packed, int64_t rows, int64_t cols, int a
     auto *po = static_cast<uint8_t *>(out);
     const bool obf = out_dtype == EXMY_BF16;
     s = launch_decode(packed, rows, cols, axis, x, y, meta, po, obf, st);
+    if (s != EXMY_OK) return s;
+    if (sp_count && sp_index && sp_bits && sp_capacity > 0)
+        s = launch_specials_scatter(sp_index, sp_bits, reinterpret_cast<const unsigned long long *>(sp_count),
+                                    sp_capacity, po, obf, st);
+    return s;
+}
+
+exmy_status exmy_block_max_exponent(const void *in, int dtype, int64_t rows, int64_t cols, int64_t block_rows,
+                                    int64_t block_cols, int y, int scheme, uint8_t *meta, void *stream) {
+    if (dtype != EXMY_F32 && dtype != EXMY_BF16) return EXMY_E_DTYPE;
+    if (rows < 0 || cols < 0 || !block_ok(rows, cols, block_rows, block_cols)) return EXMY_E_SHAPE;
+    if (y < 0 || y > 23 || (scheme != EXMY_SCHEME_MAX_BEFORE && scheme != EXMY_SCHEME_MAX_AFTER)) return EXMY_E_ARG;
+    if (rows == 0 || cols == 0) return EXMY_OK;
+    if (!in || !meta) return EXMY_E_ARG;
+    return launch_block_max(static_cast<const uint8_t *>(in), dtype == EXMY_BF16, rows, cols, block_rows, block_cols,
+                            y, scheme, meta, S(stream));
+}
+
+exmy_status exmy_quantize_blocked(const void *in, void *out, int dtype, int64_t rows, int64_t cols,
+                                  int64_t block_rows, int64_t block_cols, int x, int y, const uint8_t *meta,
+                                  void *stream) {
+    if (dtype != EXMY_F32 && dtype != EXMY_BF16) return EXMY_E_DTYPE;
+    if (!fmt_ok(x, y)) return EXMY_E_FORMAT;
+    if (rows < 0 || cols < 0 || !block_ok(rows, cols, block_rows, block_cols)) return EXMY_E_SHAPE;
+    if (rows == 0 || cols == 0) return EXMY_OK;
+    if (!in || !out || !meta) return EXMY_E_ARG;
+    return launch_quantize_blocked(static_cast<const uint8_t *>(in), static_cast<uint8_t *>(out), dtype == EXMY_BF16,
+                                   rows, cols, block_rows, block_cols, x, y, meta, S(stream));
+}
+
+exmy_status exmy_encode_blocked(const void *in, int dtype, int64_t rows, int64_t cols, int axis, int64_t block_rows,
+                                int64_t block_cols, int x, int y, const uint8_t *meta, uint8_t *packed,
+                                int64_t *sp_index, uint32_t *sp_bits, uint64_t *sp_count, int64_t sp_capacity,
+                                void *stream) {
+    if (dtype != EXMY_F32 && dtype != EXMY_BF16) return EXMY_E_DTYPE;
+    if (!fmt_ok(x, y)) return EXMY_E_FORMAT;
+    int64_t n = 0;
+    exmy_status s = check_layout(rows, cols, axis, &n);
+    if (s != EXMY_OK) return s;
+    if (!block_ok(rows, cols, block_rows, block_cols)) return EXMY_E_SHAPE;
+    if (sp_capacity < 0) return EXMY_E_CAPACITY;
+    if (sp_capacity > 0 && (!sp_index || !sp_bits)) return EXMY_E_ARG;
+    cudaStream_t st = S(stream);
+    auto *spc = reinterpret_cast<unsigned long long *>(sp_count);
+    if (spc && cudaMemsetAsync(spc, 0, sizeof(unsigned long long), st) != cudaSuccess) return EXMY_E_CUDA;
+    if (n == 0) return EXMY_OK;
+    if (!in || !packed || !meta) return EXMY_E_ARG;
+    s = launch_encode_blocked(static_cast<const uint8_t *>(in), dtype == EXMY_BF16, rows, cols, axis, block_rows,
+                              block_cols, x, y, meta, packed, sp_index, sp_bits, spc, sp_capacity, st);
+    if (s != EXMY_OK) return s;
+    if (spc && sp_capacity > 1) s = launch_specials_sort(sp_index, sp_bits, spc, sp_capacity, st);
+    return s;
+}
+
+exmy_status exmy_decode_blocked(const uint8_t *packed, int64_t rows, int64_t cols, int axis, int64_t block_rows,
+                                int64_t block_cols, int x, int y, const uint8_t *meta, const int64_t *sp_index,
+                                const uint32_t *sp_bits, const uint64_t *sp_count, int64_t sp_capacity, void *out,
+                                int out_dtype, void *stream) {
+    if (out_dtype != EXMY_F32 && out_dtype != EXMY_BF16) return EXMY_E_DTYPE;
+    if (!fmt_ok(x, y)) return EXMY_E_FORMAT;
+    int64_t n = 0;
+    exmy_status s = check_layout(rows, cols, axis, &n);
+    if (s != EXMY_OK) return s;
+    if (!block_ok(rows, cols, block_rows, block_cols)) return EXMY_E_SHAPE;
+    if (sp_capacity < 0) return EXMY_E_CAPACITY;
+    if (n == 0) return EXMY_OK;
+    if (!packed || !out || !meta) return EXMY_E_ARG;
+    cudaStream_t st = S(stream);
+    auto *po = static_cast<uint8_t *>(out);
+    const bool obf = out_dtype == EXMY_BF16;
+    s = launch_decode_blocked(packed, rows, cols, axis, block_rows, block_cols, x, y, meta, po, obf, st);
     if (s != EXMY_OK) return s;
     if (sp_count && sp_index && sp_bits && sp_capacity > 0)
         s = launch_specials_scatter(sp_index, sp_bits, reinterpret_cast<const unsigned long long *>(sp_count),

@@ -1,0 +1,602 @@
+// exmy_blocked.cuh -- block metadata:
+// per-block maximum exponent (before / after rounding) and quantize /
+// encode / decode where every (block_rows x block_cols) tile of the tensor
+// carries its own metadata byte.  The per-element arithmetic is that of
+// exmy_fast.cuh; only the quantities that depend on e_max (the subnormal
+// clamp, the exponent offset, the decode scale) become per row / per group.
+#pragma once
+#include "exmy_fast.cuh"
+
+namespace exmy {
+
+// block (i, j) of a (R, C) tensor tiled by (br x bc) owns meta[i * nbc + j]
+struct MetaMap {
+    const uint8_t *meta;
+    int64_t br, bc, nbc;
+};
+
+__device__ __forceinline__ int meta_at(const MetaMap &M, int64_t r, int64_t c) {
+    const int e = __ldg(M.meta + (r / M.br) * M.nbc + c / M.bc);
+    return e > 254 ? 254 : e;
+}
+
+__device__ __forceinline__ Fmt fmt_of(int x, int y, int e) {
+    Fmt F;
+    F.x = x; F.y = y; F.e_max = e;
+    F.top = (1 << x) - 1;
+    F.o = e - F.top;
+    F.M = (1u << (x + y)) - 1u;
+    return F;
+}
+
+// ------------------------------------------------------- per-row params
+// The e_max-dependent constants of the encode fast paths (see FastP).
+struct RowP {
+    uint32_t lo2, k3, par2;     // bf16 lanes
+    uint32_t lo, k3f, parf;     // fp32
+    bool ok;                    // fast preconditions hold for this e_max
+};
+
+template <bool SIMD>
+__device__ __forceinline__ RowP make_rowp(int e, int x, int y) {
+    RowP R;
+    const int o1 = e - ((1 << x) - 1) + 1;   // o + 1
+    R.ok = (o1 >= 1) && (e <= (SIMD ? 246 : 230) + y);
+    const uint32_t u1 = (uint32_t)o1;
+    if (SIMD) {
+        R.lo2 = u1 * (0x80u * 0x00010001u);
+        R.k3 = u1 * ((1u << y) * 0x00010001u);
+        R.par2 = (u1 & 1u) * 0x00010001u;
+        R.lo = R.k3f = R.parf = 0;
+    } else {
+        R.lo = u1 << 23;
+        R.k3f = u1 << y;
+        R.parf = u1 & 1u;
+        R.lo2 = R.k3 = R.par2 = 0;
+    }
+    return R;
+}
+
+template <int K, bool Y0>
+__device__ __forceinline__ uint32_t enc_pair_bf16_r(uint32_t w, const FastP &P, const RowP &R, uint32_t &amax) {
+    const uint32_t a2 = w & 0x7FFF7FFFu;
+    const uint32_t ecl = vmax_u16x2(w & 0x7F807F80u, R.lo2);
+    uint32_t c, t;
+    if (Y0) {
+        t = ecl >> 7;
+        c = ecl + P.k2 + ((t ^ R.par2) & 0x00010001u);
+    } else {
+        t = ecl >> P.sh_b;
+        c = ecl + P.k2;
+    }
+    const uint32_t s = hadd2_bf16(a2, c);
+    uint32_t code = s - c + t - R.k3;
+    code = vmin_u16x2(code, P.m2);
+    code |= (w >> (16 - K)) & ((1u << (K - 1)) * 0x00010001u);
+    amax = vmax_u16x2(amax, a2);
+    return code;
+}
+
+template <int K, bool Y0>
+__device__ __forceinline__ uint32_t enc_f32_fast_r(uint32_t u, const FastP &P, const RowP &R, uint32_t &amax) {
+    const uint32_t a = u & 0x7FFFFFFFu;
+    const uint32_t ecl = max(u & 0x7F800000u, R.lo);
+    uint32_t c = ecl + P.k2f;
+    if (Y0) c += ((ecl >> 23) ^ R.parf) & 1u;
+    const uint32_t s = __float_as_uint(__fadd_rn(__uint_as_float(a), __uint_as_float(c)));
+    uint32_t code = s - c + (ecl >> P.sh_f) - R.k3f;
+    code = min(code, (1u << (K - 1)) - 1u);
+    code |= (u >> (32 - K)) & (1u << (K - 1));
+    amax = max(amax, a);
+    return code;
+}
+
+template <int K, bool BF16, int MODE, int NW>
+__device__ __forceinline__ void vec_codes_r(const uint32_t (&w)[NW], uint32_t (&cp)[BF16 ? NW : NW / 2],
+                                            const FastP &P, const RowP &R, uint32_t &amax) {
+    constexpr int NP = BF16 ? NW : NW / 2;
+    if constexpr (MODE == ENC_SIMD || MODE == ENC_SIMD_Y0) {
+#pragma unroll
+        for (int t = 0; t < NP; ++t) cp[t] = enc_pair_bf16_r<K, MODE == ENC_SIMD_Y0>(w[t], P, R, amax);
+    } else {
+#pragma unroll
+        for (int t = 0; t < NP; ++t) {
+            const uint32_t lo = enc_f32_fast_r<K, MODE == ENC_F32_Y0>(wordvec_elem<BF16, NW>(w, 2 * t), P, R, amax);
+            const uint32_t hi = enc_f32_fast_r<K, MODE == ENC_F32_Y0>(wordvec_elem<BF16, NW>(w, 2 * t + 1), P, R, amax);
+            cp[t] = lo | (hi << 16);
+        }
+    }
+}
+
+// ---------------------------------------------------- generic containers
+// one container on the integer path, metadata looked up per element
+template <bool BF16, int K>
+__device__ __noinline__ void enc_container_generic_blk(const uint8_t *__restrict__ in, int64_t C, int64_t idx, int axis,
+                                                       int x, int y, const MetaMap M, uint8_t *packed,
+                                                       const SegOffsets so, int64_t *spi, uint32_t *spb,
+                                                       unsigned long long *spc, int64_t cap) {
+    uint32_t c[8];
+    int64_t e[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        e[i] = lane_elem(idx, i, C, axis);
+        const Fmt F = fmt_of(x, y, meta_at(M, e[i] / C, e[i] % C));
+        c[i] = enc_elem(load_elem_scalar<BF16>(in, e[i]), F, e[i], spi, spb, spc, cap);
+    }
+    int hi = K;
+#pragma unroll
+    for (int s = 0; s < seg_count(K); ++s) {
+        const int w = seg_width(K, s), lo = hi - w;
+        uint8_t *seg = packed + so.off[s];
+        if (w == 8) {
+            for (int i = 0; i < 8; ++i) seg[e[i]] = (uint8_t)(c[i] >> lo);
+        } else {
+            uint32_t cont = 0;
+            for (int i = 0; i < 8; ++i) cont |= ((c[i] >> lo) & ((1u << w) - 1u)) << (w * i);
+            for (int b = 0; b < w; ++b) seg[idx * w + b] = (uint8_t)(cont >> (8 * b));
+        }
+        hi = lo;
+    }
+}
+
+template <bool BF16, int K>
+__global__ void k_encode_generic_blk(const uint8_t *__restrict__ in, int64_t C, int64_t ncont, int axis, int x, int y,
+                                     MetaMap M, uint8_t *__restrict__ packed, SegOffsets so, int64_t *spi,
+                                     uint32_t *spb, unsigned long long *spc, int64_t cap) {
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < ncont;
+         idx += (int64_t)gridDim.x * blockDim.x)
+        enc_container_generic_blk<BF16, K>(in, C, idx, axis, x, y, M, packed, so, spi, spb, spc, cap);
+}
+
+// ---------------------------------------------------- encode ROWS (blocked)
+// Same tiles as k_enc_rows_fast (8 rows x 4 columns).  Host guarantees
+// bc % 4 == 0 (the 4 columns share a block column) and br == 1 or br % 8 == 0.
+template <int K, bool BF16, int MODE>
+__global__ void __launch_bounds__(256, BF16 ? 3 : 2) k_enc_rows_blk(const uint8_t *__restrict__ in, int64_t R, int64_t C,
+                                                                   int x, int y, MetaMap M,
+                                                                   uint8_t *__restrict__ packed, SegOffsets so,
+                                                                   int64_t *spi, uint32_t *spb,
+                                                                   unsigned long long *spc, int64_t cap,
+                                                                   int force_generic) {
+    using EL = Elem<BF16>;
+    constexpr int NW = BF16 ? 2 : 4;
+    constexpr bool SIMD = (MODE == ENC_SIMD || MODE == ENC_SIMD_Y0);
+    const FastP P = make_fast(fmt_of(x, y, 0), BF16, 1);   // e_max-independent constants only
+    const int64_t CV = C / 4, G = R / 8;
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= CV) return;
+    const int64_t c0 = j * 4;
+    const uint8_t *mcol = M.meta + c0 / M.bc;      // block column of this thread
+    const uint8_t *src = in + c0 * EL::ES;
+    const int64_t rstride = C * EL::ES;
+    for (int64_t g = blockIdx.y; g < G; g += gridDim.y) {
+        uint32_t w[8][NW];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) load4<BF16>(src + (8 * g + i) * rstride, w[i]);
+        bool ok = !force_generic;
+        uint32_t cp[8][2];
+        uint32_t amax = 0;
+        if (M.br == 1) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                int e = __ldg(mcol + (8 * g + i) * M.nbc);
+                const RowP Rp = make_rowp<SIMD>(e > 254 ? 254 : e, x, y);
+                ok = ok && Rp.ok;
+                vec_codes_r<K, BF16, MODE, NW>(w[i], cp[i], P, Rp, amax);
+            }
+        } else {
+            int e = __ldg(mcol + ((8 * g) / M.br) * M.nbc);
+            const RowP Rp = make_rowp<SIMD>(e > 254 ? 254 : e, x, y);
+            ok = ok && Rp.ok;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) vec_codes_r<K, BF16, MODE, NW>(w[i], cp[i], P, Rp, amax);
+        }
+        if (ok && !amax_special<BF16, MODE>(amax, P)) {
+            uint32_t RL[1][8], RH[1][8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                RL[0][i] = prmt(cp[i][0], cp[i][1], 0x6420);
+                RH[0][i] = (K == 9) ? prmt(cp[i][0] >> 1, cp[i][1] >> 1, 0x6420) : 0u;
+            }
+            rows_fast_store<K, 1, 0>(RL, RH, packed, so, g, C, c0);
+        } else {
+            for (int v = 0; v < 4; ++v)
+                enc_container_generic_blk<BF16, K>(in, C, g * C + c0 + v, 0, x, y, M, packed, so, spi, spb, spc, cap);
+        }
+    }
+}
+
+// ---------------------------------------------------- encode COLS (blocked)
+// groups of 8 consecutive elements of one row; host guarantees bc % 8 == 0.
+// Row of group q: q / gpr, computed with an fp64 reciprocal and corrected.
+__device__ __forceinline__ int64_t div_rcp(int64_t q, int64_t d, double inv) {
+    int64_t r = (int64_t)((double)q * inv);
+    if (r * d > q) --r;
+    else if ((r + 1) * d <= q) ++r;
+    return r;
+}
+
+template <int K, bool BF16, int MODE>
+__global__ void __launch_bounds__(256) k_enc_cols_blk(const uint8_t *__restrict__ in, int64_t n, int64_t C, int x,
+                                                      int y, MetaMap M, uint8_t *__restrict__ packed, SegOffsets so,
+                                                      int64_t *spi, uint32_t *spb, unsigned long long *spc,
+                                                      int64_t cap, int force_generic) {
+    using EL = Elem<BF16>;
+    constexpr int NV = BF16 ? 1 : 2;
+    constexpr int NP = EL::V / 2;
+    constexpr bool SIMD = (MODE == ENC_SIMD || MODE == ENC_SIMD_Y0);
+    const FastP P = make_fast(fmt_of(x, y, 0), BF16, 1);
+    const int64_t NG = n / 8, gpr = C / 8;
+    const double inv = 1.0 / (double)gpr;
+    const int lane = threadIdx.x & 31;
+    const int64_t step = (int64_t)gridDim.x * (blockDim.x >> 5) * 128;
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    for (int64_t base = gw * 128; base < NG; base += step) {
+        uint4 r[4][NV];
+        uint32_t cp[4][4];
+        uint32_t amax = 0;
+        bool ok = !force_generic;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t q = base + 32 * u + lane;
+            const bool in_range = q < NG;
+#pragma unroll
+            for (int t = 0; t < NV; ++t)
+                r[u][t] = in_range ? ldg_nc_v4(in + q * 8 * EL::ES + 16 * t) : make_uint4(0, 0, 0, 0);
+            int e = 0;
+            if (in_range) {
+                const int64_t row = div_rcp(q, gpr, inv);
+                e = meta_at(M, row, (q - row * gpr) * 8);
+            }
+            const RowP Rp = make_rowp<SIMD>(e, x, y);
+            ok = ok && (Rp.ok || !in_range);
+#pragma unroll
+            for (int t = 0; t < NV; ++t) {
+                uint32_t c2[NP];
+                const uint32_t ww[4] = {r[u][t].x, r[u][t].y, r[u][t].z, r[u][t].w};
+                vec_codes_r<K, BF16, MODE, 4>(ww, c2, P, Rp, amax);
+#pragma unroll
+                for (int p = 0; p < NP; ++p) cp[u][t * NP + p] = c2[p];
+            }
+        }
+        if (ok && !amax_special<BF16, MODE>(amax, P)) {
+            uint32_t RL[8], RH[8];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const uint32_t y01 = prmt(cp[0][t], cp[1][t], 0x6420), y23 = prmt(cp[2][t], cp[3][t], 0x6420);
+                RL[2 * t] = prmt(y01, y23, 0x6420);
+                RL[2 * t + 1] = prmt(y01, y23, 0x7531);
+                if (K == 9) {
+                    const uint32_t h01 = prmt(cp[0][t] >> 1, cp[1][t] >> 1, 0x6420);
+                    const uint32_t h23 = prmt(cp[2][t] >> 1, cp[3][t] >> 1, 0x6420);
+                    RH[2 * t] = prmt(h01, h23, 0x6420);
+                    RH[2 * t + 1] = prmt(h01, h23, 0x7531);
+                }
+            }
+            cols_fast_store<K, 0>(RL, RH, cp, packed, so, base + lane, NG);
+        } else {
+            for (int u = 0; u < 4; ++u) {
+                const int64_t q = base + 32 * u + lane;
+                if (q < NG) enc_container_generic_blk<BF16, K>(in, C, q, 1, x, y, M, packed, so, spi, spb, spc, cap);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------- decode (blocked)
+struct RowD {
+    uint32_t s_bf2;   // 2^o as a bf16 pair
+    float s_f;        // 2^o as fp32
+    bool ok;          // o <= 127 (one multiply)
+};
+
+__device__ __forceinline__ RowD make_rowd(int e, int x) {
+    RowD D;
+    const int o = e - ((1 << x) - 1);
+    D.ok = o <= 127;
+    const int oc = o > 127 ? 127 : o;
+    D.s_bf2 = (oc >= -133 ? bf16_pow2(oc) : 0u) * 0x00010001u;
+    D.s_f = pow2f_exact(oc < -149 ? -149 : oc);
+    return D;
+}
+
+template <int K>
+__device__ __forceinline__ uint32_t dec_pair_bf16_r(uint32_t cp, int y, const RowD &D) {
+    const uint32_t mag = cp & (((1u << (K - 1)) - 1u) * 0x00010001u);
+    const uint32_t v = hmul2_bf16(mag << (7 - y), D.s_bf2);
+    return v | ((cp << (16 - K)) & 0x80008000u);
+}
+template <int K>
+__device__ __forceinline__ uint32_t dec_f32_r(uint32_t code, int y, const RowD &D) {
+    const uint32_t mag = code & ((1u << (K - 1)) - 1u);
+    const float f = __fmul_rn(__uint_as_float(mag << (23 - y)), D.s_f);
+    return __float_as_uint(f) | ((code << (32 - K)) & 0x80000000u);
+}
+
+template <bool OBF16>
+__device__ __noinline__ void dec_container_generic_blk(const uint8_t *__restrict__ packed, int64_t C, int64_t idx,
+                                                       int axis, int x, int y, const MetaMap M, const SegOffsets so,
+                                                       int nseg, int4 widths, uint8_t *out) {
+    const int wd[4] = {widths.x, widths.y, widths.z, widths.w};
+    uint32_t c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int64_t e[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) e[i] = lane_elem(idx, i, C, axis);
+    int hi = 1 + x + y;
+    for (int s = 0; s < nseg; ++s) {
+        const int w = wd[s], lo = hi - w;
+        const uint8_t *seg = packed + so.off[s];
+        if (w == 8) {
+            for (int i = 0; i < 8; ++i) c[i] |= (uint32_t)seg[e[i]] << lo;
+        } else {
+            uint32_t cont = 0;
+            for (int b = 0; b < w; ++b) cont |= (uint32_t)seg[idx * w + b] << (8 * b);
+            for (int i = 0; i < 8; ++i) c[i] |= ((cont >> (w * i)) & ((1u << w) - 1u)) << lo;
+        }
+        hi = lo;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const Fmt F = fmt_of(x, y, meta_at(M, e[i] / C, e[i] % C));
+        if (OBF16) {
+            const uint16_t h = (uint16_t)dec_code_generic<8>(c[i], F);
+            memcpy(out + 2 * e[i], &h, 2);
+        } else {
+            const uint32_t v = dec_code_generic<24>(c[i], F);
+            memcpy(out + 4 * e[i], &v, 4);
+        }
+    }
+}
+
+template <bool OBF16>
+__global__ void k_decode_generic_blk(const uint8_t *__restrict__ packed, int64_t C, int64_t ncont, int axis, int x,
+                                     int y, MetaMap M, SegOffsets so, int nseg, int4 widths,
+                                     uint8_t *__restrict__ out) {
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < ncont;
+         idx += (int64_t)gridDim.x * blockDim.x)
+        dec_container_generic_blk<OBF16>(packed, C, idx, axis, x, y, M, so, nseg, widths, out);
+}
+
+// ROWS, 8 rows x (4*NH) columns per thread (NH = 2 for bf16 out, 1 fp32);
+// host guarantees bc % (4*NH) == 0, br == 1 or br % 8 == 0, x <= 7 (and
+// y <= 7 for bf16 out).
+template <int K, bool OBF16>
+__global__ void __launch_bounds__(256) k_dec_rows_blk(const uint8_t *__restrict__ packed, int64_t R, int64_t C, int x,
+                                                      int y, MetaMap M, SegOffsets so, uint8_t *__restrict__ out,
+                                                      int nseg, int4 widths) {
+    using EL = Elem<OBF16>;
+    constexpr int V = EL::V, NH = V / 4, TW = tile_words(K, NH);
+    const int64_t CV = C / V, G = R / 8;
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= CV) return;
+    const int64_t c0 = j * V;
+    const uint8_t *mcol = M.meta + c0 / M.bc;
+    for (int64_t g = blockIdx.y; g < G; g += gridDim.y) {
+        RowD D[8];
+        bool ok = true;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int64_t mr = (M.br == 1) ? (8 * g + i) : ((8 * g) / M.br);
+            int e = __ldg(mcol + mr * M.nbc);
+            D[i] = make_rowd(e > 254 ? 254 : e, x);
+            ok = ok && D[i].ok;
+        }
+        if (!ok) {
+            for (int v = 0; v < V; ++v)
+                dec_container_generic_blk<OBF16>(packed, C, g * C + c0 + v, 0, x, y, M, so, nseg, widths, out);
+            continue;
+        }
+        uint32_t raw[TW];
+        rows_load_raw<K, NH, 0>(raw, packed, so, g, C, c0);
+        uint32_t RL[NH][8], RH[NH][8];
+#pragma unroll
+        for (int h = 0; h < NH; ++h)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) { RL[h][i] = 0; RH[h][i] = 0; }
+        rows_unpack_raw<K, NH, 0>(raw, RL, RH);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            uint32_t o[4];
+            if (OBF16) {
+#pragma unroll
+                for (int h = 0; h < NH; ++h) {
+                    o[2 * h] = dec_pair_bf16_r<K>(pair_from_lanes<K>(RL[h][i], RH[h][i], 0x4140), y, D[i]);
+                    o[2 * h + 1] = dec_pair_bf16_r<K>(pair_from_lanes<K>(RL[h][i], RH[h][i], 0x4342), y, D[i]);
+                }
+            } else {
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    uint32_t code = (RL[0][i] >> (8 * v)) & 0xFFu;
+                    if (K == 9) code |= ((RH[0][i] >> (8 * v)) & 0xFFu) << 1;
+                    o[v] = dec_f32_r<K>(code, y, D[i]);
+                }
+            }
+            stg_v4(out + ((8 * g + i) * C + c0) * EL::ES, make_uint4(o[0], o[1], o[2], o[3]));
+        }
+    }
+}
+
+// COLS: lane handles groups q = base + 32u + lane (one metadata per group);
+// host guarantees bc % 8 == 0 and the same format conditions.
+template <int K, bool OBF16>
+__global__ void __launch_bounds__(256) k_dec_cols_blk(const uint8_t *__restrict__ packed, int64_t n, int64_t C, int x,
+                                                      int y, MetaMap M, SegOffsets so, uint8_t *__restrict__ out,
+                                                      int nseg, int4 widths) {
+    const int64_t NG = n / 8, gpr = C / 8;
+    const double inv = 1.0 / (double)gpr;
+    const int lane = threadIdx.x & 31;
+    const int64_t step = (int64_t)gridDim.x * (blockDim.x >> 5) * 128;
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    for (int64_t base = gw * 128; base < NG; base += step) {
+        uint32_t RL[8], RH[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { RL[i] = 0; RH[i] = 0; }
+        cols_fast_load<K, 0>(RL, RH, packed, so, base + lane, NG);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t q = base + 32 * u + lane;
+            if (q >= NG) continue;
+            const int64_t row = div_rcp(q, gpr, inv);
+            const RowD D = make_rowd(meta_at(M, row, (q - row * gpr) * 8), x);
+            if (!D.ok) {
+                dec_container_generic_blk<OBF16>(packed, C, q, 1, x, y, M, so, nseg, widths, out);
+                continue;
+            }
+            if (OBF16) {
+                uint32_t o[4];
+                const uint32_t sel = (uint32_t)u | ((uint32_t)(4 + u) << 4);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    uint32_t cp = prmt(RL[2 * t], RL[2 * t + 1], sel);
+                    cp = (cp & 0xFFu) | ((cp & 0xFF00u) << 8);
+                    if (K == 9) {
+                        uint32_t ch = prmt(RH[2 * t], RH[2 * t + 1], sel);
+                        cp |= ((ch & 0xFFu) | ((ch & 0xFF00u) << 8)) << 1;
+                    }
+                    o[t] = dec_pair_bf16_r<K>(cp, y, D);
+                }
+                stg_v4(out + q * 16, make_uint4(o[0], o[1], o[2], o[3]));
+            } else {
+                uint32_t o[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    uint32_t code = (RL[i] >> (8 * u)) & 0xFFu;
+                    if (K == 9) code |= ((RH[i] >> (8 * u)) & 0xFFu) << 1;
+                    o[i] = dec_f32_r<K>(code, y, D);
+                }
+                stg_v4(out + q * 32, make_uint4(o[0], o[1], o[2], o[3]));
+                stg_v4(out + q * 32 + 16, make_uint4(o[4], o[5], o[6], o[7]));
+            }
+        }
+    }
+}
+
+// ----------------------------------------------------- quantize (blocked)
+// 2D: thread = one 16-byte vector of one row (vector-aligned rows, host
+// guarantees C % V == 0 and bc % V == 0 so a vector never straddles blocks).
+template <bool BF16>
+__global__ void __launch_bounds__(256) k_quant_blk(const uint8_t *__restrict__ in, uint8_t *__restrict__ out,
+                                                   int64_t R, int64_t C, int x, int y, MetaMap M, int force_generic) {
+    using EL = Elem<BF16>;
+    const int64_t CV = C / EL::V;
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= CV) return;
+    const int64_t c0 = j * EL::V;
+    for (int64_t r = blockIdx.y; r < R; r += gridDim.y) {
+        const uint4 v = ldg_nc_v4(in + (r * C + c0) * EL::ES);
+        const Fmt F = fmt_of(x, y, meta_at(M, r, c0));
+        const FastP P = make_fast(F, BF16, force_generic);
+        const DecPath DP = make_dec_path(F, force_generic);
+        uint32_t o[4];
+        uint32_t flag = 0;
+        const bool fast = BF16 ? P.enc_simd : P.enc_f32;
+        if (fast) {
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                o[t] = BF16 ? quant_pair_bf16(word_of(v, t), P, flag) : quant_f32_fast(word_of(v, t), P, flag);
+            flag &= 0x80008000u;
+        }
+        if (!fast || flag) {
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const uint32_t w = word_of(v, t);
+                if (BF16) {
+                    const uint32_t lo = quantize_elem<true>(w << 16, F, DP);
+                    const uint32_t hi = quantize_elem<true>(w & 0xFFFF0000u, F, DP);
+                    o[t] = (lo & 0xFFFFu) | (hi << 16);
+                } else {
+                    o[t] = quantize_elem<false>(w, F, DP);
+                }
+            }
+        }
+        stg_v4(out + (r * C + c0) * EL::ES, make_uint4(o[0], o[1], o[2], o[3]));
+    }
+}
+
+template <bool BF16>
+__global__ void k_quant_blk_scalar(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, int64_t R, int64_t C,
+                                   int x, int y, MetaMap M, int force_generic) {
+    const int64_t n = R * C;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const Fmt F = fmt_of(x, y, meta_at(M, i / C, i % C));
+        const DecPath DP = make_dec_path(F, force_generic);
+        if (BF16) {
+            uint16_t b;
+            memcpy(&b, in + 2 * i, 2);
+            const uint16_t o = (uint16_t)quantize_elem<true>((uint32_t)b << 16, F, DP);
+            memcpy(out + 2 * i, &o, 2);
+        } else {
+            uint32_t u;
+            memcpy(&u, in + 4 * i, 4);
+            const uint32_t o = quantize_elem<false>(u, F, DP);
+            memcpy(out + 4 * i, &o, 4);
+        }
+    }
+}
+
+// --------------------------------------------------- block max exponent
+// biased exponent of |v| (finite, fp32 bits a) rounded RTNE to y mantissa
+// bits in its own binade, clamped to [0, 254]
+__device__ __forceinline__ int exp_after_rounding(uint32_t a, int y) {
+    if (a == 0u) return 0;
+    if (a >= 0x00800000u) {   // normal: integer RTNE at bit 23-y, carry lands in the exponent
+        if (y >= 23) return (int)(a >> 23);
+        const int sh = 23 - y;
+        const uint32_t t = a + ((1u << (sh - 1)) - 1u) + ((a >> sh) & 1u);
+        const int e = (int)(t >> 23);
+        return e > 254 ? 254 : e;
+    }
+    // fp32 subnormal: own binade is below 2^-126; only a carry to 2^-126 (exp 1) matters
+    const int L = 32 - __clz(a);          // significant bits, 1..23
+    const int p = L - 1 - y;              // rounding position
+    if (p <= 0 || L < 23) return 0;
+    const uint32_t t = a + ((1u << (p - 1)) - 1u) + ((a >> p) & 1u);
+    return t >= (1u << 23) ? 1 : 0;
+}
+
+// one warp per block: max |finite| over the block, then the scheme's exponent
+template <bool BF16>
+__global__ void __launch_bounds__(256) k_block_max(const uint8_t *__restrict__ in, int64_t R, int64_t C, int64_t br,
+                                                   int64_t bc, int y, int scheme, uint8_t *__restrict__ meta) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nbc = C / bc, nb = (R / br) * nbc;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    constexpr int V = Elem<BF16>::V;
+    const bool vec = (bc % V == 0) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0) && (C % V == 0);
+    for (int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); b < nb; b += warps) {
+        const int64_t r0 = (b / nbc) * br, c0 = (b % nbc) * bc;
+        uint32_t amax = 0;   // max finite magnitude bits (fp32 convention)
+        for (int64_t i = 0; i < br; ++i) {
+            const uint8_t *row = in + ((r0 + i) * C + c0) * Elem<BF16>::ES;
+            if (vec) {
+                for (int64_t v = lane; v < bc / V; v += 32) {
+                    const uint4 q = ldg_nc_v4(row + v * 16);
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const uint32_t w = word_of(q, t);
+                        if (BF16) {
+                            const uint32_t lo = (w << 16) & 0x7FFF0000u, hi = w & 0x7FFF0000u;
+                            if (lo < 0x7F800000u) amax = max(amax, lo);
+                            if (hi < 0x7F800000u) amax = max(amax, hi);
+                        } else {
+                            const uint32_t a = w & 0x7FFFFFFFu;
+                            if (a < 0x7F800000u) amax = max(amax, a);
+                        }
+                    }
+                }
+            } else {
+                for (int64_t c = lane; c < bc; c += 32) {
+                    const uint32_t a = load_elem_scalar<BF16>(row, c) & 0x7FFFFFFFu;
+                    if (a < 0x7F800000u) amax = max(amax, a);
+                }
+            }
+        }
+        amax = __reduce_max_sync(0xFFFFFFFFu, amax);
+        if (lane == 0) {
+            int e = scheme == 0 ? (int)(amax >> 23) : exp_after_rounding(amax, y);
+            meta[b] = (uint8_t)(e > 254 ? 254 : e);
+        }
+    }
+}
+
+}  // namespace exmy

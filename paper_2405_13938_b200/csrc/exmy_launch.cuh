@@ -6,7 +6,7 @@
 #include <cuda_runtime.h>
 
 #include "exmy.h"
-#include "exmy_fast.cuh"
+#include "exmy_blocked.cuh"
 
 namespace exmy {
 
@@ -75,5 +75,16 @@ exmy_status launch_decode(const uint8_t *packed, int64_t R, int64_t C, int axis,
                           const uint8_t *meta, uint8_t *out, bool obf16, cudaStream_t st);
 exmy_status launch_specials_scatter(const int64_t *spi, const uint32_t *spb, const unsigned long long *spc,
                                     int64_t cap, uint8_t *out, bool obf16, cudaStream_t st);
+
+// block metadata
+exmy_status launch_block_max(const uint8_t *in, bool bf16, int64_t R, int64_t C, int64_t br, int64_t bc, int y,
+                             int scheme, uint8_t *meta, cudaStream_t st);
+exmy_status launch_quantize_blocked(const uint8_t *in, uint8_t *out, bool bf16, int64_t R, int64_t C, int64_t br,
+                                    int64_t bc, int x, int y, const uint8_t *meta, cudaStream_t st);
+exmy_status launch_encode_blocked(const uint8_t *in, bool bf16, int64_t R, int64_t C, int axis, int64_t br,
+                                  int64_t bc, int x, int y, const uint8_t *meta, uint8_t *packed, int64_t *spi,
+                                  uint32_t *spb, unsigned long long *spc, int64_t cap, cudaStream_t st);
+exmy_status launch_decode_blocked(const uint8_t *packed, int64_t R, int64_t C, int axis, int64_t br, int64_t bc,
+                                  int x, int y, const uint8_t *meta, uint8_t *out, bool obf16, cudaStream_t st);
 
 }  // namespace exmy

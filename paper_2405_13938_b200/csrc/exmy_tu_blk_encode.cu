@@ -1,0 +1,97 @@
+// exmy_tu_blk_encode.cu -- encode with block metadata launchers.
+#include "exmy_launch.cuh"
+
+namespace exmy {
+
+namespace {
+template <int K, bool BF16, int MODE>
+exmy_status launch_enc_blk_km(const uint8_t *in, int64_t R, int64_t C, int axis, int x, int y, const MetaMap &M,
+                              uint8_t *packed, const Plan &p, int64_t *spi, uint32_t *spb, unsigned long long *spc,
+                              int64_t cap, cudaStream_t st) {
+    const int64_t n = R * C;
+    if (axis == EXMY_AXIS_ROWS) {
+        bool vec = aligned(in, 4 * Elem<BF16>::ES) && (C % 4 == 0) && (M.bc % 4 == 0) &&
+                   (M.br == 1 || M.br % 8 == 0);
+        for (int s = 0; s < p.nseg; ++s) vec = vec && aligned(packed + p.so.off[s], p.w[s] == 8 ? 4 : 4 * p.w[s]);
+        if (vec) {
+            const int threads = 256;
+            static int occ = 0;
+            if (!occ) occ = occupancy(k_enc_rows_blk<K, BF16, MODE>, threads, 0);
+            const int64_t CV = C / 4, G = R / 8;
+            int64_t gx = cdiv(CV, threads);
+            int64_t gy = (int64_t)num_sms() * occ / gx;
+            if (gy < 1) gy = 1;
+            if (gy > G) gy = G;
+            if (gy > 65535) gy = 65535;
+            if (gx > INT_MAX) return EXMY_E_SHAPE;
+            k_enc_rows_blk<K, BF16, MODE><<<dim3((unsigned)gx, (unsigned)gy), threads, 0, st>>>(
+                in, R, C, x, y, M, packed, p.so, spi, spb, spc, cap, g_force_generic);
+            return launch_status();
+        }
+    } else {
+        bool vec = aligned(in, 16) && (M.bc % 8 == 0);
+        for (int s = 0; s < p.nseg; ++s) vec = vec && aligned(packed + p.so.off[s], p.w[s]);
+        if (vec) {
+            const int threads = 256;
+            static int occ = 0;
+            if (!occ) occ = occupancy(k_enc_cols_blk<K, BF16, MODE>, threads, 0);
+            int64_t blocks = cdiv(cdiv(n / 8, 128), threads / 32);
+            int64_t maxb = (int64_t)num_sms() * occ;
+            if (blocks > maxb) blocks = maxb;
+            k_enc_cols_blk<K, BF16, MODE><<<(unsigned)blocks, threads, 0, st>>>(in, n, C, x, y, M, packed, p.so, spi,
+                                                                                spb, spc, cap, g_force_generic);
+            return launch_status();
+        }
+    }
+    const int64_t ncont = n / 8;
+    int64_t blocks = cdiv(ncont, 256);
+    if (blocks > (int64_t)num_sms() * 8) blocks = (int64_t)num_sms() * 8;
+    k_encode_generic_blk<BF16, K><<<(unsigned)blocks, 256, 0, st>>>(in, C, ncont, axis, x, y, M, packed, p.so, spi,
+                                                                    spb, spc, cap);
+    return launch_status();
+}
+
+template <int K, bool BF16>
+exmy_status launch_enc_blk_k(const uint8_t *in, int64_t R, int64_t C, int axis, int x, int y, const MetaMap &M,
+                             uint8_t *packed, const Plan &p, int64_t *spi, uint32_t *spb, unsigned long long *spc,
+                             int64_t cap, cudaStream_t st) {
+    if (BF16 && y <= 6) {
+        if (y == 0)
+            return launch_enc_blk_km<K, BF16, (BF16 ? ENC_SIMD_Y0 : ENC_F32_Y0)>(in, R, C, axis, x, y, M, packed, p,
+                                                                                 spi, spb, spc, cap, st);
+        return launch_enc_blk_km<K, BF16, (BF16 ? ENC_SIMD : ENC_F32)>(in, R, C, axis, x, y, M, packed, p, spi, spb,
+                                                                       spc, cap, st);
+    }
+    if (y == 0)
+        return launch_enc_blk_km<K, BF16, ENC_F32_Y0>(in, R, C, axis, x, y, M, packed, p, spi, spb, spc, cap, st);
+    return launch_enc_blk_km<K, BF16, ENC_F32>(in, R, C, axis, x, y, M, packed, p, spi, spb, spc, cap, st);
+}
+
+template <bool BF16>
+exmy_status enc_blk_dispatch(int k, const uint8_t *in, int64_t R, int64_t C, int axis, int x, int y,
+                             const MetaMap &M, uint8_t *packed, const Plan &p, int64_t *spi, uint32_t *spb,
+                             unsigned long long *spc, int64_t cap, cudaStream_t st) {
+    switch (k) {
+        case 3: return launch_enc_blk_k<3, BF16>(in, R, C, axis, x, y, M, packed, p, spi, spb, spc, cap, st);
+        case 4: return launch_enc_blk_k<4, BF16>(in, R, C, axis, x, y, M, packed, p, spi, spb, spc, cap, st);
+        case 5: return launch_enc_blk_k<5, BF16>(in, R, C, axis, x, y, M, packed, p, spi, spb, spc, cap, st);
+        case 6: return launch_enc_blk_k<6, BF16>(in, R, C, axis, x, y, M, packed, p, spi, spb, spc, cap, st);
+        case 7: return launch_enc_blk_k<7, BF16>(in, R, C, axis, x, y, M, packed, p, spi, spb, spc, cap, st);
+        case 8: return launch_enc_blk_k<8, BF16>(in, R, C, axis, x, y, M, packed, p, spi, spb, spc, cap, st);
+        case 9: return launch_enc_blk_k<9, BF16>(in, R, C, axis, x, y, M, packed, p, spi, spb, spc, cap, st);
+    }
+    return EXMY_E_FORMAT;
+}
+}  // namespace
+
+exmy_status launch_encode_blocked(const uint8_t *in, bool bf16, int64_t R, int64_t C, int axis, int64_t br,
+                                  int64_t bc, int x, int y, const uint8_t *meta, uint8_t *packed, int64_t *spi,
+                                  uint32_t *spb, unsigned long long *spc, int64_t cap, cudaStream_t st) {
+    const int k = 1 + x + y;
+    const Plan p = make_plan(k, R * C);
+    const MetaMap M{meta, br, bc, C / bc};
+    return bf16 ? enc_blk_dispatch<true>(k, in, R, C, axis, x, y, M, packed, p, spi, spb, spc, cap, st)
+                : enc_blk_dispatch<false>(k, in, R, C, axis, x, y, M, packed, p, spi, spb, spc, cap, st);
+}
+
+}  // namespace exmy

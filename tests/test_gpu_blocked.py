@@ -1,0 +1,135 @@
+"""GPU parity of the block-metadata path against the
+oracle: block max exponent (both schemes), blocked quantize / encode /
+decode, every block shape class (tensor, row, column, sub-row, 2-D tile),
+fast and scalar kernels, bit-exact."""
+import numpy as np
+import pytest
+import torch
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+@pytest.fixture(scope="module")
+def exmy():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2405_13938_b200 as m
+    m.force_generic(False)
+    return m
+
+
+def rowscaled_bits(shape, seed, dt="bf16"):
+    """rows of very different magnitude (per-row metadata matters) + specials"""
+    R, C = shape
+    rng = np.random.default_rng(seed)
+    t = W.bf16_weights(shape, seed=seed, std=0.02).float().numpy()
+    t = t * (2.0 ** rng.integers(-20, 20, size=(R, 1))).astype(np.float32)
+    t = torch.from_numpy(t.astype(np.float32))
+    if dt == "bf16":
+        t = t.to(torch.bfloat16)
+    bits = W.to_bits(t)
+    flat = bits.reshape(-1)
+    flat[rng.integers(0, flat.size, size=max(1, flat.size // 500))] = (0x7FC0 if dt == "bf16" else 0x7FC00000)
+    return bits
+
+
+BLOCKS = [("tensor", None), ("row", None), ("col", None), ("subrow32", (1, 32)), ("tile8x16", (8, 16)),
+          ("tile16x64", (16, 64)), ("odd", (2, 12))]
+
+
+def block_of(name, spec, shape):
+    R, C = shape
+    return {"tensor": (R, C), "row": (1, C), "col": (R, 1)}.get(name, spec)
+
+
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+@pytest.mark.parametrize("scheme", [0, 1])
+def test_block_max_exponent(exmy, orc, dt, scheme):
+    shape = (64, 192)
+    bits = rowscaled_bits(shape, 3, dt)
+    d = W.from_bits(bits).to(DEV)
+    for name, spec in BLOCKS:
+        blk = block_of(name, spec, shape)
+        for y in (0, 1, 3, 6):
+            got = exmy.block_max_exponent(d, blk, y, scheme).cpu().numpy()
+            ref = orc.block_max_exponent(bits, blk, y, scheme)
+            np.testing.assert_array_equal(got, ref, err_msg=f"{name} y={y}")
+    # fp32 subnormals / carries at the exponent-254 edge for the after scheme
+    edge = np.array([0x007FFFFF, 0x007FFFFE, 0x00400000, 0x7F7FFFFF, 0x00000001, 0x7F800000, 0, 0x80000000],
+                    np.uint32).reshape(1, 8)
+    for y in (0, 1, 2, 5, 22):
+        got = exmy.block_max_exponent(W.from_bits(edge).to(DEV), (1, 1), y, scheme).cpu().numpy()
+        np.testing.assert_array_equal(got, orc.block_max_exponent(edge, (1, 1), y, scheme))
+
+
+@pytest.mark.parametrize("fmt", [(3, 3), (2, 4), (4, 2), (6, 0), (1, 5), (0, 6), (2, 2), (5, 3), (2, 1), (0, 7),
+                                 (1, 7), (8, 0)], ids=lambda f: f"e{f[0]}m{f[1]}")
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+def test_blocked_codecs(exmy, orc, fmt, dt):
+    shape = (64, 192)
+    bits = rowscaled_bits(shape, fmt[0] * 10 + fmt[1], dt)
+    d = W.from_bits(bits).to(DEV)
+    x, y = fmt
+    for name, spec in BLOCKS:
+        blk = block_of(name, spec, shape)
+        for scheme in (0, 1):
+            meta = orc.block_max_exponent(bits, blk, y, scheme)
+            dm = torch.from_numpy(meta.copy()).to(DEV)
+            q = W.to_bits(exmy.quantize_blocked(d, fmt, dm, blk))
+            qref = orc.quantize_blocked(bits, fmt, meta, blk)
+            np.testing.assert_array_equal(q, qref, err_msg=f"quantize {name} scheme {scheme}")
+            for axis in ("rows", "cols"):
+                ax = orc.ROWS if axis == "rows" else orc.COLS
+                p = exmy.encode_blocked(d, fmt, dm, blk, axis=axis, specials_capacity=bits.size)
+                pref, idx, sb, ns = orc.encode_blocked(bits, fmt, meta, blk, ax)
+                np.testing.assert_array_equal(p.data.cpu().numpy(), pref, err_msg=f"encode {name} {axis}")
+                spi, spb, cnt = p.specials()
+                assert cnt == ns
+                np.testing.assert_array_equal(spi.cpu().numpy(), idx)
+                out = exmy.decode(p)
+                np.testing.assert_array_equal(W.to_bits(out), qref, err_msg=f"decode {name} {axis}")
+                od = np.uint32 if dt == "bf16" else np.uint16
+                other = exmy.decode(p, torch.float32 if dt == "bf16" else torch.bfloat16)
+                np.testing.assert_array_equal(W.to_bits(other),
+                                              orc.decode_blocked(pref, shape, fmt, meta, blk, ax, idx, sb, od))
+
+
+def test_blocked_forced_metadata_edges(exmy, orc):
+    """metadata outside the fast preconditions (e_max 0, 254, below the data)
+    per row: the tiles fall back to the integer path, results unchanged."""
+    shape = (16, 64)
+    bits = rowscaled_bits(shape, 77)
+    d = W.from_bits(bits).to(DEV)
+    meta = np.array([0, 254, 1, 100, 127, 131, 200, 3] * 2, np.uint8).reshape(16, 1)
+    dm = torch.from_numpy(meta.copy()).to(DEV)
+    for fmt in [(3, 3), (7, 1), (6, 0), (0, 6)]:
+        q = W.to_bits(exmy.quantize_blocked(d, fmt, dm, (1, 64)))
+        np.testing.assert_array_equal(q, orc.quantize_blocked(bits, fmt, meta, (1, 64)))
+        for axis in ("rows", "cols"):
+            ax = orc.ROWS if axis == "rows" else orc.COLS
+            p = exmy.encode_blocked(d, fmt, dm, (1, 64), axis=axis, specials_capacity=bits.size)
+            pref = orc.encode_blocked(bits, fmt, meta, (1, 64), ax)[0]
+            np.testing.assert_array_equal(p.data.cpu().numpy(), pref)
+            np.testing.assert_array_equal(W.to_bits(exmy.decode(p)), orc.quantize_blocked(bits, fmt, meta, (1, 64)))
+
+
+def test_per_row_config2_shape_sampled(exmy, orc):
+    """per-row metadata on the config-2 tensor (16384^2 bf16), the shape the
+    bench measures; parity on sampled row-group windows + decode == quantize."""
+    R = C = 16384
+    t = W.bf16_weights((R, C), seed=1, device=DEV)
+    meta = exmy.block_max_exponent(t, "row")
+    ws, offs = exmy.segments(7, R * C)
+    p = exmy.encode_blocked(t, "e3m3", meta, "row")
+    q = exmy.quantize_blocked(t, "e3m3", meta, "row")
+    assert torch.equal(exmy.decode(p).view(torch.int16), q.view(torch.int16))
+    for r0 in (0, 8 * 777, R - 8):
+        rows = W.to_bits(t[r0:r0 + 8])
+        m = meta[r0:r0 + 8].cpu().numpy()
+        np.testing.assert_array_equal(m, orc.block_max_exponent(rows, (1, C)))
+        ref = orc.encode_blocked(rows, "e3m3", m, (1, C), orc.ROWS)[0]
+        got = torch.cat([p.data[o + r0 * C * w // 8: o + (r0 + 8) * C * w // 8] for w, o in zip(ws, offs)])
+        np.testing.assert_array_equal(got.cpu().numpy(), ref)
