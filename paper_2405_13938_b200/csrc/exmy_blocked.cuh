@@ -151,8 +151,27 @@ __global__ void k_encode_generic_blk(const uint8_t *__restrict__ in, int64_t C, 
 // ---------------------------------------------------- encode ROWS (blocked)
 // Same tiles as k_enc_rows_fast (8 rows x 4 columns).  Host guarantees
 // bc % 4 == 0 (the 4 columns share a block column) and br == 1 or br % 8 == 0.
+// metadata bytes of the 8 rows of row group g in this thread's block column
+// (br == 1: one per row; br % 8 == 0: the same byte for all 8)
+__device__ __forceinline__ void load_tile_meta(const uint8_t *mcol, int64_t g, const MetaMap &M, uint32_t (&e)[8]) {
+    if (M.br == 1) {
+        if (M.nbc == 1 && ((reinterpret_cast<uintptr_t>(mcol) & 7) == 0)) {
+            const uint2 v = __ldg(reinterpret_cast<const uint2 *>(mcol + 8 * g));
+#pragma unroll
+            for (int i = 0; i < 4; ++i) { e[i] = (v.x >> (8 * i)) & 0xFFu; e[4 + i] = (v.y >> (8 * i)) & 0xFFu; }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) e[i] = __ldg(mcol + (8 * g + i) * M.nbc);
+        }
+    } else {
+        const uint32_t v = __ldg(mcol + ((8 * g) / M.br) * M.nbc);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) e[i] = v;
+    }
+}
+
 template <int K, bool BF16, int MODE>
-__global__ void __launch_bounds__(256, BF16 ? 3 : 2) k_enc_rows_blk(const uint8_t *__restrict__ in, int64_t R, int64_t C,
+__global__ void __launch_bounds__(256, 2) k_enc_rows_blk(const uint8_t *__restrict__ in, int64_t R, int64_t C,
                                                                    int x, int y, MetaMap M,
                                                                    uint8_t *__restrict__ packed, SegOffsets so,
                                                                    int64_t *spi, uint32_t *spb,
@@ -169,27 +188,36 @@ __global__ void __launch_bounds__(256, BF16 ? 3 : 2) k_enc_rows_blk(const uint8_
     const uint8_t *mcol = M.meta + c0 / M.bc;      // block column of this thread
     const uint8_t *src = in + c0 * EL::ES;
     const int64_t rstride = C * EL::ES;
-    for (int64_t g = blockIdx.y; g < G; g += gridDim.y) {
-        uint32_t w[8][NW];
+    // software pipeline: next tile's data and metadata in flight
+    uint32_t nw[8][NW], nm[8];
+    int64_t g = blockIdx.y;
+    if (g < G) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) load4<BF16>(src + (8 * g + i) * rstride, w[i]);
+        for (int i = 0; i < 8; ++i) load4<BF16>(src + (8 * g + i) * rstride, nw[i]);
+        load_tile_meta(mcol, g, M, nm);
+    }
+    for (; g < G; g += gridDim.y) {
+        uint32_t w[8][NW], em[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            em[i] = nm[i];
+#pragma unroll
+            for (int q = 0; q < NW; ++q) w[i][q] = nw[i][q];
+        }
+        const int64_t gn = g + gridDim.y;
+        if (gn < G) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) load4<BF16>(src + (8 * gn + i) * rstride, nw[i]);
+            load_tile_meta(mcol, gn, M, nm);
+        }
         bool ok = !force_generic;
         uint32_t cp[8][2];
         uint32_t amax = 0;
-        if (M.br == 1) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                int e = __ldg(mcol + (8 * g + i) * M.nbc);
-                const RowP Rp = make_rowp<SIMD>(e > 254 ? 254 : e, x, y);
-                ok = ok && Rp.ok;
-                vec_codes_r<K, BF16, MODE, NW>(w[i], cp[i], P, Rp, amax);
-            }
-        } else {
-            int e = __ldg(mcol + ((8 * g) / M.br) * M.nbc);
-            const RowP Rp = make_rowp<SIMD>(e > 254 ? 254 : e, x, y);
+        for (int i = 0; i < 8; ++i) {
+            const RowP Rp = make_rowp<SIMD>(em[i] > 254u ? 254 : (int)em[i], x, y);
             ok = ok && Rp.ok;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) vec_codes_r<K, BF16, MODE, NW>(w[i], cp[i], P, Rp, amax);
+            vec_codes_r<K, BF16, MODE, NW>(w[i], cp[i], P, Rp, amax);
         }
         if (ok && !amax_special<BF16, MODE>(amax, P)) {
             uint32_t RL[1][8], RH[1][8];
@@ -216,6 +244,39 @@ __device__ __forceinline__ int64_t div_rcp(int64_t q, int64_t d, double inv) {
     return r;
 }
 
+// metadata of COLS group q (8 consecutive elements of one row) without
+// 64-bit integer divisions: row, block row and block column via reciprocals
+struct GroupMeta {
+    int64_t gpr, bc8;
+    double inv_gpr, inv_br, inv_bc8;
+    __device__ __forceinline__ GroupMeta(const MetaMap &M, int64_t C) {
+        gpr = C / 8;
+        bc8 = M.bc / 8;
+        inv_gpr = 1.0 / (double)gpr;
+        inv_br = 1.0 / (double)M.br;
+        inv_bc8 = 1.0 / (double)bc8;
+    }
+    __device__ __forceinline__ int at_row(const MetaMap &M, int64_t row, int64_t gcol) const {
+        const int64_t brow = M.br == 1 ? row : div_rcp(row, M.br, inv_br);
+        const int64_t bcol = bc8 == gpr ? 0 : div_rcp(gcol, bc8, inv_bc8);
+        const int e = __ldg(M.meta + brow * M.nbc + bcol);
+        return e > 254 ? 254 : e;
+    }
+    __device__ __forceinline__ int at(const MetaMap &M, int64_t q) const {
+        const int64_t row = div_rcp(q, gpr, inv_gpr);
+        return at_row(M, row, q - row * gpr);
+    }
+    // warp tile of 128 groups starting at `base`: when a row holds >= 128
+    // groups the tile spans at most two rows, so one division per tile
+    // serves all of its groups
+    __device__ __forceinline__ int at_tile(const MetaMap &M, int64_t base, int64_t rb, int64_t qs, int t) const {
+        if (gpr < 128) return at(M, base + t);
+        const int64_t c = qs + t;
+        const bool cross = c >= gpr;
+        return at_row(M, rb + (cross ? 1 : 0), cross ? c - gpr : c);
+    }
+};
+
 template <int K, bool BF16, int MODE>
 __global__ void __launch_bounds__(256) k_enc_cols_blk(const uint8_t *__restrict__ in, int64_t n, int64_t C, int x,
                                                       int y, MetaMap M, uint8_t *__restrict__ packed, SegOffsets so,
@@ -226,12 +287,13 @@ __global__ void __launch_bounds__(256) k_enc_cols_blk(const uint8_t *__restrict_
     constexpr int NP = EL::V / 2;
     constexpr bool SIMD = (MODE == ENC_SIMD || MODE == ENC_SIMD_Y0);
     const FastP P = make_fast(fmt_of(x, y, 0), BF16, 1);
-    const int64_t NG = n / 8, gpr = C / 8;
-    const double inv = 1.0 / (double)gpr;
+    const int64_t NG = n / 8;
+    const GroupMeta GM(M, C);
     const int lane = threadIdx.x & 31;
     const int64_t step = (int64_t)gridDim.x * (blockDim.x >> 5) * 128;
     const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     for (int64_t base = gw * 128; base < NG; base += step) {
+        const int64_t rb = div_rcp(base, GM.gpr, GM.inv_gpr), qs = base - rb * GM.gpr;
         uint4 r[4][NV];
         uint32_t cp[4][4];
         uint32_t amax = 0;
@@ -243,11 +305,7 @@ __global__ void __launch_bounds__(256) k_enc_cols_blk(const uint8_t *__restrict_
 #pragma unroll
             for (int t = 0; t < NV; ++t)
                 r[u][t] = in_range ? ldg_nc_v4(in + q * 8 * EL::ES + 16 * t) : make_uint4(0, 0, 0, 0);
-            int e = 0;
-            if (in_range) {
-                const int64_t row = div_rcp(q, gpr, inv);
-                e = meta_at(M, row, (q - row * gpr) * 8);
-            }
+            const int e = in_range ? GM.at_tile(M, base, rb, qs, 32 * u + lane) : 0;
             const RowP Rp = make_rowp<SIMD>(e, x, y);
             ok = ok && (Rp.ok || !in_range);
 #pragma unroll
@@ -371,14 +429,27 @@ __global__ void __launch_bounds__(256) k_dec_rows_blk(const uint8_t *__restrict_
     if (j >= CV) return;
     const int64_t c0 = j * V;
     const uint8_t *mcol = M.meta + c0 / M.bc;
-    for (int64_t g = blockIdx.y; g < G; g += gridDim.y) {
+    uint32_t nxt[TW], nm[8];
+    int64_t g = blockIdx.y;
+    if (g < G) {
+        rows_load_raw<K, NH, 0>(nxt, packed, so, g, C, c0);
+        load_tile_meta(mcol, g, M, nm);
+    }
+    for (; g < G; g += gridDim.y) {
+        uint32_t raw[TW], em[8];
+#pragma unroll
+        for (int q = 0; q < TW; ++q) raw[q] = nxt[q];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) em[i] = nm[i];
+        if (g + gridDim.y < G) {
+            rows_load_raw<K, NH, 0>(nxt, packed, so, g + gridDim.y, C, c0);
+            load_tile_meta(mcol, g + gridDim.y, M, nm);
+        }
         RowD D[8];
         bool ok = true;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const int64_t mr = (M.br == 1) ? (8 * g + i) : ((8 * g) / M.br);
-            int e = __ldg(mcol + mr * M.nbc);
-            D[i] = make_rowd(e > 254 ? 254 : e, x);
+            D[i] = make_rowd(em[i] > 254u ? 254 : (int)em[i], x);
             ok = ok && D[i].ok;
         }
         if (!ok) {
@@ -386,8 +457,6 @@ __global__ void __launch_bounds__(256) k_dec_rows_blk(const uint8_t *__restrict_
                 dec_container_generic_blk<OBF16>(packed, C, g * C + c0 + v, 0, x, y, M, so, nseg, widths, out);
             continue;
         }
-        uint32_t raw[TW];
-        rows_load_raw<K, NH, 0>(raw, packed, so, g, C, c0);
         uint32_t RL[NH][8], RH[NH][8];
 #pragma unroll
         for (int h = 0; h < NH; ++h)
@@ -422,12 +491,13 @@ template <int K, bool OBF16>
 __global__ void __launch_bounds__(256) k_dec_cols_blk(const uint8_t *__restrict__ packed, int64_t n, int64_t C, int x,
                                                       int y, MetaMap M, SegOffsets so, uint8_t *__restrict__ out,
                                                       int nseg, int4 widths) {
-    const int64_t NG = n / 8, gpr = C / 8;
-    const double inv = 1.0 / (double)gpr;
+    const int64_t NG = n / 8;
+    const GroupMeta GM(M, C);
     const int lane = threadIdx.x & 31;
     const int64_t step = (int64_t)gridDim.x * (blockDim.x >> 5) * 128;
     const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     for (int64_t base = gw * 128; base < NG; base += step) {
+        const int64_t rb = div_rcp(base, GM.gpr, GM.inv_gpr), qs = base - rb * GM.gpr;
         uint32_t RL[8], RH[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) { RL[i] = 0; RH[i] = 0; }
@@ -436,8 +506,7 @@ __global__ void __launch_bounds__(256) k_dec_cols_blk(const uint8_t *__restrict_
         for (int u = 0; u < 4; ++u) {
             const int64_t q = base + 32 * u + lane;
             if (q >= NG) continue;
-            const int64_t row = div_rcp(q, gpr, inv);
-            const RowD D = make_rowd(meta_at(M, row, (q - row * gpr) * 8), x);
+            const RowD D = make_rowd(GM.at_tile(M, base, rb, qs, 32 * u + lane), x);
             if (!D.ok) {
                 dec_container_generic_blk<OBF16>(packed, C, q, 1, x, y, M, so, nseg, widths, out);
                 continue;

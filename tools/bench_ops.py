@@ -42,6 +42,7 @@ def main():
     ap.add_argument("--fmts", default="e0m6,e1m5,e2m4,e3m3,e4m2,e5m1,e6m0")
     ap.add_argument("--axis", default="rows")
     ap.add_argument("--hist-modes", default="0,1")
+    ap.add_argument("--block", default=None, help="row | col | tensor | BRxBC: time the block-metadata path")
     a = ap.parse_args()
     dev = torch.device("cuda")
     R, C = a.rows, a.cols
@@ -74,6 +75,25 @@ def main():
         p = exmy.encode(t, f, meta, axis=a.axis, out=buf)
         ms = timeit(lambda: exmy.decode(p, out=d))
         res[f"decode_{f}"] = {"ms": ms, "gbs": n * (es + k / 8) / ms / 1e6, "frac": n * (es + k / 8) / ms / 1e6 / peak}
+    if a.block:
+        blk = a.block if a.block in ("row", "col", "tensor") else tuple(int(v) for v in a.block.split("x"))
+        br, bc = exmy.block_shape(t.shape, blk)
+        for f in a.fmts.split(","):
+            x, y = exmy.parse_format(f)
+            k = 1 + x + y
+            m = torch.empty((R // br, C // bc), dtype=torch.uint8, device=dev)
+            ms = timeit(lambda: exmy.block_max_exponent(t, (br, bc), y, "before", out=m))
+            res[f"blkmax_{f}"] = {"ms": ms, "gbs": n * es / ms / 1e6, "frac": n * es / ms / 1e6 / peak}
+            ms = timeit(lambda: exmy.quantize_blocked(t, f, m, (br, bc), out=q))
+            res[f"bquant_{f}"] = {"ms": ms, "gbs": 2 * n * es / ms / 1e6, "frac": 2 * n * es / ms / 1e6 / peak}
+            buf = torch.empty(n * k // 8, dtype=torch.uint8, device=dev)
+            ms = timeit(lambda: exmy.encode_blocked(t, f, m, (br, bc), axis=a.axis, out=buf))
+            res[f"bencode_{f}"] = {"ms": ms, "gbs": n * (es + k / 8) / ms / 1e6,
+                                   "frac": n * (es + k / 8) / ms / 1e6 / peak}
+            p = exmy.encode_blocked(t, f, m, (br, bc), axis=a.axis, out=buf)
+            ms = timeit(lambda: exmy.decode(p, out=d))
+            res[f"bdecode_{f}"] = {"ms": ms, "gbs": n * (es + k / 8) / ms / 1e6,
+                                   "frac": n * (es + k / 8) / ms / 1e6 / peak}
     for k_, v in res.items():
         print(f"{k_:16s} {v['ms']*1e3:9.1f} us {v['gbs']:8.1f} GB/s  {v['frac']*100:5.1f}%")
     print(json.dumps(res))
