@@ -208,21 +208,22 @@ __device__ __forceinline__ uint32_t quant_pair_bf16(uint32_t w, const FastP &P, 
 
 // ------------------------------------------------------ decode helpers
 // code pair (16-bit lanes) -> bf16 pair
-template <int K>
+// TWO: o > 127, the scale 2^o is applied as an exact 2^127 then 2^(o-127)
+template <int K, bool TWO = false>
 __device__ __forceinline__ uint32_t dec_pair_bf16(uint32_t cp, const FastP &P, int y) {
     uint32_t mag = cp & (((1u << (K - 1)) - 1u) * 0x00010001u);
     uint32_t b = mag << (7 - y);
     uint32_t v = hmul2_bf16(b, P.s1_bf2);
-    if (P.two_mul) v = hmul2_bf16(v, P.s2_bf2);
+    if (TWO) v = hmul2_bf16(v, P.s2_bf2);
     return v | ((cp << (16 - K)) & 0x80008000u);
 }
 
-template <int K>
+template <int K, bool TWO = false>
 __device__ __forceinline__ uint32_t dec_f32_fast(uint32_t code, const FastP &P, int y) {
     uint32_t mag = code & ((1u << (K - 1)) - 1u);
     float f = __uint_as_float(mag << (23 - y));
     f = __fmul_rn(f, P.s1_f);
-    if (P.two_mul) f = __fmul_rn(f, P.s2_f);
+    if (TWO) f = __fmul_rn(f, P.s2_f);
     return __float_as_uint(f) | ((code << (32 - K)) & 0x80000000u);
 }
 
@@ -635,7 +636,7 @@ __device__ __forceinline__ uint32_t pair_from_lanes(uint32_t rl, uint32_t rh, ui
 // pair of codes -> pair of output words (bf16: one word; fp32: two words)
 template <int K>
 __device__ __forceinline__ uint32_t dec_pair_to_bf16(uint32_t cp, const FastP &P, const Fmt &F) {
-    if (P.dec_fast_bf) return dec_pair_bf16<K>(cp, P, F.y);
+    if (P.dec_fast_bf) return P.two_mul ? dec_pair_bf16<K, true>(cp, P, F.y) : dec_pair_bf16<K, false>(cp, P, F.y);
     return dec_code_generic<8>(cp & 0xFFFFu, F) | (dec_code_generic<8>(cp >> 16, F) << 16);
 }
 template <int K>
@@ -707,27 +708,29 @@ __device__ __forceinline__ void rows_unpack_raw(const uint32_t (&raw)[tile_words
     }
 }
 
-enum DecMode { DEC_FAST = 0, DEC_GENERIC = 1 };
+// DEC_FAST2: the fast path with o > 127 (two multiplies); kernels launched
+// as DEC_FAST switch to it on the device (warp-uniform, once per launch)
+enum DecMode { DEC_FAST = 0, DEC_GENERIC = 1, DEC_FAST2 = 2 };
 
 template <int K, bool OBF16, int MODE>
 __device__ __forceinline__ uint32_t dec_pair_bf16_m(uint32_t cp, const FastP &P, const Fmt &F) {
-    if constexpr (MODE == DEC_FAST) return dec_pair_bf16<K>(cp, P, F.y);
+    if constexpr (MODE == DEC_FAST) return dec_pair_bf16<K, false>(cp, P, F.y);
+    else if constexpr (MODE == DEC_FAST2) return dec_pair_bf16<K, true>(cp, P, F.y);
     else return dec_code_generic<8>(cp & 0xFFFFu, F) | (dec_code_generic<8>(cp >> 16, F) << 16);
 }
 template <int K, int MODE>
 __device__ __forceinline__ uint32_t dec_f32_m(uint32_t code, const FastP &P, const Fmt &F) {
-    if constexpr (MODE == DEC_FAST) return dec_f32_fast<K>(code, P, F.y);
+    if constexpr (MODE == DEC_FAST) return dec_f32_fast<K, false>(code, P, F.y);
+    else if constexpr (MODE == DEC_FAST2) return dec_f32_fast<K, true>(code, P, F.y);
     else return dec_code_generic<24>(code, F);
 }
 
 template <int K, bool OBF16, int MODE>
-__global__ void __launch_bounds__(256) k_dec_rows_fast(const uint8_t *__restrict__ packed, int64_t R, int64_t C,
-                                                       int x, int y, const uint8_t *__restrict__ meta, SegOffsets so,
-                                                       uint8_t *__restrict__ out) {
+__device__ __forceinline__ void dec_rows_body(const uint8_t *__restrict__ packed, int64_t R, int64_t C,
+                                              SegOffsets so, uint8_t *__restrict__ out, const Fmt &F,
+                                              const FastP &P) {
     using EL = Elem<OBF16>;
     constexpr int V = EL::V, NH = V / 4, TW = tile_words(K, NH);
-    const Fmt F = load_fmt(x, y, meta);
-    const FastP P = make_fast(F, false, 0);
     const int64_t CV = C / V, G = R / 8;
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= CV) return;
@@ -766,6 +769,16 @@ __global__ void __launch_bounds__(256) k_dec_rows_fast(const uint8_t *__restrict
             stg_v4(out + ((8 * g + i) * C + c0) * EL::ES, make_uint4(o[0], o[1], o[2], o[3]));
         }
     }
+}
+
+template <int K, bool OBF16, int MODE>
+__global__ void __launch_bounds__(256) k_dec_rows_fast(const uint8_t *__restrict__ packed, int64_t R, int64_t C,
+                                                       int x, int y, const uint8_t *__restrict__ meta, SegOffsets so,
+                                                       uint8_t *__restrict__ out) {
+    const Fmt F = load_fmt(x, y, meta);
+    const FastP P = make_fast(F, false, 0);
+    if (MODE == DEC_FAST && P.two_mul) dec_rows_body<K, OBF16, DEC_FAST2>(packed, R, C, so, out, F, P);
+    else dec_rows_body<K, OBF16, MODE>(packed, R, C, so, out, F, P);
 }
 
 // ---------------------------------------------------------- decode COLS
@@ -815,11 +828,8 @@ __device__ __forceinline__ void cols_fast_load(uint32_t (&RL)[8], uint32_t (&RH)
 }
 
 template <int K, bool OBF16, int MODE>
-__global__ void __launch_bounds__(256) k_dec_cols_fast(const uint8_t *__restrict__ packed, int64_t n, int x, int y,
-                                                       const uint8_t *__restrict__ meta, SegOffsets so,
-                                                       uint8_t *__restrict__ out) {
-    const Fmt F = load_fmt(x, y, meta);
-    const FastP P = make_fast(F, false, 0);
+__device__ __forceinline__ void dec_cols_body(const uint8_t *__restrict__ packed, int64_t n, SegOffsets so,
+                                              uint8_t *__restrict__ out, const Fmt &F, const FastP &P) {
     const int64_t NG = n / 8;
     const int lane = threadIdx.x & 31;
     const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -878,6 +888,16 @@ __global__ void __launch_bounds__(256) k_dec_cols_fast(const uint8_t *__restrict
             }
         }
     }
+}
+
+template <int K, bool OBF16, int MODE>
+__global__ void __launch_bounds__(256) k_dec_cols_fast(const uint8_t *__restrict__ packed, int64_t n, int x, int y,
+                                                       const uint8_t *__restrict__ meta, SegOffsets so,
+                                                       uint8_t *__restrict__ out) {
+    const Fmt F = load_fmt(x, y, meta);
+    const FastP P = make_fast(F, false, 0);
+    if (MODE == DEC_FAST && P.two_mul) dec_cols_body<K, OBF16, DEC_FAST2>(packed, n, so, out, F, P);
+    else dec_cols_body<K, OBF16, MODE>(packed, n, so, out, F, P);
 }
 
 // -------------------------------------------------------------- quantize
