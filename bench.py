@@ -301,6 +301,11 @@ def run_ours(args):
     }
     result["clocks"] = clk.summary()
 
+    # ---------------- block metadata: per-row e_max, e3m3,
+    # same tensor; timed separately (not part of `value`)
+    if not args.no_blocked:
+        result["per_row_metadata"] = bench_blocked(exmy, t, args, peak, st)
+
     # ---------------- e2e through the C ABI with host buffers (rank-local)
     e2e_steps = max(1, min(args.steps, 3))
     hc = {}
@@ -349,6 +354,56 @@ def run_ours(args):
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def bench_blocked(exmy, t, args, peak, st):
+    """Per-row metadata (the paper's quality recipe) on the bench
+    tensor: block max exponent, quantize, encode, decode (ROWS), e3m3."""
+    R_, C_ = t.shape
+    n = R_ * C_
+    x, y = 3, 3
+    k = 7
+    meta = torch.empty((R_, 1), dtype=torch.uint8, device=t.device)
+    q = torch.empty_like(t)
+    d = torch.empty_like(t)
+    buf = torch.empty(n * k // 8, dtype=torch.uint8, device=t.device)
+    ops = {
+        "block_max": (lambda: exmy.block_max_exponent(t, "row", y, "before", out=meta), 2 * n, 2 * n),
+        "quantize": (lambda: exmy.quantize_blocked(t, (x, y), meta, "row", out=q), 2 * n, 4 * n),
+        "encode": (lambda: exmy.encode_blocked(t, (x, y), meta, "row", out=buf), 2 * n, 2 * n + n * k // 8),
+    }
+    res = {}
+    reps = max(args.steps, 5)
+    for name, (fn, in_b, alg_b) in ops.items():
+        for _ in range(3):
+            fn()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(reps):
+            fn()
+        b.record(st)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / reps
+        res[name] = {"us_per_call": round(ms * 1e3, 2), "hbm_gbs": round(alg_b / ms / 1e6, 1),
+                     "frac_of_measured": round(alg_b / ms / 1e6 / peak, 4)}
+    p = exmy.encode_blocked(t, (x, y), meta, "row", out=buf)
+    for _ in range(3):
+        exmy.decode(p, out=d)
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    for _ in range(reps):
+        exmy.decode(p, out=d)
+    b.record(st)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    alg = n * k // 8 + 2 * n
+    res["decode"] = {"us_per_call": round(ms * 1e3, 2), "hbm_gbs": round(alg / ms / 1e6, 1),
+                     "frac_of_measured": round(alg / ms / 1e6 / peak, 4)}
+    res["config"] = "e3m3, ROWS packing, one metadata byte per row (block 1 x 16384), scheme max-before; " \
+                    "timed back-to-back through the Python binding (includes its per-call overhead)"
+    return res
 
 
 # ------------------------------------------------------ the oracle arm
@@ -420,6 +475,7 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--no-blocked", action="store_true", help="skip the per-row metadata section")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
