@@ -210,6 +210,18 @@ exmy_status exmy_decode_blocked(const uint8_t *packed, int64_t rows, int64_t col
                                 const uint32_t *sp_bits, const uint64_t *sp_count,
                                 int64_t sp_capacity, void *out, int out_dtype, void *stream);
 
+/* Row gather-decode (embedding lookup, "decoding
+ * ... during serving ... is performance critical").  Needs the COLS layout,
+ * where row r is the contiguous byte range off_j + [r*cols*w_j/8,
+ * (r+1)*cols*w_j/8) of every segment.  out[i, :] = decode(row row_index[i])
+ * (n_index x cols, fp32/bf16, 16-byte aligned).  meta: the per-tensor byte
+ * (meta_per_row = 0) or one byte per row (meta_per_row = 1, block 1 x cols).
+ * Row indices must lie in [0, rows) (not checked on the device).  NaN/Inf
+ * recorded out of band are NOT restored (decode the tensor for those). */
+exmy_status exmy_decode_rows(const uint8_t *packed, int64_t rows, int64_t cols, int x, int y,
+                             const uint8_t *meta, int meta_per_row, const int64_t *row_index,
+                             int64_t n_index, void *out, int out_dtype, void *stream);
+
 /* ------------------------------------------------ host-buffer conveniences */
 
 /* End-to-end encode of a HOST tensor (pinned memory recommended): H2D copy

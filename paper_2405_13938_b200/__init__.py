@@ -66,6 +66,7 @@ def _load():
         "exmy_quantize_blocked": ([vp, vp, i32, i64, i64, i64, i64, i32, i32, vp, vp], i32),
         "exmy_encode_blocked": ([vp, i32, i64, i64, i32, i64, i64, i32, i32, vp, vp, vp, vp, vp, i64, vp], i32),
         "exmy_decode_blocked": ([vp, i64, i64, i32, i64, i64, i32, i32, vp, vp, vp, vp, i64, vp, i32, vp], i32),
+        "exmy_decode_rows": ([vp, i64, i64, i32, i32, vp, i32, vp, i64, vp, i32, vp], i32),
         "exmy_encode_host": ([vp, i32, i64, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, i64, vp, vp, vp], i32),
         "exmy_decode_host": ([vp, i64, i64, i32, i32, i32, vp, vp, vp, vp, i64, vp, vp, i32, vp, vp], i32),
     }
@@ -83,7 +84,7 @@ EXPORTED = ["exmy_version", "exmy_status_string", "exmy_format_valid", "exmy_pac
             "exmy_debug_force_generic", "exmy_debug_hist_mode", "exmy_exponent_histogram",
             "exmy_emax_from_histogram", "exmy_quantize", "exmy_encode", "exmy_decode", "exmy_encode_host",
             "exmy_decode_host", "exmy_block_max_exponent", "exmy_quantize_blocked", "exmy_encode_blocked",
-            "exmy_decode_blocked"]
+            "exmy_decode_blocked", "exmy_decode_rows"]
 
 
 def lib():
@@ -411,6 +412,25 @@ def encode_blocked(t: torch.Tensor, fmt, meta: torch.Tensor | None, block, axis=
     _check(_lib.exmy_encode_blocked(_ptr(t), _dtype_code(t.dtype), R, C, ax, br, bc, x, y, _ptr(meta), _ptr(out),
                                     _ptr(spi), _ptr(spb), _ptr(spc), cap, _stream(dev)), "encode_blocked")
     return Packed(out, meta, spi, spb, spc, tuple(t.shape), x, y, ax, t.dtype, (br, bc))
+
+
+def decode_rows(p: Packed, row_index: torch.Tensor, dtype: torch.dtype | None = None,
+                out: torch.Tensor | None = None) -> torch.Tensor:
+    """Gather-decode rows of a COLS-packed tensor (embedding lookup)."""
+    if p.axis != COLS:
+        raise ValueError("row gather needs the COLS layout (rows are contiguous byte ranges)")
+    dtype = p.dtype if dtype is None else dtype
+    idx = row_index.to(device=p.data.device, dtype=torch.int64).contiguous()
+    if out is None:
+        out = torch.empty((idx.numel(), p.cols), dtype=dtype, device=p.data.device)
+    per_row = 0
+    if p.block is not None:
+        if p.block != (1, p.cols):
+            raise ValueError("gather supports per-tensor or per-row metadata")
+        per_row = 1
+    _check(_lib.exmy_decode_rows(_ptr(p.data), p.rows, p.cols, p.x, p.y, _ptr(p.meta), per_row, _ptr(idx), idx.numel(),
+                                 _ptr(out), _dtype_code(dtype), _stream(p.data.device)), "decode_rows")
+    return out
 
 
 def decode_raw(data: torch.Tensor, rows: int, cols: int, fmt, meta, axis="rows", dtype=torch.bfloat16,

@@ -269,6 +269,19 @@ exmy_status exmy_decode_blocked(const uint8_t *packed, int64_t rows, int64_t col
     return s;
 }
 
+exmy_status exmy_decode_rows(const uint8_t *packed, int64_t rows, int64_t cols, int x, int y, const uint8_t *meta,
+                             int meta_per_row, const int64_t *row_index, int64_t n_index, void *out, int out_dtype,
+                             void *stream) {
+    if (out_dtype != EXMY_F32 && out_dtype != EXMY_BF16) return EXMY_E_DTYPE;
+    if (!fmt_ok(x, y)) return EXMY_E_FORMAT;
+    if (rows < 0 || cols < 0 || cols % 8 || n_index < 0) return EXMY_E_SHAPE;
+    if (n_index == 0 || cols == 0) return EXMY_OK;
+    if (!packed || !meta || !row_index || !out) return EXMY_E_ARG;
+    if (!aligned(out, 16) || !aligned(row_index, 8)) return EXMY_E_ALIGN;
+    return launch_decode_rows_gather(packed, rows, cols, x, y, meta, meta_per_row != 0, row_index, n_index,
+                                     static_cast<uint8_t *>(out), out_dtype == EXMY_BF16, S(stream));
+}
+
 exmy_status exmy_encode_host(const void *host_in, int dtype, int64_t rows, int64_t cols, int axis, int x, int y,
                              void *dev_in, uint64_t *dev_hist, uint8_t *dev_meta, uint8_t *dev_packed,
                              int64_t *sp_index, uint32_t *sp_bits, uint64_t *sp_count, int64_t sp_capacity,

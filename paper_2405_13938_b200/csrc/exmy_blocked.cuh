@@ -669,3 +669,135 @@ __global__ void __launch_bounds__(256) k_block_max(const uint8_t *__restrict__ i
 }
 
 }  // namespace exmy
+
+namespace exmy {
+
+// ------------------------------------------- row gather-decode (COLS layout)
+// decode an arbitrary list of rows (embedding lookup).
+// In the COLS layout row r's containers are groups r*gpr .. r*gpr+gpr-1, a
+// contiguous byte range per segment, so a looked-up row reads exactly its
+// own n*k/8 bytes.  Output row i = decode(source row idx[i]).
+template <int K, int S>
+__device__ __forceinline__ void cols_gather_load(uint32_t (&RL)[8], uint32_t (&RH)[8], const uint8_t *packed,
+                                                 const SegOffsets &so, const int64_t (&src)[4], const bool (&ok)[4]) {
+    if constexpr (S < seg_count(K)) {
+        constexpr int W = seg_width(K, S), LO = seg_lo(K, S);
+        const uint8_t *seg = packed + so.off[S];
+        if constexpr (W == 8) {
+            uint32_t a[4], b[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint2 t = ok[u] ? __ldg((const uint2 *)(seg + 8 * src[u])) : make_uint2(0, 0);
+                a[u] = t.x;
+                b[u] = t.y;
+            }
+            uint32_t *dst = (K == 9) ? RH : RL;
+            const uint32_t a0 = prmt(a[0], a[1], 0x5140), a1 = prmt(a[2], a[3], 0x5140);
+            const uint32_t a2 = prmt(a[0], a[1], 0x7362), a3 = prmt(a[2], a[3], 0x7362);
+            dst[0] = prmt(a0, a1, 0x5410); dst[1] = prmt(a0, a1, 0x7632);
+            dst[2] = prmt(a2, a3, 0x5410); dst[3] = prmt(a2, a3, 0x7632);
+            const uint32_t b0 = prmt(b[0], b[1], 0x5140), b1 = prmt(b[2], b[3], 0x5140);
+            const uint32_t b2 = prmt(b[0], b[1], 0x7362), b3 = prmt(b[2], b[3], 0x7362);
+            dst[4] = prmt(b0, b1, 0x5410); dst[5] = prmt(b0, b1, 0x7632);
+            dst[6] = prmt(b2, b3, 0x5410); dst[7] = prmt(b2, b3, 0x7632);
+        } else {
+            uint32_t in[W];
+#pragma unroll
+            for (int q = 0; q < W; ++q) in[q] = 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (ok[u]) {
+                    if constexpr (W == 4) in[u] = __ldg((const unsigned int *)(seg + 4 * src[u]));
+                    else if constexpr (W == 2)
+                        in[u >> 1] |= (uint32_t)__ldg((const unsigned short *)(seg + 2 * src[u])) << (16 * (u & 1));
+                    else in[0] |= (uint32_t)__ldg((const unsigned char *)(seg + src[u])) << (8 * u);
+                }
+            }
+            swar_unpack4<W, LO>(in, RL);
+        }
+        cols_gather_load<K, S + 1>(RL, RH, packed, so, src, ok);
+    }
+}
+
+template <int K, bool OBF16, bool PERROW>
+__global__ void __launch_bounds__(256) k_dec_gather(const uint8_t *__restrict__ packed, int64_t C, int x, int y,
+                                                    const uint8_t *__restrict__ meta, const int64_t *__restrict__ idx,
+                                                    int64_t nidx, SegOffsets so, uint8_t *__restrict__ out,
+                                                    int fmt_fast) {
+    const int64_t gpr = C / 8, NG = nidx * gpr;
+    const double inv = 1.0 / (double)gpr;
+    const int lane = threadIdx.x & 31;
+    const int64_t step = (int64_t)gridDim.x * (blockDim.x >> 5) * 128;
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    RowD D0;
+    if (!PERROW) D0 = make_rowd(min((int)__ldg(meta), 254), x);
+    for (int64_t base = gw * 128; base < NG; base += step) {
+        int64_t src[4];
+        bool ok[4];
+        RowD D[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t q = base + 32 * u + lane;
+            ok[u] = q < NG;
+            const int64_t i = ok[u] ? div_rcp(q, gpr, inv) : 0;
+            const int64_t r = ok[u] ? __ldg(idx + i) : 0;
+            src[u] = r * gpr + (q - i * gpr);
+            D[u] = PERROW ? make_rowd(ok[u] ? min((int)__ldg(meta + r), 254) : 127, x) : D0;
+            D[u].ok = D[u].ok && fmt_fast;
+        }
+        uint32_t RL[8], RH[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { RL[i] = 0; RH[i] = 0; }
+        cols_gather_load<K, 0>(RL, RH, packed, so, src, ok);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t q = base + 32 * u + lane;
+            if (!OBF16) {
+                uint32_t o[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    uint32_t code = (RL[i] >> (8 * u)) & 0xFFu;
+                    if (K == 9) code |= ((RH[i] >> (8 * u)) & 0xFFu) << 1;
+                    o[i] = D[u].ok ? dec_f32_r<K>(code, y, D[u])
+                                   : dec_code_generic<24>(code, fmt_of(x, y, PERROW ? min((int)__ldg(meta + (src[u] / gpr)), 254) : min((int)__ldg(meta), 254)));
+                }
+                const int64_t g0 = base + 32 * u;   // 512-byte full-sector stores (see k_dec_cols_fast)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int srcl = 16 * h + (lane >> 1);
+                    const bool hi = lane & 1;
+                    uint32_t v[4];
+#pragma unroll
+                    for (int k2 = 0; k2 < 4; ++k2) {
+                        const uint32_t a = __shfl_sync(0xFFFFFFFFu, o[k2], srcl);
+                        const uint32_t b = __shfl_sync(0xFFFFFFFFu, o[4 + k2], srcl);
+                        v[k2] = hi ? b : a;
+                    }
+                    if (g0 + srcl < NG) stg_v4(out + (g0 * 32) + (32 * h + lane) * 16, make_uint4(v[0], v[1], v[2], v[3]));
+                }
+                continue;
+            }
+            if (q >= NG) continue;
+            uint32_t o[4];
+            const uint32_t sel = (uint32_t)u | ((uint32_t)(4 + u) << 4);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                uint32_t cp = prmt(RL[2 * t], RL[2 * t + 1], sel);
+                cp = (cp & 0xFFu) | ((cp & 0xFF00u) << 8);
+                if (K == 9) {
+                    uint32_t ch = prmt(RH[2 * t], RH[2 * t + 1], sel);
+                    cp |= ((ch & 0xFFu) | ((ch & 0xFF00u) << 8)) << 1;
+                }
+                if (D[u].ok) {
+                    o[t] = dec_pair_bf16_r<K>(cp, y, D[u]);
+                } else {
+                    const Fmt F = fmt_of(x, y, PERROW ? min((int)__ldg(meta + (src[u] / gpr)), 254) : min((int)__ldg(meta), 254));
+                    o[t] = dec_code_generic<8>(cp & 0xFFFFu, F) | (dec_code_generic<8>(cp >> 16, F) << 16);
+                }
+            }
+            stg_v4(out + q * 16, make_uint4(o[0], o[1], o[2], o[3]));
+        }
+    }
+}
+
+}  // namespace exmy

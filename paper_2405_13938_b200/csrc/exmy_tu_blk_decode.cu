@@ -70,7 +70,50 @@ exmy_status dec_blk_dispatch(int k, const uint8_t *packed, int64_t R, int64_t C,
     }
     return EXMY_E_FORMAT;
 }
+template <int K, bool OBF16>
+exmy_status launch_gather_k(const uint8_t *packed, int64_t R, int64_t C, int x, int y, const uint8_t *meta,
+                            bool per_row, const int64_t *idx, int64_t nidx, uint8_t *out, cudaStream_t st) {
+    const Plan p = make_plan(K, R * C);
+    const int fmt_fast = (!g_force_generic && x <= 7 && (!OBF16 || y <= 7)) ? 1 : 0;
+    const int threads = 256;
+    static int occ = 0;
+    if (!occ) occ = occupancy(k_dec_gather<K, OBF16, true>, threads, 0);
+    int64_t blocks = cdiv(cdiv(nidx * (C / 8), 128), threads / 32);
+    int64_t maxb = (int64_t)num_sms() * occ;
+    if (blocks > maxb) blocks = maxb;
+    if (blocks < 1) blocks = 1;
+    if (per_row)
+        k_dec_gather<K, OBF16, true><<<(unsigned)blocks, threads, 0, st>>>(packed, C, x, y, meta, idx, nidx, p.so,
+                                                                         out, fmt_fast);
+    else
+        k_dec_gather<K, OBF16, false><<<(unsigned)blocks, threads, 0, st>>>(packed, C, x, y, meta, idx, nidx, p.so,
+                                                                          out, fmt_fast);
+    return launch_status();
+}
+
+template <bool OBF16>
+exmy_status gather_dispatch(int k, const uint8_t *packed, int64_t R, int64_t C, int x, int y, const uint8_t *meta,
+                            bool per_row, const int64_t *idx, int64_t nidx, uint8_t *out, cudaStream_t st) {
+    switch (k) {
+        case 3: return launch_gather_k<3, OBF16>(packed, R, C, x, y, meta, per_row, idx, nidx, out, st);
+        case 4: return launch_gather_k<4, OBF16>(packed, R, C, x, y, meta, per_row, idx, nidx, out, st);
+        case 5: return launch_gather_k<5, OBF16>(packed, R, C, x, y, meta, per_row, idx, nidx, out, st);
+        case 6: return launch_gather_k<6, OBF16>(packed, R, C, x, y, meta, per_row, idx, nidx, out, st);
+        case 7: return launch_gather_k<7, OBF16>(packed, R, C, x, y, meta, per_row, idx, nidx, out, st);
+        case 8: return launch_gather_k<8, OBF16>(packed, R, C, x, y, meta, per_row, idx, nidx, out, st);
+        case 9: return launch_gather_k<9, OBF16>(packed, R, C, x, y, meta, per_row, idx, nidx, out, st);
+    }
+    return EXMY_E_FORMAT;
+}
 }  // namespace
+
+exmy_status launch_decode_rows_gather(const uint8_t *packed, int64_t R, int64_t C, int x, int y, const uint8_t *meta,
+                                      bool per_row, const int64_t *idx, int64_t nidx, uint8_t *out, bool obf16,
+                                      cudaStream_t st) {
+    const int k = 1 + x + y;
+    return obf16 ? gather_dispatch<true>(k, packed, R, C, x, y, meta, per_row, idx, nidx, out, st)
+                 : gather_dispatch<false>(k, packed, R, C, x, y, meta, per_row, idx, nidx, out, st);
+}
 
 exmy_status launch_decode_blocked(const uint8_t *packed, int64_t R, int64_t C, int axis, int64_t br, int64_t bc,
                                   int x, int y, const uint8_t *meta, uint8_t *out, bool obf16, cudaStream_t st) {

@@ -133,3 +133,35 @@ def test_per_row_config2_shape_sampled(exmy, orc):
         ref = orc.encode_blocked(rows, "e3m3", m, (1, C), orc.ROWS)[0]
         got = torch.cat([p.data[o + r0 * C * w // 8: o + (r0 + 8) * C * w // 8] for w, o in zip(ws, offs)])
         np.testing.assert_array_equal(got.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("fmt", [(4, 2), (3, 1), (5, 3), (2, 4), (8, 0), (0, 8)], ids=lambda f: f"e{f[0]}m{f[1]}")
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+@pytest.mark.parametrize("per_row", [False, True])
+def test_row_gather_decode(exmy, orc, fmt, dt, per_row):
+    """Embedding lookup (config 5 access pattern): decode an arbitrary list of
+    rows of a COLS-packed table == the same rows of the full decode."""
+    R, C = 1000, 136
+    t = W.f32_embedding(R, C, seed=5)
+    t = t * torch.exp2(torch.randint(-8, 8, (R, 1)).float())
+    if dt == "bf16":
+        t = t.to(torch.bfloat16)
+    bits = W.to_bits(t)
+    d = t.to(DEV)
+    rng = np.random.default_rng(1)
+    idx = rng.integers(0, R, size=777)
+    idx[:5] = [0, R - 1, 3, 3, 3]
+    if per_row:
+        meta = orc.block_max_exponent(bits, (1, C))
+        p = exmy.encode_blocked(d, fmt, torch.from_numpy(meta.copy()).to(DEV), (1, C), axis="cols")
+        full = orc.decode_blocked(orc.encode_blocked(bits, fmt, meta, (1, C), orc.COLS)[0], (R, C), fmt, meta, (1, C),
+                                  orc.COLS, out_dtype=bits.dtype)
+    else:
+        e = orc.emax(orc.histogram(bits))
+        p = exmy.encode(d, fmt, e, axis="cols")
+        full = orc.decode(orc.encode(bits, fmt, e, orc.COLS)[0], (R, C), fmt, e, orc.COLS, out_dtype=bits.dtype)
+    got = exmy.decode_rows(p, torch.from_numpy(idx))
+    np.testing.assert_array_equal(W.to_bits(got), full[idx])
+    other = torch.bfloat16 if dt == "f32" else torch.float32
+    got2 = exmy.decode_rows(p, torch.from_numpy(idx), dtype=other)
+    np.testing.assert_array_equal(W.to_bits(got2), W.to_bits(exmy.decode(p, other))[idx])
