@@ -125,6 +125,15 @@ exmy_status exmy_exponent_histogram(const void *in, int dtype, int64_t n,
  * top populated bin in [0,254] (0 if none).  One tiny launch; graph-safe. */
 exmy_status exmy_emax_from_histogram(const uint64_t *hist, uint8_t *meta, void *stream);
 
+/* Per-tensor metadata straight from the data (A2 without A1): *meta = the
+ * largest 8-bit biased exponent field of a finite element, clamped to 254
+ * (0 if none) -- the same byte exmy_emax_from_histogram gives -- as one
+ * read-only max reduction (CTAs combine with a byte compare-and-swap on the
+ * 32-bit word holding *meta; the other three bytes are preserved).  Needs a
+ * 16-byte aligned `in` (else EXMY_E_ALIGN: use the histogram path).  Use it
+ * when X is already chosen and only the bias is data-derived. */
+exmy_status exmy_max_exponent(const void *in, int dtype, int64_t n, uint8_t *meta, void *stream);
+
 /* Emulation / quantize (A3): out[i] = the eXmY grid value nearest
  * to in[i] (RTNE, saturating, subnormals, signed zero), converted RTNE to
  * the same container dtype (D21); NaN/Inf bit patterns pass through

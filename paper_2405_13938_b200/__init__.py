@@ -59,6 +59,7 @@ def _load():
         "exmy_debug_hist_mode": ([i32], i32),
         "exmy_exponent_histogram": ([vp, i32, i64, vp, vp], i32),
         "exmy_emax_from_histogram": ([vp, vp, vp], i32),
+        "exmy_max_exponent": ([vp, i32, i64, vp, vp], i32),
         "exmy_quantize": ([vp, vp, i32, i64, i32, i32, vp, vp], i32),
         "exmy_encode": ([vp, i32, i64, i64, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp], i32),
         "exmy_decode": ([vp, i64, i64, i32, i32, i32, vp, vp, vp, vp, i64, vp, i32, vp], i32),
@@ -84,7 +85,7 @@ EXPORTED = ["exmy_version", "exmy_status_string", "exmy_format_valid", "exmy_pac
             "exmy_debug_force_generic", "exmy_debug_hist_mode", "exmy_exponent_histogram",
             "exmy_emax_from_histogram", "exmy_quantize", "exmy_encode", "exmy_decode", "exmy_encode_host",
             "exmy_decode_host", "exmy_block_max_exponent", "exmy_quantize_blocked", "exmy_encode_blocked",
-            "exmy_decode_blocked", "exmy_decode_rows"]
+            "exmy_decode_blocked", "exmy_decode_rows", "exmy_max_exponent"]
 
 
 def lib():
@@ -234,9 +235,18 @@ def emax(hist: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
     return out
 
 
-def max_exponent(t: torch.Tensor) -> torch.Tensor:
-    """Histogram + e_max in one call: the per-tensor metadata of t."""
-    return emax(histogram(t))
+def max_exponent(t: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Per-tensor metadata of t (max biased exponent): one
+    read-only reduction (falls back to histogram + e_max for unaligned t)."""
+    _require_cuda(t)
+    t = t.contiguous()
+    if out is None:
+        out = torch.empty(1, dtype=torch.uint8, device=t.device)
+    s = _lib.exmy_max_exponent(_ptr(t), _dtype_code(t.dtype), t.numel(), _ptr(out), _stream(t.device))
+    if s == 5:   # E_ALIGN
+        return emax(histogram(t), out=out)
+    _check(s, "max_exponent")
+    return out
 
 
 def quantize(t: torch.Tensor, fmt, meta=None, out: torch.Tensor | None = None) -> torch.Tensor:

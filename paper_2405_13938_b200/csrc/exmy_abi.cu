@@ -138,6 +138,18 @@ exmy_status exmy_exponent_histogram(const void *in, int dtype, int64_t n, uint64
                             reinterpret_cast<unsigned long long *>(hist), S(stream));
 }
 
+exmy_status exmy_max_exponent(const void *in, int dtype, int64_t n, uint8_t *meta, void *stream) {
+    if (dtype != EXMY_F32 && dtype != EXMY_BF16) return EXMY_E_DTYPE;
+    if (n < 0) return EXMY_E_SHAPE;
+    if (!meta) return EXMY_E_ARG;
+    if (n == 0) return cudaMemsetAsync(meta, 0, 1, S(stream)) == cudaSuccess ? EXMY_OK : EXMY_E_CUDA;
+    if (!in) return EXMY_E_ARG;
+    if (!aligned(in, 16)) {   // scalar inputs: the histogram path
+        return EXMY_E_ALIGN;
+    }
+    return launch_max_exponent(static_cast<const uint8_t *>(in), dtype == EXMY_BF16, n, meta, S(stream));
+}
+
 exmy_status exmy_emax_from_histogram(const uint64_t *hist, uint8_t *meta, void *stream) {
     if (!hist || !meta) return EXMY_E_ARG;
     return launch_emax(reinterpret_cast<const unsigned long long *>(hist), meta, S(stream));

@@ -802,3 +802,89 @@ __global__ void k_specials_scatter(const int64_t *__restrict__ idx, const uint32
 }
 
 }  // namespace exmy
+
+namespace exmy {
+
+// ------------------------------------------------- K1c tensor max exponent
+// meta := max biased exponent field over the finite elements (= the top
+// populated histogram bin in [0, 254]) without building the
+// histogram: a read-only max reduction.  Grid-wide combination: each CTA
+// raises the metadata byte with a compare-and-swap on its enclosing 32-bit
+// word (other bytes preserved), skipped when the byte is already >= its max.
+__device__ __forceinline__ void byte_atomic_max(uint8_t *p, uint32_t v) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    unsigned int *w = reinterpret_cast<unsigned int *>(a & ~uintptr_t(3));
+    const int sh = (int)(a & 3) * 8;
+    unsigned int old = *reinterpret_cast<volatile unsigned int *>(w);
+    while (((old >> sh) & 0xFFu) < v) {
+        const unsigned int nw = (old & ~(0xFFu << sh)) | (v << sh);
+        const unsigned int prev = atomicCAS(w, old, nw);
+        if (prev == old) break;
+        old = prev;
+    }
+}
+
+template <bool BF16>
+__global__ void __launch_bounds__(256) k_max_exp(const uint8_t *__restrict__ in, int64_t n, uint8_t *meta) {
+    using EL = Elem<BF16>;
+    const int64_t nvec = n / EL::V;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    uint32_t amax = 0;   // bf16: 16-bit lanes of magnitudes; fp32: magnitude bits
+    constexpr int U = 4;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; base < nvec; base += stride * U) {
+        uint4 r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t vi = base + u * stride;
+            r[u] = vi < nvec ? ldg_nc_v4(in + vi * 16) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t w[4] = {r[u].x, r[u].y, r[u].z, r[u].w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (BF16) {
+                    // zero the NaN/Inf lanes (exponent 255), then lane-wise max
+                    const uint32_t a2 = w[q] & 0x7FFF7FFFu;
+                    const uint32_t sp = (a2 + 0x00800080u) & 0x80008000u;   // bit 15 of special lanes
+                    const uint32_t keep = ~((sp >> 15) * 0xFFFFu);
+                    uint32_t d;
+                    asm("max.u16x2 %0, %1, %2;" : "=r"(d) : "r"(amax), "r"(a2 & keep));
+                    amax = d;
+                } else {
+                    const uint32_t a = w[q] & 0x7FFFFFFFu;
+                    amax = max(amax, a < 0x7F800000u ? a : 0u);
+                }
+            }
+        }
+    }
+    if (blockIdx.x == 0) {   // tail elements
+        for (int64_t i = nvec * EL::V + threadIdx.x; i < n; i += blockDim.x) {
+            const uint32_t u = BF16 ? ((uint32_t)((const uint16_t *)in)[i] << 16) : ((const uint32_t *)in)[i];
+            const uint32_t a = u & 0x7FFFFFFFu;
+            if (a < 0x7F800000u) {
+                if (BF16) {
+                    uint32_t d;
+                    asm("max.u16x2 %0, %1, %2;" : "=r"(d) : "r"(amax), "r"(a >> 16));
+                    amax = d;
+                } else {
+                    amax = max(amax, a);
+                }
+            }
+        }
+    }
+    // to an exponent: bf16 lanes -> fp32 convention
+    uint32_t e = BF16 ? max((amax & 0xFFFFu) >> 7, amax >> 23) : (amax >> 23);
+    e = __reduce_max_sync(0xFFFFFFFFu, e);
+    __shared__ uint32_t wm[8];
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = e;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t m = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) m = max(m, wm[i]);
+        if (m > 254u) m = 254u;
+        byte_atomic_max(meta, m);
+    }
+}
+
+}  // namespace exmy

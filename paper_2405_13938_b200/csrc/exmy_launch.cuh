@@ -63,6 +63,7 @@ inline Plan make_plan(int k, int64_t n) {
 
 // launchers (arguments already validated by the ABI layer)
 exmy_status launch_histogram(const uint8_t *in, bool bf16, int64_t n, unsigned long long *hist, cudaStream_t st);
+exmy_status launch_max_exponent(const uint8_t *in, bool bf16, int64_t n, uint8_t *meta, cudaStream_t st);
 exmy_status launch_emax(const unsigned long long *hist, uint8_t *meta, cudaStream_t st);
 exmy_status launch_quantize(const uint8_t *in, uint8_t *out, bool bf16, int64_t n, int x, int y,
                             const uint8_t *meta, cudaStream_t st);

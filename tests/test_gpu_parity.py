@@ -352,3 +352,34 @@ def test_beyond_2e32_elements(exmy, orc, axis):
         np.testing.assert_array_equal(W.to_bits(q[r0:r0 + 8]), orc.quantize(W.to_bits(t[r0:r0 + 8]), "e3m3", e))
     h = exmy.histogram(t).cpu().numpy().astype(np.uint64)
     assert int(h.sum()) == R * C
+
+
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+@pytest.mark.parametrize("n", [1, 7, 8 * 1000 + 5, 1 << 20, (1 << 22) + 3])
+def test_max_exponent_reduction(exmy, orc, dt, n):
+    """exmy_max_exponent == top populated histogram bin in [0,254]"""
+    bits = W.random_bits_bf16(n, n + 1) if dt == "bf16" else W.random_bits_f32(n, n + 1)
+    d = dev_bits(bits)
+    assert int(exmy.max_exponent(d).item()) == orc.emax(orc.histogram(bits))
+    # peaked data, NaN/Inf-only and zero-only tensors
+    t = W.bf16_weights((n,), seed=n) if dt == "bf16" else W.f32_gradients(n, seed=n)
+    b2 = W.to_bits(t)
+    assert int(exmy.max_exponent(t.to(DEV)).item()) == orc.emax(orc.histogram(b2))
+    sp = np.full(n, 0x7FC0 if dt == "bf16" else 0x7F800000, bits.dtype)
+    assert int(exmy.max_exponent(dev_bits(sp)).item()) == 0
+    z = np.zeros(n, bits.dtype)
+    z[-1] = 0x0001    # one subnormal at the tail
+    assert int(exmy.max_exponent(dev_bits(z)).item()) == 0
+
+
+def test_max_exponent_preserves_neighbour_bytes(exmy):
+    """the byte compare-and-swap touches only the addressed metadata byte"""
+    t = W.bf16_weights((4096,), seed=2).to(DEV)
+    metas = torch.tensor([11, 22, 33, 44, 55, 66, 77, 88], dtype=torch.uint8, device=DEV)
+    for i in range(8):
+        exmy.max_exponent(t, out=metas[i:i + 1])
+    ref = int(exmy.emax(exmy.histogram(t)).item())
+    assert metas.tolist() == [ref] * 8
+    m2 = torch.tensor([1, 2, 3, 4], dtype=torch.uint8, device=DEV)
+    exmy.max_exponent(t, out=m2[2:3])
+    assert m2.tolist() == [1, 2, ref, 4]
