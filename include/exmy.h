@@ -219,6 +219,18 @@ exmy_status exmy_decode_blocked(const uint8_t *packed, int64_t rows, int64_t col
                                 const uint32_t *sp_bits, const uint64_t *sp_count,
                                 int64_t sp_capacity, void *out, int out_dtype, void *stream);
 
+/* Per-row metadata and encode in one call (the paper's per-row recipe,
+ * P:622-627): meta[r] (device, rows bytes) := the row's
+ * maximum exponent under `scheme`, then the tensor is encoded with block
+ * (1, cols) -- bit-identical to exmy_block_max_exponent + exmy_encode_blocked.
+ * ROWS with aligned 16-byte rows runs one fused kernel (each CTA reduces a
+ * row group's maxima and re-reads the rows from L2 to encode them, so HBM
+ * reads the input once); other layouts take the two-launch path. */
+exmy_status exmy_encode_rowwise(const void *in, int dtype, int64_t rows, int64_t cols, int axis,
+                                int x, int y, int scheme, uint8_t *meta, uint8_t *packed,
+                                int64_t *sp_index, uint32_t *sp_bits, uint64_t *sp_count,
+                                int64_t sp_capacity, void *stream);
+
 /* Row gather-decode (embedding lookup, "decoding
  * ... during serving ... is performance critical").  Needs the COLS layout,
  * where row r is the contiguous byte range off_j + [r*cols*w_j/8,

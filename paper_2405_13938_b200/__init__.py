@@ -67,6 +67,7 @@ def _load():
         "exmy_quantize_blocked": ([vp, vp, i32, i64, i64, i64, i64, i32, i32, vp, vp], i32),
         "exmy_encode_blocked": ([vp, i32, i64, i64, i32, i64, i64, i32, i32, vp, vp, vp, vp, vp, i64, vp], i32),
         "exmy_decode_blocked": ([vp, i64, i64, i32, i64, i64, i32, i32, vp, vp, vp, vp, i64, vp, i32, vp], i32),
+        "exmy_encode_rowwise": ([vp, i32, i64, i64, i32, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp], i32),
         "exmy_decode_rows": ([vp, i64, i64, i32, i32, vp, i32, vp, i64, vp, i32, vp], i32),
         "exmy_encode_host": ([vp, i32, i64, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, i64, vp, vp, vp], i32),
         "exmy_decode_host": ([vp, i64, i64, i32, i32, i32, vp, vp, vp, vp, i64, vp, vp, i32, vp, vp], i32),
@@ -85,7 +86,7 @@ EXPORTED = ["exmy_version", "exmy_status_string", "exmy_format_valid", "exmy_pac
             "exmy_debug_force_generic", "exmy_debug_hist_mode", "exmy_exponent_histogram",
             "exmy_emax_from_histogram", "exmy_quantize", "exmy_encode", "exmy_decode", "exmy_encode_host",
             "exmy_decode_host", "exmy_block_max_exponent", "exmy_quantize_blocked", "exmy_encode_blocked",
-            "exmy_decode_blocked", "exmy_decode_rows", "exmy_max_exponent"]
+            "exmy_decode_blocked", "exmy_decode_rows", "exmy_max_exponent", "exmy_encode_rowwise"]
 
 
 def lib():
@@ -422,6 +423,29 @@ def encode_blocked(t: torch.Tensor, fmt, meta: torch.Tensor | None, block, axis=
     _check(_lib.exmy_encode_blocked(_ptr(t), _dtype_code(t.dtype), R, C, ax, br, bc, x, y, _ptr(meta), _ptr(out),
                                     _ptr(spi), _ptr(spb), _ptr(spc), cap, _stream(dev)), "encode_blocked")
     return Packed(out, meta, spi, spb, spc, tuple(t.shape), x, y, ax, t.dtype, (br, bc))
+
+
+def encode_rowwise(t: torch.Tensor, fmt, axis="rows", scheme="before", specials_capacity: int = 4096,
+                   out: torch.Tensor | None = None, meta_out: torch.Tensor | None = None) -> Packed:
+    """Per-row metadata + encode in one call (fused single-pass kernel for ROWS)."""
+    _require_cuda(t)
+    x, y = parse_format(fmt)
+    ax = _AXES[axis]
+    t = t.contiguous()
+    R, C = _as_2d(t)
+    dev = t.device
+    n = R * C
+    k = 1 + x + y
+    if out is None:
+        out = torch.empty(n * k // 8 if n % 8 == 0 else 0, dtype=torch.uint8, device=dev)
+    meta = meta_out if meta_out is not None else torch.empty((R, 1), dtype=torch.uint8, device=dev)
+    cap = int(specials_capacity)
+    spi = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
+    spb = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    spc = torch.zeros(1, dtype=torch.int64, device=dev)
+    _check(_lib.exmy_encode_rowwise(_ptr(t), _dtype_code(t.dtype), R, C, ax, x, y, SCHEMES[scheme], _ptr(meta),
+                                    _ptr(out), _ptr(spi), _ptr(spb), _ptr(spc), cap, _stream(dev)), "encode_rowwise")
+    return Packed(out, meta, spi, spb, spc, tuple(t.shape), x, y, ax, t.dtype, (1, C))
 
 
 def decode_rows(p: Packed, row_index: torch.Tensor, dtype: torch.dtype | None = None,

@@ -281,6 +281,39 @@ exmy_status exmy_decode_blocked(const uint8_t *packed, int64_t rows, int64_t col
     return s;
 }
 
+exmy_status exmy_encode_rowwise(const void *in, int dtype, int64_t rows, int64_t cols, int axis, int x, int y,
+                                int scheme, uint8_t *meta, uint8_t *packed, int64_t *sp_index, uint32_t *sp_bits,
+                                uint64_t *sp_count, int64_t sp_capacity, void *stream) {
+    if (dtype != EXMY_F32 && dtype != EXMY_BF16) return EXMY_E_DTYPE;
+    if (!fmt_ok(x, y)) return EXMY_E_FORMAT;
+    int64_t n = 0;
+    exmy_status s = check_layout(rows, cols, axis, &n);
+    if (s != EXMY_OK) return s;
+    if (scheme != EXMY_SCHEME_MAX_BEFORE && scheme != EXMY_SCHEME_MAX_AFTER) return EXMY_E_ARG;
+    if (sp_capacity < 0) return EXMY_E_CAPACITY;
+    if (sp_capacity > 0 && (!sp_index || !sp_bits)) return EXMY_E_ARG;
+    cudaStream_t st = S(stream);
+    auto *spc = reinterpret_cast<unsigned long long *>(sp_count);
+    if (spc && cudaMemsetAsync(spc, 0, sizeof(unsigned long long), st) != cudaSuccess) return EXMY_E_CUDA;
+    if (n == 0) return EXMY_OK;
+    if (!in || !packed || !meta) return EXMY_E_ARG;
+    auto *pin = static_cast<const uint8_t *>(in);
+    const bool bf = dtype == EXMY_BF16;
+    s = EXMY_E_ALIGN;
+    if (axis == EXMY_AXIS_ROWS && !g_force_generic)
+        s = launch_encode_rowwise(pin, bf, rows, cols, x, y, scheme, meta, packed, sp_index, sp_bits, spc,
+                                  sp_capacity, st);
+    if (s == EXMY_E_ALIGN) {   // two launches: row maxima, then the blocked encode
+        s = launch_block_max(pin, bf, rows, cols, 1, cols, y, scheme, meta, st);
+        if (s != EXMY_OK) return s;
+        s = launch_encode_blocked(pin, bf, rows, cols, axis, 1, cols, x, y, meta, packed, sp_index, sp_bits, spc,
+                                  sp_capacity, st);
+    }
+    if (s != EXMY_OK) return s;
+    if (spc && sp_capacity > 1) s = launch_specials_sort(sp_index, sp_bits, spc, sp_capacity, st);
+    return s;
+}
+
 exmy_status exmy_decode_rows(const uint8_t *packed, int64_t rows, int64_t cols, int x, int y, const uint8_t *meta,
                              int meta_per_row, const int64_t *row_index, int64_t n_index, void *out, int out_dtype,
                              void *stream) {

@@ -801,3 +801,144 @@ __global__ void __launch_bounds__(256) k_dec_gather(const uint8_t *__restrict__ 
 }
 
 }  // namespace exmy
+
+namespace exmy {
+
+// ------------------------------------- fused per-row metadata + encode (ROWS)
+// "a CTA owns whole rows, so the block max fuses into one
+// encode pass".  One CTA per row group of 8 rows: pass 1 reduces the 8 row
+// maxima (16-byte loads), pass 2 re-reads the same rows -- now L2-resident,
+// the CTAs' working set is ~16*C bytes each -- and encodes them with the
+// per-row constants.  HBM reads the input once.
+
+// ROWS container (g, c) on the integer path with the 8 rows' e_max given
+template <bool BF16, int K>
+__device__ __noinline__ void enc_container_generic_rows8(const uint8_t *__restrict__ in, int64_t C, int64_t g,
+                                                         int64_t c, int x, int y, const int *e8, uint8_t *packed,
+                                                         const SegOffsets so, int64_t *spi, uint32_t *spb,
+                                                         unsigned long long *spc, int64_t cap) {
+    uint32_t cd[8];
+    int64_t e[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        e[i] = (8 * g + i) * C + c;
+        cd[i] = enc_elem(load_elem_scalar<BF16>(in, e[i]), fmt_of(x, y, e8[i]), e[i], spi, spb, spc, cap);
+    }
+    const int64_t idx = g * C + c;
+    int hi = K;
+#pragma unroll
+    for (int s = 0; s < seg_count(K); ++s) {
+        const int w = seg_width(K, s), lo = hi - w;
+        uint8_t *seg = packed + so.off[s];
+        if (w == 8) {
+            for (int i = 0; i < 8; ++i) seg[e[i]] = (uint8_t)(cd[i] >> lo);
+        } else {
+            uint32_t cont = 0;
+            for (int i = 0; i < 8; ++i) cont |= ((cd[i] >> lo) & ((1u << w) - 1u)) << (w * i);
+            for (int b = 0; b < w; ++b) seg[idx * w + b] = (uint8_t)(cont >> (8 * b));
+        }
+        hi = lo;
+    }
+}
+
+// running max of finite magnitudes (fp32-convention bits) of one 16-byte vector
+template <bool BF16>
+__device__ __forceinline__ uint32_t vec_max_mag(const uint4 &v, uint32_t m) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if (BF16) {
+            const uint32_t a2 = w[q] & 0x7FFF7FFFu;
+            const uint32_t sp = (a2 + 0x00800080u) & 0x80008000u;
+            m = vmax_u16x2(m, a2 & ~((sp >> 15) * 0xFFFFu));
+        } else {
+            const uint32_t a = w[q] & 0x7FFFFFFFu;
+            m = max(m, a < 0x7F800000u ? a : 0u);
+        }
+    }
+    return m;
+}
+
+constexpr int RW_THREADS = 512;
+
+template <int K, bool BF16, int MODE>
+__global__ void __launch_bounds__(RW_THREADS) k_enc_rowwise_rows(const uint8_t *__restrict__ in, int64_t R, int64_t C,
+                                                                 int x, int y, int scheme, uint8_t *__restrict__ meta,
+                                                                 uint8_t *__restrict__ packed, SegOffsets so,
+                                                                 int64_t *spi, uint32_t *spb,
+                                                                 unsigned long long *spc, int64_t cap,
+                                                                 int force_generic) {
+    using EL = Elem<BF16>;
+    constexpr int NW = BF16 ? 2 : 4;
+    constexpr bool SIMD = (MODE == ENC_SIMD || MODE == ENC_SIMD_Y0);
+    __shared__ uint32_t s_m[RW_THREADS / 32][8];
+    __shared__ int s_e[8];
+    const FastP P = make_fast(fmt_of(x, y, 0), BF16, 1);
+    const int64_t G = R / 8, CV16 = C / EL::V, CV4 = C / 4;
+    const int64_t rstride = C * EL::ES;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int64_t g = blockIdx.x; g < G; g += gridDim.x) {
+        // ---- pass 1: row maxima
+        uint32_t m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        const uint8_t *rg = in + 8 * g * rstride;
+        for (int64_t j = tid; j < CV16; j += RW_THREADS) {
+            uint4 v[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] = ldg_nc_v4(rg + i * rstride + j * 16);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) m[i] = vec_max_mag<BF16>(v[i], m[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t mm = BF16 ? max((m[i] & 0xFFFFu) << 16, m[i] & 0xFFFF0000u) : m[i];
+            const uint32_t r = __reduce_max_sync(0xFFFFFFFFu, mm);
+            if (lane == 0) s_m[warp][i] = r;
+        }
+        __syncthreads();
+        if (tid < 8) {
+            uint32_t r = 0;
+#pragma unroll
+            for (int w = 0; w < RW_THREADS / 32; ++w) r = max(r, s_m[w][tid]);
+            int e = scheme == 0 ? (int)(r >> 23) : exp_after_rounding(r, y);
+            e = e > 254 ? 254 : e;
+            s_e[tid] = e;
+            meta[8 * g + tid] = (uint8_t)e;
+        }
+        __syncthreads();
+        int e8[8];
+        RowP Rp[8];
+        bool ok = !force_generic;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            e8[i] = s_e[i];
+            Rp[i] = make_rowp<SIMD>(e8[i], x, y);
+            ok = ok && Rp[i].ok;
+        }
+        // ---- pass 2: encode the row group (8 x 4 tiles), input now in L2
+        for (int64_t jj = tid; jj < CV4; jj += RW_THREADS) {
+            const int64_t c0 = jj * 4;
+            uint32_t w[8][NW];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) load4<BF16>(rg + i * rstride + c0 * EL::ES, w[i]);
+            uint32_t cp[8][2];
+            uint32_t amax = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) vec_codes_r<K, BF16, MODE, NW>(w[i], cp[i], P, Rp[i], amax);
+            if (ok && !amax_special<BF16, MODE>(amax, P)) {
+                uint32_t RL[1][8], RH[1][8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    RL[0][i] = prmt(cp[i][0], cp[i][1], 0x6420);
+                    RH[0][i] = (K == 9) ? prmt(cp[i][0] >> 1, cp[i][1] >> 1, 0x6420) : 0u;
+                }
+                rows_fast_store<K, 1, 0>(RL, RH, packed, so, g, C, c0);
+            } else {
+                for (int v = 0; v < 4; ++v)
+                    enc_container_generic_rows8<BF16, K>(in, C, g, c0 + v, x, y, e8, packed, so, spi, spb, spc, cap);
+            }
+        }
+        __syncthreads();   // s_e / s_m reused by the next row group
+    }
+}
+
+}  // namespace exmy

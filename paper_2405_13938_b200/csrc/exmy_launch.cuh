@@ -87,6 +87,9 @@ exmy_status launch_encode_blocked(const uint8_t *in, bool bf16, int64_t R, int64
                                   uint32_t *spb, unsigned long long *spc, int64_t cap, cudaStream_t st);
 exmy_status launch_decode_blocked(const uint8_t *packed, int64_t R, int64_t C, int axis, int64_t br, int64_t bc,
                                   int x, int y, const uint8_t *meta, uint8_t *out, bool obf16, cudaStream_t st);
+exmy_status launch_encode_rowwise(const uint8_t *in, bool bf16, int64_t R, int64_t C, int x, int y, int scheme,
+                                  uint8_t *meta, uint8_t *packed, int64_t *spi, uint32_t *spb,
+                                  unsigned long long *spc, int64_t cap, cudaStream_t st);
 exmy_status launch_decode_rows_gather(const uint8_t *packed, int64_t R, int64_t C, int x, int y, const uint8_t *meta,
                                       bool per_row, const int64_t *idx, int64_t nidx, uint8_t *out, bool obf16,
                                       cudaStream_t st);

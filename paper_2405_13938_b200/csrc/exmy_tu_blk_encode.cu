@@ -82,7 +82,73 @@ exmy_status enc_blk_dispatch(int k, const uint8_t *in, int64_t R, int64_t C, int
     }
     return EXMY_E_FORMAT;
 }
+template <int K, bool BF16, int MODE>
+exmy_status launch_rowwise_km(const uint8_t *in, int64_t R, int64_t C, int x, int y, int scheme, uint8_t *meta,
+                              uint8_t *packed, const Plan &p, int64_t *spi, uint32_t *spb, unsigned long long *spc,
+                              int64_t cap, cudaStream_t st) {
+    static int occ = 0;
+    if (!occ) occ = occupancy(k_enc_rowwise_rows<K, BF16, MODE>, RW_THREADS, 0);
+    // the two passes of a row group must meet in L2: bound the CTAs in flight
+    // so that their working sets (16*C bytes bf16, 32*C fp32) stay well inside it
+    const int64_t ws = 8 * C * Elem<BF16>::ES;
+    int64_t maxb = (int64_t)(48ll << 20) / (ws > 0 ? ws : 1);
+    const int64_t fill = (int64_t)num_sms() * occ;
+    if (maxb > fill) maxb = fill;
+    if (maxb < num_sms()) maxb = num_sms();
+    int64_t blocks = R / 8;
+    if (blocks > maxb) blocks = maxb;
+    k_enc_rowwise_rows<K, BF16, MODE><<<(unsigned)blocks, RW_THREADS, 0, st>>>(in, R, C, x, y, scheme, meta, packed,
+                                                                               p.so, spi, spb, spc, cap,
+                                                                               g_force_generic);
+    return launch_status();
+}
+
+template <int K, bool BF16>
+exmy_status launch_rowwise_k(const uint8_t *in, int64_t R, int64_t C, int x, int y, int scheme, uint8_t *meta,
+                             uint8_t *packed, const Plan &p, int64_t *spi, uint32_t *spb, unsigned long long *spc,
+                             int64_t cap, cudaStream_t st) {
+    if (BF16 && y <= 6) {
+        if (y == 0)
+            return launch_rowwise_km<K, BF16, (BF16 ? ENC_SIMD_Y0 : ENC_F32_Y0)>(in, R, C, x, y, scheme, meta, packed,
+                                                                                 p, spi, spb, spc, cap, st);
+        return launch_rowwise_km<K, BF16, (BF16 ? ENC_SIMD : ENC_F32)>(in, R, C, x, y, scheme, meta, packed, p, spi,
+                                                                       spb, spc, cap, st);
+    }
+    if (y == 0)
+        return launch_rowwise_km<K, BF16, ENC_F32_Y0>(in, R, C, x, y, scheme, meta, packed, p, spi, spb, spc, cap, st);
+    return launch_rowwise_km<K, BF16, ENC_F32>(in, R, C, x, y, scheme, meta, packed, p, spi, spb, spc, cap, st);
+}
+
+template <bool BF16>
+exmy_status rowwise_dispatch(int k, const uint8_t *in, int64_t R, int64_t C, int x, int y, int scheme, uint8_t *meta,
+                             uint8_t *packed, const Plan &p, int64_t *spi, uint32_t *spb, unsigned long long *spc,
+                             int64_t cap, cudaStream_t st) {
+    switch (k) {
+        case 3: return launch_rowwise_k<3, BF16>(in, R, C, x, y, scheme, meta, packed, p, spi, spb, spc, cap, st);
+        case 4: return launch_rowwise_k<4, BF16>(in, R, C, x, y, scheme, meta, packed, p, spi, spb, spc, cap, st);
+        case 5: return launch_rowwise_k<5, BF16>(in, R, C, x, y, scheme, meta, packed, p, spi, spb, spc, cap, st);
+        case 6: return launch_rowwise_k<6, BF16>(in, R, C, x, y, scheme, meta, packed, p, spi, spb, spc, cap, st);
+        case 7: return launch_rowwise_k<7, BF16>(in, R, C, x, y, scheme, meta, packed, p, spi, spb, spc, cap, st);
+        case 8: return launch_rowwise_k<8, BF16>(in, R, C, x, y, scheme, meta, packed, p, spi, spb, spc, cap, st);
+        case 9: return launch_rowwise_k<9, BF16>(in, R, C, x, y, scheme, meta, packed, p, spi, spb, spc, cap, st);
+    }
+    return EXMY_E_FORMAT;
+}
 }  // namespace
+
+// returns EXMY_E_ALIGN when the fused kernel does not apply (caller then
+// runs block max + blocked encode)
+exmy_status launch_encode_rowwise(const uint8_t *in, bool bf16, int64_t R, int64_t C, int x, int y, int scheme,
+                                  uint8_t *meta, uint8_t *packed, int64_t *spi, uint32_t *spb,
+                                  unsigned long long *spc, int64_t cap, cudaStream_t st) {
+    const int k = 1 + x + y;
+    const Plan p = make_plan(k, R * C);
+    bool vec = aligned(in, 16) && (C % (bf16 ? 8 : 4) == 0);
+    for (int s = 0; s < p.nseg; ++s) vec = vec && aligned(packed + p.so.off[s], p.w[s] == 8 ? 4 : 4 * p.w[s]);
+    if (!vec) return EXMY_E_ALIGN;
+    return bf16 ? rowwise_dispatch<true>(k, in, R, C, x, y, scheme, meta, packed, p, spi, spb, spc, cap, st)
+                : rowwise_dispatch<false>(k, in, R, C, x, y, scheme, meta, packed, p, spi, spb, spc, cap, st);
+}
 
 exmy_status launch_encode_blocked(const uint8_t *in, bool bf16, int64_t R, int64_t C, int axis, int64_t br,
                                   int64_t bc, int x, int y, const uint8_t *meta, uint8_t *packed, int64_t *spi,

@@ -165,3 +165,38 @@ def test_row_gather_decode(exmy, orc, fmt, dt, per_row):
     other = torch.bfloat16 if dt == "f32" else torch.float32
     got2 = exmy.decode_rows(p, torch.from_numpy(idx), dtype=other)
     np.testing.assert_array_equal(W.to_bits(got2), W.to_bits(exmy.decode(p, other))[idx])
+
+
+@pytest.mark.parametrize("fmt", [(3, 3), (2, 4), (6, 0), (0, 6), (5, 3), (3, 1), (1, 7), (8, 0)],
+                         ids=lambda f: f"e{f[0]}m{f[1]}")
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+def test_encode_rowwise_fused(exmy, orc, fmt, dt):
+    """fused per-row metadata + encode == block max (row) + blocked encode"""
+    for shape in [(64, 192), (24, 40), (8, 4104)]:
+        bits = rowscaled_bits(shape, shape[1] + fmt[1], dt)
+        d = W.from_bits(bits).to(DEV)
+        for scheme in (0, 1):
+            meta = orc.block_max_exponent(bits, (1, shape[1]), fmt[1], scheme)
+            for axis in ("rows", "cols"):
+                if axis == "cols" and shape[1] % 8:
+                    continue
+                ax = orc.ROWS if axis == "rows" else orc.COLS
+                p = exmy.encode_rowwise(d, fmt, axis=axis, scheme=scheme, specials_capacity=bits.size)
+                np.testing.assert_array_equal(p.meta.cpu().numpy(), meta, err_msg=f"meta {shape} {axis}")
+                pref, idx, sb, ns = orc.encode_blocked(bits, fmt, meta, (1, shape[1]), ax)
+                np.testing.assert_array_equal(p.data.cpu().numpy(), pref, err_msg=f"packed {shape} {axis} {scheme}")
+                spi, spb, cnt = p.specials()
+                assert cnt == ns
+                np.testing.assert_array_equal(spi.cpu().numpy(), idx)
+                np.testing.assert_array_equal(W.to_bits(exmy.decode(p)),
+                                              orc.quantize_blocked(bits, fmt, meta, (1, shape[1])))
+
+
+def test_encode_rowwise_config2_shape(exmy, orc):
+    R = C = 16384
+    t = W.bf16_weights((R, C), seed=1, device=DEV)
+    p = exmy.encode_rowwise(t, "e3m3")
+    m = exmy.block_max_exponent(t, "row")
+    assert torch.equal(p.meta, m)
+    p2 = exmy.encode_blocked(t, "e3m3", m, "row")
+    assert torch.equal(p.data, p2.data)

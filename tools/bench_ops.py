@@ -90,6 +90,10 @@ def main():
             ms = timeit(lambda: exmy.encode_blocked(t, f, m, (br, bc), axis=a.axis, out=buf))
             res[f"bencode_{f}"] = {"ms": ms, "gbs": n * (es + k / 8) / ms / 1e6,
                                    "frac": n * (es + k / 8) / ms / 1e6 / peak}
+            if (br, bc) == (1, C):
+                ms = timeit(lambda: exmy.encode_rowwise(t, f, axis=a.axis, out=buf, meta_out=m))
+                res[f"rowwise_{f}"] = {"ms": ms, "gbs": n * (es + k / 8) / ms / 1e6,
+                                       "frac": n * (es + k / 8) / ms / 1e6 / peak}
             p = exmy.encode_blocked(t, f, m, (br, bc), axis=a.axis, out=buf)
             ms = timeit(lambda: exmy.decode(p, out=d))
             res[f"bdecode_{f}"] = {"ms": ms, "gbs": n * (es + k / 8) / ms / 1e6,
