@@ -223,9 +223,10 @@ exmy_status exmy_decode_blocked(const uint8_t *packed, int64_t rows, int64_t col
  * P:622-627): meta[r] (device, rows bytes) := the row's
  * maximum exponent under `scheme`, then the tensor is encoded with block
  * (1, cols) -- bit-identical to exmy_block_max_exponent + exmy_encode_blocked.
- * ROWS with aligned 16-byte rows runs one fused kernel (each CTA reduces a
- * row group's maxima and re-reads the rows from L2 to encode them, so HBM
- * reads the input once); other layouts take the two-launch path. */
+ * ROWS with aligned rows of at most 16 KB runs one fused kernel (each CTA
+ * reduces a row group's maxima and re-reads its rows from L2 to encode
+ * them); longer rows and COLS take the two-launch path (their L2 re-read
+ * misses; measured in DESIGN.md). */
 exmy_status exmy_encode_rowwise(const void *in, int dtype, int64_t rows, int64_t cols, int axis,
                                 int x, int y, int scheme, uint8_t *meta, uint8_t *packed,
                                 int64_t *sp_index, uint32_t *sp_bits, uint64_t *sp_count,

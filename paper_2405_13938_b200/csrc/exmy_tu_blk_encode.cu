@@ -143,7 +143,10 @@ exmy_status launch_encode_rowwise(const uint8_t *in, bool bf16, int64_t R, int64
                                   unsigned long long *spc, int64_t cap, cudaStream_t st) {
     const int k = 1 + x + y;
     const Plan p = make_plan(k, R * C);
-    bool vec = aligned(in, 16) && (C % (bf16 ? 8 : 4) == 0);
+    // measured (config-2 rows x 2048..16384 columns): the fused two-pass kernel
+    // beats block max + blocked encode while a row group (8 rows) stays within
+    // 128 KB; beyond that its second pass misses L2 and the two launches win
+    bool vec = aligned(in, 16) && (C % (bf16 ? 8 : 4) == 0) && (C * (bf16 ? 2 : 4) <= 16384);
     for (int s = 0; s < p.nseg; ++s) vec = vec && aligned(packed + p.so.off[s], p.w[s] == 8 ? 4 : 4 * p.w[s]);
     if (!vec) return EXMY_E_ALIGN;
     return bf16 ? rowwise_dispatch<true>(k, in, R, C, x, y, scheme, meta, packed, p, spi, spb, spc, cap, st)
