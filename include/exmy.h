@@ -56,6 +56,7 @@
  */
 #ifndef EXMY_H
 #define EXMY_H
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -243,6 +244,57 @@ exmy_status exmy_encode_rowwise(const void *in, int dtype, int64_t rows, int64_t
 exmy_status exmy_decode_rows(const uint8_t *packed, int64_t rows, int64_t cols, int x, int y,
                              const uint8_t *meta, int meta_per_row, const int64_t *row_index,
                              int64_t n_index, void *out, int out_dtype, void *stream);
+
+/* ------------------------------------------ grouped launch (tensor table)
+ * a model is many tensors (Llama-3 8B: 291, P:600-606
+ * "the weights of Llama"), each compressed under its own per-tensor
+ * metadata.  These calls run the per-tensor max exponent,
+ * encode (ROWS) and decode over a whole table in a constant number of
+ * launches, bit-identical to calling exmy_max_exponent / exmy_encode /
+ * exmy_decode on each entry.
+ *
+ * Usage: fill exmy_group_entry[n] (host), call exmy_group_plan into a host
+ * buffer of exmy_group_plan_bytes(n) bytes, copy those bytes once to device
+ * memory (16-byte aligned), then pass both copies to the group calls (the
+ * host copy sizes the launch, the device copy is what the kernels read).  A
+ * plan stays valid while its buffers do and can be captured in a CUDA
+ * graph.  All entries share one input dtype, one format (x, y) and one
+ * output dtype. */
+typedef struct exmy_group_entry {
+    const void *in;           /* encode / max: rows*cols elements (dtype), 16-byte aligned; may be NULL for decode-only plans */
+    void *out;                /* decode: rows*cols elements (out_dtype), 16-byte aligned; may be NULL for encode-only plans */
+    uint8_t *packed;          /* rows*cols*k/8 bytes, ROWS layout (exmy_encode's), 16-byte aligned */
+    uint8_t *meta;            /* device, one byte: the tensor's max biased exponent (written by exmy_group_max_exponent) */
+    int64_t *sp_index;        /* specials as in exmy_encode / exmy_decode (per entry); all may be NULL / 0 */
+    uint32_t *sp_bits;
+    uint64_t *sp_count;
+    int64_t sp_capacity;
+    int64_t rows, cols;       /* rows % 8 == 0, cols % 4 == 0 (ROWS layout, 8x4-element tiles) */
+} exmy_group_entry;
+
+/* Size of the plan for n entries (n >= 1). */
+size_t exmy_group_plan_bytes(int n);
+
+/* Validate the table and write the plan into `plan` (host, plan_bytes >=
+ * exmy_group_plan_bytes(n)).  dtype: input dtype; out_dtype: decode output.
+ * Errors: E_DTYPE, E_FORMAT, E_SHAPE (rows%8, cols%4, n < 1), E_ALIGN
+ * (an entry pointer not 16-byte aligned), E_ARG (NULL packed/meta, plan too
+ * small), E_CAPACITY (negative capacity).  Entries with rows*cols == 0 are
+ * allowed and skipped. */
+exmy_status exmy_group_plan(const exmy_group_entry *entries, int n, int dtype, int x, int y,
+                            int out_dtype, void *plan, size_t plan_bytes);
+
+/* meta of every entry := its max biased exponent over finite elements
+ * (== exmy_max_exponent / the top histogram bin; 0 for all-zero tensors).
+ * Two launches (clear, reduce).  Needs every entry's `in`. */
+exmy_status exmy_group_max_exponent(const void *plan_host, const void *plan_device, void *stream);
+
+/* Encode every entry (ROWS) under its meta byte; per-entry specials as in
+ * exmy_encode (counts cleared, list sorted by index).  Three launches. */
+exmy_status exmy_group_encode(const void *plan_host, const void *plan_device, void *stream);
+
+/* Decode every entry into its `out` (+ out-of-band specials).  Two launches. */
+exmy_status exmy_group_decode(const void *plan_host, const void *plan_device, void *stream);
 
 /* ------------------------------------------------ host-buffer conveniences */
 

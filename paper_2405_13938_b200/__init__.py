@@ -71,6 +71,11 @@ def _load():
         "exmy_decode_rows": ([vp, i64, i64, i32, i32, vp, i32, vp, i64, vp, i32, vp], i32),
         "exmy_encode_host": ([vp, i32, i64, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, i64, vp, vp, vp], i32),
         "exmy_decode_host": ([vp, i64, i64, i32, i32, i32, vp, vp, vp, vp, i64, vp, vp, i32, vp, vp], i32),
+        "exmy_group_plan_bytes": ([i32], ctypes.c_size_t),
+        "exmy_group_plan": ([vp, i32, i32, i32, i32, i32, vp, ctypes.c_size_t], i32),
+        "exmy_group_max_exponent": ([vp, vp, vp], i32),
+        "exmy_group_encode": ([vp, vp, vp], i32),
+        "exmy_group_decode": ([vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -86,7 +91,9 @@ EXPORTED = ["exmy_version", "exmy_status_string", "exmy_format_valid", "exmy_pac
             "exmy_debug_force_generic", "exmy_debug_hist_mode", "exmy_exponent_histogram",
             "exmy_emax_from_histogram", "exmy_quantize", "exmy_encode", "exmy_decode", "exmy_encode_host",
             "exmy_decode_host", "exmy_block_max_exponent", "exmy_quantize_blocked", "exmy_encode_blocked",
-            "exmy_decode_blocked", "exmy_decode_rows", "exmy_max_exponent", "exmy_encode_rowwise"]
+            "exmy_decode_blocked", "exmy_decode_rows", "exmy_max_exponent", "exmy_encode_rowwise",
+            "exmy_group_plan_bytes", "exmy_group_plan", "exmy_group_max_exponent", "exmy_group_encode",
+            "exmy_group_decode"]
 
 
 def lib():
@@ -277,6 +284,7 @@ class Packed:
     axis: int
     dtype: torch.dtype        # source dtype
     block: tuple | None = None   # (block_rows, block_cols) when meta is per block
+    layout: tuple | None = None  # (rows, cols) packed when not the 2-D view of shape (grouped 1-D tensors)
 
     @property
     def k(self) -> int:
@@ -284,11 +292,11 @@ class Packed:
 
     @property
     def rows(self) -> int:
-        return _as_2d_shape(self.shape)[0]
+        return (self.layout or _as_2d_shape(self.shape))[0]
 
     @property
     def cols(self) -> int:
-        return _as_2d_shape(self.shape)[1]
+        return (self.layout or _as_2d_shape(self.shape))[1]
 
     def segments(self):
         """[(width, uint8 view)] in decomposition order."""
@@ -516,3 +524,128 @@ class HostCodec:
                                      _ptr(self.spi), _ptr(self.spb), _ptr(self.spc), self.cap, _ptr(self.dev_packed),
                                      _ptr(self.dev_out), _dtype_code(self.dtype), _ptr(host_out),
                                      _stream(self.device)), "decode_host")
+
+
+# ------------------------------------------------- grouped launch (tensor table)
+class _GroupEntry(ctypes.Structure):
+    """exmy_group_entry (include/exmy.h)"""
+    _fields_ = [("in_", ctypes.c_void_p), ("out", ctypes.c_void_p), ("packed", ctypes.c_void_p),
+                ("meta", ctypes.c_void_p), ("sp_index", ctypes.c_void_p), ("sp_bits", ctypes.c_void_p),
+                ("sp_count", ctypes.c_void_p), ("sp_capacity", ctypes.c_int64), ("rows", ctypes.c_int64),
+                ("cols", ctypes.c_int64)]
+
+
+def group_layout(shape) -> tuple[int, int]:
+    """(rows, cols) a tensor is packed as in a group (ROWS layout): the 2-D view
+    of its shape; a 1-D tensor of n elements (a norm / bias vector, no rows of
+    its own) is packed as (8, n/8).  Needs rows % 8 == 0 and cols % 4 == 0."""
+    shape = tuple(shape)
+    if len(shape) == 1:
+        return (8, shape[0] // 8) if shape[0] % 32 == 0 else (-1, -1)
+    return _as_2d_shape(shape)
+
+
+def group_plan(entries, dtype, fmt, out_dtype=None) -> bytes:
+    """Host plan bytes for a list of dicts with keys of exmy_group_entry
+    (pointers as ints / tensors).  Low-level: see GroupCodec."""
+    x, y = parse_format(fmt)
+    n = len(entries)
+    arr = (_GroupEntry * max(n, 1))()
+    for i, e in enumerate(entries):
+        for f, _ in _GroupEntry._fields_:
+            v = e.get(f[:-1] if f == "in_" else f, 0)
+            if isinstance(v, torch.Tensor):
+                v = v.data_ptr()
+            setattr(arr[i], f, v or 0)
+    nb = _lib.exmy_group_plan_bytes(n)
+    buf = (ctypes.c_uint64 * max(1, (nb + 7) // 8))()
+    _check(_lib.exmy_group_plan(arr if n else None, n, _dtype_code(dtype), x, y,
+                                _dtype_code(out_dtype if out_dtype is not None else dtype), buf, nb), "group_plan")
+    return bytes(buf)[:nb]
+
+
+class GroupCodec:
+    """Whole-model codec over a table of tensors: per-tensor
+    metadata (max biased exponent), ROWS encode and decode of every
+    tensor in a constant number of launches (exmy_group_*), bit-identical to
+    exmy.encode / exmy.decode of each tensor in its group_layout.
+
+        g = GroupCodec(weights, "e3m3")
+        packed = g.encode()          # list[Packed]
+        outs = g.decode()            # list[Tensor] (out_dtype, default: input dtype)
+
+    The device buffers (packed bytes, metadata, specials, outputs) are owned
+    here and reused by every call; the plan is copied to the device once, so
+    the calls can be captured in a CUDA graph."""
+
+    def __init__(self, tensors, fmt, out_dtype=None, specials_capacity: int = 0, decode_outputs: bool = True):
+        tensors = [t.contiguous() for t in tensors]
+        if not tensors:
+            raise ValueError("empty tensor table")
+        _require_cuda(*tensors)
+        self.x, self.y = parse_format(fmt)
+        self.k = 1 + self.x + self.y
+        self.dtype = tensors[0].dtype
+        if any(t.dtype != self.dtype for t in tensors):
+            raise TypeError("all tensors of a group share one dtype")
+        self.out_dtype = self.dtype if out_dtype is None else out_dtype
+        self.device = tensors[0].device
+        dev = self.device
+        self.tensors = tensors
+        self.layouts = [group_layout(t.shape) for t in tensors]
+        n = len(tensors)
+        self.meta = torch.zeros(n, dtype=torch.uint8, device=dev)
+        self.packed = [torch.empty(max(R * C, 0) * self.k // 8, dtype=torch.uint8, device=dev)
+                       for R, C in self.layouts]
+        cap = int(specials_capacity)
+        self.cap = cap
+        self.spi = torch.empty((n, max(cap, 1)), dtype=torch.int64, device=dev)
+        self.spb = torch.empty((n, max(cap, 1)), dtype=torch.int32, device=dev)
+        self.spc = torch.zeros(n, dtype=torch.int64, device=dev)
+        self.outs = [torch.empty(t.shape, dtype=self.out_dtype, device=dev) for t in tensors] if decode_outputs \
+            else None
+        ents = []
+        for i, (t, (R, C)) in enumerate(zip(tensors, self.layouts)):
+            if R < 0 or C < 0:
+                raise ValueError(f"tensor {i} of shape {tuple(t.shape)}: a 1-D group member needs n % 32 == 0")
+            ents.append({"in": t.data_ptr(), "out": self.outs[i].data_ptr() if self.outs else 0,
+                         "packed": self.packed[i].data_ptr(), "meta": self.meta.data_ptr() + i,
+                         "sp_index": self.spi[i].data_ptr() if cap else 0,
+                         "sp_bits": self.spb[i].data_ptr() if cap else 0,
+                         "sp_count": self.spc[i].data_ptr(), "sp_capacity": cap, "rows": R, "cols": C})
+        self.plan_host = torch.frombuffer(bytearray(group_plan(ents, self.dtype, (self.x, self.y), self.out_dtype)),
+                                          dtype=torch.uint8).clone()   # torch allocation: 64-byte aligned
+        self.plan_dev = self.plan_host.to(dev)
+        self._ph = ctypes.c_void_p(self.plan_host.data_ptr())
+
+    def _call(self, fn, what):
+        _check(fn(self._ph, _ptr(self.plan_dev), _stream(self.device)), what)
+
+    def max_exponent(self) -> torch.Tensor:
+        """meta[i] := max biased exponent of tensor i (2 launches)."""
+        self._call(_lib.exmy_group_max_exponent, "group_max_exponent")
+        return self.meta
+
+    def encode(self, meta: torch.Tensor | None = None) -> list:
+        """Encode every tensor; meta=None derives the per-tensor metadata first."""
+        if meta is None:
+            self.max_exponent()
+        else:
+            self.meta.copy_(meta)
+        self._call(_lib.exmy_group_encode, "group_encode")
+        return self.packed_list()
+
+    def packed_list(self) -> list:
+        res = []
+        for i, (t, lay) in enumerate(zip(self.tensors, self.layouts)):
+            res.append(Packed(self.packed[i], self.meta[i:i + 1], self.spi[i], self.spb[i], self.spc[i:i + 1],
+                              tuple(t.shape), self.x, self.y, ROWS, self.dtype, None,
+                              lay if t.dim() == 1 else None))
+        return res
+
+    def decode(self) -> list:
+        """Decode every tensor's packed bytes into self.outs (+ specials)."""
+        if self.outs is None:
+            raise ValueError("GroupCodec built with decode_outputs=False")
+        self._call(_lib.exmy_group_decode, "group_decode")
+        return self.outs

@@ -20,8 +20,8 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v
 
 # one translation unit per op family so they compile in parallel
 UNITS = ["exmy_abi.cu", "exmy_tu_hist.cu", "exmy_tu_quant.cu", "exmy_tu_encode.cu", "exmy_tu_decode.cu",
-         "exmy_tu_blk_encode.cu", "exmy_tu_blk_decode.cu"]
-HEADERS = ["exmy_device.cuh", "exmy_kernels.cuh", "exmy_fast.cuh", "exmy_blocked.cuh", "exmy_launch.cuh"]
+         "exmy_tu_blk_encode.cu", "exmy_tu_blk_decode.cu", "exmy_tu_grouped.cu"]
+HEADERS = ["exmy_device.cuh", "exmy_kernels.cuh", "exmy_fast.cuh", "exmy_blocked.cuh", "exmy_launch.cuh", "exmy_grouped.cuh"]
 
 
 def _sources():
@@ -68,6 +68,31 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         print(f"built {LIB}", file=sys.stderr)
     return LIB
+
+
+def build_variant(out: str, extra: list[str], units=("exmy_tu_grouped.cu",)) -> str:
+    """A/B builds: recompile `units` with extra nvcc flags (e.g. -DNAME=V) and
+    link them with the main build's other objects into `out`."""
+    build()
+    vdir = os.path.join(BUILD, "variant_" + os.path.basename(out).replace(".so", ""))
+    os.makedirs(vdir, exist_ok=True)
+    objs = []
+    for u in UNITS:
+        if u in units:
+            obj = os.path.join(vdir, u.replace(".cu", ".o"))
+            r = subprocess.run([NVCC, *ARCH, *FLAGS, *extra, "-c", os.path.join(CSRC, u), "-o", obj],
+                               capture_output=True, text=True)
+            if r.returncode != 0:
+                raise RuntimeError(f"nvcc failed for {u}:\n{r.stderr}")
+            with open(os.path.join(vdir, "ptxas.log"), "w") as f:
+                f.write(r.stdout + r.stderr)
+            objs.append(obj)
+        else:
+            objs.append(os.path.join(BUILD, u.replace(".cu", ".o")))
+    r = subprocess.run([NVCC, *ARCH, "-shared", "-o", out, *objs, "-lcudart"], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"link failed:\n{r.stderr}")
+    return out
 
 
 if __name__ == "__main__":

@@ -20,7 +20,11 @@ exmy_status launch_encode_km(const uint8_t *in, int64_t R, int64_t C, int axis, 
             if (!occ) occ = occupancy(k_enc_rows_fast<K, BF16, MODE>, threads, 0);
             const int64_t CV = C / 4, G = R / 8;
             int64_t gx = cdiv(CV, threads);
+#ifdef ENC_OCC_CAP   // A/B experiments: CTAs per SM
+            int64_t target = (int64_t)num_sms() * (occ < ENC_OCC_CAP ? occ : ENC_OCC_CAP);
+#else
             int64_t target = (int64_t)num_sms() * occ;
+#endif
             int64_t gy = target / gx;
             if (gy < 1) gy = 1;
             if (gy > G) gy = G;

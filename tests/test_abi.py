@@ -113,3 +113,59 @@ def test_device_ops_validate_before_launch(exmy):
     assert L.exmy_emax_from_histogram(None, fake, None) == 8
     for s in range(9):
         assert L.exmy_status_string(s)
+
+
+def test_group_plan_host(exmy):
+    """exmy_group_plan is host code: chunk bookkeeping and validation
+    (include/exmy.h, grouped launch) checked without a device."""
+    import struct
+    import torch
+    A = 0x10000
+
+    def ent(i, rows, cols, **kw):
+        e = {"in": A * (i + 1), "packed": A * (i + 100), "meta": A * 1000 + i, "rows": rows, "cols": cols}
+        e.update(kw)
+        return e
+
+    # bf16: 8 elements per 16-byte vector, 1024 vectors per max chunk; 256 8x4 tiles per tile chunk
+    ents = [ent(0, 64, 4096), ent(1, 0, 4), ent(2, 8, 4), ent(3, 8, 512)]
+    b = exmy.group_plan(ents, torch.bfloat16, "e3m3")
+    assert len(b) == 64 + 4 * 128
+    magic, n, dt, x, y, odt, vc, tc, dc, nh, sp = struct.unpack("<Iiiiiiqqqii", b[:56])
+    assert (n, dt, x, y, odt, nh, sp) == (4, 1, 3, 3, 1, 1, 0)   # cols 4 -> 8x4 decode tiles
+    vchunks = [32, 0, 1, 1]                  # 64*4096/8/1024, -, 32/8 -> 1, 4096/8/1024 -> 1
+    tchunks = [(8 * 1024) // 2048, 0, 1, 1]  # encode: CTA chunks of 8 x 256 8x4 tiles
+    dchunks = [(8 * 1024) // 256, 0, 1, 1]   # decode: CTA chunks of 256 tiles
+    assert vc == sum(vchunks) and tc == sum(tchunks) and dc == sum(dchunks)
+    for i in range(4):
+        rows, cols, vb, tb, db = struct.unpack("<qqqqq", b[64 + 128 * i + 64:64 + 128 * i + 104])
+        assert (rows, cols) == (ents[i]["rows"], ents[i]["cols"])
+        assert vb == sum(vchunks[:i]) and tb == sum(tchunks[:i]) and db == sum(dchunks[:i])
+    # every cols % 8 == 0 and bf16 output: 8x8 decode tiles, half the chunks
+    b = exmy.group_plan([ent(0, 64, 4096), ent(1, 8, 8)], torch.bfloat16, "e3m3")
+    tc, dc, nh = struct.unpack("<qqi", b[32:52])
+    assert (tc, dc, nh) == (4 + 1, 16 + 1, 2)
+    # fp32: 4 elements per vector
+    b = exmy.group_plan([ent(0, 64, 4096)], torch.float32, "e2m4", torch.bfloat16)
+    assert struct.unpack("<q", b[24:32])[0] == 64 * 4096 // 4 // 1024
+    bad = [
+        ([ent(0, 12, 8)], 3),                      # rows % 8
+        ([ent(0, 8, 6)], 3),                       # cols % 4
+        ([ent(0, 8, 8, packed=0)], 8),             # NULL packed
+        ([ent(0, 8, 8, meta=0)], 8),               # NULL meta
+        ([ent(0, 8, 8, packed=A + 8)], 5),         # misaligned
+        ([ent(0, 8, 8, sp_capacity=-1)], 6),
+        ([ent(0, 8, 8, sp_capacity=4)], 8),        # capacity without buffers
+    ]
+    for ents, status in bad:
+        with pytest.raises(exmy.ExmyError) as ei:
+            exmy.group_plan(ents, torch.bfloat16, "e3m3")
+        assert ei.value.status == status
+    with pytest.raises(exmy.ExmyError):
+        exmy.group_plan([], torch.bfloat16, "e3m3")
+    assert exmy.group_layout((4096,)) == (8, 512)
+    assert exmy.group_layout((3, 5, 8)) == (15, 8)
+    # the device calls check the plan before launching anything
+    L = exmy.lib()
+    junk = (ctypes.c_uint64 * 16)()
+    assert L.exmy_group_encode(junk, junk, None) == 8

@@ -2,7 +2,8 @@
 params, N(0,0.02^2), norms = 1), per-tensor metadata from the histogram,
 ROWS packing to e2m2 / e3m3 / e2m4.  Times the whole model: histogram ->
 e_max -> encode per tensor, then decode, with eager launches and with the
-same launches captured in a CUDA graph.
+same launches captured in a CUDA graph; and the grouped launch
+(GroupCodec: max exponent + encode of all tensors in 3 launches, decode in 1).
 python tools/bench_llama.py [--fmt e3m3] [--layers 32]"""
 import argparse
 import json
@@ -23,6 +24,8 @@ def main():
     ap.add_argument("--fmt", default="e3m3")
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--only", default="", help="comma list of timings to run (default: all)")
+    ap.add_argument("--no-graph", action="store_true")
     a = ap.parse_args()
     dev = torch.device("cuda")
     shapes = [s for s in W.llama3_8b_shapes() if not s[0].startswith("layers.") or
@@ -80,9 +83,25 @@ def main():
         torch.cuda.synchronize()
         return s.elapsed_time(e) / a.reps
 
+    grp = exmy.GroupCodec([t for t, _ in tensors], (x, y))
+
+    def group_encode():   # grouped launch: meta (2 launches) + encode (1)
+        grp.encode()
+
+    def group_decode():
+        grp.decode()
+
     res = {"tensors": len(tensors), "params": nparams, "fmt": a.fmt}
-    for name, fn in (("encode", encode_all), ("encode_maxexp", encode_all_max), ("decode", decode_all)):
+    nl = {"encode": 3 * len(tensors), "encode_maxexp": 2 * len(tensors), "decode": len(tensors),
+          "group_encode": 3, "group_decode": 1}
+    for name, fn in (("encode", encode_all), ("encode_maxexp", encode_all_max), ("decode", decode_all),
+                     ("group_encode", group_encode), ("group_decode", group_decode)):
+        if a.only and name not in a.only.split(","):
+            continue
         ms = time(fn)
+        if a.no_graph:
+            print(f"{name}: eager {ms:.3f} ms")
+            continue
         g = torch.cuda.CUDAGraph()
         st = torch.cuda.Stream()
         st.wait_stream(torch.cuda.current_stream())
@@ -92,10 +111,10 @@ def main():
         with torch.cuda.graph(g):
             fn()
         ms_g = time(g.replay)
-        alg = nparams * ((2 + 2 + k / 8) if name.startswith("encode") else (k / 8 + 2))
+        alg = nparams * ((2 + 2 + k / 8) if "encode" in name else (k / 8 + 2))
         res[name] = {"eager_ms": ms, "graph_ms": ms_g, "eager_hbm_gbs": alg / ms / 1e6,
                      "graph_hbm_gbs": alg / ms_g / 1e6,
-                     "launches": len(tensors) * {"encode": 3, "encode_maxexp": 2, "decode": 1}[name]}
+                     "launches": nl[name]}
         print(f"{name}: eager {ms:.3f} ms ({alg / ms / 1e6:.0f} GB/s)  graph {ms_g:.3f} ms ({alg / ms_g / 1e6:.0f} GB/s)")
     print(json.dumps(res))
 
