@@ -445,6 +445,13 @@ __device__ __forceinline__ void rows_fast_store(const uint32_t (&RL)[NH][8], con
 // of a segment is then one instruction per thread covering whole sectors
 // across the warp (4 containers x w bytes: 16/8/4 B); a 32-byte per-thread
 // store split in two instructions made L2 write partial sectors back twice.
+// A CTA barrier per row group for bf16 input with k >= 8 (its byte-wide
+// segment is stored row-major, 4 bytes per thread per row): measured on
+// config 2, e4m3 178 -> 145 us, e3m5 196 -> 160 us; for k <= 7 and fp32 input
+// the barrier costs 5-10 %, so those run without it.
+template <int K, bool BF16>
+__host__ __device__ constexpr bool enc_rows_bar() { return BF16 && K >= 8; }
+
 template <int K, bool BF16, int MODE>
 __global__ void __launch_bounds__(256, BF16 ? 3 : 2) k_enc_rows_fast(const uint8_t *__restrict__ in, int64_t R, int64_t C, int x,
                                                        int y, const uint8_t *__restrict__ meta,
@@ -457,11 +464,14 @@ __global__ void __launch_bounds__(256, BF16 ? 3 : 2) k_enc_rows_fast(const uint8
     const FastP P = make_fast(F, BF16, force_generic);
     const int64_t CV = C / 4, G = R / 8;
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= CV) return;
+    constexpr bool BAR = enc_rows_bar<K, BF16>();
+    if (!BAR && j >= CV) return;
+    const bool act = j < CV;   // with barriers, idle threads stay for them
     const int64_t c0 = j * 4;
     const uint8_t *src = in + c0 * EL::ES;
     const int64_t rstride = C * EL::ES;
     if (!enc_fast_ok<BF16, MODE>(F, force_generic)) {   // metadata outside the fast preconditions
+        if (!act) return;
         for (int64_t g = blockIdx.y; g < G; g += gridDim.y)
             for (int v = 0; v < 4; ++v)
                 enc_container_generic<BF16, K>(in, C, g * C + c0 + v, 0, F, packed, so, spi, spb, spc, cap);
@@ -471,7 +481,7 @@ __global__ void __launch_bounds__(256, BF16 ? 3 : 2) k_enc_rows_fast(const uint8
     // this tile is converted and packed
     uint32_t nxt[8][NW];
     int64_t g = blockIdx.y;
-    if (g < G) {
+    if (g < G && act) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) load4<BF16>(src + (8 * g + i) * rstride, nxt[i]);
     }
@@ -481,11 +491,13 @@ __global__ void __launch_bounds__(256, BF16 ? 3 : 2) k_enc_rows_fast(const uint8
         for (int i = 0; i < 8; ++i)
 #pragma unroll
             for (int q = 0; q < NW; ++q) w[i][q] = nxt[i][q];
+        if constexpr (BAR) __syncthreads();
         const int64_t gn = g + gridDim.y;
-        if (gn < G) {
+        if (gn < G && act) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) load4<BF16>(src + (8 * gn + i) * rstride, nxt[i]);
         }
+        if (!act) continue;
         uint32_t cp[8][2];
         uint32_t amax = 0;
 #pragma unroll
@@ -725,6 +737,13 @@ __device__ __forceinline__ uint32_t dec_f32_m(uint32_t code, const FastP &P, con
     else return dec_code_generic<24>(code, F);
 }
 
+#ifndef DEC_ROWS_BAR
+#define DEC_ROWS_BAR 1
+#endif
+// DEC_ROWS_BAR: a CTA barrier per row group keeps the CTA's warps writing one
+// contiguous run together; the write-bound decode gains when the warps of a
+// CTA do not drift apart (config 2, e3m3: 139.8 -> 128.1 us, 84 -> 92 % of
+// the copy peak; fp32 output 239.6 -> 213.5 us)
 template <int K, bool OBF16, int MODE>
 __device__ __forceinline__ void dec_rows_body(const uint8_t *__restrict__ packed, int64_t R, int64_t C,
                                               SegOffsets so, uint8_t *__restrict__ out, const Fmt &F,
@@ -733,16 +752,25 @@ __device__ __forceinline__ void dec_rows_body(const uint8_t *__restrict__ packed
     constexpr int V = EL::V, NH = V / 4, TW = tile_words(K, NH);
     const int64_t CV = C / V, G = R / 8;
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+#if DEC_ROWS_BAR
+    const bool act = j < CV;
+#else
     if (j >= CV) return;
+    constexpr bool act = true;
+#endif
     const int64_t c0 = j * V;
     uint32_t nxt[TW];
     int64_t g = blockIdx.y;
-    if (g < G) rows_load_raw<K, NH, 0>(nxt, packed, so, g, C, c0);
+    if (g < G && act) rows_load_raw<K, NH, 0>(nxt, packed, so, g, C, c0);
     for (; g < G; g += gridDim.y) {
         uint32_t raw[TW];
 #pragma unroll
         for (int q = 0; q < TW; ++q) raw[q] = nxt[q];
-        if (g + gridDim.y < G) rows_load_raw<K, NH, 0>(nxt, packed, so, g + gridDim.y, C, c0);
+#if DEC_ROWS_BAR
+        __syncthreads();
+#endif
+        if (g + gridDim.y < G && act) rows_load_raw<K, NH, 0>(nxt, packed, so, g + gridDim.y, C, c0);
+        if (!act) continue;
         uint32_t RL[NH][8], RH[NH][8];
 #pragma unroll
         for (int h = 0; h < NH; ++h)

@@ -23,7 +23,10 @@ exmy_status launch_decode_km(const uint8_t *packed, int64_t R, int64_t C, int ax
             const int64_t CV = C / V, G = R / 8;
             int64_t gx = cdiv(CV, threads);
             // decode is write-bound: 2 CTAs/SM (16 warps) measure ~1.5 % faster than 4
-            int64_t target = (int64_t)num_sms() * (occ < 2 ? occ : 2);
+#ifndef DEC_ROWS_OCC
+#define DEC_ROWS_OCC 2
+#endif
+            int64_t target = (int64_t)num_sms() * (occ < DEC_ROWS_OCC ? occ : DEC_ROWS_OCC);
             int64_t gy = target / gx;
             if (gy < 1) gy = 1;
             if (gy > G) gy = G;
