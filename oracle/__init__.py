@@ -28,7 +28,7 @@ def build(force: bool = False) -> str:
     newest = max(os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "exmy_oracle.h")))
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < newest:
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-fno-tree-vectorize", "-std=c11", "-Wall", "-Wextra",
+        subprocess.check_call(["gcc", "-O2", "-fno-tree-vectorize", "-ffp-contract=off", "-std=c11", "-Wall", "-Wextra",
                                "-shared", "-fPIC", "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
@@ -73,6 +73,17 @@ def lib():
         L.oracle_encode_blocked.argtypes = [vp, i32, i64, i64, i32, i64, i64, i32, i32, vp, vp, vp, vp, i64]
         L.oracle_encode_blocked.restype = i64
         L.oracle_decode_blocked.argtypes = [vp, i64, i64, i32, i64, i64, i32, i32, vp, vp, vp, i64, vp, i32]
+        L.oracle_fs_grid_top.argtypes = [i32, i32]
+        L.oracle_fs_grid_top.restype = dbl
+        L.oracle_block_float_scale.argtypes = [vp, i32, i64, i64, i64, i64, vp]
+        L.oracle_fs_scale_in.argtypes = [u32, u32, i32, i32]
+        L.oracle_fs_scale_in.restype = u32
+        L.oracle_fs_scale_out.argtypes = [u32, u32, i32, i32]
+        L.oracle_fs_scale_out.restype = u32
+        L.oracle_quantize_fs.argtypes = [vp, vp, i32, i64, i64, i64, i64, i32, i32, vp]
+        L.oracle_encode_fs.argtypes = [vp, i32, i64, i64, i32, i64, i64, i32, i32, vp, vp, vp, vp, i64]
+        L.oracle_encode_fs.restype = i64
+        L.oracle_decode_fs.argtypes = [vp, i64, i64, i32, i64, i64, i32, i32, vp, vp, vp, i64, vp, i32]
     return _lib
 
 
@@ -284,5 +295,81 @@ def decode_blocked(packed, shape, fmt, meta, block, axis: int = ROWS, sp_index=N
     odt = BF16 if out.dtype == np.uint16 else F32
     if lib().oracle_decode_blocked(_p(packed), rows, cols, axis, block[0], block[1], x, y, _p(m), _p(sp_index),
                                    _p(sp_bits), cnt, _p(out), odt):
+        raise ValueError("invalid arguments")
+    return out
+
+
+# ------------------------------------------------------------ float scaling
+# reading D23: per-block fp32 metadata = largest finite |v|, e_max fixed 127
+def fs_grid_top(fmt) -> float:
+    x, y = parse_format(fmt)
+    return lib().oracle_fs_grid_top(x, y)
+
+
+def block_float_scale(bits: np.ndarray, block) -> np.ndarray:
+    """fp32 bit patterns (uint32) of each block's largest finite magnitude."""
+    bits = np.ascontiguousarray(bits)
+    rows, cols = bits.shape
+    br, bc = block
+    amax = np.zeros((rows // br) * (cols // bc), np.uint32)
+    if lib().oracle_block_float_scale(_p(bits), _dtype_code(bits), rows, cols, br, bc, _p(amax)):
+        raise ValueError("bad block shape")
+    return amax.reshape(rows // br, cols // bc)
+
+
+def fs_scale_in(v_bits: int, amax_bits: int, fmt) -> int:
+    x, y = parse_format(fmt)
+    return lib().oracle_fs_scale_in(v_bits, amax_bits, x, y)
+
+
+def fs_scale_out(code: int, amax_bits: int, fmt) -> int:
+    x, y = parse_format(fmt)
+    return lib().oracle_fs_scale_out(code, amax_bits, x, y)
+
+
+def quantize_fs(bits: np.ndarray, fmt, amax: np.ndarray, block) -> np.ndarray:
+    x, y = parse_format(fmt)
+    bits = np.ascontiguousarray(bits)
+    rows, cols = bits.shape
+    a = np.ascontiguousarray(amax, np.uint32)
+    out = np.empty_like(bits)
+    if lib().oracle_quantize_fs(_p(bits), _p(out), _dtype_code(bits), rows, cols, block[0], block[1], x, y, _p(a)):
+        raise ValueError("invalid arguments")
+    return out
+
+
+def encode_fs(bits: np.ndarray, fmt, amax: np.ndarray, block, axis: int = ROWS):
+    x, y = parse_format(fmt)
+    bits = np.ascontiguousarray(bits)
+    rows, cols = bits.shape
+    a = np.ascontiguousarray(amax, np.uint32)
+    k = 1 + x + y
+    packed = np.empty(rows * cols * k // 8, np.uint8)
+    cap = rows * cols
+    idx = np.empty(max(cap, 1), np.int64)
+    sb = np.empty(max(cap, 1), np.uint32)
+    ns = lib().oracle_encode_fs(_p(bits), _dtype_code(bits), rows, cols, axis, block[0], block[1], x, y, _p(a),
+                                _p(packed), _p(idx), _p(sb), cap)
+    if ns < 0:
+        raise ValueError("invalid arguments")
+    return packed, idx[:ns].copy(), sb[:ns].copy(), int(ns)
+
+
+def decode_fs(packed, shape, fmt, amax, block, axis: int = ROWS, sp_index=None, sp_bits=None,
+              out_dtype=np.uint16) -> np.ndarray:
+    x, y = parse_format(fmt)
+    rows, cols = shape
+    packed = np.ascontiguousarray(packed, dtype=np.uint8)
+    a = np.ascontiguousarray(amax, np.uint32)
+    if sp_index is None:
+        sp_index, sp_bits, cnt = np.zeros(1, np.int64), np.zeros(1, np.uint32), 0
+    else:
+        sp_index = np.ascontiguousarray(sp_index, np.int64)
+        sp_bits = np.ascontiguousarray(sp_bits, np.uint32)
+        cnt = sp_index.size
+    out = np.empty((rows, cols), dtype=out_dtype)
+    odt = BF16 if out.dtype == np.uint16 else F32
+    if lib().oracle_decode_fs(_p(packed), rows, cols, axis, block[0], block[1], x, y, _p(a), _p(sp_index),
+                              _p(sp_bits), cnt, _p(out), odt):
         raise ValueError("invalid arguments")
     return out

@@ -616,3 +616,184 @@ int oracle_decode_blocked(const uint8_t *packed, int64_t rows, int64_t cols, int
     }
     return 0;
 }
+
+/* ======================================================= float scaling */
+/* The third Fig. 2 scheme, "float scaling with maximum exponent of 127"
+ * ("an additional bfloat16 or float32 scaling factor").
+ * Reading D23: every block stores one fp32 metadata value, its
+ * largest finite magnitude amax, and uses e_max = 127, whose grid top is
+ * G = the largest magnitude code's value at e_max 127.  The block is mapped
+ * onto that grid by the factor G/amax and decoded with amax/G, so its maximum
+ * lands on G and comes back as amax ("captures the largest value in the
+ * block accurately").  Step by step, with amax = A1 * 2^p, A1 in [1, 2):
+ *   encode  r  = RN32(G / A1)                      (exact quotient, rounded once)
+ *           u  = RN32(v * r * 2^-p)                (exact product, rounded once)
+ *           code = the e_max-127 code of u         (as oracle_encode)
+ *   decode  c  = RN64(1 / G)
+ *           s  = RN64(A1 * c) * 2^p                (fp64; the power of 2 is exact)
+ *           out = RN32(RN64(g * s)), g = the code's value at e_max 127;
+ *           bf16 output = RN16 of that fp32 value  (reading D24)
+ * amax = 0 (no finite non-zero element): u = v * 0, codes are signed zeros. */
+
+double oracle_fs_grid_top(int x, int y)
+{
+    return oracle_code_magnitude((1u << (x + y)) - 1u, x, y, 127);
+}
+
+/* amax = A1 * 2^p, A1 in [1, 2) (subnormal amax normalised) */
+static void fs_split(uint32_t amax_bits, double *A1, int *p)
+{
+    double a = f32_value(amax_bits & 0x7FFFFFFFu);
+    int e;
+    double f = frexp(a, &e);          /* a = f * 2^e, f in [0.5, 1) */
+    *A1 = 2.0 * f;                    /* exact */
+    *p = e - 1;
+}
+
+/* RN32 of the exact quotient n / d of two positive doubles holding at most
+ * 25 significant bits each: long division of their integer significands. */
+static uint32_t rn32_div(double n, double d)
+{
+    int en, ed;
+    double fn = frexp(n, &en), fd = frexp(d, &ed);
+    uint64_t N = (uint64_t)ldexp(fn, 30), D = (uint64_t)ldexp(fd, 30);   /* exact integers < 2^30 */
+    /* n/d = (N/D) * 2^(en-ed); N/D in (1/2, 2) */
+    unsigned __int128 num = (unsigned __int128)N << 60;
+    uint64_t q = (uint64_t)(num / D), rem = (uint64_t)(num % D);
+    /* q has 60..61 significant bits; fold the remainder into a sticky bit and
+     * keep 52 bits so that the value is exact in a double */
+    int sh = 0;
+    while ((q >> sh) >= (1ull << 52)) ++sh;
+    uint64_t lost = q & ((1ull << sh) - 1ull);
+    uint64_t qs = (q >> sh) | ((lost | rem) ? 1ull : 0ull);
+    /* qs's last bit is a sticky bit 28+ bits below fp32's rounding position */
+    return oracle_round_f32(ldexp((double)qs, sh - 60 + en - ed));
+}
+
+/* fp32 bits of the per-block float-scale metadata: the largest finite |v| */
+int oracle_block_float_scale(const void *in, int dtype, int64_t rows, int64_t cols,
+                             int64_t br, int64_t bc, uint32_t *amax)
+{
+    if (!oracle_block_shape_ok(rows, cols, br, bc)) return -1;
+    int64_t nb = (rows / br) * (cols / bc);
+    for (int64_t b = 0; b < nb; ++b) amax[b] = 0;
+    for (int64_t e = 0; e < rows * cols; ++e) {
+        uint32_t u = load_u32(in, dtype, e);
+        if (is_special(u)) continue;
+        int64_t b = block_of(e, cols, br, bc);
+        if (fabs(f32_value(u)) > f32_value(amax[b])) amax[b] = u & 0x7FFFFFFFu;
+    }
+    return 0;
+}
+
+/* scaled fp32 value u of the finite element v (bits) under block max amax */
+uint32_t oracle_fs_scale_in(uint32_t v, uint32_t amax, int x, int y)
+{
+    if ((amax & 0x7FFFFFFFu) == 0) return v & 0x80000000u;      /* v * 0 */
+    double A1;
+    int p;
+    fs_split(amax, &A1, &p);
+    uint32_t r = rn32_div(oracle_fs_grid_top(x, y), A1);
+    double prod = f32_value(v) * f32_value(r);                  /* exact: 24 x 24 bits */
+    return oracle_round_f32(ldexp(prod, -p));
+}
+
+/* decoded fp32 bits of code under block max amax */
+uint32_t oracle_fs_scale_out(uint32_t code, uint32_t amax, int x, int y)
+{
+    double g = oracle_code_value(code, x, y, 127);
+    double A1 = 0.0;
+    int p = 0;
+    if ((amax & 0x7FFFFFFFu) != 0) fs_split(amax, &A1, &p);
+    volatile double c = 1.0 / oracle_fs_grid_top(x, y);        /* RN64 (volatile: no contraction) */
+    volatile double s1 = A1 * c;                                /* RN64 */
+    double s = ldexp(s1, p);                                    /* exact */
+    volatile double o = g * s;                                  /* RN64 */
+    return oracle_round_f32(o);
+}
+
+static uint32_t fs_encode_code(const grid *g127, uint32_t u_in, uint32_t amax)
+{
+    return encode_finite(g127, oracle_fs_scale_in(u_in, amax, g127->x, g127->y));
+}
+
+static void fs_store(void *out, int dtype, int64_t i, uint32_t f32bits)
+{
+    if (dtype == ORACLE_BF16) ((uint16_t *)out)[i] = oracle_round_bf16(f32_value(f32bits));
+    else ((uint32_t *)out)[i] = f32bits;
+}
+
+int oracle_quantize_fs(const void *in, void *out, int dtype, int64_t rows, int64_t cols,
+                       int64_t br, int64_t bc, int x, int y, const uint32_t *amax)
+{
+    if (!oracle_format_valid(x, y, 127) || !oracle_block_shape_ok(rows, cols, br, bc)) return -1;
+    grid g;
+    if (grid_build(&g, x, y, 127)) return -1;
+    for (int64_t e = 0; e < rows * cols; ++e) {
+        uint32_t u = load_u32(in, dtype, e);
+        if (is_special(u)) {
+            if (dtype == ORACLE_BF16) ((uint16_t *)out)[e] = ((const uint16_t *)in)[e];
+            else ((uint32_t *)out)[e] = u;
+            continue;
+        }
+        uint32_t a = amax[block_of(e, cols, br, bc)];
+        fs_store(out, dtype, e, oracle_fs_scale_out(fs_encode_code(&g, u, a), a, x, y));
+    }
+    grid_free(&g);
+    return 0;
+}
+
+int64_t oracle_encode_fs(const void *in, int dtype, int64_t rows, int64_t cols, int axis,
+                         int64_t br, int64_t bc, int x, int y, const uint32_t *amax, uint8_t *packed,
+                         int64_t *sp_index, uint32_t *sp_bits, int64_t sp_capacity)
+{
+    if (!oracle_format_valid(x, y, 127) || !oracle_shape_ok(rows, cols, axis) ||
+        !oracle_block_shape_ok(rows, cols, br, bc) || 1 + x + y > ORACLE_MAX_PACK_K) return -1;
+    int64_t n = rows * cols;
+    uint16_t *codes = (uint16_t *)malloc(sizeof(uint16_t) * (size_t)(n ? n : 1));
+    grid g;
+    if (!codes || grid_build(&g, x, y, 127)) { free(codes); return -1; }
+    int64_t ns = 0;
+    for (int64_t e = 0; e < n; ++e) {
+        uint32_t u = load_u32(in, dtype, e);
+        if (is_special(u)) {
+            codes[e] = 0;
+            if (ns < sp_capacity) { sp_index[ns] = e; sp_bits[ns] = u; }
+            ++ns;
+        } else {
+            codes[e] = (uint16_t)fs_encode_code(&g, u, amax[block_of(e, cols, br, bc)]);
+        }
+    }
+    grid_free(&g);
+    oracle_pack(codes, rows, cols, axis, 1 + x + y, packed);
+    free(codes);
+    return ns;
+}
+
+int oracle_decode_fs(const uint8_t *packed, int64_t rows, int64_t cols, int axis,
+                     int64_t br, int64_t bc, int x, int y, const uint32_t *amax,
+                     const int64_t *sp_index, const uint32_t *sp_bits, int64_t sp_count,
+                     void *out, int out_dtype)
+{
+    if (!oracle_format_valid(x, y, 127) || !oracle_shape_ok(rows, cols, axis) ||
+        !oracle_block_shape_ok(rows, cols, br, bc) || 1 + x + y > ORACLE_MAX_PACK_K) return -1;
+    int64_t n = rows * cols;
+    uint16_t *codes = (uint16_t *)malloc(sizeof(uint16_t) * (size_t)(n ? n : 1));
+    if (!codes) return -1;
+    oracle_unpack(packed, rows, cols, axis, 1 + x + y, codes);
+    for (int64_t e = 0; e < n; ++e)
+        fs_store(out, out_dtype, e, oracle_fs_scale_out(codes[e], amax[block_of(e, cols, br, bc)], x, y));
+    free(codes);
+    for (int64_t j = 0; j < sp_count; ++j) {
+        int64_t i = sp_index[j];
+        uint32_t u = sp_bits[j];
+        if (out_dtype == ORACLE_BF16) {
+            uint16_t b = (uint16_t)(u >> 16);
+            if ((u & 0x7FFFFFu) != 0 && (b & 0x7Fu) == 0) b |= 0x40u;
+            ((uint16_t *)out)[i] = b;
+        } else {
+            ((uint32_t *)out)[i] = u;
+        }
+    }
+    return 0;
+}
