@@ -245,6 +245,42 @@ exmy_status exmy_decode_rows(const uint8_t *packed, int64_t rows, int64_t cols, 
                              const uint8_t *meta, int meta_per_row, const int64_t *row_index,
                              int64_t n_index, void *out, int out_dtype, void *stream);
 
+/* ------------------------------------------------ float scaling (reading D23)
+ * Fig. 2's third scheme, "float scaling with maximum exponent of 127"
+ * ("an additional bfloat16 or float32 scaling factor").
+ * Each block_rows x block_cols block carries one fp32 metadata value, its
+ * largest finite magnitude amax (0 if it has none); codes live on the
+ * e_max = 127 grid, whose top is G (2 - 2^-y for x >= 1).  With amax =
+ * A1 * 2^p, A1 in [1,2):
+ *   encode  u = RN32(v * RN32(G/A1) * 2^-p), code = the e_max-127 code of u
+ *   decode  out = RN32(RN64(g * RN64(A1 * RN64(1/G)) * 2^p)); bf16 = RN16(out)
+ * so each block's maximum decodes to exactly amax ("captures the largest
+ * value in the block accurately").  Layout, specials and error codes
+ * as exmy_encode_blocked / exmy_decode_blocked; scale is device memory,
+ * (rows/block_rows) * (cols/block_cols) floats in block-row-major order. */
+
+/* scale[b] := max |finite v| over block b (fp32).  One warp per block. */
+exmy_status exmy_block_float_scale(const void *in, int dtype, int64_t rows, int64_t cols,
+                                   int64_t block_rows, int64_t block_cols, float *scale,
+                                   void *stream);
+
+/* Emulation: out = decode(encode(v)) in v's dtype, NaN/Inf passed through.
+ * in/out 16-byte aligned and rows*cols a multiple of 8 (bf16) / 4 (fp32),
+ * else E_ALIGN. */
+exmy_status exmy_quantize_fs(const void *in, void *out, int dtype, int64_t rows, int64_t cols,
+                             int64_t block_rows, int64_t block_cols, int x, int y,
+                             const float *scale, void *stream);
+exmy_status exmy_encode_fs(const void *in, int dtype, int64_t rows, int64_t cols, int axis,
+                           int64_t block_rows, int64_t block_cols, int x, int y,
+                           const float *scale, uint8_t *packed, int64_t *sp_index,
+                           uint32_t *sp_bits, uint64_t *sp_count, int64_t sp_capacity,
+                           void *stream);
+exmy_status exmy_decode_fs(const uint8_t *packed, int64_t rows, int64_t cols, int axis,
+                           int64_t block_rows, int64_t block_cols, int x, int y,
+                           const float *scale, const int64_t *sp_index, const uint32_t *sp_bits,
+                           const uint64_t *sp_count, int64_t sp_capacity, void *out,
+                           int out_dtype, void *stream);
+
 /* ------------------------------------------ grouped launch (tensor table)
  * a model is many tensors (Llama-3 8B: 291, P:600-606
  * "the weights of Llama"), each compressed under its own per-tensor

@@ -71,6 +71,10 @@ def _load():
         "exmy_decode_rows": ([vp, i64, i64, i32, i32, vp, i32, vp, i64, vp, i32, vp], i32),
         "exmy_encode_host": ([vp, i32, i64, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, i64, vp, vp, vp], i32),
         "exmy_decode_host": ([vp, i64, i64, i32, i32, i32, vp, vp, vp, vp, i64, vp, vp, i32, vp, vp], i32),
+        "exmy_block_float_scale": ([vp, i32, i64, i64, i64, i64, vp, vp], i32),
+        "exmy_quantize_fs": ([vp, vp, i32, i64, i64, i64, i64, i32, i32, vp, vp], i32),
+        "exmy_encode_fs": ([vp, i32, i64, i64, i32, i64, i64, i32, i32, vp, vp, vp, vp, vp, i64, vp], i32),
+        "exmy_decode_fs": ([vp, i64, i64, i32, i64, i64, i32, i32, vp, vp, vp, vp, i64, vp, i32, vp], i32),
         "exmy_group_plan_bytes": ([i32], ctypes.c_size_t),
         "exmy_group_plan": ([vp, i32, i32, i32, i32, i32, vp, ctypes.c_size_t], i32),
         "exmy_group_max_exponent": ([vp, vp, vp], i32),
@@ -93,7 +97,7 @@ EXPORTED = ["exmy_version", "exmy_status_string", "exmy_format_valid", "exmy_pac
             "exmy_decode_host", "exmy_block_max_exponent", "exmy_quantize_blocked", "exmy_encode_blocked",
             "exmy_decode_blocked", "exmy_decode_rows", "exmy_max_exponent", "exmy_encode_rowwise",
             "exmy_group_plan_bytes", "exmy_group_plan", "exmy_group_max_exponent", "exmy_group_encode",
-            "exmy_group_decode"]
+            "exmy_group_decode", "exmy_block_float_scale", "exmy_quantize_fs", "exmy_encode_fs", "exmy_decode_fs"]
 
 
 def lib():
@@ -285,6 +289,7 @@ class Packed:
     dtype: torch.dtype        # source dtype
     block: tuple | None = None   # (block_rows, block_cols) when meta is per block
     layout: tuple | None = None  # (rows, cols) packed when not the 2-D view of shape (grouped 1-D tensors)
+    scale: torch.Tensor | None = None   # float-scaling metadata: per-block fp32 amax (reading D23)
 
     @property
     def k(self) -> int:
@@ -351,6 +356,11 @@ def decode(p: Packed, dtype: torch.dtype | None = None, out: torch.Tensor | None
     if out is None:
         out = torch.empty(p.shape, dtype=dtype, device=dev)
     cap = p.sp_index.numel() if p.sp_count is not None else 0
+    if p.scale is not None:
+        _check(_lib.exmy_decode_fs(_ptr(p.data), R, C, p.axis, p.block[0], p.block[1], p.x, p.y, _ptr(p.scale),
+                                   _ptr(p.sp_index), _ptr(p.sp_bits), _ptr(p.sp_count), cap, _ptr(out),
+                                   _dtype_code(dtype), _stream(dev)), "decode_fs")
+        return out
     if p.block is not None:
         _check(_lib.exmy_decode_blocked(_ptr(p.data), R, C, p.axis, p.block[0], p.block[1], p.x, p.y, _ptr(p.meta),
                                         _ptr(p.sp_index), _ptr(p.sp_bits), _ptr(p.sp_count), cap, _ptr(out),
@@ -486,6 +496,63 @@ def decode_raw(data: torch.Tensor, rows: int, cols: int, fmt, meta, axis="rows",
     _check(_lib.exmy_decode(_ptr(data), rows, cols, _AXES[axis], x, y, _ptr(m), None, None, None, 0, _ptr(out),
                             _dtype_code(dtype), _stream(dev)), "decode")
     return out
+
+
+# ------------------------------------------------------------ float scaling
+def block_float_scale(t: torch.Tensor, block, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Float-scaling metadata (Fig. 2's third scheme, reading D23): per block
+    the largest finite magnitude, fp32, shape (R/br, C/bc)."""
+    _require_cuda(t)
+    t = t.contiguous()
+    R, C = _as_2d(t)
+    br, bc = block_shape((R, C), block)
+    if out is None:
+        out = torch.empty((R // br, C // bc), dtype=torch.float32, device=t.device)
+    _check(_lib.exmy_block_float_scale(_ptr(t), _dtype_code(t.dtype), R, C, br, bc, _ptr(out), _stream(t.device)),
+           "block_float_scale")
+    return out
+
+
+def quantize_fs(t: torch.Tensor, fmt, scale: torch.Tensor | None, block, out: torch.Tensor | None = None):
+    """Float-scaled emulation: decode(encode(t)) in t's dtype (scale=None:
+    derived with block_float_scale)."""
+    _require_cuda(t)
+    x, y = parse_format(fmt)
+    t = t.contiguous()
+    R, C = _as_2d(t)
+    br, bc = block_shape((R, C), block)
+    if scale is None:
+        scale = block_float_scale(t, (br, bc))
+    if out is None:
+        out = torch.empty_like(t)
+    _check(_lib.exmy_quantize_fs(_ptr(t), _ptr(out), _dtype_code(t.dtype), R, C, br, bc, x, y, _ptr(scale),
+                                 _stream(t.device)), "quantize_fs")
+    return out
+
+
+def encode_fs(t: torch.Tensor, fmt, scale: torch.Tensor | None, block, axis="rows", specials_capacity: int = 4096,
+              out: torch.Tensor | None = None) -> Packed:
+    """Encode with float-scaling metadata (reading D23); Packed.scale holds it."""
+    _require_cuda(t)
+    x, y = parse_format(fmt)
+    ax = _AXES[axis]
+    t = t.contiguous()
+    R, C = _as_2d(t)
+    dev = t.device
+    br, bc = block_shape((R, C), block)
+    if scale is None:
+        scale = block_float_scale(t, (br, bc))
+    n = R * C
+    if out is None:
+        out = torch.empty(n * (1 + x + y) // 8 if n % 8 == 0 else 0, dtype=torch.uint8, device=dev)
+    cap = int(specials_capacity)
+    spi = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
+    spb = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    spc = torch.zeros(1, dtype=torch.int64, device=dev)
+    _check(_lib.exmy_encode_fs(_ptr(t), _dtype_code(t.dtype), R, C, ax, br, bc, x, y, _ptr(scale), _ptr(out),
+                               _ptr(spi), _ptr(spb), _ptr(spc), cap, _stream(dev)), "encode_fs")
+    meta = torch.full((1,), 127, dtype=torch.uint8, device=dev)
+    return Packed(out, meta, spi, spb, spc, tuple(t.shape), x, y, ax, t.dtype, (br, bc), None, scale)
 
 
 # ------------------------------------------------------- host-buffer path

@@ -1,0 +1,415 @@
+// exmy_fscale.cuh -- the float-scaling block scheme (Fig. 2's third scheme,
+// "float scaling with maximum exponent of 127"; reading D23 in
+// DESIGN.md).  Each block carries one fp32 metadata value, its largest finite
+// magnitude amax = A1 * 2^p (A1 in [1,2)); codes live on the e_max = 127 grid
+// whose top is G.
+//   encode: u = RN32(v * RN32(G / A1) * 2^-p)         (FMUL when the factor is
+//           a normal fp32, else one fp64 product), code = e_max-127 code of u
+//   decode: out = RN32(RN64(g * RN64(A1 * RN64(1/G)) * 2^p))
+// so the block maximum decodes to exactly amax.
+#pragma once
+#include "exmy_blocked.cuh"
+
+namespace exmy {
+
+// block (i, j) of a (R, C) tensor tiled by (br x bc) owns amax[i * nbc + j]
+struct FsMap {
+    const float *amax;
+    int64_t br, bc, nbc;
+};
+
+__device__ __forceinline__ uint32_t fs_amax_at(const FsMap &S, int64_t r, int64_t c) {
+    return __float_as_uint(__ldg(S.amax + (r / S.br) * S.nbc + c / S.bc)) & 0x7FFFFFFFu;
+}
+
+// amax = A1 * 2^p, A1 in [1, 2) (a subnormal amax is normalised); amax != 0
+__device__ __forceinline__ void fs_split(uint32_t a, float &A1, int &p) {
+    const int E = (int)(a >> 23);
+    if (E == 0) {
+        const int hb = 31 - __clz(a);   // highest set bit, < 23
+        const int s = 23 - hb;
+        A1 = __uint_as_float(0x3F800000u | ((a << s) & 0x7FFFFFu));
+        p = -126 - s;
+    } else {
+        A1 = __uint_as_float(0x3F800000u | (a & 0x7FFFFFu));
+        p = E - 127;
+    }
+}
+
+__device__ __forceinline__ double fs_pow2d(int e) {   // e in [-1022, 1023]
+    return __longlong_as_double((long long)(e + 1023) << 52);
+}
+
+// encode factor of one block
+struct FsE {
+    float rr;     // RN32(G/A1) * 2^-p when that is a normal fp32 (mode 1)
+    float r1;     // RN32(G/A1)
+    int p;
+    int mode;     // 0: amax = 0 (u = v * 0), 1: fp32 multiply, 2: fp64 product
+};
+
+__device__ __forceinline__ FsE fs_enc(uint32_t amax, float G) {
+    FsE q;
+    if (amax == 0u) {
+        q.mode = 0; q.rr = q.r1 = 0.f; q.p = 0;
+        return q;
+    }
+    float A1;
+    fs_split(amax, A1, q.p);
+    q.r1 = __fdiv_rn(G, A1);   // in (G/2, G] with G in [1, 2): exponent -1 or 0 (x = 0, y = 1: G = 1)
+    // r1 * 2^-p is a normal fp32 for -126 <= e(r1) - p <= 127
+    q.mode = (q.p >= -126 && q.p <= 125) ? 1 : 2;
+    q.rr = q.mode == 1 ? __fmul_rn(q.r1, __uint_as_float((uint32_t)(127 - q.p) << 23)) : 0.f;   // exact
+    return q;
+}
+
+// scaled fp32 pattern of a finite input pattern v
+__device__ __forceinline__ uint32_t fs_in(uint32_t v, const FsE &q) {
+    if (q.mode == 1) return __float_as_uint(__fmul_rn(__uint_as_float(v), q.rr));
+    if (q.mode == 0) return v & 0x80000000u;
+    const double prod = (double)__uint_as_float(v) * (double)q.r1;   // exact (24 x 24 bits)
+    return __float_as_uint(__double2float_rn(prod * fs_pow2d(-q.p)));  // exact scaling, one rounding
+}
+
+// decode factor s = RN64(A1 * cG) * 2^p of one block (0 for amax = 0)
+__device__ __forceinline__ double fs_dec(uint32_t amax, double cG) {
+    if (amax == 0u) return 0.0;
+    float A1;
+    int p;
+    fs_split(amax, A1, p);
+    return __dmul_rn((double)A1, cG) * fs_pow2d(p);
+}
+
+__device__ __forceinline__ uint32_t fs_out32(uint32_t gbits, double s) {
+    return __float_as_uint(__double2float_rn(__dmul_rn((double)__uint_as_float(gbits), s)));
+}
+
+// exact value of a code at e_max 127 as a double (x = 8 grids reach below
+// the fp32 range: 2^(1-255-y)); Table 1 / P:172-175 with bias = 2^x - 1
+__device__ __forceinline__ double fs_grid_d(uint32_t code, int x, int y) {
+    const int k = 1 + x + y;
+    const uint32_t mag = code & ((1u << (k - 1)) - 1u);
+    const int bias = (1 << x) - 1;
+    const uint32_t e = x == 0 ? 0u : (mag >> y), m = mag & ((1u << y) - 1u);
+    double v = e == 0 ? (double)m * fs_pow2d(1 - bias - y) : (double)((1u << y) + m) * fs_pow2d((int)e - bias - y);
+    return (code >> (k - 1)) & 1u ? -v : v;
+}
+
+__device__ __forceinline__ uint32_t fs_out32d(double g, double s) {
+    return __float_as_uint(__double2float_rn(__dmul_rn(g, s)));
+}
+
+__device__ __forceinline__ uint32_t f32_to_bf16_bits(uint32_t f) {   // RTNE, finite input (no carry past Inf:
+    return (f + 0x7FFFu + ((f >> 16) & 1u)) >> 16;                     // |f| <= amax < 2^128 rounds to <= max)
+}
+
+// ------------------------------------------------------------ block max
+// one warp per block: the largest finite magnitude (fp32 bits) -> amax[b]
+template <bool BF16>
+__global__ void __launch_bounds__(256) k_block_amax(const uint8_t *__restrict__ in, int64_t R, int64_t C, int64_t br,
+                                                    int64_t bc, float *__restrict__ amax_out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nbc = C / bc, nb = (R / br) * nbc;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    constexpr int V = Elem<BF16>::V;
+    const bool vec = (bc % V == 0) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0) && (C % V == 0);
+    for (int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); b < nb; b += warps) {
+        const int64_t r0 = (b / nbc) * br, c0 = (b % nbc) * bc;
+        uint32_t am = 0;
+        for (int64_t i = 0; i < br; ++i) {
+            const uint8_t *row = in + ((r0 + i) * C + c0) * Elem<BF16>::ES;
+            if (vec) {
+                for (int64_t v = lane; v < bc / V; v += 32) {
+                    const uint4 q = ldg_nc_v4(row + v * 16);
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const uint32_t w = word_of(q, t);
+                        if (BF16) {
+                            const uint32_t lo = (w << 16) & 0x7FFF0000u, hi = w & 0x7FFF0000u;
+                            if (lo < 0x7F800000u) am = max(am, lo);
+                            if (hi < 0x7F800000u) am = max(am, hi);
+                        } else {
+                            const uint32_t a = w & 0x7FFFFFFFu;
+                            if (a < 0x7F800000u) am = max(am, a);
+                        }
+                    }
+                }
+            } else {
+                for (int64_t c = lane; c < bc; c += 32) {
+                    const uint32_t a = load_elem_scalar<BF16>(row, c) & 0x7FFFFFFFu;
+                    if (a < 0x7F800000u) am = max(am, a);
+                }
+            }
+        }
+        am = __reduce_max_sync(0xFFFFFFFFu, am);
+        if (lane == 0) amax_out[b] = __uint_as_float(am);
+    }
+}
+
+// ------------------------------------------------------ generic containers
+template <bool BF16, int K>
+__device__ __noinline__ void fs_enc_container(const uint8_t *__restrict__ in, int64_t C, int64_t idx, int axis, int x,
+                                              int y, const FsMap S, float G, uint8_t *packed, const SegOffsets so,
+                                              int64_t *spi, uint32_t *spb, unsigned long long *spc, int64_t cap) {
+    const Fmt F = fmt_of(x, y, 127);
+    uint32_t c[8];
+    int64_t e[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        e[i] = lane_elem(idx, i, C, axis);
+        const uint32_t v = load_elem_scalar<BF16>(in, e[i]);
+        if (is_special_f32(v)) {
+            push_special(e[i], v, spi, spb, spc, cap);
+            c[i] = 0u;
+        } else {
+            c[i] = enc_code_generic(fs_in(v, fs_enc(fs_amax_at(S, e[i] / C, e[i] % C), G)), F);
+        }
+    }
+    int hi = K;
+#pragma unroll
+    for (int s = 0; s < seg_count(K); ++s) {
+        const int w = seg_width(K, s), lo = hi - w;
+        uint8_t *seg = packed + so.off[s];
+        if (w == 8) {
+            for (int i = 0; i < 8; ++i) seg[e[i]] = (uint8_t)(c[i] >> lo);
+        } else {
+            uint32_t cont = 0;
+            for (int i = 0; i < 8; ++i) cont |= ((c[i] >> lo) & ((1u << w) - 1u)) << (w * i);
+            for (int b = 0; b < w; ++b) seg[idx * w + b] = (uint8_t)(cont >> (8 * b));
+        }
+        hi = lo;
+    }
+}
+
+template <bool BF16, int K>
+__global__ void k_fs_encode_generic(const uint8_t *__restrict__ in, int64_t C, int64_t ncont, int axis, int x, int y,
+                                    FsMap S, float G, uint8_t *__restrict__ packed, SegOffsets so, int64_t *spi,
+                                    uint32_t *spb, unsigned long long *spc, int64_t cap) {
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < ncont;
+         idx += (int64_t)gridDim.x * blockDim.x)
+        fs_enc_container<BF16, K>(in, C, idx, axis, x, y, S, G, packed, so, spi, spb, spc, cap);
+}
+
+template <bool OBF16>
+__device__ __noinline__ void fs_dec_container(const uint8_t *__restrict__ packed, int64_t C, int64_t idx, int axis,
+                                              int x, int y, const FsMap S, double cG, const SegOffsets so, int nseg,
+                                              int4 widths, uint8_t *out) {
+    const int wd[4] = {widths.x, widths.y, widths.z, widths.w};
+    const Fmt F = fmt_of(x, y, 127);
+    uint32_t c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int64_t e[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) e[i] = lane_elem(idx, i, C, axis);
+    int hi = 1 + x + y;
+    for (int s = 0; s < nseg; ++s) {
+        const int w = wd[s], lo = hi - w;
+        const uint8_t *seg = packed + so.off[s];
+        if (w == 8) {
+            for (int i = 0; i < 8; ++i) c[i] |= (uint32_t)seg[e[i]] << lo;
+        } else {
+            uint32_t cont = 0;
+            for (int b = 0; b < w; ++b) cont |= (uint32_t)seg[idx * w + b] << (8 * b);
+            for (int i = 0; i < 8; ++i) c[i] |= ((cont >> (w * i)) & ((1u << w) - 1u)) << lo;
+        }
+        hi = lo;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t o = fs_out32d(fs_grid_d(c[i], x, y), fs_dec(fs_amax_at(S, e[i] / C, e[i] % C), cG));
+        if (OBF16) {
+            const uint16_t h = (uint16_t)f32_to_bf16_bits(o);
+            memcpy(out + 2 * e[i], &h, 2);
+        } else {
+            memcpy(out + 4 * e[i], &o, 4);
+        }
+    }
+}
+
+template <bool OBF16>
+__global__ void k_fs_decode_generic(const uint8_t *__restrict__ packed, int64_t C, int64_t ncont, int axis, int x, int y,
+                                    FsMap S, double cG, SegOffsets so, int nseg, int4 widths,
+                                    uint8_t *__restrict__ out) {
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < ncont;
+         idx += (int64_t)gridDim.x * blockDim.x)
+        fs_dec_container<OBF16>(packed, C, idx, axis, x, y, S, cG, so, nseg, widths, out);
+}
+
+// ------------------------------------------------------------ emulation
+// out = decode(encode(v)) in v's dtype; one 16-byte vector per thread, whose
+// elements share one block when bc % V == 0 (else per element).  FAST: the
+// e_max-127 grid rounding by the one-addition fp32 trick (x <= 7), else the
+// integer code path.
+template <bool BF16, bool FAST>
+__global__ void __launch_bounds__(256) k_fs_quant(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, int64_t R,
+                                                  int64_t C, int x, int y, FsMap S, float G, double cG, int shared) {
+    using EL = Elem<BF16>;
+    constexpr int V = EL::V;
+    const Fmt F = fmt_of(x, y, 127);
+    const FastP P = make_fast(F, false, 0);
+    const int64_t nvec = R * C / V;
+    for (int64_t vi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; vi < nvec;
+         vi += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e0 = vi * V;
+        const uint4 q = ldg_nc_v4(in + vi * 16);
+        uint32_t w[4] = {q.x, q.y, q.z, q.w};
+        uint32_t am = 0;
+        FsE fe;
+        double sd = 0.0;
+        if (shared) {
+            am = fs_amax_at(S, e0 / C, e0 % C);
+            fe = fs_enc(am, G);
+            sd = fs_dec(am, cG);
+        }
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const uint32_t u = vec_elem<BF16>(q, v);
+            uint32_t o;
+            if (is_special_f32(u)) {
+                o = u;
+            } else {
+                if (!shared) {
+                    const int64_t e = e0 + v;
+                    am = fs_amax_at(S, e / C, e % C);
+                    fe = fs_enc(am, G);
+                    sd = fs_dec(am, cG);
+                }
+                const uint32_t us = fs_in(u, fe);
+                if (FAST) {
+                    uint32_t flag = 0;
+                    o = fs_out32(quant_f32_fast(us, P, flag), sd);
+                } else {
+                    o = fs_out32d(fs_grid_d(enc_code_generic(us, F), x, y), sd);
+                }
+                if (BF16) o = f32_to_bf16_bits(o) << 16;
+            }
+            if (BF16) {
+                const uint32_t h = o >> 16;
+                w[v >> 1] = (v & 1) ? ((w[v >> 1] & 0xFFFFu) | (h << 16)) : ((w[v >> 1] & 0xFFFF0000u) | h);
+            } else {
+                w[v] = o;
+            }
+        }
+        stg_v4(out + vi * 16, make_uint4(w[0], w[1], w[2], w[3]));
+    }
+}
+
+// ------------------------------------------------------- encode ROWS fast
+// 8-row x 4-column tiles as k_enc_rows_fast (host: bc % 4 == 0, so the 4
+// columns of a row share a block).  Per row one FsE (one division); the
+// scaled patterns go through the fp32 one-addition code path at e_max 127.
+// Tiles with NaN/Inf, amax = 0 or an extreme amax take the integer path.
+template <int K, bool BF16, bool Y0>
+__global__ void __launch_bounds__(256, 2) k_fs_enc_rows(const uint8_t *__restrict__ in, int64_t R, int64_t C, int x,
+                                                        int y, FsMap S, float G, uint8_t *__restrict__ packed,
+                                                        SegOffsets so, int64_t *spi, uint32_t *spb,
+                                                        unsigned long long *spc, int64_t cap) {
+    using EL = Elem<BF16>;
+    constexpr int NW = BF16 ? 2 : 4;
+    const Fmt F = fmt_of(x, y, 127);
+    const FastP P = make_fast(F, false, 0);
+    const int64_t CV = C / 4, G8 = R / 8;
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= CV) return;
+    const int64_t c0 = j * 4;
+    const uint8_t *src = in + c0 * EL::ES;
+    const int64_t rstride = C * EL::ES;
+    uint32_t nxt[8][NW];
+    int64_t g = blockIdx.y;
+    if (g < G8) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) load4<BF16>(src + (8 * g + i) * rstride, nxt[i]);
+    }
+    for (; g < G8; g += gridDim.y) {
+        uint32_t w[8][NW];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int q = 0; q < NW; ++q) w[i][q] = nxt[i][q];
+        const int64_t gn = g + gridDim.y;
+        if (gn < G8) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) load4<BF16>(src + (8 * gn + i) * rstride, nxt[i]);
+        }
+        uint32_t vmax = 0, amax = 0;
+        bool ok = true;
+        uint32_t cp[8][2];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const FsE fe = fs_enc(fs_amax_at(S, 8 * g + i, c0), G);
+            ok = ok && fe.mode == 1;
+            uint32_t cd[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const uint32_t u = wordvec_elem<BF16, NW>(w[i], v);
+                vmax = max(vmax, u & 0x7FFFFFFFu);
+                cd[v] = enc_f32_fast<K, Y0>(__float_as_uint(__fmul_rn(__uint_as_float(u), fe.rr)), P, amax);
+            }
+            cp[i][0] = cd[0] | (cd[1] << 16);
+            cp[i][1] = cd[2] | (cd[3] << 16);
+        }
+        if (ok && vmax < 0x7F800000u) {
+            uint32_t RL[1][8], RH[1][8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                RL[0][i] = prmt(cp[i][0], cp[i][1], 0x6420);
+                RH[0][i] = (K == 9) ? prmt(cp[i][0] >> 1, cp[i][1] >> 1, 0x6420) : 0u;
+            }
+            rows_fast_store<K, 1, 0>(RL, RH, packed, so, g, C, c0);
+        } else {
+            for (int v = 0; v < 4; ++v)
+                fs_enc_container<BF16, K>(in, C, g * C + c0 + v, 0, x, y, S, G, packed, so, spi, spb, spc, cap);
+        }
+    }
+}
+
+// ------------------------------------------------------- decode ROWS fast
+// 8-row x 4-column tiles; codes -> e_max-127 values by one multiply (x <= 7)
+// -> times the row's fp64 factor -> RN32 (-> RN16 for bf16 output).  A CTA
+// barrier per row group, as k_dec_rows_fast.
+template <int K, bool OBF16, bool FAST>
+__global__ void __launch_bounds__(256) k_fs_dec_rows(const uint8_t *__restrict__ packed, int64_t R, int64_t C, int x,
+                                                     int y, FsMap S, double cG, SegOffsets so,
+                                                     uint8_t *__restrict__ out) {
+    using EL = Elem<OBF16>;
+    constexpr int TW = tile_words(K, 1);
+    const Fmt F = fmt_of(x, y, 127);
+    const FastP P = make_fast(F, false, 0);
+    const int64_t CV = C / 4, G8 = R / 8;
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool act = j < CV;
+    const int64_t c0 = j * 4;
+    uint32_t nxt[TW];
+    int64_t g = blockIdx.y;
+    if (g < G8 && act) rows_load_raw<K, 1, 0>(nxt, packed, so, g, C, c0);
+    for (; g < G8; g += gridDim.y) {
+        uint32_t raw[TW];
+#pragma unroll
+        for (int q = 0; q < TW; ++q) raw[q] = nxt[q];
+        __syncthreads();
+        if (g + gridDim.y < G8 && act) rows_load_raw<K, 1, 0>(nxt, packed, so, g + gridDim.y, C, c0);
+        if (!act) continue;
+        uint32_t RL[1][8], RH[1][8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { RL[0][i] = 0; RH[0][i] = 0; }
+        rows_unpack_raw<K, 1, 0>(raw, RL, RH);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const double sd = fs_dec(fs_amax_at(S, 8 * g + i, c0), cG);
+            uint32_t o[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                uint32_t code = (RL[0][i] >> (8 * v)) & 0xFFu;
+                if (K == 9) code |= ((RH[0][i] >> (8 * v)) & 0xFFu) << 1;
+                o[v] = FAST ? fs_out32(dec_f32_fast<K, false>(code, P, y), sd) : fs_out32d(fs_grid_d(code, x, y), sd);
+            }
+            uint8_t *dst = out + ((8 * g + i) * C + c0) * EL::ES;
+            if (OBF16)
+                stg_v2(dst, f32_to_bf16_bits(o[0]) | (f32_to_bf16_bits(o[1]) << 16),
+                       f32_to_bf16_bits(o[2]) | (f32_to_bf16_bits(o[3]) << 16));
+            else
+                stg_v4(dst, make_uint4(o[0], o[1], o[2], o[3]));
+        }
+    }
+}
+
+}  // namespace exmy
