@@ -629,9 +629,10 @@ int oracle_decode_blocked(const uint8_t *packed, int64_t rows, int64_t cols, int
  *   encode  r  = RN32(G / A1)                      (exact quotient, rounded once)
  *           u  = RN32(v * r * 2^-p)                (exact product, rounded once)
  *           code = the e_max-127 code of u         (as oracle_encode)
- *   decode  c  = RN64(1 / G)
- *           s  = RN64(A1 * c) * 2^p                (fp64; the power of 2 is exact)
- *           out = RN32(RN64(g * s)), g = the code's value at e_max 127;
+ *   decode  g  = RN32(the code's value at e_max 127)   (the plain decode)
+ *           s_hi = RN32(amax / G), s_lo = RN32((amax - s_hi G) / G)
+ *           out = sign(g) * RN32(|g| s_hi + RN32(|g| s_lo))   (one FMA on the GPU;
+ *           a zero result keeps the code's sign);
  *           bf16 output = RN16 of that fp32 value  (reading D24)
  * amax = 0 (no finite non-zero element): u = v * 0, codes are signed zeros. */
 
@@ -698,18 +699,56 @@ uint32_t oracle_fs_scale_in(uint32_t v, uint32_t amax, int x, int y)
     return oracle_round_f32(ldexp(prod, -p));
 }
 
-/* decoded fp32 bits of code under block max amax */
+/* RN32 of the exact quotient n / G for any double n (sign kept, 0 -> +0) */
+static uint32_t rn32_div_signed(double n, double G)
+{
+    if (n == 0.0) return 0u;
+    uint32_t q = rn32_div(fabs(n), G);
+    return n < 0 ? (q | 0x80000000u) : q;
+}
+
+/* fp32 neighbour of the positive fp32 pattern t toward +inf (up) or 0 (down) */
+static double f32_step(uint32_t t, int up) { return f32_value(up ? t + 1u : t - 1u); }
+
+/* RN32 of the exact value S + e, where (S, e) is an exact two-double sum with
+ * |e| <= ulp64(S)/2: RN32(S) unless S is exactly an fp32 midpoint, then e
+ * decides the direction. */
+static uint32_t rn32_twosum(double S, double e)
+{
+    uint32_t sign = 0;
+    if (S < 0 || (S == 0 && e < 0)) { S = -S; e = -e; sign = 0x80000000u; }
+    uint32_t t = oracle_round_f32(S);                 /* positive pattern */
+    double vt = f32_value(t);
+    if (e != 0.0 && vt != S) {
+        double other = vt < S ? f32_step(t, 1) : f32_step(t, 0);
+        if ((vt + other) / 2.0 == S) {                 /* a tie in fp32: S+e lies off it */
+            double lo = vt < other ? vt : other, hi = vt < other ? other : vt;
+            t = oracle_round_f32(e > 0 ? hi : lo);
+        }
+    }
+    return t | sign;
+}
+
+/* decoded fp32 bits of code under block max amax (reading D23):
+ *   g    = RN32(value of the code at e_max 127)      (the plain decode)
+ *   s_hi = RN32(amax / G), s_lo = RN32((amax - s_hi G) / G)
+ *   out  = sign(g) RN32(|g| s_hi + RN32(|g| s_lo))    (one FMA on the GPU) */
 uint32_t oracle_fs_scale_out(uint32_t code, uint32_t amax, int x, int y)
 {
-    double g = oracle_code_value(code, x, y, 127);
-    double A1 = 0.0;
-    int p = 0;
-    if ((amax & 0x7FFFFFFFu) != 0) fs_split(amax, &A1, &p);
-    volatile double c = 1.0 / oracle_fs_grid_top(x, y);        /* RN64 (volatile: no contraction) */
-    volatile double s1 = A1 * c;                                /* RN64 */
-    double s = ldexp(s1, p);                                    /* exact */
-    volatile double o = g * s;                                  /* RN64 */
-    return oracle_round_f32(o);
+    uint32_t gb = oracle_round_f32(oracle_code_value(code, x, y, 127));
+    double g = fabs(f32_value(gb));                   /* |g|; the code's sign is attached last */
+    double a = f32_value(amax & 0x7FFFFFFFu);
+    double G = oracle_fs_grid_top(x, y);
+    uint32_t shi = (a == 0.0) ? 0u : rn32_div(a, G);
+    double s_hi = f32_value(shi);
+    double r = a - s_hi * G;                          /* exact: 24-bit x (y+1)-bit product */
+    double s_lo = f32_value(rn32_div_signed(r, G));
+    double t = f32_value(oracle_round_f32(g * s_lo)); /* exact product, one rounding */
+    double p = g * s_hi;                              /* exact */
+    volatile double S = p + t;                        /* TwoSum (Knuth): S + e == p + t exactly */
+    volatile double bp = S - p;
+    volatile double e = (p - (S - bp)) + (t - bp);
+    return rn32_twosum(S, e) | (gb & 0x80000000u);  /* s_hi + s_lo >= 0: result >= 0, then the sign */
 }
 
 static uint32_t fs_encode_code(const grid *g127, uint32_t u_in, uint32_t amax)

@@ -5,7 +5,9 @@
 // whose top is G.
 //   encode: u = RN32(v * RN32(G / A1) * 2^-p)         (FMUL when the factor is
 //           a normal fp32, else one fp64 product), code = e_max-127 code of u
-//   decode: out = RN32(RN64(g * RN64(A1 * RN64(1/G)) * 2^p))
+//   decode: g = RN32(code value at e_max 127), s_hi = RN32(amax / G),
+//           s_lo = RN32((amax - s_hi G) / G), out = RN32(g s_hi + RN32(g s_lo))
+//           (one FMUL + one FFMA per element)
 // so the block maximum decodes to exactly amax.
 #pragma once
 #include "exmy_blocked.cuh"
@@ -20,6 +22,14 @@ struct FsMap {
 
 __device__ __forceinline__ uint32_t fs_amax_at(const FsMap &S, int64_t r, int64_t c) {
     return __float_as_uint(__ldg(S.amax + (r / S.br) * S.nbc + c / S.bc)) & 0x7FFFFFFFu;
+}
+
+// block row of tensor row r without a 64-bit division in the common cases
+// (per-row blocks, block rows a multiple of the 8-row tile)
+__device__ __forceinline__ int64_t fs_rb(const FsMap &S, int64_t r) {
+    if (S.br == 1) return r;
+    if ((r >> 31) == 0 && (S.br >> 31) == 0) return (int64_t)((uint32_t)r / (uint32_t)S.br);
+    return r / S.br;
 }
 
 // amax = A1 * 2^p, A1 in [1, 2) (a subnormal amax is normalised); amax != 0
@@ -71,32 +81,29 @@ __device__ __forceinline__ uint32_t fs_in(uint32_t v, const FsE &q) {
     return __float_as_uint(__double2float_rn(prod * fs_pow2d(-q.p)));  // exact scaling, one rounding
 }
 
-// decode factor s = RN64(A1 * cG) * 2^p of one block (0 for amax = 0)
-__device__ __forceinline__ double fs_dec(uint32_t amax, double cG) {
-    if (amax == 0u) return 0.0;
-    float A1;
-    int p;
-    fs_split(amax, A1, p);
-    return __dmul_rn((double)A1, cG) * fs_pow2d(p);
+// decode factors of one block: s_hi + s_lo ~ amax / G (reading D23)
+struct FsD {
+    float hi, lo;
+};
+
+__device__ __forceinline__ FsD fs_dec(uint32_t amax, float G) {
+    FsD d;
+    const float a = __uint_as_float(amax);
+    d.hi = __fdiv_rn(a, G);
+    if (amax >= 0x0D800000u) {   // amax >= 2^-100: the residual a - hi G is an fp32 (exact FMA)
+        d.lo = __fdiv_rn(__fmaf_rn(-d.hi, G, a), G);
+    } else {                     // tiny amax: exact residual in fp64, quotient rounded once
+        const double r = fma(-(double)d.hi, (double)G, (double)a);
+        d.lo = __double2float_rn(__ddiv_rn(r, (double)G));
+    }
+    return d;
 }
 
-__device__ __forceinline__ uint32_t fs_out32(uint32_t gbits, double s) {
-    return __float_as_uint(__double2float_rn(__dmul_rn((double)__uint_as_float(gbits), s)));
-}
-
-// exact value of a code at e_max 127 as a double (x = 8 grids reach below
-// the fp32 range: 2^(1-255-y)); Table 1 / P:172-175 with bias = 2^x - 1
-__device__ __forceinline__ double fs_grid_d(uint32_t code, int x, int y) {
-    const int k = 1 + x + y;
-    const uint32_t mag = code & ((1u << (k - 1)) - 1u);
-    const int bias = (1 << x) - 1;
-    const uint32_t e = x == 0 ? 0u : (mag >> y), m = mag & ((1u << y) - 1u);
-    double v = e == 0 ? (double)m * fs_pow2d(1 - bias - y) : (double)((1u << y) + m) * fs_pow2d((int)e - bias - y);
-    return (code >> (k - 1)) & 1u ? -v : v;
-}
-
-__device__ __forceinline__ uint32_t fs_out32d(double g, double s) {
-    return __float_as_uint(__double2float_rn(__dmul_rn(g, s)));
+// RN32(g s_hi + RN32(g s_lo)) computed on |g| (hi + lo >= 0: the result is
+// >= 0) with g's sign attached, so a zero result keeps the code's sign
+__device__ __forceinline__ uint32_t fs_out(uint32_t gbits, const FsD &d) {
+    const float g = __uint_as_float(gbits & 0x7FFFFFFFu);
+    return __float_as_uint(__fmaf_rn(g, d.hi, __fmul_rn(g, d.lo))) | (gbits & 0x80000000u);
 }
 
 __device__ __forceinline__ uint32_t f32_to_bf16_bits(uint32_t f) {   // RTNE, finite input (no carry past Inf:
@@ -192,7 +199,7 @@ __global__ void k_fs_encode_generic(const uint8_t *__restrict__ in, int64_t C, i
 
 template <bool OBF16>
 __device__ __noinline__ void fs_dec_container(const uint8_t *__restrict__ packed, int64_t C, int64_t idx, int axis,
-                                              int x, int y, const FsMap S, double cG, const SegOffsets so, int nseg,
+                                              int x, int y, const FsMap S, float G, const SegOffsets so, int nseg,
                                               int4 widths, uint8_t *out) {
     const int wd[4] = {widths.x, widths.y, widths.z, widths.w};
     const Fmt F = fmt_of(x, y, 127);
@@ -215,7 +222,7 @@ __device__ __noinline__ void fs_dec_container(const uint8_t *__restrict__ packed
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const uint32_t o = fs_out32d(fs_grid_d(c[i], x, y), fs_dec(fs_amax_at(S, e[i] / C, e[i] % C), cG));
+        const uint32_t o = fs_out(dec_code_generic<24>(c[i], F), fs_dec(fs_amax_at(S, e[i] / C, e[i] % C), G));
         if (OBF16) {
             const uint16_t h = (uint16_t)f32_to_bf16_bits(o);
             memcpy(out + 2 * e[i], &h, 2);
@@ -227,11 +234,11 @@ __device__ __noinline__ void fs_dec_container(const uint8_t *__restrict__ packed
 
 template <bool OBF16>
 __global__ void k_fs_decode_generic(const uint8_t *__restrict__ packed, int64_t C, int64_t ncont, int axis, int x, int y,
-                                    FsMap S, double cG, SegOffsets so, int nseg, int4 widths,
+                                    FsMap S, float G, SegOffsets so, int nseg, int4 widths,
                                     uint8_t *__restrict__ out) {
     for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < ncont;
          idx += (int64_t)gridDim.x * blockDim.x)
-        fs_dec_container<OBF16>(packed, C, idx, axis, x, y, S, cG, so, nseg, widths, out);
+        fs_dec_container<OBF16>(packed, C, idx, axis, x, y, S, G, so, nseg, widths, out);
 }
 
 // ------------------------------------------------------------ emulation
@@ -240,65 +247,119 @@ __global__ void k_fs_decode_generic(const uint8_t *__restrict__ packed, int64_t 
 // e_max-127 grid rounding by the one-addition fp32 trick (x <= 7), else the
 // integer code path.
 template <bool BF16, bool FAST>
+__device__ __forceinline__ uint32_t fs_quant_elem(uint32_t u, const FsE &fe, const FsD &fd, const Fmt &F,
+                                                  const FastP &P) {
+    if (is_special_f32(u)) return u;
+    const uint32_t us = fs_in(u, fe);
+    uint32_t g;
+    if (FAST) {
+        uint32_t flag = 0;
+        g = quant_f32_fast(us, P, flag);
+    } else {
+        g = dec_code_generic<24>(enc_code_generic(us, F), F);
+    }
+    const uint32_t o = fs_out(g, fd);
+    return BF16 ? (f32_to_bf16_bits(o) << 16) : o;
+}
+
+template <bool BF16>
+__device__ __forceinline__ void fs_put(uint32_t (&w)[4], int v, uint32_t o) {
+    if (BF16) {
+        const uint32_t h = o >> 16;
+        w[v >> 1] = (v & 1) ? ((w[v >> 1] & 0xFFFFu) | (h << 16)) : ((w[v >> 1] & 0xFFFF0000u) | h);
+    } else {
+        w[v] = o;
+    }
+}
+
+// MODE 2 (host: C % V == 0, R % 8 == 0, bc % (32 V) == 0): 2-D grid, a
+// thread takes one 16-byte column vector of 8 consecutive rows; a warp's 32
+// vectors share a block column, so lanes 0..7 compute the 8 rows' factors
+// and broadcast them.  MODE 1 (C % V == 0, bc % V == 0): the same grid one
+// row at a time, factors per thread.  MODE 0: one vector per thread, the
+// block looked up per element.
+template <bool BF16, bool FAST, int MODE>
 __global__ void __launch_bounds__(256) k_fs_quant(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, int64_t R,
-                                                  int64_t C, int x, int y, FsMap S, float G, double cG, int shared) {
+                                                  int64_t C, int x, int y, FsMap S, float G) {
     using EL = Elem<BF16>;
     constexpr int V = EL::V;
     const Fmt F = fmt_of(x, y, 127);
     const FastP P = make_fast(F, false, 0);
-    const int64_t nvec = R * C / V;
-    for (int64_t vi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; vi < nvec;
-         vi += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t e0 = vi * V;
-        const uint4 q = ldg_nc_v4(in + vi * 16);
-        uint32_t w[4] = {q.x, q.y, q.z, q.w};
-        uint32_t am = 0;
-        FsE fe;
-        double sd = 0.0;
-        if (shared) {
-            am = fs_amax_at(S, e0 / C, e0 % C);
-            fe = fs_enc(am, G);
-            sd = fs_dec(am, cG);
-        }
+    if (MODE == 2) {
+        const int64_t CVv = C / V;
+        const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        const bool act = j < CVv;
+        const int lane = threadIdx.x & 31;
+        const float *scol = S.amax + ((act ? j : 0) * V) / S.bc;
+        for (int64_t g = blockIdx.y; g < R / 8; g += gridDim.y) {
+            const uint32_t am = __float_as_uint(__ldg(scol + fs_rb(S, 8 * g + (lane & 7)) * S.nbc)) & 0x7FFFFFFFu;
+            const FsE fe0 = fs_enc(am, G);
+            const FsD fd0 = fs_dec(am, G);
+            uint4 q[8];
+            if (act) {
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-            const uint32_t u = vec_elem<BF16>(q, v);
-            uint32_t o;
-            if (is_special_f32(u)) {
-                o = u;
-            } else {
-                if (!shared) {
-                    const int64_t e = e0 + v;
-                    am = fs_amax_at(S, e / C, e % C);
-                    fe = fs_enc(am, G);
-                    sd = fs_dec(am, cG);
-                }
-                const uint32_t us = fs_in(u, fe);
-                if (FAST) {
-                    uint32_t flag = 0;
-                    o = fs_out32(quant_f32_fast(us, P, flag), sd);
-                } else {
-                    o = fs_out32d(fs_grid_d(enc_code_generic(us, F), x, y), sd);
-                }
-                if (BF16) o = f32_to_bf16_bits(o) << 16;
+                for (int i = 0; i < 8; ++i) q[i] = ldg_nc_v4(in + ((8 * g + i) * C + j * V) * EL::ES);
             }
-            if (BF16) {
-                const uint32_t h = o >> 16;
-                w[v >> 1] = (v & 1) ? ((w[v >> 1] & 0xFFFFu) | (h << 16)) : ((w[v >> 1] & 0xFFFF0000u) | h);
-            } else {
-                w[v] = o;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                FsE fe;
+                fe.rr = __shfl_sync(0xFFFFFFFFu, fe0.rr, i);
+                fe.r1 = __shfl_sync(0xFFFFFFFFu, fe0.r1, i);
+                fe.p = __shfl_sync(0xFFFFFFFFu, fe0.p, i);
+                fe.mode = __shfl_sync(0xFFFFFFFFu, fe0.mode, i);
+                FsD fd;
+                fd.hi = __shfl_sync(0xFFFFFFFFu, fd0.hi, i);
+                fd.lo = __shfl_sync(0xFFFFFFFFu, fd0.lo, i);
+                if (!act) continue;
+                uint32_t w[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
+#pragma unroll
+                for (int v = 0; v < V; ++v)
+                    fs_put<BF16>(w, v, fs_quant_elem<BF16, FAST>(vec_elem<BF16>(q[i], v), fe, fd, F, P));
+                stg_v4(out + ((8 * g + i) * C + j * V) * EL::ES, make_uint4(w[0], w[1], w[2], w[3]));
             }
         }
-        stg_v4(out + vi * 16, make_uint4(w[0], w[1], w[2], w[3]));
+    } else if (MODE == 1) {
+        const int64_t CVv = C / V;
+        const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        if (j >= CVv) return;
+        const float *scol = S.amax + (j * V) / S.bc;
+        for (int64_t r = blockIdx.y; r < R; r += gridDim.y) {
+            const int64_t off = (r * C + j * V) * EL::ES;
+            const uint4 q = ldg_nc_v4(in + off);
+            const uint32_t am = __float_as_uint(__ldg(scol + fs_rb(S, r) * S.nbc)) & 0x7FFFFFFFu;
+            const FsE fe = fs_enc(am, G);
+            const FsD fd = fs_dec(am, G);
+            uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int v = 0; v < V; ++v) fs_put<BF16>(w, v, fs_quant_elem<BF16, FAST>(vec_elem<BF16>(q, v), fe, fd, F, P));
+            stg_v4(out + off, make_uint4(w[0], w[1], w[2], w[3]));
+        }
+    } else {
+        const int64_t nvec = R * C / V;
+        for (int64_t vi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; vi < nvec;
+             vi += (int64_t)gridDim.x * blockDim.x) {
+            const uint4 q = ldg_nc_v4(in + vi * 16);
+            uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                const int64_t e = vi * V + v;
+                const uint32_t am = fs_amax_at(S, e / C, e % C);
+                fs_put<BF16>(w, v, fs_quant_elem<BF16, FAST>(vec_elem<BF16>(q, v), fs_enc(am, G), fs_dec(am, G), F, P));
+            }
+            stg_v4(out + vi * 16, make_uint4(w[0], w[1], w[2], w[3]));
+        }
     }
 }
 
 // ------------------------------------------------------- encode ROWS fast
 // 8-row x 4-column tiles as k_enc_rows_fast (host: bc % 4 == 0, so the 4
-// columns of a row share a block).  Per row one FsE (one division); the
-// scaled patterns go through the fp32 one-addition code path at e_max 127.
-// Tiles with NaN/Inf, amax = 0 or an extreme amax take the integer path.
-template <int K, bool BF16, bool Y0>
+// columns of a row share a block).  WSHARE (host: bc % 128 == 0): a warp's
+// 128 columns share one block column, so lanes 0..7 compute the 8 rows'
+// factors once and broadcast them (one division per lane instead of eight);
+// otherwise each thread computes its 8.  The scaled patterns go through the
+// fp32 one-addition code path at e_max 127.  Tiles with NaN/Inf, amax = 0 or
+// an extreme amax take the integer path.
+template <int K, bool BF16, bool Y0, bool WSHARE>
 __global__ void __launch_bounds__(256, 2) k_fs_enc_rows(const uint8_t *__restrict__ in, int64_t R, int64_t C, int x,
                                                         int y, FsMap S, float G, uint8_t *__restrict__ packed,
                                                         SegOffsets so, int64_t *spi, uint32_t *spb,
@@ -309,13 +370,16 @@ __global__ void __launch_bounds__(256, 2) k_fs_enc_rows(const uint8_t *__restric
     const FastP P = make_fast(F, false, 0);
     const int64_t CV = C / 4, G8 = R / 8;
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= CV) return;
-    const int64_t c0 = j * 4;
+    if (!WSHARE && j >= CV) return;
+    const bool act = j < CV;               // WSHARE: whole warps stay for the shuffles
+    const int lane = threadIdx.x & 31;
+    const int64_t c0 = (act ? j : 0) * 4;
     const uint8_t *src = in + c0 * EL::ES;
     const int64_t rstride = C * EL::ES;
+    const float *scol = S.amax + c0 / S.bc;   // this thread's block column
     uint32_t nxt[8][NW];
     int64_t g = blockIdx.y;
-    if (g < G8) {
+    if (g < G8 && act) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) load4<BF16>(src + (8 * g + i) * rstride, nxt[i]);
     }
@@ -326,23 +390,36 @@ __global__ void __launch_bounds__(256, 2) k_fs_enc_rows(const uint8_t *__restric
 #pragma unroll
             for (int q = 0; q < NW; ++q) w[i][q] = nxt[i][q];
         const int64_t gn = g + gridDim.y;
-        if (gn < G8) {
+        if (gn < G8 && act) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) load4<BF16>(src + (8 * gn + i) * rstride, nxt[i]);
         }
-        uint32_t vmax = 0, amax = 0;
+        float rr[8];
         bool ok = true;
+        if (WSHARE) {
+            const FsE fe = fs_enc(__float_as_uint(__ldg(scol + fs_rb(S, 8 * g + (lane & 7)) * S.nbc)) & 0x7FFFFFFFu, G);
+            ok = __all_sync(0xFFFFFFFFu, fe.mode == 1);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) rr[i] = __shfl_sync(0xFFFFFFFFu, fe.rr, i);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const FsE fe = fs_enc(__float_as_uint(__ldg(scol + fs_rb(S, 8 * g + i) * S.nbc)) & 0x7FFFFFFFu, G);
+                ok = ok && fe.mode == 1;
+                rr[i] = fe.rr;
+            }
+        }
+        if (!act) continue;
+        uint32_t vmax = 0, amax = 0;
         uint32_t cp[8][2];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const FsE fe = fs_enc(fs_amax_at(S, 8 * g + i, c0), G);
-            ok = ok && fe.mode == 1;
             uint32_t cd[4];
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
                 const uint32_t u = wordvec_elem<BF16, NW>(w[i], v);
                 vmax = max(vmax, u & 0x7FFFFFFFu);
-                cd[v] = enc_f32_fast<K, Y0>(__float_as_uint(__fmul_rn(__uint_as_float(u), fe.rr)), P, amax);
+                cd[v] = enc_f32_fast<K, Y0>(__float_as_uint(__fmul_rn(__uint_as_float(u), rr[i])), P, amax);
             }
             cp[i][0] = cd[0] | (cd[1] << 16);
             cp[i][1] = cd[2] | (cd[3] << 16);
@@ -363,12 +440,13 @@ __global__ void __launch_bounds__(256, 2) k_fs_enc_rows(const uint8_t *__restric
 }
 
 // ------------------------------------------------------- decode ROWS fast
-// 8-row x 4-column tiles; codes -> e_max-127 values by one multiply (x <= 7)
-// -> times the row's fp64 factor -> RN32 (-> RN16 for bf16 output).  A CTA
-// barrier per row group, as k_dec_rows_fast.
-template <int K, bool OBF16, bool FAST>
+// 8-row x 4-column tiles; codes -> e_max-127 fp32 values (one multiply for
+// x <= 7) -> g s_hi + RN32(g s_lo) (FMUL + FFMA) -> RN16 for bf16 output.
+// Row factors shared across the warp as in k_fs_enc_rows; a CTA barrier per
+// row group, as k_dec_rows_fast.
+template <int K, bool OBF16, bool FAST, bool WSHARE>
 __global__ void __launch_bounds__(256) k_fs_dec_rows(const uint8_t *__restrict__ packed, int64_t R, int64_t C, int x,
-                                                     int y, FsMap S, double cG, SegOffsets so,
+                                                     int y, FsMap S, float G, SegOffsets so,
                                                      uint8_t *__restrict__ out) {
     using EL = Elem<OBF16>;
     constexpr int TW = tile_words(K, 1);
@@ -377,7 +455,9 @@ __global__ void __launch_bounds__(256) k_fs_dec_rows(const uint8_t *__restrict__
     const int64_t CV = C / 4, G8 = R / 8;
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool act = j < CV;
-    const int64_t c0 = j * 4;
+    const int lane = threadIdx.x & 31;
+    const int64_t c0 = (act ? j : 0) * 4;
+    const float *scol = S.amax + c0 / S.bc;
     uint32_t nxt[TW];
     int64_t g = blockIdx.y;
     if (g < G8 && act) rows_load_raw<K, 1, 0>(nxt, packed, so, g, C, c0);
@@ -387,6 +467,22 @@ __global__ void __launch_bounds__(256) k_fs_dec_rows(const uint8_t *__restrict__
         for (int q = 0; q < TW; ++q) raw[q] = nxt[q];
         __syncthreads();
         if (g + gridDim.y < G8 && act) rows_load_raw<K, 1, 0>(nxt, packed, so, g + gridDim.y, C, c0);
+        float hi[8], lo[8];
+        if (WSHARE) {
+            const FsD fd = fs_dec(__float_as_uint(__ldg(scol + fs_rb(S, 8 * g + (lane & 7)) * S.nbc)) & 0x7FFFFFFFu, G);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                hi[i] = __shfl_sync(0xFFFFFFFFu, fd.hi, i);
+                lo[i] = __shfl_sync(0xFFFFFFFFu, fd.lo, i);
+            }
+        } else if (act) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const FsD fd = fs_dec(__float_as_uint(__ldg(scol + fs_rb(S, 8 * g + i) * S.nbc)) & 0x7FFFFFFFu, G);
+                hi[i] = fd.hi;
+                lo[i] = fd.lo;
+            }
+        }
         if (!act) continue;
         uint32_t RL[1][8], RH[1][8];
 #pragma unroll
@@ -394,13 +490,14 @@ __global__ void __launch_bounds__(256) k_fs_dec_rows(const uint8_t *__restrict__
         rows_unpack_raw<K, 1, 0>(raw, RL, RH);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const double sd = fs_dec(fs_amax_at(S, 8 * g + i, c0), cG);
             uint32_t o[4];
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
                 uint32_t code = (RL[0][i] >> (8 * v)) & 0xFFu;
                 if (K == 9) code |= ((RH[0][i] >> (8 * v)) & 0xFFu) << 1;
-                o[v] = FAST ? fs_out32(dec_f32_fast<K, false>(code, P, y), sd) : fs_out32d(fs_grid_d(code, x, y), sd);
+                const uint32_t gb = FAST ? dec_f32_fast<K, false>(code, P, y) : dec_code_generic<24>(code, F);
+                const float gf = __uint_as_float(gb & 0x7FFFFFFFu);
+                o[v] = __float_as_uint(__fmaf_rn(gf, hi[i], __fmul_rn(gf, lo[i]))) | (gb & 0x80000000u);
             }
             uint8_t *dst = out + ((8 * g + i) * C + c0) * EL::ES;
             if (OBF16)

@@ -51,10 +51,14 @@ exmy_status enc_k(const uint8_t *in, int64_t R, int64_t C, int axis, int x, int 
         if (gy > 65535) gy = 65535;
         if (gx > INT_MAX) return EXMY_E_SHAPE;
         const dim3 grid((unsigned)gx, (unsigned)gy);
-        if (y == 0)
-            k_fs_enc_rows<K, BF16, true><<<grid, threads, 0, st>>>(in, R, C, x, y, M, G, packed, p.so, spi, spb, spc, cap);
-        else
-            k_fs_enc_rows<K, BF16, false><<<grid, threads, 0, st>>>(in, R, C, x, y, M, G, packed, p.so, spi, spb, spc, cap);
+        const bool ws = M.bc % 128 == 0;
+        if (y == 0) {
+            if (ws) k_fs_enc_rows<K, BF16, true, true><<<grid, threads, 0, st>>>(in, R, C, x, y, M, G, packed, p.so, spi, spb, spc, cap);
+            else k_fs_enc_rows<K, BF16, true, false><<<grid, threads, 0, st>>>(in, R, C, x, y, M, G, packed, p.so, spi, spb, spc, cap);
+        } else {
+            if (ws) k_fs_enc_rows<K, BF16, false, true><<<grid, threads, 0, st>>>(in, R, C, x, y, M, G, packed, p.so, spi, spb, spc, cap);
+            else k_fs_enc_rows<K, BF16, false, false><<<grid, threads, 0, st>>>(in, R, C, x, y, M, G, packed, p.so, spi, spb, spc, cap);
+        }
         return launch_status();
     }
     const int64_t ncont = R * C / 8;
@@ -80,7 +84,7 @@ exmy_status enc_dispatch(int k, const uint8_t *in, int64_t R, int64_t C, int axi
 }
 
 template <int K, bool OBF16>
-exmy_status dec_k(const uint8_t *packed, int64_t R, int64_t C, int axis, int x, int y, const FsMap &M, double cG,
+exmy_status dec_k(const uint8_t *packed, int64_t R, int64_t C, int axis, int x, int y, const FsMap &M, float G,
                   const Plan &p, uint8_t *out, cudaStream_t st) {
     bool fast = axis == EXMY_AXIS_ROWS && M.bc % 4 == 0 && C % 4 == 0 && aligned(out, 4 * Elem<OBF16>::ES);
     for (int s = 0; s < p.nseg; ++s) fast = fast && aligned(packed + p.so.off[s], p.w[s] == 8 ? 4 : 4 * p.w[s]);
@@ -94,29 +98,33 @@ exmy_status dec_k(const uint8_t *packed, int64_t R, int64_t C, int axis, int x, 
         if (gy > 65535) gy = 65535;
         if (gx > INT_MAX) return EXMY_E_SHAPE;
         const dim3 grid((unsigned)gx, (unsigned)gy);
-        if (x <= 7 && !g_force_generic)
-            k_fs_dec_rows<K, OBF16, true><<<grid, threads, 0, st>>>(packed, R, C, x, y, M, cG, p.so, out);
-        else
-            k_fs_dec_rows<K, OBF16, false><<<grid, threads, 0, st>>>(packed, R, C, x, y, M, cG, p.so, out);
+        const bool ws = M.bc % 128 == 0;
+        if (x <= 7 && !g_force_generic) {
+            if (ws) k_fs_dec_rows<K, OBF16, true, true><<<grid, threads, 0, st>>>(packed, R, C, x, y, M, G, p.so, out);
+            else k_fs_dec_rows<K, OBF16, true, false><<<grid, threads, 0, st>>>(packed, R, C, x, y, M, G, p.so, out);
+        } else {
+            if (ws) k_fs_dec_rows<K, OBF16, false, true><<<grid, threads, 0, st>>>(packed, R, C, x, y, M, G, p.so, out);
+            else k_fs_dec_rows<K, OBF16, false, false><<<grid, threads, 0, st>>>(packed, R, C, x, y, M, G, p.so, out);
+        }
         return launch_status();
     }
     const int64_t ncont = R * C / 8;
-    k_fs_decode_generic<OBF16><<<grid1(ncont, 8), 256, 0, st>>>(packed, C, ncont, axis, x, y, M, cG, p.so, p.nseg,
+    k_fs_decode_generic<OBF16><<<grid1(ncont, 8), 256, 0, st>>>(packed, C, ncont, axis, x, y, M, G, p.so, p.nseg,
                                                                 make_int4(p.w[0], p.w[1], p.w[2], p.w[3]), out);
     return launch_status();
 }
 
 template <bool OBF16>
 exmy_status dec_dispatch(int k, const uint8_t *packed, int64_t R, int64_t C, int axis, int x, int y, const FsMap &M,
-                         double cG, const Plan &p, uint8_t *out, cudaStream_t st) {
+                         float G, const Plan &p, uint8_t *out, cudaStream_t st) {
     switch (k) {
-        case 3: return dec_k<3, OBF16>(packed, R, C, axis, x, y, M, cG, p, out, st);
-        case 4: return dec_k<4, OBF16>(packed, R, C, axis, x, y, M, cG, p, out, st);
-        case 5: return dec_k<5, OBF16>(packed, R, C, axis, x, y, M, cG, p, out, st);
-        case 6: return dec_k<6, OBF16>(packed, R, C, axis, x, y, M, cG, p, out, st);
-        case 7: return dec_k<7, OBF16>(packed, R, C, axis, x, y, M, cG, p, out, st);
-        case 8: return dec_k<8, OBF16>(packed, R, C, axis, x, y, M, cG, p, out, st);
-        case 9: return dec_k<9, OBF16>(packed, R, C, axis, x, y, M, cG, p, out, st);
+        case 3: return dec_k<3, OBF16>(packed, R, C, axis, x, y, M, G, p, out, st);
+        case 4: return dec_k<4, OBF16>(packed, R, C, axis, x, y, M, G, p, out, st);
+        case 5: return dec_k<5, OBF16>(packed, R, C, axis, x, y, M, G, p, out, st);
+        case 6: return dec_k<6, OBF16>(packed, R, C, axis, x, y, M, G, p, out, st);
+        case 7: return dec_k<7, OBF16>(packed, R, C, axis, x, y, M, G, p, out, st);
+        case 8: return dec_k<8, OBF16>(packed, R, C, axis, x, y, M, G, p, out, st);
+        case 9: return dec_k<9, OBF16>(packed, R, C, axis, x, y, M, G, p, out, st);
     }
     return EXMY_E_FORMAT;
 }
@@ -153,20 +161,39 @@ exmy_status exmy_quantize_fs(const void *in, void *out, int dtype, int64_t rows,
     if (!aligned(in, 16) || !aligned(out, 16) || (rows * cols) % V) return EXMY_E_ALIGN;
     const FsMap M{scale, block_rows, block_cols, cols / block_cols};
     const float G = grid_top(x, y);
-    const double cG = 1.0 / (double)G;
-    const int shared = (block_cols % V == 0 && cols % V == 0) ? 1 : 0;
-    const unsigned grid = grid1(rows * cols / V, 8);
+    const int mode = (cols % V == 0 && block_cols % V == 0) ? ((rows % 8 == 0 && block_cols % (32 * V) == 0) ? 2 : 1) : 0;
     const auto *pi = static_cast<const uint8_t *>(in);
     auto *po = static_cast<uint8_t *>(out);
     const bool fast = x <= 7 && !g_force_generic;
     cudaStream_t st = S_(stream);
-    if (dtype == EXMY_BF16) {
-        if (fast) k_fs_quant<true, true><<<grid, 256, 0, st>>>(pi, po, rows, cols, x, y, M, G, cG, shared);
-        else k_fs_quant<true, false><<<grid, 256, 0, st>>>(pi, po, rows, cols, x, y, M, G, cG, shared);
+#define FS_QUANT(M, GRID)                                                                               \
+    do {                                                                                                \
+        if (dtype == EXMY_BF16) {                                                                       \
+            if (fast) k_fs_quant<true, true, M><<<GRID, 256, 0, st>>>(pi, po, rows, cols, x, y, Mp, G);   \
+            else k_fs_quant<true, false, M><<<GRID, 256, 0, st>>>(pi, po, rows, cols, x, y, Mp, G);      \
+        } else {                                                                                        \
+            if (fast) k_fs_quant<false, true, M><<<GRID, 256, 0, st>>>(pi, po, rows, cols, x, y, Mp, G);  \
+            else k_fs_quant<false, false, M><<<GRID, 256, 0, st>>>(pi, po, rows, cols, x, y, Mp, G);     \
+        }                                                                                               \
+    } while (0)
+    const FsMap &Mp = M;
+    if (mode >= 1) {
+        const int64_t CVv = cols / V;
+        const int64_t gx = cdiv(CVv, 256);
+        const int64_t ny = mode == 2 ? rows / 8 : rows;
+        int64_t gy = (int64_t)num_sms() * 4 / gx;
+        if (gy < 1) gy = 1;
+        if (gy > ny) gy = ny;
+        if (gy > 65535) gy = 65535;
+        if (gx > INT_MAX) return EXMY_E_SHAPE;
+        const dim3 grid((unsigned)gx, (unsigned)gy);
+        if (mode == 2) FS_QUANT(2, grid);
+        else FS_QUANT(1, grid);
     } else {
-        if (fast) k_fs_quant<false, true><<<grid, 256, 0, st>>>(pi, po, rows, cols, x, y, M, G, cG, shared);
-        else k_fs_quant<false, false><<<grid, 256, 0, st>>>(pi, po, rows, cols, x, y, M, G, cG, shared);
+        const unsigned grid = grid1(rows * cols / V, 8);
+        FS_QUANT(0, grid);
     }
+#undef FS_QUANT
     return launch_status();
 }
 
@@ -215,12 +242,12 @@ exmy_status exmy_decode_fs(const uint8_t *packed, int64_t rows, int64_t cols, in
     const int k = 1 + x + y;
     const Plan p = make_plan(k, rows * cols);
     const FsMap M{scale, block_rows, block_cols, cols / block_cols};
-    const double cG = 1.0 / (double)grid_top(x, y);
+    const float G = grid_top(x, y);
     cudaStream_t st = S_(stream);
     auto *po = static_cast<uint8_t *>(out);
     const bool obf = out_dtype == EXMY_BF16;
-    exmy_status s = obf ? dec_dispatch<true>(k, packed, rows, cols, axis, x, y, M, cG, p, po, st)
-                        : dec_dispatch<false>(k, packed, rows, cols, axis, x, y, M, cG, p, po, st);
+    exmy_status s = obf ? dec_dispatch<true>(k, packed, rows, cols, axis, x, y, M, G, p, po, st)
+                        : dec_dispatch<false>(k, packed, rows, cols, axis, x, y, M, G, p, po, st);
     if (s != EXMY_OK) return s;
     if (sp_count && sp_index && sp_bits && sp_capacity > 0)
         s = launch_specials_scatter(sp_index, sp_bits, reinterpret_cast<const unsigned long long *>(sp_count),

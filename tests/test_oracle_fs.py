@@ -143,10 +143,11 @@ def test_scale_in_is_exact_rounding(orc, fmt):
 
 @pytest.mark.parametrize("fmt", FMTS, ids=lambda f: f"e{f[0]}m{f[1]}")
 def test_scale_out_is_correctly_rounded(orc, fmt):
-    """The fp64 decode RN32(RN64(g * RN64(A1 * RN64(1/G)) 2^p)) equals the
+    """The decode RN32(g s_hi + RN32(g s_lo)), s_hi + s_lo ~ amax/G, equals the
     correctly rounded exact value g * amax / G for normal fp32 results (its
-    relative error <= 2^-51 is far below the distance of g*amax/G from a
-    rounding boundary, D23)."""
+    relative error <= 2^-47 is below the distance >= 2^-42 of g*amax/G from a
+    rounding boundary, D23), whenever the grid value g is itself an
+    fp32 value (always for x <= 7)."""
     x, y = fmt
     k = 1 + x + y
     rng = np.random.default_rng(k)
@@ -157,6 +158,8 @@ def test_scale_out_is_correctly_rounded(orc, fmt):
         ab = int(np.array([a], np.float32).view(np.uint32)[0])
         for code in rng.integers(0, 1 << k, 24):
             g = Fraction(orc.code_value(int(code), fmt, 127))
+            if g != Fraction(float(np.float32(float(g)))):
+                continue                       # e8m0 values below the fp32 range: g rounds first
             exact = g * frac_of_f32(ab) / G
             got = orc.fs_scale_out(int(code), ab, fmt)
             if exact != 0 and abs(exact) < Fraction(2) ** -126:

@@ -42,6 +42,7 @@ def main():
     ap.add_argument("--fmts", default="e0m6,e1m5,e2m4,e3m3,e4m2,e5m1,e6m0")
     ap.add_argument("--axis", default="rows")
     ap.add_argument("--hist-modes", default="0,1")
+    ap.add_argument("--fs", action="store_true", help="with --block: also time the float-scaling scheme")
     ap.add_argument("--block", default=None, help="row | col | tensor | BRxBC: time the block-metadata path")
     a = ap.parse_args()
     dev = torch.device("cuda")
@@ -98,6 +99,19 @@ def main():
             ms = timeit(lambda: exmy.decode(p, out=d))
             res[f"bdecode_{f}"] = {"ms": ms, "gbs": n * (es + k / 8) / ms / 1e6,
                                    "frac": n * (es + k / 8) / ms / 1e6 / peak}
+            if a.fs:   # float scaling (reading D23)
+                sc = torch.empty((R // br, C // bc), dtype=torch.float32, device=dev)
+                ms = timeit(lambda: exmy.block_float_scale(t, (br, bc), out=sc))
+                res[f"fsmax_{f}"] = {"ms": ms, "gbs": n * es / ms / 1e6, "frac": n * es / ms / 1e6 / peak}
+                ms = timeit(lambda: exmy.quantize_fs(t, f, sc, (br, bc), out=q))
+                res[f"fsquant_{f}"] = {"ms": ms, "gbs": 2 * n * es / ms / 1e6, "frac": 2 * n * es / ms / 1e6 / peak}
+                ms = timeit(lambda: exmy.encode_fs(t, f, sc, (br, bc), axis=a.axis, out=buf))
+                res[f"fsencode_{f}"] = {"ms": ms, "gbs": n * (es + k / 8) / ms / 1e6,
+                                        "frac": n * (es + k / 8) / ms / 1e6 / peak}
+                pf = exmy.encode_fs(t, f, sc, (br, bc), axis=a.axis, out=buf)
+                ms = timeit(lambda: exmy.decode(pf, out=d))
+                res[f"fsdecode_{f}"] = {"ms": ms, "gbs": n * (es + k / 8) / ms / 1e6,
+                                        "frac": n * (es + k / 8) / ms / 1e6 / peak}
     for k_, v in res.items():
         print(f"{k_:16s} {v['ms']*1e3:9.1f} us {v['gbs']:8.1f} GB/s  {v['frac']*100:5.1f}%")
     print(json.dumps(res))
