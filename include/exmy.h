@@ -281,6 +281,26 @@ exmy_status exmy_decode_fs(const uint8_t *packed, int64_t rows, int64_t cols, in
                            const uint64_t *sp_count, int64_t sp_capacity, void *out,
                            int out_dtype, void *stream);
 
+/* ----------------------------------- fused encode + all-gather (push)
+ * SURVEY 8(f) row 2 ("encode before ... network
+ * communication"; P:343-344 shards reconstruct independently).  The caller
+ * (one rank) encodes its row shard: rows [row0, row0+rows) of a
+ * (total_rows, cols) tensor, ROWS layout, under the GLOBAL metadata byte
+ * `meta`, and the kernel writes the shard's packed bytes straight into each
+ * of the `ndst` destination buffers (a host array of device pointers, each
+ * total_rows*cols*k/8 bytes: normally every rank's gathered buffer, peers'
+ * mapped over NVLink through CUDA IPC / symmetric memory) at the shard's
+ * global offsets.  Once every rank has run (and the group has synchronised)
+ * every buffer holds exactly exmy_encode of the whole tensor: the
+ * all-gather happens in the encode's own stores.  rows, row0, total_rows
+ * multiples of 8, cols % 4 == 0, 1 <= ndst <= 8; destination segments
+ * aligned as for exmy_encode's vector path, else E_ALIGN.  Specials: the
+ * shard's NaN/Inf with GLOBAL element indices, sorted. */
+exmy_status exmy_encode_push(const void *in, int dtype, int64_t rows, int64_t cols, int64_t row0,
+                             int64_t total_rows, int x, int y, const uint8_t *meta,
+                             uint8_t *const *dst, int ndst, int64_t *sp_index, uint32_t *sp_bits,
+                             uint64_t *sp_count, int64_t sp_capacity, void *stream);
+
 /* ------------------------------------------ grouped launch (tensor table)
  * a model is many tensors (Llama-3 8B: 291, P:600-606
  * "the weights of Llama"), each compressed under its own per-tensor

@@ -75,6 +75,7 @@ def _load():
         "exmy_quantize_fs": ([vp, vp, i32, i64, i64, i64, i64, i32, i32, vp, vp], i32),
         "exmy_encode_fs": ([vp, i32, i64, i64, i32, i64, i64, i32, i32, vp, vp, vp, vp, vp, i64, vp], i32),
         "exmy_decode_fs": ([vp, i64, i64, i32, i64, i64, i32, i32, vp, vp, vp, vp, i64, vp, i32, vp], i32),
+        "exmy_encode_push": ([vp, i32, i64, i64, i64, i64, i32, i32, vp, vp, i32, vp, vp, vp, i64, vp], i32),
         "exmy_group_plan_bytes": ([i32], ctypes.c_size_t),
         "exmy_group_plan": ([vp, i32, i32, i32, i32, i32, vp, ctypes.c_size_t], i32),
         "exmy_group_max_exponent": ([vp, vp, vp], i32),
@@ -97,7 +98,8 @@ EXPORTED = ["exmy_version", "exmy_status_string", "exmy_format_valid", "exmy_pac
             "exmy_decode_host", "exmy_block_max_exponent", "exmy_quantize_blocked", "exmy_encode_blocked",
             "exmy_decode_blocked", "exmy_decode_rows", "exmy_max_exponent", "exmy_encode_rowwise",
             "exmy_group_plan_bytes", "exmy_group_plan", "exmy_group_max_exponent", "exmy_group_encode",
-            "exmy_group_decode", "exmy_block_float_scale", "exmy_quantize_fs", "exmy_encode_fs", "exmy_decode_fs"]
+            "exmy_group_decode", "exmy_block_float_scale", "exmy_quantize_fs", "exmy_encode_fs", "exmy_decode_fs",
+            "exmy_encode_push"]
 
 
 def lib():
@@ -496,6 +498,30 @@ def decode_raw(data: torch.Tensor, rows: int, cols: int, fmt, meta, axis="rows",
     _check(_lib.exmy_decode(_ptr(data), rows, cols, _AXES[axis], x, y, _ptr(m), None, None, None, 0, _ptr(out),
                             _dtype_code(dtype), _stream(dev)), "decode")
     return out
+
+
+# ----------------------------------------------- fused encode + all-gather
+def encode_push(shard: torch.Tensor, fmt, meta: torch.Tensor, row0: int, total_rows: int, dsts,
+                specials_capacity: int = 4096):
+    """Encode the row shard [row0, row0+rows) of a (total_rows, cols) tensor and
+    store its packed bytes, at their global offsets, into every buffer of
+    ``dsts`` (device uint8 tensors or raw device pointers of
+    total_rows*cols*k/8 bytes; peers' buffers on a multi-GPU node).  Returns
+    (sp_index, sp_bits, sp_count) of the shard's specials (global indices)."""
+    _require_cuda(shard)
+    x, y = parse_format(fmt)
+    shard = shard.contiguous()
+    R, C = _as_2d(shard)
+    ptrs = (ctypes.c_void_p * len(dsts))(*[d.data_ptr() if isinstance(d, torch.Tensor) else int(d) for d in dsts])
+    dev = shard.device
+    cap = int(specials_capacity)
+    spi = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
+    spb = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    spc = torch.zeros(1, dtype=torch.int64, device=dev)
+    _check(_lib.exmy_encode_push(_ptr(shard), _dtype_code(shard.dtype), R, C, int(row0), int(total_rows), x, y,
+                                 _ptr(_meta_tensor(meta, dev)), ptrs, len(dsts), _ptr(spi), _ptr(spb), _ptr(spc), cap,
+                                 _stream(dev)), "encode_push")
+    return spi, spb, spc
 
 
 # ------------------------------------------------------------ float scaling

@@ -1,0 +1,208 @@
+// exmy_tu_push.cu -- fused encode + all-gather by remote stores (SURVEY 8(f)
+// row 2; "encode before ... network communication"
+// "each shard can be independently reconstructed").  A rank encodes its row
+// shard and its stores go straight to every destination buffer -- on a
+// multi-GPU node the peers' packed buffers mapped over NVLink (CUDA IPC /
+// symmetric memory), so the all-gather is the encode's own store stream and
+// overlaps the conversion tile by tile; no NCCL call, no staging buffer.
+#include <climits>
+
+#include "exmy_launch.cuh"
+
+using namespace exmy;
+
+namespace {
+
+constexpr int PUSH_MAX = 8;
+struct PushDst {
+    uint8_t *p[PUSH_MAX];
+    int n;
+};
+
+// one container on the integer path: codes of the shard's elements, stored
+// at the container's GLOBAL index in every destination; specials recorded
+// once with global element indices
+template <bool BF16, int K>
+__device__ __noinline__ void push_container_generic(const uint8_t *__restrict__ in, int64_t C, int64_t lidx, int64_t g0,
+                                                    const Fmt F, const PushDst D, const SegOffsets so, int64_t *spi,
+                                                    uint32_t *spb, unsigned long long *spc, int64_t cap) {
+    uint32_t c[8];
+    int64_t e[8];
+    const int64_t eoff = g0 * 8 * C;   // first element of the shard
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        e[i] = lane_elem(lidx, i, C, EXMY_AXIS_ROWS);
+        c[i] = enc_elem(load_elem_scalar<BF16>(in, e[i]), F, eoff + e[i], spi, spb, spc, cap);
+    }
+    const int64_t gidx = lidx + g0 * C;
+    for (int d = 0; d < D.n; ++d) {
+        int hi = K;
+#pragma unroll
+        for (int s = 0; s < seg_count(K); ++s) {
+            const int w = seg_width(K, s), lo = hi - w;
+            uint8_t *seg = D.p[d] + so.off[s];
+            if (w == 8) {
+                for (int i = 0; i < 8; ++i) seg[eoff + e[i]] = (uint8_t)(c[i] >> lo);
+            } else {
+                uint32_t cont = 0;
+                for (int i = 0; i < 8; ++i) cont |= ((c[i] >> lo) & ((1u << w) - 1u)) << (w * i);
+                for (int b = 0; b < w; ++b) seg[gidx * w + b] = (uint8_t)(cont >> (8 * b));
+            }
+            hi = lo;
+        }
+    }
+}
+
+// k_enc_rows_fast's tiles (8 rows x 4 columns, one tile ahead in flight);
+// every segment store is issued once per destination
+template <int K, bool BF16, int MODE>
+__global__ void __launch_bounds__(256, 2) k_enc_push(const uint8_t *__restrict__ in, int64_t R, int64_t C, int64_t g0,
+                                                     int x, int y, const uint8_t *__restrict__ meta, PushDst D,
+                                                     SegOffsets so, int64_t *spi, uint32_t *spb,
+                                                     unsigned long long *spc, int64_t cap, int force_generic) {
+    using EL = Elem<BF16>;
+    constexpr int NW = BF16 ? 2 : 4;
+    const Fmt F = load_fmt(x, y, meta);
+    const FastP P = make_fast(F, BF16, force_generic);
+    const int64_t CV = C / 4, G = R / 8;
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= CV) return;
+    const int64_t c0 = j * 4;
+    const uint8_t *src = in + c0 * EL::ES;
+    const int64_t rstride = C * EL::ES;
+    if (!enc_fast_ok<BF16, MODE>(F, force_generic)) {
+        for (int64_t g = blockIdx.y; g < G; g += gridDim.y)
+            for (int v = 0; v < 4; ++v)
+                push_container_generic<BF16, K>(in, C, g * C + c0 + v, g0, F, D, so, spi, spb, spc, cap);
+        return;
+    }
+    uint32_t nxt[8][NW];
+    int64_t g = blockIdx.y;
+    if (g < G) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) load4<BF16>(src + (8 * g + i) * rstride, nxt[i]);
+    }
+    for (; g < G; g += gridDim.y) {
+        uint32_t w[8][NW];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int q = 0; q < NW; ++q) w[i][q] = nxt[i][q];
+        const int64_t gn = g + gridDim.y;
+        if (gn < G) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) load4<BF16>(src + (8 * gn + i) * rstride, nxt[i]);
+        }
+        uint32_t cp[8][2];
+        uint32_t amax = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) vec_codes<K, BF16, MODE, NW>(w[i], cp[i], P, amax);
+        if (!amax_special<BF16, MODE>(amax, P)) {
+            uint32_t RL[1][8], RH[1][8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                RL[0][i] = prmt(cp[i][0], cp[i][1], 0x6420);
+                RH[0][i] = (K == 9) ? prmt(cp[i][0] >> 1, cp[i][1] >> 1, 0x6420) : 0u;
+            }
+            for (int d = 0; d < D.n; ++d) rows_fast_store<K, 1, 0>(RL, RH, D.p[d], so, g + g0, C, c0);
+        } else {
+            for (int v = 0; v < 4; ++v)
+                push_container_generic<BF16, K>(in, C, g * C + c0 + v, g0, F, D, so, spi, spb, spc, cap);
+        }
+    }
+}
+
+template <int K, bool BF16, int MODE>
+exmy_status launch_push_km(const uint8_t *in, int64_t R, int64_t C, int64_t g0, int x, int y, const uint8_t *meta,
+                           const PushDst &D, const SegOffsets &so, int64_t *spi, uint32_t *spb,
+                           unsigned long long *spc, int64_t cap, cudaStream_t st) {
+    const int threads = 256;
+    static int occ = 0;
+    if (!occ) occ = occupancy(k_enc_push<K, BF16, MODE>, threads, 0);
+    const int64_t CV = C / 4, G = R / 8;
+    const int64_t gx = cdiv(CV, threads);
+    int64_t gy = (int64_t)num_sms() * occ / gx;
+    if (gy < 1) gy = 1;
+    if (gy > G) gy = G;
+    if (gy > 65535) gy = 65535;
+    if (gx > INT_MAX) return EXMY_E_SHAPE;
+    k_enc_push<K, BF16, MODE><<<dim3((unsigned)gx, (unsigned)gy), threads, 0, st>>>(in, R, C, g0, x, y, meta, D, so, spi,
+                                                                                   spb, spc, cap, g_force_generic);
+    return launch_status();
+}
+
+template <int K, bool BF16>
+exmy_status launch_push_k(const uint8_t *in, int64_t R, int64_t C, int64_t g0, int x, int y, const uint8_t *meta,
+                          const PushDst &D, const SegOffsets &so, int64_t *spi, uint32_t *spb,
+                          unsigned long long *spc, int64_t cap, cudaStream_t st) {
+    if (BF16 && y <= 6)   // mode choice as exmy_encode
+        return y == 0 ? launch_push_km<K, BF16, (BF16 ? ENC_SIMD_Y0 : ENC_F32_Y0)>(in, R, C, g0, x, y, meta, D, so, spi,
+                                                                                   spb, spc, cap, st)
+                      : launch_push_km<K, BF16, (BF16 ? ENC_SIMD : ENC_F32)>(in, R, C, g0, x, y, meta, D, so, spi, spb,
+                                                                             spc, cap, st);
+    return y == 0 ? launch_push_km<K, BF16, ENC_F32_Y0>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st)
+                  : launch_push_km<K, BF16, ENC_F32>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st);
+}
+
+template <bool BF16>
+exmy_status push_dispatch(int k, const uint8_t *in, int64_t R, int64_t C, int64_t g0, int x, int y,
+                          const uint8_t *meta, const PushDst &D, const SegOffsets &so, int64_t *spi, uint32_t *spb,
+                          unsigned long long *spc, int64_t cap, cudaStream_t st) {
+    switch (k) {
+        case 3: return launch_push_k<3, BF16>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st);
+        case 4: return launch_push_k<4, BF16>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st);
+        case 5: return launch_push_k<5, BF16>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st);
+        case 6: return launch_push_k<6, BF16>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st);
+        case 7: return launch_push_k<7, BF16>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st);
+        case 8: return launch_push_k<8, BF16>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st);
+        case 9: return launch_push_k<9, BF16>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st);
+    }
+    return EXMY_E_FORMAT;
+}
+
+bool fmt_ok(int x, int y) {
+    if (x < 0 || x > 8 || y < 0) return false;
+    const int k = 1 + x + y;
+    return k >= 3 && k <= 9;
+}
+
+}  // namespace
+
+extern "C" exmy_status exmy_encode_push(const void *in, int dtype, int64_t rows, int64_t cols, int64_t row0,
+                                        int64_t total_rows, int x, int y, const uint8_t *meta, uint8_t *const *dst,
+                                        int ndst, int64_t *sp_index, uint32_t *sp_bits, uint64_t *sp_count,
+                                        int64_t sp_capacity, void *stream) {
+    if (dtype != EXMY_F32 && dtype != EXMY_BF16) return EXMY_E_DTYPE;
+    if (!fmt_ok(x, y)) return EXMY_E_FORMAT;
+    if (rows < 0 || cols < 0 || row0 < 0 || total_rows < 0 || row0 + rows > total_rows) return EXMY_E_SHAPE;
+    if (rows % 8 || row0 % 8 || total_rows % 8) return EXMY_E_SHAPE;
+    if (cols && total_rows > INT64_MAX / cols) return EXMY_E_SHAPE;
+    if (ndst < 1 || ndst > PUSH_MAX || !dst) return EXMY_E_ARG;
+    if (sp_capacity < 0) return EXMY_E_CAPACITY;
+    if (sp_capacity > 0 && (!sp_index || !sp_bits)) return EXMY_E_ARG;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    auto *spc = reinterpret_cast<unsigned long long *>(sp_count);
+    if (spc && cudaMemsetAsync(spc, 0, sizeof(unsigned long long), st) != cudaSuccess) return EXMY_E_CUDA;
+    if (rows == 0 || cols == 0) return EXMY_OK;
+    if (!in || !meta) return EXMY_E_ARG;
+    const int k = 1 + x + y;
+    const Plan p = make_plan(k, total_rows * cols);   // the WHOLE tensor's segment offsets
+    PushDst D{};
+    D.n = ndst;
+    for (int d = 0; d < ndst; ++d) {
+        if (!dst[d]) return EXMY_E_ARG;
+        D.p[d] = dst[d];
+        for (int s = 0; s < p.nseg; ++s)
+            if (!aligned(dst[d] + p.so.off[s], p.w[s] == 8 ? 4 : 4 * p.w[s])) return EXMY_E_ALIGN;
+    }
+    const auto *pi = static_cast<const uint8_t *>(in);
+    if (!aligned(pi, 4 * (dtype == EXMY_BF16 ? 2 : 4)) || cols % 4) return EXMY_E_ALIGN;
+    exmy_status s = dtype == EXMY_BF16
+                        ? push_dispatch<true>(k, pi, rows, cols, row0 / 8, x, y, meta, D, p.so, sp_index, sp_bits, spc,
+                                              sp_capacity, st)
+                        : push_dispatch<false>(k, pi, rows, cols, row0 / 8, x, y, meta, D, p.so, sp_index, sp_bits, spc,
+                                               sp_capacity, st);
+    if (s != EXMY_OK) return s;
+    if (spc && sp_capacity > 1) s = launch_specials_sort(sp_index, sp_bits, spc, sp_capacity, st);
+    return s;
+}

@@ -111,3 +111,36 @@ def sharded_roundtrip(shard: torch.Tensor, fmt, axis="rows", group=None, codec=N
     dec = [codec.decode_raw(out[r * nb:(r + 1) * nb], R_local, C, (p.x, p.y), meta, axis=axis, dtype=shard.dtype)
            for r in range(G)]
     return glob, torch.cat(dec, 0)
+
+
+# --------------------------------------------- fused encode + all-gather (push)
+def symmetric_packed_buffers(nbytes: int, group=None):
+    """This rank's gathered packed buffer plus every rank's, mapped into this
+    process (NVLink peer memory through torch symmetric memory): the
+    destinations of `pushed_encode`.  Needs CUDA peers (NCCL group)."""
+    from torch.distributed import _symmetric_memory as symm_mem
+    buf = symm_mem.empty(nbytes, dtype=torch.uint8, device=torch.device("cuda", torch.cuda.current_device()))
+    h = symm_mem.rendezvous(buf, group=dist.group.WORLD if group is None else group)
+    peers = [h.get_buffer(r, (nbytes,), torch.uint8) for r in range(h.world_size)]
+    return buf, peers
+
+
+def pushed_encode(shard: torch.Tensor, fmt, total_rows: int, row0: int, peer_buffers, group=None, codec=None,
+                  meta=None):
+    """Fused encode + all-gather: the global metadata from
+    the 2 KiB histogram all-reduce (unless given), then ONE kernel encodes this
+    rank's row shard and stores its bytes at their global offsets into every
+    rank's buffer (peer_buffers), then a barrier.  Afterwards every rank's
+    buffer holds the single-GPU encode of the whole tensor -- no NCCL
+    all-gather, no staging copy, the transfer overlaps the conversion.
+    Returns (meta, specials of the shard with global indices)."""
+    codec = codec or _default_codec()
+    if meta is None:
+        hist = codec.histogram(shard)
+        allreduce_histogram(hist, group)
+        meta = codec.emax(hist)
+    sp = codec.encode_push(shard, fmt, meta, row0, total_rows, peer_buffers)
+    if shard.is_cuda:
+        torch.cuda.current_stream(shard.device).synchronize()   # the stores have landed before peers read
+    dist.barrier(group)
+    return meta, sp

@@ -51,6 +51,27 @@ class OracleCodec:
         return W.from_bits(out)
 
 
+class OraclePushCodec(OracleCodec):
+    """encode_push on CPU: the shard's oracle bytes copied to their global
+    offsets in each destination (shared-memory tensors standing in for the
+    NVLink-mapped peer buffers)."""
+
+    def encode_push(self, shard, fmt, meta, row0, total_rows, dsts):
+        import workloads as W
+        x, y = self.o.parse_format(fmt)
+        k = 1 + x + y
+        R, C = shard.shape
+        packed = self.o.encode(W.to_bits(shard), (x, y), int(meta.item()), self.o.ROWS)[0]
+        ws, offs_local = self.o.segments(k, R * C)
+        _, offs_glob = self.o.segments(k, total_rows * C)
+        for w, ol, og in zip(ws, offs_local, offs_glob):
+            n = R * C * w // 8
+            start = og + row0 * C * w // 8
+            for d in dsts:
+                d[start:start + n] = torch.from_numpy(packed[ol:ol + n])
+        return None
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -112,3 +133,54 @@ def test_shard_rows_validation():
     with pytest.raises(ValueError):
         xdist.shard_rows(64, 4, 0, True) if False else xdist.shard_rows(48, 4, 0, True)
     assert xdist.shard_rows(48, 4, 0, False) == (0, 12)
+
+
+def _push_worker(rank, ws, port, fmt, paths, results):
+    import sys
+    sys.path.insert(0, ROOT)
+    import workloads as W
+    from paper_2405_13938_b200 import dist as xdist
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=ws)
+    try:
+        full = W.bf16_weights((64, 48), seed=13, std=0.05)
+        r0, r1 = xdist.shard_rows(64, ws, rank, True)
+        codec = OraclePushCodec()
+        x, y = codec.o.parse_format(fmt)
+        nb = 64 * 48 * (1 + x + y) // 8
+        # every rank maps every rank's buffer (the symmetric-memory picture)
+        peers = [torch.from_file(p, shared=True, size=nb, dtype=torch.uint8) for p in paths]
+        meta, _ = xdist.pushed_encode(full[r0:r1].contiguous(), fmt, 64, r0, peers, codec=codec)
+        results[rank] = (peers[rank].numpy().tobytes(), int(meta.item()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ws", [2, 4])
+@pytest.mark.parametrize("fmt", ["e3m3", "e2m1", "e4m4"])
+def test_pushed_encode_gloo(orc, tmp_path, ws, fmt):
+    """fused encode + all-gather host wiring: each rank's buffer ends as the
+    single encode of the whole tensor, with the all-reduced global e_max"""
+    import workloads as W
+    x, y = orc.parse_format(fmt)
+    nb = 64 * 48 * (1 + x + y) // 8
+    paths = []
+    for r in range(ws):
+        p = tmp_path / f"peer{r}.bin"
+        p.write_bytes(bytes(nb))
+        paths.append(str(p))
+    ctx = mp.get_context("spawn")
+    results = ctx.Manager().dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_push_worker, args=(r, ws, port, fmt, paths, results)) for r in range(ws)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    bits = W.to_bits(W.bf16_weights((64, 48), seed=13, std=0.05))
+    e = orc.emax(orc.histogram(bits))
+    ref = orc.encode(bits, fmt, e, orc.ROWS)[0]
+    for r in range(ws):
+        buf, meta = results[r]
+        assert meta == e
+        assert np.frombuffer(buf, np.uint8).tolist() == ref.tolist()
