@@ -72,7 +72,10 @@ typedef enum {
     EXMY_E_ALIGN = 5,     /* reserved: misaligned tensors take the scalar kernels */
     EXMY_E_CAPACITY = 6,
     EXMY_E_CUDA = 7,
-    EXMY_E_ARG = 8
+    EXMY_E_ARG = 8,
+    EXMY_E_IO = 9,         /* checkpoint file: open / read / write failed */
+    EXMY_E_CONTAINER = 10, /* checkpoint file: bad magic, version or manifest */
+    EXMY_E_CHECKSUM = 11   /* checkpoint file: CRC32 mismatch */
 } exmy_status;
 
 typedef enum { EXMY_F32 = 0, EXMY_BF16 = 1 } exmy_dtype;
@@ -351,6 +354,65 @@ exmy_status exmy_group_encode(const void *plan_host, const void *plan_device, vo
 
 /* Decode every entry into its `out` (+ out-of-band specials).  Two launches. */
 exmy_status exmy_group_decode(const void *plan_host, const void *plan_device, void *stream);
+
+/* ------------------------------------------------ checkpoint container
+ * "encoding and decoding tensors and checkpoints"
+ * (P:17-18); file layout after S:369-378 (little-endian):
+ *   "EXMY" | version u8 = 1 | entry_count u32, then per tensor
+ *   name_len u16 | name | rank u8 | dims u32 x rank | x u8 | y u8 | scheme u8
+ *   (0 max-before, 1 max-after, 2 float-scale) | block_kind u8 (0 tensor,
+ *   1 row, 2 col, 3 sub-row + L u32, 4 tile + r u32, c u32) | flags u8 (bit0
+ *   scale, bit1 specials, bit2 COLS packing, bit3 bf16 source) | (offset u64,
+ *   length u64) of metadata, each packed segment (descending width), scale
+ *   array, specials | crc32 u32 (IEEE) of the tensor's payload bytes;
+ *   payloads follow the manifest, one tensor's sections contiguous.
+ * Specials are stored as count u64 indices then count u32 fp32 patterns.
+ * Host code (pread / pwrite); every buffer here is HOST memory. */
+typedef struct exmy_ckpt_tensor {
+    const char *name;              /* unique, <= 65535 bytes */
+    int rank;                      /* 0..8 */
+    int64_t dims[8];               /* each < 2^32; prod(dims) % 8 == 0 */
+    int x, y, scheme, block_kind;
+    int64_t block_p0, block_p1;    /* sub-row L / tile (r, c) */
+    int axis;                      /* EXMY_AXIS_ROWS / COLS */
+    int src_dtype;                 /* EXMY_F32 / EXMY_BF16 */
+    const void *meta;              /* metadata bytes (u8 e_max per block) */
+    int64_t meta_bytes;
+    const void *packed;            /* the n*k/8 packed bytes, segments in order */
+    int64_t packed_bytes;
+    const void *scale;             /* float-scale metadata (fp32 per block) or NULL */
+    int64_t scale_bytes;
+    const int64_t *sp_index;       /* specials (sorted) */
+    const uint32_t *sp_bits;
+    int64_t specials_count;
+} exmy_ckpt_tensor;
+
+typedef struct exmy_ckpt exmy_ckpt;   /* opaque reader */
+
+/* Write n tensors; returns the file size in bytes, or -status (E_ARG,
+ * E_SHAPE: packed_bytes != prod(dims)*k/8, E_IO).  n = 0 writes a valid
+ * empty container. */
+int64_t exmy_ckpt_write(const char *path, const exmy_ckpt_tensor *tensors, int n);
+
+/* Open: reads the header and manifest only (E_IO, E_CONTAINER for bad
+ * magic / version / truncated manifest / sections outside the file). */
+exmy_status exmy_ckpt_open(const char *path, exmy_ckpt **out);
+int exmy_ckpt_count(const exmy_ckpt *h);
+/* Tensor i's manifest entry: sizes filled, data pointers NULL; `name` stays
+ * valid until exmy_ckpt_close. */
+exmy_status exmy_ckpt_info(const exmy_ckpt *h, int i, exmy_ckpt_tensor *info);
+/* index of the tensor called `name`, -1 if none */
+int exmy_ckpt_find(const exmy_ckpt *h, const char *name);
+/* Lazy read of tensor i: each non-NULL destination (host) receives exactly
+ * that section (sizes from exmy_ckpt_info); no other tensor's bytes are
+ * touched.  No CRC check (see exmy_ckpt_verify). */
+exmy_status exmy_ckpt_read(exmy_ckpt *h, int i, void *meta, void *packed, void *scale,
+                           int64_t *sp_index, uint32_t *sp_bits);
+/* Recompute tensor i's CRC32 over its payload: EXMY_OK or E_CHECKSUM. */
+exmy_status exmy_ckpt_verify(exmy_ckpt *h, int i);
+/* payload bytes read through this handle so far (instrumentation) */
+int64_t exmy_ckpt_bytes_read(const exmy_ckpt *h);
+void exmy_ckpt_close(exmy_ckpt *h);
 
 /* ------------------------------------------------ host-buffer conveniences */
 

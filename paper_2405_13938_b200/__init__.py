@@ -29,7 +29,7 @@ ROWS, COLS = 0, 1
 _AXES = {"rows": ROWS, "cols": COLS, ROWS: ROWS, COLS: COLS}
 
 STATUS = {0: "ok", 1: "E_FORMAT", 2: "E_META", 3: "E_SHAPE", 4: "E_DTYPE", 5: "E_ALIGN",
-          6: "E_CAPACITY", 7: "E_CUDA", 8: "E_ARG"}
+          6: "E_CAPACITY", 7: "E_CUDA", 8: "E_ARG", 9: "E_IO", 10: "E_CONTAINER", 11: "E_CHECKSUM"}
 
 
 class ExmyError(RuntimeError):
@@ -76,6 +76,15 @@ def _load():
         "exmy_encode_fs": ([vp, i32, i64, i64, i32, i64, i64, i32, i32, vp, vp, vp, vp, vp, i64, vp], i32),
         "exmy_decode_fs": ([vp, i64, i64, i32, i64, i64, i32, i32, vp, vp, vp, vp, i64, vp, i32, vp], i32),
         "exmy_encode_push": ([vp, i32, i64, i64, i64, i64, i32, i32, vp, vp, i32, vp, vp, vp, i64, vp], i32),
+        "exmy_ckpt_write": ([ctypes.c_char_p, vp, i32], i64),
+        "exmy_ckpt_open": ([ctypes.c_char_p, vp], i32),
+        "exmy_ckpt_count": ([vp], i32),
+        "exmy_ckpt_info": ([vp, i32, vp], i32),
+        "exmy_ckpt_find": ([vp, ctypes.c_char_p], i32),
+        "exmy_ckpt_read": ([vp, i32, vp, vp, vp, vp, vp], i32),
+        "exmy_ckpt_verify": ([vp, i32], i32),
+        "exmy_ckpt_bytes_read": ([vp], i64),
+        "exmy_ckpt_close": ([vp], None),
         "exmy_group_plan_bytes": ([i32], ctypes.c_size_t),
         "exmy_group_plan": ([vp, i32, i32, i32, i32, i32, vp, ctypes.c_size_t], i32),
         "exmy_group_max_exponent": ([vp, vp, vp], i32),
@@ -99,7 +108,8 @@ EXPORTED = ["exmy_version", "exmy_status_string", "exmy_format_valid", "exmy_pac
             "exmy_decode_blocked", "exmy_decode_rows", "exmy_max_exponent", "exmy_encode_rowwise",
             "exmy_group_plan_bytes", "exmy_group_plan", "exmy_group_max_exponent", "exmy_group_encode",
             "exmy_group_decode", "exmy_block_float_scale", "exmy_quantize_fs", "exmy_encode_fs", "exmy_decode_fs",
-            "exmy_encode_push"]
+            "exmy_encode_push", "exmy_ckpt_write", "exmy_ckpt_open", "exmy_ckpt_count", "exmy_ckpt_info",
+            "exmy_ckpt_find", "exmy_ckpt_read", "exmy_ckpt_verify", "exmy_ckpt_bytes_read", "exmy_ckpt_close"]
 
 
 def lib():
@@ -742,3 +752,150 @@ class GroupCodec:
             raise ValueError("GroupCodec built with decode_outputs=False")
         self._call(_lib.exmy_group_decode, "group_decode")
         return self.outs
+
+
+# ------------------------------------------------------ checkpoint container
+class _CkptTensor(ctypes.Structure):
+    """exmy_ckpt_tensor (include/exmy.h)"""
+    _fields_ = [("name", ctypes.c_char_p), ("rank", ctypes.c_int), ("dims", ctypes.c_int64 * 8),
+                ("x", ctypes.c_int), ("y", ctypes.c_int), ("scheme", ctypes.c_int), ("block_kind", ctypes.c_int),
+                ("block_p0", ctypes.c_int64), ("block_p1", ctypes.c_int64), ("axis", ctypes.c_int),
+                ("src_dtype", ctypes.c_int), ("meta", ctypes.c_void_p), ("meta_bytes", ctypes.c_int64),
+                ("packed", ctypes.c_void_p), ("packed_bytes", ctypes.c_int64), ("scale", ctypes.c_void_p),
+                ("scale_bytes", ctypes.c_int64), ("sp_index", ctypes.c_void_p), ("sp_bits", ctypes.c_void_p),
+                ("specials_count", ctypes.c_int64)]
+
+
+def _block_kind(p: Packed):
+    """(block_kind, p0, p1) of S:375 for a Packed's metadata granularity"""
+    if p.block is None:
+        return 0, 0, 0
+    R, C = p.rows, p.cols
+    br, bc = p.block
+    if (br, bc) == (R, C):
+        return 0, 0, 0
+    if (br, bc) == (1, C):
+        return 1, 0, 0
+    if (br, bc) == (R, 1):
+        return 2, 0, 0
+    if br == 1:
+        return 3, bc, 0
+    return 4, br, bc
+
+
+def save_checkpoint(path: str, tensors: dict) -> int:
+    """Write {name: Packed} to an EXMY container (host copies of the device
+    buffers); returns the file size.  Layout in include/exmy.h."""
+    keep = []
+    arr = (_CkptTensor * max(len(tensors), 1))()
+    for i, (name, p) in enumerate(tensors.items()):
+        dims = list(p.layout) if p.layout is not None else list(p.shape)
+        data = p.data.detach().cpu().contiguous()
+        meta = p.meta.detach().cpu().contiguous()
+        scale = p.scale.detach().cpu().contiguous() if p.scale is not None else None
+        cnt = int(p.sp_count.item()) if p.sp_count is not None else 0
+        cnt = min(cnt, p.sp_index.numel()) if cnt else 0
+        spi = p.sp_index[:cnt].detach().cpu().contiguous() if cnt else None
+        spb = p.sp_bits[:cnt].detach().cpu().contiguous() if cnt else None
+        nm = name.encode()
+        keep += [data, meta, scale, spi, spb, nm]
+        e = arr[i]
+        e.name = nm
+        e.rank = len(dims)
+        for d, v in enumerate(dims):
+            e.dims[d] = int(v)
+        e.x, e.y = p.x, p.y
+        e.scheme = 2 if p.scale is not None else 0
+        e.block_kind, e.block_p0, e.block_p1 = _block_kind(p)
+        e.axis = p.axis
+        e.src_dtype = _dtype_code(p.dtype)
+        e.meta, e.meta_bytes = meta.data_ptr(), meta.numel()
+        e.packed, e.packed_bytes = data.data_ptr(), data.numel()
+        if scale is not None:
+            e.scale, e.scale_bytes = scale.data_ptr(), scale.numel() * 4
+        if cnt:
+            e.sp_index, e.sp_bits, e.specials_count = spi.data_ptr(), spb.data_ptr(), cnt
+    n = _lib.exmy_ckpt_write(path.encode(), arr, len(tensors))
+    if n < 0:
+        raise ExmyError(int(-n), "ckpt_write")
+    return int(n)
+
+
+class Checkpoint:
+    """Lazy reader of an EXMY container: opening reads the manifest only;
+    ``load(name)`` reads that tensor's byte ranges (pread) and moves them to
+    the device; ``verify(name)`` checks its CRC32."""
+
+    def __init__(self, path: str):
+        h = ctypes.c_void_p()
+        _check(_lib.exmy_ckpt_open(path.encode(), ctypes.byref(h)), "ckpt_open")
+        self._h = h
+        self.names = []
+        for i in range(_lib.exmy_ckpt_count(h)):
+            self.names.append(self.info(i).name.decode())
+
+    def close(self):
+        if self._h:
+            _lib.exmy_ckpt_close(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _index(self, name) -> int:
+        i = name if isinstance(name, int) else _lib.exmy_ckpt_find(self._h, name.encode())
+        if i < 0:
+            raise KeyError(name)
+        return i
+
+    def info(self, name) -> _CkptTensor:
+        e = _CkptTensor()
+        _check(_lib.exmy_ckpt_info(self._h, self._index(name), ctypes.byref(e)), "ckpt_info")
+        return e
+
+    @property
+    def bytes_read(self) -> int:
+        return int(_lib.exmy_ckpt_bytes_read(self._h))
+
+    def verify(self, name) -> bool:
+        s = _lib.exmy_ckpt_verify(self._h, self._index(name))
+        if s == 11:
+            return False
+        _check(s, "ckpt_verify")
+        return True
+
+    def load(self, name, device="cuda") -> Packed:
+        i = self._index(name)
+        e = self.info(i)
+        pin = torch.cuda.is_available()
+        meta = torch.empty(e.meta_bytes, dtype=torch.uint8, pin_memory=pin)
+        data = torch.empty(e.packed_bytes, dtype=torch.uint8, pin_memory=pin)
+        scale = torch.empty(e.scale_bytes // 4, dtype=torch.float32, pin_memory=pin) if e.scale_bytes else None
+        cnt = e.specials_count
+        spi = torch.empty(max(cnt, 1), dtype=torch.int64)
+        spb = torch.empty(max(cnt, 1), dtype=torch.int32)
+        _check(_lib.exmy_ckpt_read(self._h, i, _ptr(meta), _ptr(data), _ptr(scale), _ptr(spi) if cnt else None,
+                                   _ptr(spb) if cnt else None), "ckpt_read")
+        dims = tuple(int(e.dims[d]) for d in range(e.rank))
+        R, C = _as_2d_shape(dims)
+        kind = e.block_kind
+        block = {0: None, 1: (1, C), 2: (R, 1), 3: (1, int(e.block_p0)), 4: (int(e.block_p0), int(e.block_p1))}[kind]
+        if scale is not None and block is None:
+            block = (R, C)
+        if block is not None and scale is None:
+            meta = meta.reshape(R // block[0], C // block[1])
+        dev = torch.device(device)
+        to = (lambda t: t.to(dev, non_blocking=True) if t is not None else None)
+        spc = torch.tensor([cnt], dtype=torch.int64)
+        dt = torch.bfloat16 if e.src_dtype == BF16 else torch.float32
+        return Packed(to(data), to(meta), to(spi), to(spb), to(spc), dims, int(e.x), int(e.y), int(e.axis), dt,
+                      block, None, to(scale.reshape(R // block[0], C // block[1])) if scale is not None else None)

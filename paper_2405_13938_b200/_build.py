@@ -21,7 +21,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v
 # one translation unit per op family so they compile in parallel
 UNITS = ["exmy_abi.cu", "exmy_tu_hist.cu", "exmy_tu_quant.cu", "exmy_tu_encode.cu", "exmy_tu_decode.cu",
          "exmy_tu_blk_encode.cu", "exmy_tu_blk_decode.cu", "exmy_tu_grouped.cu",
-         "exmy_tu_fscale.cu", "exmy_tu_push.cu"]
+         "exmy_tu_fscale.cu", "exmy_tu_push.cu", "exmy_ckpt.cpp"]
 HEADERS = ["exmy_device.cuh", "exmy_kernels.cuh", "exmy_fast.cuh", "exmy_blocked.cuh", "exmy_launch.cuh", "exmy_grouped.cuh",
            "exmy_fscale.cuh"]
 
@@ -48,7 +48,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     log = []
 
     def compile_one(src):
-        obj = os.path.join(BUILD, os.path.basename(src).replace(".cu", ".o"))
+        obj = os.path.join(BUILD, os.path.splitext(os.path.basename(src))[0] + ".o")
         cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         log.append((src, r.stdout + r.stderr))
@@ -81,7 +81,7 @@ def build_variant(out: str, extra: list[str], units=("exmy_tu_grouped.cu",)) -> 
     objs = []
     for u in UNITS:
         if u in units:
-            obj = os.path.join(vdir, u.replace(".cu", ".o"))
+            obj = os.path.join(vdir, os.path.splitext(u)[0] + ".o")
             r = subprocess.run([NVCC, *ARCH, *FLAGS, *extra, "-c", os.path.join(CSRC, u), "-o", obj],
                                capture_output=True, text=True)
             if r.returncode != 0:
@@ -90,7 +90,7 @@ def build_variant(out: str, extra: list[str], units=("exmy_tu_grouped.cu",)) -> 
                 f.write(r.stdout + r.stderr)
             objs.append(obj)
         else:
-            objs.append(os.path.join(BUILD, u.replace(".cu", ".o")))
+            objs.append(os.path.join(BUILD, os.path.splitext(u)[0] + ".o"))
     r = subprocess.run([NVCC, *ARCH, "-shared", "-o", out, *objs, "-lcudart"], capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -56,6 +56,9 @@ const char *exmy_status_string(int s) {
         case EXMY_E_CAPACITY: return "invalid specials capacity";
         case EXMY_E_CUDA: return "CUDA launch error";
         case EXMY_E_ARG: return "invalid argument (NULL pointer)";
+        case EXMY_E_IO: return "checkpoint file I/O error";
+        case EXMY_E_CONTAINER: return "not a valid EXMY container (magic, version or manifest)";
+        case EXMY_E_CHECKSUM: return "checkpoint CRC32 mismatch";
     }
     return "unknown status";
 }
