@@ -828,14 +828,16 @@ template <bool BF16>
 __global__ void __launch_bounds__(256) k_max_exp(const uint8_t *__restrict__ in, int64_t n, uint8_t *meta) {
     using EL = Elem<BF16>;
     const int64_t nvec = n / EL::V;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     uint32_t amax = 0;   // bf16: 16-bit lanes of magnitudes; fp32: magnitude bits
     constexpr int U = 4;
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; base < nvec; base += stride * U) {
+    // a CTA reads one contiguous 16 KB chunk per iteration (4 coalesced
+    // 16-byte loads per thread), chunks grid-strided: whole DRAM pages per CTA
+    const int64_t chunk = (int64_t)blockDim.x * U;
+    for (int64_t c0 = (int64_t)blockIdx.x * chunk; c0 < nvec; c0 += (int64_t)gridDim.x * chunk) {
         uint4 r[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int64_t vi = base + u * stride;
+            const int64_t vi = c0 + u * blockDim.x + threadIdx.x;
             r[u] = vi < nvec ? ldg_nc_v4(in + vi * 16) : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll

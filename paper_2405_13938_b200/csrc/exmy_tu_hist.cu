@@ -43,9 +43,11 @@ exmy_status launch_histogram(const uint8_t *in, bool bf16, int64_t n, unsigned l
 exmy_status launch_max_exponent(const uint8_t *in, bool bf16, int64_t n, uint8_t *meta, cudaStream_t st) {
     if (cudaMemsetAsync(meta, 0, 1, st) != cudaSuccess) return EXMY_E_CUDA;
     const int64_t nvec = n / (bf16 ? 8 : 4);
-    int64_t blocks = cdiv(cdiv(nvec, 4), 256);
+    int64_t blocks = cdiv(nvec, 1024);   // 16 KB chunks
     if (blocks < 1) blocks = 1;
-    if (blocks > (int64_t)num_sms() * 4) blocks = (int64_t)num_sms() * 4;
+    static int occ = 0;
+    if (!occ) occ = occupancy(k_max_exp<true>, 256, 0);
+    if (blocks > (int64_t)num_sms() * occ) blocks = (int64_t)num_sms() * occ;
     if (bf16) k_max_exp<true><<<(unsigned)blocks, 256, 0, st>>>(in, n, meta);
     else k_max_exp<false><<<(unsigned)blocks, 256, 0, st>>>(in, n, meta);
     return launch_status();
