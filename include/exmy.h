@@ -176,8 +176,10 @@ exmy_status exmy_decode(const uint8_t *packed, int64_t rows, int64_t cols, int a
  * exmy_debug_force_generic(1) routes every element through the integer
  * generic encode/decode paths instead of the fast paths, so both can be
  * checked against the oracle; exmy_debug_hist_mode selects the histogram
- * counter-update variant (0: lane-private read-modify-write, 1 (default):
- * lane-private shared-memory atomics).  Pass -1 to query.  Return the previous value. */
+ * counter-update variant (0: lane-private read-modify-write, 1: lane-private
+ * shared-memory atomics, 2 (default): the same atomics with both bf16
+ * elements' counter offsets from one shift+mask and red.shared on 32-bit
+ * shared addresses).  Pass -1 to query.  Return the previous value. */
 int exmy_debug_force_generic(int on);
 int exmy_debug_hist_mode(int mode);
 

@@ -9,7 +9,7 @@
 
 namespace exmy {
 int g_force_generic = 0;
-int g_hist_mode = 1;
+int g_hist_mode = 2;
 }  // namespace exmy
 
 using namespace exmy;

@@ -90,6 +90,14 @@ __device__ __forceinline__ void hist_flush_warp(uint32_t *warpbase, int lane, un
     __syncwarp();
 }
 
+// MODE 2: both counter-word offsets of a bf16 pair from one shift + mask
+// (16-bit lanes: ((w >> 1) & 0x3F803F80) = (bin >> 1) * 128 bytes for both
+// elements), the increments from the exponent LSBs by select, and
+// red.shared on 32-bit shared addresses: 5.5 instead of 7 ops / element.
+__device__ __forceinline__ void red_shared_add(uint32_t addr, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
 template <bool BF16, int MODE>
 __global__ void __launch_bounds__(HIST_THREADS) k_hist(const uint8_t *__restrict__ in, int64_t n,
                                                        unsigned long long *__restrict__ hist) {
@@ -98,6 +106,7 @@ __global__ void __launch_bounds__(HIST_THREADS) k_hist(const uint8_t *__restrict
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t *warpbase = hsm + warp * HIST_WORDS_PER_WARP;
     uint32_t *lanebase = warpbase + lane;
+    const uint32_t lane_sa = (uint32_t)__cvta_generic_to_shared(lanebase);   // shared-window byte address
     for (int i = threadIdx.x; i < HIST_WARPS * HIST_WORDS_PER_WARP; i += HIST_THREADS) hsm[i] = 0;
     __syncthreads();
 
@@ -131,9 +140,18 @@ __global__ void __launch_bounds__(HIST_THREADS) k_hist(const uint8_t *__restrict
                 const uint32_t w[4] = {r[u].x, r[u].y, r[u].z, r[u].w};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    if (BF16) {
+                    if (BF16 && MODE == 2) {
+                        const uint32_t off = (w[q] >> 1) & 0x3F803F80u;   // both elements' word offsets (bytes)
+                        const uint32_t inc_lo = (w[q] & 0x80u) ? 0x10000u : 1u;
+                        const uint32_t inc_hi = (w[q] & 0x800000u) ? 0x10000u : 1u;
+                        red_shared_add(lane_sa + (off & 0xFFFFu), inc_lo);
+                        red_shared_add(lane_sa + (off >> 16), inc_hi);
+                    } else if (BF16) {
                         hist_bump(lanebase, (w[q] >> 7) & 0xFFu, MODE);
                         hist_bump(lanebase, (w[q] >> 23) & 0xFFu, MODE);
+                    } else if (MODE == 2) {
+                        const uint32_t wq = w[q];
+                        red_shared_add(lane_sa + ((wq >> 17) & 0x3F80u), (wq & 0x800000u) ? 0x10000u : 1u);
                     } else {
                         hist_bump(lanebase, (w[q] >> 23) & 0xFFu, MODE);
                     }

@@ -36,6 +36,7 @@ exmy_status launch_histogram(const uint8_t *in, bool bf16, int64_t n, unsigned l
     }
     switch (g_hist_mode) {
         case 0: return bf16 ? launch_hist_vec<true, 0>(in, n, hist, st) : launch_hist_vec<false, 0>(in, n, hist, st);
+        case 2: return bf16 ? launch_hist_vec<true, 2>(in, n, hist, st) : launch_hist_vec<false, 2>(in, n, hist, st);
         default: return bf16 ? launch_hist_vec<true, 1>(in, n, hist, st) : launch_hist_vec<false, 1>(in, n, hist, st);
     }
 }

@@ -58,7 +58,7 @@ def oracle_boundary_f32(orc, fmt, e_max):
 
 
 # ----------------------------------------------------------------- K1 / K1b
-@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("mode", [0, 1, 2])
 @pytest.mark.parametrize("dt", ["bf16", "f32"])
 @pytest.mark.parametrize("n", [0, 1, 7, 8 * 1000 + 5, 1 << 20, (1 << 22) + 3])
 def test_histogram_parity(exmy, orc, dt, n, mode):
@@ -68,7 +68,7 @@ def test_histogram_parity(exmy, orc, dt, n, mode):
         h = exmy.histogram(dev_bits(bits)).cpu().numpy().astype(np.uint64)
         np.testing.assert_array_equal(h, orc.histogram(bits))
     finally:
-        exmy.hist_mode(1)
+        exmy.hist_mode(2)
 
 
 @pytest.mark.parametrize("dt", ["bf16", "f32"])
