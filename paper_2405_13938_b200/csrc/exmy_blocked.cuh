@@ -266,6 +266,14 @@ struct GroupMeta {
         const int64_t row = div_rcp(q, gpr, inv_gpr);
         return at_row(M, row, q - row * gpr);
     }
+    // blocks spanning whole rows (bc == C) and rows of >= 128 groups: a warp
+    // tile covers at most rows rb and rb+1, so two metadata bytes serve it
+    __device__ __forceinline__ bool whole_rows() const { return bc8 == gpr && gpr >= 128; }
+    __device__ __forceinline__ int row_meta(const MetaMap &M, int64_t row) const {
+        const int64_t brow = M.br == 1 ? row : div_rcp(row, M.br, inv_br);
+        const int e = __ldg(M.meta + brow * M.nbc);
+        return e > 254 ? 254 : e;
+    }
     // warp tile of 128 groups starting at `base`: when a row holds >= 128
     // groups the tile spans at most two rows, so one division per tile
     // serves all of its groups
@@ -278,7 +286,7 @@ struct GroupMeta {
 };
 
 template <int K, bool BF16, int MODE>
-__global__ void __launch_bounds__(256) k_enc_cols_blk(const uint8_t *__restrict__ in, int64_t n, int64_t C, int x,
+__global__ void __launch_bounds__(256, 2) k_enc_cols_blk(const uint8_t *__restrict__ in, int64_t n, int64_t C, int x,
                                                       int y, MetaMap M, uint8_t *__restrict__ packed, SegOffsets so,
                                                       int64_t *spi, uint32_t *spb, unsigned long long *spc,
                                                       int64_t cap, int force_generic) {
@@ -292,21 +300,50 @@ __global__ void __launch_bounds__(256) k_enc_cols_blk(const uint8_t *__restrict_
     const int lane = threadIdx.x & 31;
     const int64_t step = (int64_t)gridDim.x * (blockDim.x >> 5) * 128;
     const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    // software pipeline (as k_enc_cols_fast): the next tile's groups are in
+    // flight while this tile is converted and packed
+    uint4 nxt[4][NV];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int64_t q = gw * 128 + 32 * u + lane;
+#pragma unroll
+        for (int t = 0; t < NV; ++t)
+            nxt[u][t] = q < NG ? ldg_nc_v4(in + q * 8 * EL::ES + 16 * t) : make_uint4(0, 0, 0, 0);
+    }
     for (int64_t base = gw * 128; base < NG; base += step) {
         const int64_t rb = div_rcp(base, GM.gpr, GM.inv_gpr), qs = base - rb * GM.gpr;
         uint4 r[4][NV];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t qn = base + step + 32 * u + lane;
+#pragma unroll
+            for (int t = 0; t < NV; ++t) {
+                r[u][t] = nxt[u][t];
+                nxt[u][t] = qn < NG ? ldg_nc_v4(in + qn * 8 * EL::ES + 16 * t) : make_uint4(0, 0, 0, 0);
+            }
+        }
         uint32_t cp[4][4];
         uint32_t amax = 0;
         bool ok = !force_generic;
 #pragma unroll
+        // whole-row blocks: the tile's two possible rows' parameters, once per tile
+        const bool wr = GM.whole_rows();
+        const int64_t split = GM.gpr - qs;   // tile groups t < split lie in row rb
+        RowP R0, R1;
+        if (wr) {
+            R0 = make_rowp<SIMD>(GM.row_meta(M, rb), x, y);
+            R1 = make_rowp<SIMD>(rb + 1 < NG / GM.gpr ? GM.row_meta(M, rb + 1) : 0, x, y);
+        }
+#pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int64_t q = base + 32 * u + lane;
             const bool in_range = q < NG;
-#pragma unroll
-            for (int t = 0; t < NV; ++t)
-                r[u][t] = in_range ? ldg_nc_v4(in + q * 8 * EL::ES + 16 * t) : make_uint4(0, 0, 0, 0);
-            const int e = in_range ? GM.at_tile(M, base, rb, qs, 32 * u + lane) : 0;
-            const RowP Rp = make_rowp<SIMD>(e, x, y);
+            RowP Rp;
+            if (wr) {
+                Rp = (32 * u + lane) < split ? R0 : R1;
+            } else {
+                Rp = make_rowp<SIMD>(in_range ? GM.at_tile(M, base, rb, qs, 32 * u + lane) : 0, x, y);
+            }
             ok = ok && (Rp.ok || !in_range);
 #pragma unroll
             for (int t = 0; t < NV; ++t) {
@@ -502,11 +539,18 @@ __global__ void __launch_bounds__(256) k_dec_cols_blk(const uint8_t *__restrict_
 #pragma unroll
         for (int i = 0; i < 8; ++i) { RL[i] = 0; RH[i] = 0; }
         cols_fast_load<K, 0>(RL, RH, packed, so, base + lane, NG);
+        const bool wr = GM.whole_rows();
+        const int64_t split = GM.gpr - qs;
+        RowD D0, D1;
+        if (wr) {
+            D0 = make_rowd(GM.row_meta(M, rb), x);
+            D1 = make_rowd(rb + 1 < NG / GM.gpr ? GM.row_meta(M, rb + 1) : 0, x);
+        }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int64_t q = base + 32 * u + lane;
             if (q >= NG) continue;
-            const RowD D = make_rowd(GM.at_tile(M, base, rb, qs, 32 * u + lane), x);
+            const RowD D = wr ? ((32 * u + lane) < split ? D0 : D1) : make_rowd(GM.at_tile(M, base, rb, qs, 32 * u + lane), x);
             if (!D.ok) {
                 dec_container_generic_blk<OBF16>(packed, C, q, 1, x, y, M, so, nseg, widths, out);
                 continue;
