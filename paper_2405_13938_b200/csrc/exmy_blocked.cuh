@@ -525,9 +525,14 @@ __global__ void __launch_bounds__(256) k_dec_rows_blk(const uint8_t *__restrict_
 // COLS: lane handles groups q = base + 32u + lane (one metadata per group);
 // host guarantees bc % 8 == 0 and the same format conditions.
 template <int K, bool OBF16>
-__global__ void __launch_bounds__(256) k_dec_cols_blk(const uint8_t *__restrict__ packed, int64_t n, int64_t C, int x,
-                                                      int y, MetaMap M, SegOffsets so, uint8_t *__restrict__ out,
-                                                      int nseg, int4 widths) {
+// 3 CTAs / SM (80 registers): per-row COLS decode e3m3 238 -> 187 us
+#ifndef DEC_COLS_BLK_MINB
+#define DEC_COLS_BLK_MINB 3
+#endif
+__global__ void __launch_bounds__(256, DEC_COLS_BLK_MINB) k_dec_cols_blk(const uint8_t *__restrict__ packed, int64_t n,
+                                                                         int64_t C, int x, int y, MetaMap M,
+                                                                         SegOffsets so, uint8_t *__restrict__ out,
+                                                                         int nseg, int4 widths) {
     const int64_t NG = n / 8;
     const GroupMeta GM(M, C);
     const int lane = threadIdx.x & 31;
