@@ -938,23 +938,30 @@ __global__ void __launch_bounds__(256) k_quant_fast(const uint8_t *__restrict__ 
     const FastP P = make_fast(F, BF16, force_generic);
     const DecPath DP = make_dec_path(F, force_generic);
     const int64_t nvec = n / EL::V;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     constexpr int U = 4;
     const bool fast = BF16 ? P.enc_simd : P.enc_f32;
+    // a CTA owns one contiguous chunk of U*256 vectors (16 KB in, 16 KB out)
+    // per iteration (vector = chunk*U*256 + u*256 + tid), chunks grid-strided,
+    // and a barrier per chunk keeps its warps reading and writing the chunk
+    // together (config 2 bf16: 181 -> 170 us, 90 -> 96 % of the copy peak;
+    // fp32 383 -> 353 us)
+    const int64_t stride = blockDim.x;
+    const int64_t cstep = (int64_t)gridDim.x * blockDim.x * U;
+    const int64_t base0 = (int64_t)blockIdx.x * blockDim.x * U + threadIdx.x;
     // software pipeline: the next U vectors are in flight while these are processed
     uint4 nxt[U];
-    const int64_t base0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int64_t vi = base0 + u * stride;
         if (vi < nvec) nxt[u] = ldg_nc_v4(in + vi * 16);
     }
-    for (int64_t base = base0; base < nvec; base += stride * U) {
+    for (int64_t base = base0; base < nvec + threadIdx.x; base += cstep) {   // CTA-uniform trip count
+        __syncthreads();
         uint4 r[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             r[u] = nxt[u];
-            const int64_t vn = base + (U + u) * stride;
+            const int64_t vn = base + cstep + u * stride;
             if (vn < nvec) nxt[u] = ldg_nc_v4(in + vn * 16);
         }
 #pragma unroll
