@@ -608,9 +608,12 @@ __global__ void __launch_bounds__(256) k_quant_blk(const uint8_t *__restrict__ i
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= CV) return;
     const int64_t c0 = j * EL::V;
+    const uint8_t *mcol = M.meta + c0 / M.bc;   // this thread's block column (one division per thread)
     for (int64_t r = blockIdx.y; r < R; r += gridDim.y) {
         const uint4 v = ldg_nc_v4(in + (r * C + c0) * EL::ES);
-        const Fmt F = fmt_of(x, y, meta_at(M, r, c0));
+        const int64_t rb = M.br == 1 ? r : r / M.br;
+        const int em = __ldg(mcol + rb * M.nbc);
+        const Fmt F = fmt_of(x, y, em > 254 ? 254 : em);
         const FastP P = make_fast(F, BF16, force_generic);
         const DecPath DP = make_dec_path(F, force_generic);
         uint32_t o[4];
