@@ -169,3 +169,22 @@ def test_group_plan_host(exmy):
     L = exmy.lib()
     junk = (ctypes.c_uint64 * 16)()
     assert L.exmy_group_encode(junk, junk, None) == 8
+
+
+def test_no_cpu_fallback(exmy, tmp_path):
+    """the product path fails loudly: importing without libexmy.so raises, and
+    CPU tensors are refused (never computed on the host)"""
+    import subprocess
+    import sys
+    import torch
+    code = ("import os, sys; sys.path.insert(0, %r); os.environ['EXMY_LIB_PATH'] = %r\n"
+            "try:\n    import paper_2405_13938_b200\nexcept ImportError as e:\n    print('IMPORT-ERROR', e)\n")
+    out = subprocess.run([sys.executable, "-c", code % (ROOT, str(tmp_path / "missing.so"))],
+                         capture_output=True, text=True, timeout=120)
+    assert "IMPORT-ERROR" in out.stdout and "no CPU fallback" in out.stdout
+    t = torch.zeros((8, 8), dtype=torch.bfloat16)
+    for call in (lambda: exmy.histogram(t), lambda: exmy.quantize(t, "e3m3", 127),
+                 lambda: exmy.encode(t, "e3m3", 127), lambda: exmy.encode_fs(t, "e2m1", None, "row"),
+                 lambda: exmy.GroupCodec([t], "e3m3")):
+        with pytest.raises(ValueError, match="CUDA"):
+            call()
