@@ -683,6 +683,59 @@ __device__ __forceinline__ int exp_after_rounding(uint32_t a, int y) {
     return t >= (1u << 23) ? 1 : 0;
 }
 
+// Sub-row blocks (1 x bc, bc / V in {1, 2, 4, 8, 16, 32}: "a sub row",
+// P:230-241, the small blocks e2m1 / e1m2 want): one thread per
+// 16-byte vector, four vectors in flight, and the bc / V lanes holding a
+// block combine their maxima with xor-shuffles; the group's first lane
+// writes the block's byte (MODE 0 / 1: exponent before / after rounding) or
+// its fp32 maximum (MODE 2, float scaling).  A warp-per-block kernel would
+// leave most lanes idle for such blocks.
+template <bool BF16, int MODE>
+__global__ void __launch_bounds__(256) k_block_max_small(const uint8_t *__restrict__ in, int64_t nvec, int gsz,
+                                                         int y, uint8_t *__restrict__ meta, float *__restrict__ amax_out) {
+    constexpr int U = 4;
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x - lane; v0 < nvec; v0 += stride * U) {
+        // warp-uniform: this warp's 32 consecutive vectors, then the next 3 strides
+        uint4 r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t vi = v0 + u * stride + lane;
+            r[u] = vi < nvec ? ldg_nc_v4(in + vi * 16) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t vb = v0 + u * stride;
+            if (vb >= nvec) break;   // warp-uniform
+            uint32_t am = 0;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const uint32_t w = word_of(r[u], t);
+                if (BF16) {
+                    const uint32_t lo = (w << 16) & 0x7FFF0000u, hi = w & 0x7FFF0000u;
+                    if (lo < 0x7F800000u) am = max(am, lo);
+                    if (hi < 0x7F800000u) am = max(am, hi);
+                } else {
+                    const uint32_t a = w & 0x7FFFFFFFu;
+                    if (a < 0x7F800000u) am = max(am, a);
+                }
+            }
+            for (int o = 1; o < gsz; o <<= 1) am = max(am, __shfl_xor_sync(0xFFFFFFFFu, am, o));
+            const int64_t vi = vb + lane;
+            if ((lane & (gsz - 1)) == 0 && vi < nvec) {
+                const int64_t b = vi / gsz;
+                if (MODE == 2) {
+                    amax_out[b] = __uint_as_float(am);
+                } else {
+                    const int e = MODE == 0 ? (int)(am >> 23) : exp_after_rounding(am, y);
+                    meta[b] = (uint8_t)(e > 254 ? 254 : e);
+                }
+            }
+        }
+    }
+}
+
 // one warp per block: max |finite| over the block, then the scheme's exponent
 template <bool BF16>
 __global__ void __launch_bounds__(256) k_block_max(const uint8_t *__restrict__ in, int64_t R, int64_t C, int64_t br,

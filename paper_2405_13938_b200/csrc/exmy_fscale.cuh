@@ -353,9 +353,10 @@ __global__ void __launch_bounds__(256) k_fs_quant(const uint8_t *__restrict__ in
 
 // ------------------------------------------------------- encode ROWS fast
 // 8-row x 4-column tiles as k_enc_rows_fast (host: bc % 4 == 0, so the 4
-// columns of a row share a block).  WSHARE (host: bc % 128 == 0): a warp's
-// 128 columns share one block column, so lanes 0..7 compute the 8 rows'
-// factors once and broadcast them (one division per lane instead of eight);
+// columns of a row share a block).  WSHARE (host: bc % 128 == 0, or bc = 32 /
+// 64): a warp's 128 columns span 1, 2 or 4 block columns, so 8 x that many
+// lanes compute the 8 rows' factors once and broadcast them (one division per
+// lane instead of eight);
 // otherwise each thread computes its 8.  The scaled patterns go through the
 // fp32 one-addition code path at e_max 127.  Tiles with NaN/Inf, amax = 0 or
 // an extreme amax take the integer path.
@@ -363,7 +364,7 @@ template <int K, bool BF16, bool Y0, bool WSHARE>
 __global__ void __launch_bounds__(256, 2) k_fs_enc_rows(const uint8_t *__restrict__ in, int64_t R, int64_t C, int x,
                                                         int y, FsMap S, float G, uint8_t *__restrict__ packed,
                                                         SegOffsets so, int64_t *spi, uint32_t *spb,
-                                                        unsigned long long *spc, int64_t cap) {
+                                                        unsigned long long *spc, int64_t cap, int lpb) {
     using EL = Elem<BF16>;
     constexpr int NW = BF16 ? 2 : 4;
     const Fmt F = fmt_of(x, y, 127);
@@ -377,6 +378,13 @@ __global__ void __launch_bounds__(256, 2) k_fs_enc_rows(const uint8_t *__restric
     const uint8_t *src = in + c0 * EL::ES;
     const int64_t rstride = C * EL::ES;
     const float *scol = S.amax + c0 / S.bc;   // this thread's block column
+    // WSHARE: lanes (8q .. 8q+7) compute the 8 rows' factors of the warp's
+    // q-th block column (lpb lanes per block column); lane t reads row i from
+    // lane i + 8 (t / lpb)
+    const int nbw = 32 / lpb, qb = (lane >> 3) < nbw ? (lane >> 3) : 0, src8 = 8 * (lane / lpb);
+    int64_t pcol = ((j - lane) * 4 + (int64_t)qb * lpb * 4) / S.bc;
+    if (pcol >= S.nbc) pcol = S.nbc - 1;   // lanes past the right edge of a partial warp
+    const float *scol_w = S.amax + pcol;
     uint32_t nxt[8][NW];
     int64_t g = blockIdx.y;
     if (g < G8 && act) {
@@ -397,10 +405,10 @@ __global__ void __launch_bounds__(256, 2) k_fs_enc_rows(const uint8_t *__restric
         float rr[8];
         bool ok = true;
         if (WSHARE) {
-            const FsE fe = fs_enc(__float_as_uint(__ldg(scol + fs_rb(S, 8 * g + (lane & 7)) * S.nbc)) & 0x7FFFFFFFu, G);
+            const FsE fe = fs_enc(__float_as_uint(__ldg(scol_w + fs_rb(S, 8 * g + (lane & 7)) * S.nbc)) & 0x7FFFFFFFu, G);
             ok = __all_sync(0xFFFFFFFFu, fe.mode == 1);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) rr[i] = __shfl_sync(0xFFFFFFFFu, fe.rr, i);
+            for (int i = 0; i < 8; ++i) rr[i] = __shfl_sync(0xFFFFFFFFu, fe.rr, i + src8);
         } else {
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -447,7 +455,7 @@ __global__ void __launch_bounds__(256, 2) k_fs_enc_rows(const uint8_t *__restric
 template <int K, bool OBF16, bool FAST, bool WSHARE>
 __global__ void __launch_bounds__(256) k_fs_dec_rows(const uint8_t *__restrict__ packed, int64_t R, int64_t C, int x,
                                                      int y, FsMap S, float G, SegOffsets so,
-                                                     uint8_t *__restrict__ out) {
+                                                     uint8_t *__restrict__ out, int lpb) {
     using EL = Elem<OBF16>;
     constexpr int TW = tile_words(K, 1);
     const Fmt F = fmt_of(x, y, 127);
@@ -458,6 +466,10 @@ __global__ void __launch_bounds__(256) k_fs_dec_rows(const uint8_t *__restrict__
     const int lane = threadIdx.x & 31;
     const int64_t c0 = (act ? j : 0) * 4;
     const float *scol = S.amax + c0 / S.bc;
+    const int nbw = 32 / lpb, qb = (lane >> 3) < nbw ? (lane >> 3) : 0, src8 = 8 * (lane / lpb);
+    int64_t pcol = ((j - lane) * 4 + (int64_t)qb * lpb * 4) / S.bc;
+    if (pcol >= S.nbc) pcol = S.nbc - 1;   // lanes past the right edge of a partial warp
+    const float *scol_w = S.amax + pcol;
     uint32_t nxt[TW];
     int64_t g = blockIdx.y;
     if (g < G8 && act) rows_load_raw<K, 1, 0>(nxt, packed, so, g, C, c0);
@@ -469,11 +481,11 @@ __global__ void __launch_bounds__(256) k_fs_dec_rows(const uint8_t *__restrict__
         if (g + gridDim.y < G8 && act) rows_load_raw<K, 1, 0>(nxt, packed, so, g + gridDim.y, C, c0);
         float hi[8], lo[8];
         if (WSHARE) {
-            const FsD fd = fs_dec(__float_as_uint(__ldg(scol + fs_rb(S, 8 * g + (lane & 7)) * S.nbc)) & 0x7FFFFFFFu, G);
+            const FsD fd = fs_dec(__float_as_uint(__ldg(scol_w + fs_rb(S, 8 * g + (lane & 7)) * S.nbc)) & 0x7FFFFFFFu, G);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                hi[i] = __shfl_sync(0xFFFFFFFFu, fd.hi, i);
-                lo[i] = __shfl_sync(0xFFFFFFFFu, fd.lo, i);
+                hi[i] = __shfl_sync(0xFFFFFFFFu, fd.hi, i + src8);
+                lo[i] = __shfl_sync(0xFFFFFFFFu, fd.lo, i + src8);
             }
         } else if (act) {
 #pragma unroll

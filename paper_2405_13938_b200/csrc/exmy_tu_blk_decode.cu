@@ -150,6 +150,22 @@ exmy_status launch_quantize_blocked(const uint8_t *in, uint8_t *out, bool bf16, 
 
 exmy_status launch_block_max(const uint8_t *in, bool bf16, int64_t R, int64_t C, int64_t br, int64_t bc, int y,
                              int scheme, uint8_t *meta, cudaStream_t st) {
+    const int V = bf16 ? 8 : 4;
+    if (br == 1 && bc % V == 0 && C % V == 0 && bc / V <= 32 && ((bc / V) & (bc / V - 1)) == 0 && aligned(in, 16)) {
+        const int64_t nvec = R * C / V;
+        int64_t blocks = cdiv(nvec, 256 * 4);
+        if (blocks > (int64_t)num_sms() * 8) blocks = (int64_t)num_sms() * 8;
+        if (blocks < 1) blocks = 1;
+        const int gsz = (int)(bc / V);
+        if (bf16) {
+            if (scheme == 0) k_block_max_small<true, 0><<<(unsigned)blocks, 256, 0, st>>>(in, nvec, gsz, y, meta, nullptr);
+            else k_block_max_small<true, 1><<<(unsigned)blocks, 256, 0, st>>>(in, nvec, gsz, y, meta, nullptr);
+        } else {
+            if (scheme == 0) k_block_max_small<false, 0><<<(unsigned)blocks, 256, 0, st>>>(in, nvec, gsz, y, meta, nullptr);
+            else k_block_max_small<false, 1><<<(unsigned)blocks, 256, 0, st>>>(in, nvec, gsz, y, meta, nullptr);
+        }
+        return launch_status();
+    }
     const int64_t nb = (R / br) * (C / bc);
     int64_t blocks = cdiv(nb, 8);
     if (blocks > (int64_t)num_sms() * 8) blocks = (int64_t)num_sms() * 8;

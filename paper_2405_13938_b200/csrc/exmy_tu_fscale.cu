@@ -51,13 +51,14 @@ exmy_status enc_k(const uint8_t *in, int64_t R, int64_t C, int axis, int x, int 
         if (gy > 65535) gy = 65535;
         if (gx > INT_MAX) return EXMY_E_SHAPE;
         const dim3 grid((unsigned)gx, (unsigned)gy);
-        const bool ws = M.bc % 128 == 0;
+        const bool ws = M.bc % 128 == 0 || M.bc == 32 || M.bc == 64;
+        const int lpb = M.bc >= 128 ? 32 : (int)(M.bc / 4);   // lanes per block column in a warp
         if (y == 0) {
-            if (ws) k_fs_enc_rows<K, BF16, true, true><<<grid, threads, 0, st>>>(in, R, C, x, y, M, G, packed, p.so, spi, spb, spc, cap);
-            else k_fs_enc_rows<K, BF16, true, false><<<grid, threads, 0, st>>>(in, R, C, x, y, M, G, packed, p.so, spi, spb, spc, cap);
+            if (ws) k_fs_enc_rows<K, BF16, true, true><<<grid, threads, 0, st>>>(in, R, C, x, y, M, G, packed, p.so, spi, spb, spc, cap, lpb);
+            else k_fs_enc_rows<K, BF16, true, false><<<grid, threads, 0, st>>>(in, R, C, x, y, M, G, packed, p.so, spi, spb, spc, cap, 32);
         } else {
-            if (ws) k_fs_enc_rows<K, BF16, false, true><<<grid, threads, 0, st>>>(in, R, C, x, y, M, G, packed, p.so, spi, spb, spc, cap);
-            else k_fs_enc_rows<K, BF16, false, false><<<grid, threads, 0, st>>>(in, R, C, x, y, M, G, packed, p.so, spi, spb, spc, cap);
+            if (ws) k_fs_enc_rows<K, BF16, false, true><<<grid, threads, 0, st>>>(in, R, C, x, y, M, G, packed, p.so, spi, spb, spc, cap, lpb);
+            else k_fs_enc_rows<K, BF16, false, false><<<grid, threads, 0, st>>>(in, R, C, x, y, M, G, packed, p.so, spi, spb, spc, cap, 32);
         }
         return launch_status();
     }
@@ -98,13 +99,14 @@ exmy_status dec_k(const uint8_t *packed, int64_t R, int64_t C, int axis, int x, 
         if (gy > 65535) gy = 65535;
         if (gx > INT_MAX) return EXMY_E_SHAPE;
         const dim3 grid((unsigned)gx, (unsigned)gy);
-        const bool ws = M.bc % 128 == 0;
+        const bool ws = M.bc % 128 == 0 || M.bc == 32 || M.bc == 64;
+        const int lpb = M.bc >= 128 ? 32 : (int)(M.bc / 4);
         if (x <= 7 && !g_force_generic) {
-            if (ws) k_fs_dec_rows<K, OBF16, true, true><<<grid, threads, 0, st>>>(packed, R, C, x, y, M, G, p.so, out);
-            else k_fs_dec_rows<K, OBF16, true, false><<<grid, threads, 0, st>>>(packed, R, C, x, y, M, G, p.so, out);
+            if (ws) k_fs_dec_rows<K, OBF16, true, true><<<grid, threads, 0, st>>>(packed, R, C, x, y, M, G, p.so, out, lpb);
+            else k_fs_dec_rows<K, OBF16, true, false><<<grid, threads, 0, st>>>(packed, R, C, x, y, M, G, p.so, out, 32);
         } else {
-            if (ws) k_fs_dec_rows<K, OBF16, false, true><<<grid, threads, 0, st>>>(packed, R, C, x, y, M, G, p.so, out);
-            else k_fs_dec_rows<K, OBF16, false, false><<<grid, threads, 0, st>>>(packed, R, C, x, y, M, G, p.so, out);
+            if (ws) k_fs_dec_rows<K, OBF16, false, true><<<grid, threads, 0, st>>>(packed, R, C, x, y, M, G, p.so, out, lpb);
+            else k_fs_dec_rows<K, OBF16, false, false><<<grid, threads, 0, st>>>(packed, R, C, x, y, M, G, p.so, out, 32);
         }
         return launch_status();
     }
@@ -139,6 +141,20 @@ exmy_status exmy_block_float_scale(const void *in, int dtype, int64_t rows, int6
     if (!block_ok(rows, cols, block_rows, block_cols)) return EXMY_E_SHAPE;
     if (rows == 0 || cols == 0) return EXMY_OK;
     if (!in || !scale) return EXMY_E_ARG;
+    const int V = dtype == EXMY_BF16 ? 8 : 4;
+    const int64_t gsz = block_cols / V;
+    if (block_rows == 1 && block_cols % V == 0 && cols % V == 0 && gsz <= 32 && (gsz & (gsz - 1)) == 0 &&
+        aligned(in, 16)) {   // sub-row blocks: segmented warp reduction (exmy_blocked.cuh)
+        const int64_t nvec = rows * cols / V;
+        const unsigned g = grid1(nvec / 4, 8);
+        if (dtype == EXMY_BF16)
+            k_block_max_small<true, 2><<<g, 256, 0, S_(stream)>>>(static_cast<const uint8_t *>(in), nvec, (int)gsz, 0,
+                                                                 nullptr, scale);
+        else
+            k_block_max_small<false, 2><<<g, 256, 0, S_(stream)>>>(static_cast<const uint8_t *>(in), nvec, (int)gsz, 0,
+                                                                  nullptr, scale);
+        return launch_status();
+    }
     const int64_t nb = (rows / block_rows) * (cols / block_cols);
     const unsigned grid = grid1(nb * 32, 8);
     if (dtype == EXMY_BF16)

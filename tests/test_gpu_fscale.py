@@ -53,7 +53,7 @@ def extreme_bits(dt):
 
 
 BLOCKS = [("tensor", None), ("row", None), ("col", None), ("subrow16", (1, 16)), ("tile8x8", (8, 8)),
-          ("odd", (2, 6))]
+          ("odd", (2, 6)), ("subrow32", (1, 32)), ("tile8x64", (8, 64))]
 
 
 def blk(name, spec, shape):
