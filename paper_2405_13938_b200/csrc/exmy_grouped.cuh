@@ -62,9 +62,6 @@ __device__ __forceinline__ SegOffsets grp_so(int64_t n) {
 #ifndef GRP_ENC_MINB
 #define GRP_ENC_MINB 2   // encode CTAs per SM (launch bounds)
 #endif
-#ifndef GRP_ENC_CACHE
-#define GRP_ENC_CACHE 1  // keep the tensor's format constants across chunks
-#endif
 #ifndef GRP_DEC_BAR
 #define GRP_DEC_BAR 1    // decode: CTA barrier per chunk (config 3: 4.15 -> 3.80 ms)
 #endif
@@ -309,9 +306,8 @@ __global__ void __launch_bounds__(GRP_THREADS, GRP_ENC_MINB) k_grouped_encode(co
     uint32_t nxt[8][NW];
     if (u.g < u.G) grp_enc_load<BF16, NW>(tab, u, nxt);
     int cur = -1;
-    Fmt F;
-    FastP P;
-    bool fast = false;
+    FastP P;            // only the fast path's constants stay live; the integer
+    bool fast = false;  // path rebuilds its Fmt from the metadata byte
     for (bool more = true; more;) {
         const int te = u.e, tg = u.g, tc = u.c;
         const bool ok = u.g < u.G;
@@ -322,20 +318,13 @@ __global__ void __launch_bounds__(GRP_THREADS, GRP_ENC_MINB) k_grouped_encode(co
             for (int q = 0; q < NW; ++q) w[i][q] = nxt[i][q];
         more = grp_next<1, GRP_TILE, GRP_ENC_BAR != 0>(u, tab, sb, n, nchunks, wstride);   // warp-uniform
         if (more && u.g < u.G) grp_enc_load<BF16, NW>(tab, u, nxt);
-#if GRP_ENC_CACHE
         if (te != cur) {   // new tensor: its format constants
             cur = te;
-            F = load_fmt(x, y, tab[cur].meta);
+            const Fmt F = load_fmt(x, y, tab[cur].meta);
             P = make_fast(F, BF16, force_generic);
             fast = enc_fast_ok<BF16, MODE>(F, force_generic);
         }
         if (!ok) continue;
-#else
-        if (!ok) continue;
-        F = load_fmt(x, y, tab[te].meta);
-        P = make_fast(F, BF16, force_generic);
-        fast = enc_fast_ok<BF16, MODE>(F, force_generic);
-#endif
         const GroupEntry &E = tab[te];
         const int64_t C = E.cols;
         const SegOffsets so = grp_so<K>(E.rows * C);
@@ -354,6 +343,7 @@ __global__ void __launch_bounds__(GRP_THREADS, GRP_ENC_MINB) k_grouped_encode(co
             }
             rows_fast_store<K, 1, 0>(RL, RH, E.packed, so, tg, C, tc);
         } else {   // NaN/Inf in the tile or metadata outside the fast range
+            const Fmt F = load_fmt(x, y, E.meta);
             for (int v = 0; v < 4; ++v)
                 enc_container_generic<BF16, K>(E.in, C, (int64_t)tg * C + tc + v, 0, F, E.packed, so, E.spi, E.spb,
                                                E.spc, E.cap);
