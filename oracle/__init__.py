@@ -84,6 +84,7 @@ def lib():
         L.oracle_encode_fs.argtypes = [vp, i32, i64, i64, i32, i64, i64, i32, i32, vp, vp, vp, vp, i64]
         L.oracle_encode_fs.restype = i64
         L.oracle_decode_fs.argtypes = [vp, i64, i64, i32, i64, i64, i32, i32, vp, vp, vp, i64, vp, i32]
+        L.oracle_embedding_bag.argtypes = [vp, i64, i64, i32, i32, vp, i32, vp, vp, i64, vp, i32, vp]
     return _lib
 
 
@@ -371,5 +372,25 @@ def decode_fs(packed, shape, fmt, amax, block, axis: int = ROWS, sp_index=None, 
     odt = BF16 if out.dtype == np.uint16 else F32
     if lib().oracle_decode_fs(_p(packed), rows, cols, axis, block[0], block[1], x, y, _p(a), _p(sp_index),
                               _p(sp_bits), cnt, _p(out), odt):
+        raise ValueError("invalid arguments")
+    return out
+
+
+# ------------------------------------------------------------ embedding bag
+def embedding_bag(packed, shape, fmt, meta, indices, offsets, weights=None, mode="sum") -> np.ndarray:
+    """Pooled decode of rows of a COLS-packed table (reading D25): fp32
+    (nbags, cols); meta: one byte (per tensor) or one per row."""
+    x, y = parse_format(fmt)
+    rows, cols = shape
+    packed = np.ascontiguousarray(packed, dtype=np.uint8)
+    m = np.ascontiguousarray(np.asarray(meta, dtype=np.uint8).reshape(-1))
+    per_row = 1 if m.size == rows and rows != 1 else 0
+    idx = np.ascontiguousarray(indices, dtype=np.int64)
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    nb = off.size - 1
+    w = None if weights is None else np.ascontiguousarray(weights, dtype=np.float32)
+    out = np.zeros((nb, cols), np.float32)
+    if lib().oracle_embedding_bag(_p(packed), rows, cols, x, y, _p(m), per_row, _p(idx), _p(off), nb,
+                                  None if w is None else _p(w), 0 if mode == "sum" else 1, _p(out)):
         raise ValueError("invalid arguments")
     return out

@@ -836,3 +836,69 @@ int oracle_decode_fs(const uint8_t *packed, int64_t rows, int64_t cols, int axis
     }
     return 0;
 }
+
+/* ================================================= embedding bag (decode + pool) */
+/* SURVEY 8(f) row 3, "decode fused into a GEMM/embedding-bag prologue" (config 5,
+ * P:293-298 serving decode is performance critical).  Reading D25: bag b pools
+ * the rows indices[offsets[b] .. offsets[b+1]) of a COLS-packed (rows, cols)
+ * table: each row decoded to fp32 exactly as oracle_decode does (NaN/Inf kept
+ * out of band are NOT restored, as exmy_decode_rows), then accumulated in fp32
+ * in index order, acc = RN32(acc + v), or acc = RN32(w v + acc) (one fused
+ * rounding) with per-sample weights; mode 1 (mean) divides by the bag size
+ * (RN32); an empty bag gives +0. */
+
+/* code of element (r, c) of a COLS-packed table: container g = r*(cols/8) + c/8,
+ * lane c%8, segment bits as oracle_pack lays them out */
+static uint32_t cols_code_at(const uint8_t *packed, int64_t rows, int64_t cols, int k, int64_t r, int64_t c)
+{
+    int widths[4];
+    int64_t offs[4];
+    int ns = oracle_segments(k, widths, rows * cols, offs);
+    int64_t g = r * (cols / 8) + c / 8;
+    int lane = (int)(c % 8);
+    uint32_t code = 0;
+    int hi = k;
+    for (int s = 0; s < ns; ++s) {
+        int w = widths[s], lo = hi - w;
+        const uint8_t *seg = packed + offs[s];
+        uint32_t field;
+        if (w == 8) {
+            field = seg[r * cols + c];
+        } else {
+            uint32_t cont = 0;
+            for (int b = 0; b < w; ++b) cont |= (uint32_t)seg[g * w + b] << (8 * b);
+            field = (cont >> (w * lane)) & ((1u << w) - 1u);
+        }
+        code |= field << lo;
+        hi = lo;
+    }
+    return code;
+}
+
+int oracle_embedding_bag(const uint8_t *packed, int64_t rows, int64_t cols, int x, int y,
+                         const uint8_t *meta, int meta_per_row, const int64_t *indices,
+                         const int64_t *offsets, int64_t nbags, const float *weights, int mode,
+                         float *out)
+{
+    if (!oracle_format_valid(x, y, 0) || cols % 8 || (mode != 0 && mode != 1)) return -1;
+    int k = 1 + x + y;
+    for (int64_t b = 0; b < nbags; ++b) {
+        int64_t i0 = offsets[b], i1 = offsets[b + 1];
+        for (int64_t c = 0; c < cols; ++c) {
+            volatile float acc = 0.0f;
+            for (int64_t i = i0; i < i1; ++i) {
+                int64_t r = indices[i];
+                int e = meta[meta_per_row ? r : 0];
+                if (e > 254) e = 254;
+                uint32_t vb = oracle_round_f32(oracle_code_value(cols_code_at(packed, rows, cols, k, r, c), x, y, e));
+                float v;
+                memcpy(&v, &vb, 4);
+                if (weights) acc = fmaf(weights[i], v, acc);   /* one rounding of w v + acc */
+                else acc = acc + v;
+            }
+            if (mode == 1 && i1 > i0) acc = acc / (float)(i1 - i0);
+            out[b * cols + c] = acc;
+        }
+    }
+    return 0;
+}

@@ -29,6 +29,12 @@ int oracle_decode_fs(const uint8_t *packed, int64_t rows, int64_t cols, int axis
                      const int64_t *sp_index, const uint32_t *sp_bits, int64_t sp_count,
                      void *out, int out_dtype);
 
+/* embedding bag over a COLS-packed table (reading D25) */
+int oracle_embedding_bag(const uint8_t *packed, int64_t rows, int64_t cols, int x, int y,
+                         const uint8_t *meta, int meta_per_row, const int64_t *indices,
+                         const int64_t *offsets, int64_t nbags, const float *weights, int mode,
+                         float *out);
+
 #endif
 int oracle_format_valid(int x, int y, int e_max);
 int oracle_bias(int x, int e_max);
@@ -84,6 +90,12 @@ int oracle_decode_fs(const uint8_t *packed, int64_t rows, int64_t cols, int axis
                      const int64_t *sp_index, const uint32_t *sp_bits, int64_t sp_count,
                      void *out, int out_dtype);
 
+/* embedding bag over a COLS-packed table (reading D25) */
+int oracle_embedding_bag(const uint8_t *packed, int64_t rows, int64_t cols, int x, int y,
+                         const uint8_t *meta, int meta_per_row, const int64_t *indices,
+                         const int64_t *offsets, int64_t nbags, const float *weights, int mode,
+                         float *out);
+
 #endif
 /* float scaling (reading D23) */
 double oracle_fs_grid_top(int x, int y);
@@ -100,5 +112,11 @@ int oracle_decode_fs(const uint8_t *packed, int64_t rows, int64_t cols, int axis
                      int64_t br, int64_t bc, int x, int y, const uint32_t *amax,
                      const int64_t *sp_index, const uint32_t *sp_bits, int64_t sp_count,
                      void *out, int out_dtype);
+
+/* embedding bag over a COLS-packed table (reading D25) */
+int oracle_embedding_bag(const uint8_t *packed, int64_t rows, int64_t cols, int x, int y,
+                         const uint8_t *meta, int meta_per_row, const int64_t *indices,
+                         const int64_t *offsets, int64_t nbags, const float *weights, int mode,
+                         float *out);
 
 #endif
