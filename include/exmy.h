@@ -416,6 +416,22 @@ exmy_status exmy_ckpt_verify(exmy_ckpt *h, int i);
 int64_t exmy_ckpt_bytes_read(const exmy_ckpt *h);
 void exmy_ckpt_close(exmy_ckpt *h);
 
+/* Embedding bag over a COLS-packed table ("decode fused
+ * into a ... embedding-bag prologue"; config 5; reading D25).  out[b, :] =
+ * the fp32 pool of rows indices[offsets[b] .. offsets[b+1]) -- each row
+ * decoded exactly as exmy_decode does, accumulated in fp32 in index order
+ * (acc + v, or fma(weights[i], v, acc) when weights != NULL); mode 0 sum,
+ * 1 mean (divide by the bag size); empty bags give +0.  Decoded rows never
+ * reach HBM.  indices / offsets (nbags + 1 entries) / weights are device
+ * arrays; meta is one byte (meta_per_row = 0) or one per row; out is
+ * (nbags, cols) fp32, 16-byte aligned; packed 8-byte aligned.  Row indices
+ * must lie in [0, rows) (not checked).  Out-of-band NaN/Inf are not
+ * restored (as exmy_decode_rows). */
+exmy_status exmy_embedding_bag(const uint8_t *packed, int64_t rows, int64_t cols, int x, int y,
+                               const uint8_t *meta, int meta_per_row, const int64_t *indices,
+                               const int64_t *offsets, int64_t nbags, const float *weights,
+                               int mode, float *out, void *stream);
+
 /* ------------------------------------------------ host-buffer conveniences */
 
 /* End-to-end encode of a HOST tensor (pinned memory recommended): H2D copy

@@ -76,6 +76,7 @@ def _load():
         "exmy_encode_fs": ([vp, i32, i64, i64, i32, i64, i64, i32, i32, vp, vp, vp, vp, vp, i64, vp], i32),
         "exmy_decode_fs": ([vp, i64, i64, i32, i64, i64, i32, i32, vp, vp, vp, vp, i64, vp, i32, vp], i32),
         "exmy_encode_push": ([vp, i32, i64, i64, i64, i64, i32, i32, vp, vp, i32, vp, vp, vp, i64, vp], i32),
+        "exmy_embedding_bag": ([vp, i64, i64, i32, i32, vp, i32, vp, vp, i64, vp, i32, vp, vp], i32),
         "exmy_ckpt_write": ([ctypes.c_char_p, vp, i32], i64),
         "exmy_ckpt_open": ([ctypes.c_char_p, vp], i32),
         "exmy_ckpt_count": ([vp], i32),
@@ -108,7 +109,7 @@ EXPORTED = ["exmy_version", "exmy_status_string", "exmy_format_valid", "exmy_pac
             "exmy_decode_blocked", "exmy_decode_rows", "exmy_max_exponent", "exmy_encode_rowwise",
             "exmy_group_plan_bytes", "exmy_group_plan", "exmy_group_max_exponent", "exmy_group_encode",
             "exmy_group_decode", "exmy_block_float_scale", "exmy_quantize_fs", "exmy_encode_fs", "exmy_decode_fs",
-            "exmy_encode_push", "exmy_ckpt_write", "exmy_ckpt_open", "exmy_ckpt_count", "exmy_ckpt_info",
+            "exmy_encode_push", "exmy_embedding_bag", "exmy_ckpt_write", "exmy_ckpt_open", "exmy_ckpt_count", "exmy_ckpt_info",
             "exmy_ckpt_find", "exmy_ckpt_read", "exmy_ckpt_verify", "exmy_ckpt_bytes_read", "exmy_ckpt_close"]
 
 
@@ -494,6 +495,30 @@ def decode_rows(p: Packed, row_index: torch.Tensor, dtype: torch.dtype | None = 
         per_row = 1
     _check(_lib.exmy_decode_rows(_ptr(p.data), p.rows, p.cols, p.x, p.y, _ptr(p.meta), per_row, _ptr(idx), idx.numel(),
                                  _ptr(out), _dtype_code(dtype), _stream(p.data.device)), "decode_rows")
+    return out
+
+
+def embedding_bag(p: Packed, indices: torch.Tensor, offsets: torch.Tensor, per_sample_weights=None, mode="sum",
+                  out: torch.Tensor | None = None) -> torch.Tensor:
+    """Pooled decode of rows of a COLS-packed table (reading D25): fp32
+    (nbags, cols), like torch.nn.functional.embedding_bag with offsets of
+    length nbags + 1; the decoded rows never reach HBM."""
+    if p.axis != COLS:
+        raise ValueError("embedding_bag needs the COLS layout (rows are contiguous byte ranges)")
+    dev = p.data.device
+    idx = indices.to(device=dev, dtype=torch.int64).contiguous()
+    off = offsets.to(device=dev, dtype=torch.int64).contiguous()
+    nb = off.numel() - 1
+    w = None if per_sample_weights is None else per_sample_weights.to(device=dev, dtype=torch.float32).contiguous()
+    per_row = 0
+    if p.block is not None:
+        if p.block != (1, p.cols):
+            raise ValueError("embedding_bag supports per-tensor or per-row metadata")
+        per_row = 1
+    if out is None:
+        out = torch.empty((nb, p.cols), dtype=torch.float32, device=dev)
+    _check(_lib.exmy_embedding_bag(_ptr(p.data), p.rows, p.cols, p.x, p.y, _ptr(p.meta), per_row, _ptr(idx), _ptr(off),
+                                   nb, _ptr(w), {"sum": 0, "mean": 1}[mode], _ptr(out), _stream(dev)), "embedding_bag")
     return out
 
 
