@@ -306,6 +306,19 @@ exmy_status exmy_encode_push(const void *in, int dtype, int64_t rows, int64_t co
                              uint8_t *const *dst, int ndst, int64_t *sp_index, uint32_t *sp_bits,
                              uint64_t *sp_count, int64_t sp_capacity, void *stream);
 
+/* Pull decode, the mirror of exmy_encode_push ("decode
+ * reads peers' packed shards over NVLink"): decodes the whole
+ * (nsrc * shard_rows, cols) tensor whose row shard s is the independent
+ * packed tensor (ROWS layout, shard_rows x cols) at srcs[s] -- on a node,
+ * every rank's packed shard mapped into this process -- so the all-gather of
+ * packed bytes happens in the decode's loads.  Same per-tensor metadata for
+ * every shard (the global e_max); 1 <= nsrc <= 8, shard_rows % 8 == 0;
+ * out (fp32 / bf16) 16-byte aligned with cols a multiple of 4 / 8, shard
+ * segments aligned as exmy_decode's vector path, else E_ALIGN.  Out-of-band
+ * NaN/Inf are not restored (as exmy_decode with no specials). */
+exmy_status exmy_decode_pull(const uint8_t *const *srcs, int nsrc, int64_t shard_rows, int64_t cols,
+                             int x, int y, const uint8_t *meta, void *out, int out_dtype, void *stream);
+
 /* ------------------------------------------ grouped launch (tensor table)
  * a model is many tensors (Llama-3 8B: 291, P:600-606
  * "the weights of Llama"), each compressed under its own per-tensor

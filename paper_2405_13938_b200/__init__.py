@@ -77,6 +77,7 @@ def _load():
         "exmy_decode_fs": ([vp, i64, i64, i32, i64, i64, i32, i32, vp, vp, vp, vp, i64, vp, i32, vp], i32),
         "exmy_encode_push": ([vp, i32, i64, i64, i64, i64, i32, i32, vp, vp, i32, vp, vp, vp, i64, vp], i32),
         "exmy_embedding_bag": ([vp, i64, i64, i32, i32, vp, i32, vp, vp, i64, vp, i32, vp, vp], i32),
+        "exmy_decode_pull": ([vp, i32, i64, i64, i32, i32, vp, vp, i32, vp], i32),
         "exmy_ckpt_write": ([ctypes.c_char_p, vp, i32], i64),
         "exmy_ckpt_open": ([ctypes.c_char_p, vp], i32),
         "exmy_ckpt_count": ([vp], i32),
@@ -109,7 +110,7 @@ EXPORTED = ["exmy_version", "exmy_status_string", "exmy_format_valid", "exmy_pac
             "exmy_decode_blocked", "exmy_decode_rows", "exmy_max_exponent", "exmy_encode_rowwise",
             "exmy_group_plan_bytes", "exmy_group_plan", "exmy_group_max_exponent", "exmy_group_encode",
             "exmy_group_decode", "exmy_block_float_scale", "exmy_quantize_fs", "exmy_encode_fs", "exmy_decode_fs",
-            "exmy_encode_push", "exmy_embedding_bag", "exmy_ckpt_write", "exmy_ckpt_open", "exmy_ckpt_count", "exmy_ckpt_info",
+            "exmy_encode_push", "exmy_decode_pull", "exmy_embedding_bag", "exmy_ckpt_write", "exmy_ckpt_open", "exmy_ckpt_count", "exmy_ckpt_info",
             "exmy_ckpt_find", "exmy_ckpt_read", "exmy_ckpt_verify", "exmy_ckpt_bytes_read", "exmy_ckpt_close"]
 
 
@@ -557,6 +558,22 @@ def encode_push(shard: torch.Tensor, fmt, meta: torch.Tensor, row0: int, total_r
                                  _ptr(_meta_tensor(meta, dev)), ptrs, len(dsts), _ptr(spi), _ptr(spb), _ptr(spc), cap,
                                  _stream(dev)), "encode_push")
     return spi, spb, spc
+
+
+def decode_pull(srcs, shard_rows: int, cols: int, fmt, meta, dtype=torch.bfloat16, out: torch.Tensor | None = None,
+                device=None):
+    """Decode the (len(srcs) * shard_rows, cols) tensor whose row shard s is the
+    packed tensor at srcs[s] (device uint8 tensors or raw device pointers, e.g.
+    peers' buffers mapped over NVLink): the all-gather happens in the loads."""
+    x, y = parse_format(fmt)
+    first = next((s_ for s_ in srcs if isinstance(s_, torch.Tensor)), None)
+    dev = torch.device(device) if device is not None else (first.device if first is not None else torch.device("cuda"))
+    ptrs = (ctypes.c_void_p * len(srcs))(*[s_.data_ptr() if isinstance(s_, torch.Tensor) else int(s_) for s_ in srcs])
+    if out is None:
+        out = torch.empty((len(srcs) * shard_rows, cols), dtype=dtype, device=dev)
+    _check(_lib.exmy_decode_pull(ptrs, len(srcs), shard_rows, cols, x, y, _ptr(_meta_tensor(meta, dev)), _ptr(out),
+                                 _dtype_code(out.dtype), _stream(dev)), "decode_pull")
+    return out
 
 
 # ------------------------------------------------------------ float scaling

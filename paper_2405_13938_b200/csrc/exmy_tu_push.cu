@@ -206,3 +206,142 @@ extern "C" exmy_status exmy_encode_push(const void *in, int dtype, int64_t rows,
     if (spc && sp_capacity > 1) s = launch_specials_sort(sp_index, sp_bits, spc, sp_capacity, st);
     return s;
 }
+
+// ------------------------------------------------- pull decode (gather on read)
+// The mirror of exmy_encode_push ("decode reads peers'
+// packed shards over NVLink"): the whole (nsrc * shard_rows, cols) tensor is
+// decoded by one kernel whose tiles read row shard s straight from srcs[s]
+// -- on a node, every rank's packed shard mapped into this process -- so the
+// all-gather of packed bytes happens in the decode's loads and only the
+// decoded output is written locally.  k_dec_rows_fast's tiles (8 rows x
+// 4*NH columns, next tile in flight, CTA barrier per row group).
+namespace {
+
+struct PullSrc {
+    const uint8_t *p[PUSH_MAX];
+    int n;
+};
+
+template <int K, bool OBF16, int MODE>
+__device__ __forceinline__ void pull_body(const PullSrc &S, int64_t shard_rows, int64_t C, const SegOffsets &so,
+                                          uint8_t *__restrict__ out, const Fmt &F, const FastP &P) {
+    using EL = Elem<OBF16>;
+    constexpr int V = EL::V, NH = V / 4, TW = tile_words(K, NH);
+    const int64_t CV = C / V, gps = shard_rows / 8, G = gps * S.n;
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool act = j < CV;
+    const int64_t c0 = j * V;
+    uint32_t nxt[TW];
+    int64_t g = blockIdx.y;
+    if (g < G && act) {
+        const int s = (int)(g / gps);
+        rows_load_raw<K, NH, 0>(nxt, S.p[s], so, g - s * gps, C, c0);
+    }
+    for (; g < G; g += gridDim.y) {
+        uint32_t raw[TW];
+#pragma unroll
+        for (int q = 0; q < TW; ++q) raw[q] = nxt[q];
+        __syncthreads();
+        const int64_t gn = g + gridDim.y;
+        if (gn < G && act) {
+            const int s = (int)(gn / gps);
+            rows_load_raw<K, NH, 0>(nxt, S.p[s], so, gn - s * gps, C, c0);
+        }
+        if (!act) continue;
+        uint32_t RL[NH][8], RH[NH][8];
+#pragma unroll
+        for (int h = 0; h < NH; ++h)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) { RL[h][i] = 0; RH[h][i] = 0; }
+        rows_unpack_raw<K, NH, 0>(raw, RL, RH);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            uint32_t o[4];
+            if (OBF16) {
+#pragma unroll
+                for (int h = 0; h < NH; ++h) {
+                    o[2 * h] = dec_pair_bf16_m<K, OBF16, MODE>(pair_from_lanes<K>(RL[h][i], RH[h][i], 0x4140), P, F);
+                    o[2 * h + 1] = dec_pair_bf16_m<K, OBF16, MODE>(pair_from_lanes<K>(RL[h][i], RH[h][i], 0x4342), P, F);
+                }
+            } else {
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    uint32_t code = (RL[0][i] >> (8 * v)) & 0xFFu;
+                    if (K == 9) code |= ((RH[0][i] >> (8 * v)) & 0xFFu) << 1;
+                    o[v] = dec_f32_m<K, MODE>(code, P, F);
+                }
+            }
+            stg_v4(out + ((8 * g + i) * C + c0) * EL::ES, make_uint4(o[0], o[1], o[2], o[3]));
+        }
+    }
+}
+
+template <int K, bool OBF16, int MODE>
+__global__ void __launch_bounds__(256) k_dec_pull(PullSrc S, int64_t shard_rows, int64_t C, int x, int y,
+                                                  const uint8_t *__restrict__ meta, SegOffsets so,
+                                                  uint8_t *__restrict__ out) {
+    const Fmt F = load_fmt(x, y, meta);
+    const FastP P = make_fast(F, false, 0);
+    if (MODE == DEC_FAST && P.two_mul) pull_body<K, OBF16, DEC_FAST2>(S, shard_rows, C, so, out, F, P);
+    else pull_body<K, OBF16, MODE>(S, shard_rows, C, so, out, F, P);
+}
+
+template <int K, bool OBF16>
+exmy_status launch_pull_k(const PullSrc &S, int64_t shard_rows, int64_t C, int x, int y, const uint8_t *meta,
+                          const SegOffsets &so, uint8_t *out, cudaStream_t st) {
+    constexpr int V = Elem<OBF16>::V;
+    const int threads = 256;
+    const int64_t CV = C / V, G = shard_rows / 8 * S.n;
+    const int64_t gx = cdiv(CV, threads);
+    int64_t gy = (int64_t)num_sms() * 2 / gx;
+    if (gy < 1) gy = 1;
+    if (gy > G) gy = G;
+    if (gy > 65535) gy = 65535;
+    if (gx > INT_MAX) return EXMY_E_SHAPE;
+    const dim3 grid((unsigned)gx, (unsigned)gy);
+    // the multiply path needs x <= 7 (and y <= 7 for bf16 output), as exmy_decode
+    if (!g_force_generic && x <= 7 && (!OBF16 || y <= 7)) {
+        k_dec_pull<K, OBF16, DEC_FAST><<<grid, threads, 0, st>>>(S, shard_rows, C, x, y, meta, so, out);
+    } else {
+        k_dec_pull<K, OBF16, DEC_GENERIC><<<grid, threads, 0, st>>>(S, shard_rows, C, x, y, meta, so, out);
+    }
+    return launch_status();
+}
+
+}  // namespace
+
+extern "C" exmy_status exmy_decode_pull(const uint8_t *const *srcs, int nsrc, int64_t shard_rows, int64_t cols, int x,
+                                        int y, const uint8_t *meta, void *out, int out_dtype, void *stream) {
+    if (out_dtype != EXMY_F32 && out_dtype != EXMY_BF16) return EXMY_E_DTYPE;
+    if (!fmt_ok(x, y)) return EXMY_E_FORMAT;
+    if (nsrc < 1 || nsrc > PUSH_MAX || !srcs) return EXMY_E_ARG;
+    if (shard_rows < 0 || cols < 0 || shard_rows % 8) return EXMY_E_SHAPE;
+    if (cols && shard_rows > INT64_MAX / cols / nsrc) return EXMY_E_SHAPE;
+    if (shard_rows == 0 || cols == 0) return EXMY_OK;
+    if (!meta || !out) return EXMY_E_ARG;
+    const bool obf = out_dtype == EXMY_BF16;
+    const int V = obf ? 8 : 4;
+    const int k = 1 + x + y;
+    const Plan p = make_plan(k, shard_rows * cols);   // every shard is an independent packed tensor
+    PullSrc S{};
+    S.n = nsrc;
+    for (int s = 0; s < nsrc; ++s) {
+        if (!srcs[s]) return EXMY_E_ARG;
+        S.p[s] = srcs[s];
+        for (int q = 0; q < p.nseg; ++q) {
+            const size_t a = p.w[q] == 8 ? (size_t)V : (size_t)((V * p.w[q]) < 16 ? V * p.w[q] : 16);
+            if (!aligned(srcs[s] + p.so.off[q], a)) return EXMY_E_ALIGN;
+        }
+    }
+    if (!aligned(out, 16) || cols % V) return EXMY_E_ALIGN;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    auto *po = static_cast<uint8_t *>(out);
+    switch (k) {
+#define PULL_K(KK)                                                                                             \
+        case KK: return obf ? launch_pull_k<KK, true>(S, shard_rows, cols, x, y, meta, p.so, po, st)          \
+                            : launch_pull_k<KK, false>(S, shard_rows, cols, x, y, meta, p.so, po, st);
+        PULL_K(3) PULL_K(4) PULL_K(5) PULL_K(6) PULL_K(7) PULL_K(8) PULL_K(9)
+#undef PULL_K
+    }
+    return EXMY_E_FORMAT;
+}

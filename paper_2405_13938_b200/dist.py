@@ -144,3 +144,16 @@ def pushed_encode(shard: torch.Tensor, fmt, total_rows: int, row0: int, peer_buf
         torch.cuda.current_stream(shard.device).synchronize()   # the stores have landed before peers read
     dist.barrier(group)
     return meta, sp
+
+
+def pulled_decode(local_packed: torch.Tensor, shard_rows: int, cols: int, fmt, meta, peer_buffers, group=None,
+                  codec=None, dtype=torch.bfloat16):
+    """Decode the whole tensor from every rank's packed shard (peer_buffers:
+    this process's mappings of each rank's packed shard buffer, symmetric
+    memory), the mirror of `pushed_encode`: one kernel, the all-gather happens
+    in its loads.  A barrier first makes every rank's shard complete."""
+    codec = codec or _default_codec()
+    if local_packed.is_cuda:
+        torch.cuda.current_stream(local_packed.device).synchronize()
+    dist.barrier(group)
+    return codec.decode_pull(peer_buffers, shard_rows, cols, fmt, meta, dtype=dtype)

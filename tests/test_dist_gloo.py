@@ -71,6 +71,13 @@ class OraclePushCodec(OracleCodec):
                 d[start:start + n] = torch.from_numpy(packed[ol:ol + n])
         return None
 
+    def decode_pull(self, srcs, shard_rows, cols, fmt, meta, dtype=torch.bfloat16):
+        import workloads as W
+        od = np.uint16 if dtype == torch.bfloat16 else np.uint32
+        parts = [self.o.decode(s_.numpy(), (shard_rows, cols), fmt, int(meta.item()), self.o.ROWS, out_dtype=od)
+                 for s_ in srcs]
+        return W.from_bits(np.concatenate(parts))
+
 
 def _free_port():
     s = socket.socket()
@@ -184,3 +191,56 @@ def test_pushed_encode_gloo(orc, tmp_path, ws, fmt):
         buf, meta = results[r]
         assert meta == e
         assert np.frombuffer(buf, np.uint8).tolist() == ref.tolist()
+
+
+def _pull_worker(rank, ws, port, fmt, paths, results):
+    import sys
+    sys.path.insert(0, ROOT)
+    import workloads as W
+    from paper_2405_13938_b200 import dist as xdist
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=ws)
+    try:
+        full = W.bf16_weights((64, 48), seed=17, std=0.05)
+        r0, r1 = xdist.shard_rows(64, ws, rank, True)
+        codec = OraclePushCodec()
+        x, y = codec.o.parse_format(fmt)
+        per = 64 // ws
+        nb = per * 48 * (1 + x + y) // 8
+        hist = codec.histogram(full[r0:r1].contiguous())
+        xdist.allreduce_histogram(hist)
+        meta = codec.emax(hist)
+        # this rank's packed shard into its own shared buffer, then pull everything
+        mine = torch.from_file(paths[rank], shared=True, size=nb, dtype=torch.uint8)
+        mine.copy_(codec.encode(full[r0:r1].contiguous(), fmt, meta).data)
+        peers = [torch.from_file(p_, shared=True, size=nb, dtype=torch.uint8) for p_ in paths]
+        out = xdist.pulled_decode(mine, per, 48, fmt, meta, peers, codec=codec)
+        results[rank] = W.to_bits(out).tobytes()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ws", [2, 4])
+def test_pulled_decode_gloo(orc, tmp_path, ws):
+    """pull-decode host wiring: every rank decodes the whole tensor from all
+    ranks' packed shards == the oracle's quantize of the whole tensor"""
+    import workloads as W
+    fmt = "e3m3"
+    nb = (64 // ws) * 48 * 7 // 8
+    paths = []
+    for r in range(ws):
+        p = tmp_path / f"shard{r}.bin"
+        p.write_bytes(bytes(nb))
+        paths.append(str(p))
+    ctx = mp.get_context("spawn")
+    results = ctx.Manager().dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_pull_worker, args=(r, ws, port, fmt, paths, results)) for r in range(ws)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    bits = W.to_bits(W.bf16_weights((64, 48), seed=17, std=0.05))
+    ref = orc.quantize(bits, fmt, orc.emax(orc.histogram(bits)))
+    for r in range(ws):
+        np.testing.assert_array_equal(np.frombuffer(results[r], np.uint16).reshape(64, 48), ref)

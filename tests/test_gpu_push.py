@@ -100,3 +100,37 @@ def test_push_argument_errors(exmy):
         exmy.encode_push(t, "e3m3", 100, 56, 64, [buf])         # past the end
     with pytest.raises(exmy.ExmyError):
         exmy.encode_push(t, "e3m3", 100, 0, 64, [buf] * 9)      # > 8 destinations
+
+
+@pytest.mark.parametrize("fmt", [(3, 3), (2, 4), (6, 0), (4, 3), (3, 5), (8, 0), (0, 8), (1, 7)],
+                         ids=lambda f: f"e{f[0]}m{f[1]}")
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+def test_pull_decode_equals_whole_decode(exmy, orc, fmt, dt):
+    """exmy_decode_pull over G independently encoded row shards (global e_max)
+    == decode of the whole tensor == the oracle's quantize (no specials)"""
+    R, C = 256, 192
+    t = W.f32_wide((R, C), seed=fmt[0] * 3 + fmt[1])
+    if dt == "bf16":
+        t = t.to(torch.bfloat16)
+    bits = W.to_bits(t)
+    d = t.to(DEV)
+    e = orc.emax(orc.histogram(bits))
+    ref = orc.quantize(bits, fmt, e)
+    for G in (1, 4, 8):
+        per = R // G
+        shards = [exmy.encode(d[r * per:(r + 1) * per], fmt, e).data for r in range(G)]
+        for odt in (torch.bfloat16, torch.float32):
+            out = exmy.decode_pull(shards, per, C, fmt, e, dtype=odt)
+            whole = exmy.decode(exmy.encode(d, fmt, e), odt)
+            assert torch.equal(out.view(torch.uint8), whole.view(torch.uint8)), (G, odt)
+        same = exmy.decode_pull(shards, per, C, fmt, e, dtype=t.dtype)
+        np.testing.assert_array_equal(W.to_bits(same), ref)
+
+
+def test_pull_decode_large_emax_two_multiplies(exmy):
+    """o > 127 (metadata near the top): the two-multiply fast path"""
+    t = (torch.randn(64, 256) * 2.0 ** 120).to(torch.bfloat16).to(DEV)
+    m = exmy.max_exponent(t)
+    shards = [exmy.encode(t[i * 16:(i + 1) * 16], "e2m3", m).data for i in range(4)]
+    out = exmy.decode_pull(shards, 16, 256, "e2m3", m, dtype=torch.bfloat16)
+    assert torch.equal(out, exmy.quantize(t, "e2m3", m))
