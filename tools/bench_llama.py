@@ -85,6 +85,21 @@ def main():
 
     grp = exmy.GroupCodec([t for t, _ in tensors], (x, y))
 
+    # the paper's quality recipe: one metadata byte per row; 1-D norms as one row
+    row_metas = [torch.zeros((R, 1), dtype=torch.uint8, device=dev) for (_, (R, C)) in tensors]
+
+    def encode_all_rowwise():   # per-row max exponent + encode (fused kernel for rows <= 16 KB)
+        sp = exmy._stream(dev)
+        for (t, (R, C)), rm, p in zip(tensors, row_metas, packed):
+            ax = exmy.ROWS if R % 8 == 0 else exmy.COLS
+            L.exmy_encode_rowwise(P(t), exmy.BF16, R, C, ax, x, y, 0, P(rm), P(p), None, None, None, 0, sp)
+
+    def decode_all_rowwise():
+        sp = exmy._stream(dev)
+        for (t, (R, C)), rm, p, o in zip(tensors, row_metas, packed, outs):
+            ax = exmy.ROWS if R % 8 == 0 else exmy.COLS
+            L.exmy_decode_blocked(P(p), R, C, ax, 1, C, x, y, P(rm), None, None, None, 0, P(o), exmy.BF16, sp)
+
     def group_encode():   # grouped launch: meta (2 launches) + encode (1)
         grp.encode()
 
@@ -93,8 +108,10 @@ def main():
 
     res = {"tensors": len(tensors), "params": nparams, "fmt": a.fmt}
     nl = {"encode": 3 * len(tensors), "encode_maxexp": 2 * len(tensors), "decode": len(tensors),
+          "encode_rowwise": len(tensors), "decode_rowwise": len(tensors),
           "group_encode": 3, "group_decode": 1}
     for name, fn in (("encode", encode_all), ("encode_maxexp", encode_all_max), ("decode", decode_all),
+                     ("encode_rowwise", encode_all_rowwise), ("decode_rowwise", decode_all_rowwise),
                      ("group_encode", group_encode), ("group_decode", group_decode)):
         if a.only and name not in a.only.split(","):
             continue
