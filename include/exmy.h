@@ -358,6 +358,16 @@ size_t exmy_group_plan_bytes(int n);
 exmy_status exmy_group_plan(const exmy_group_entry *entries, int n, int dtype, int x, int y,
                             int out_dtype, void *plan, size_t plan_bytes);
 
+/* Same table, per-row metadata ("quantized the weights with the
+ * maximum exponent of each row"): entry i's `meta` points to rows bytes
+ * (8-byte aligned), byte r = row r's max biased exponent; the group calls
+ * then run per row, bit-identical to exmy_block_max_exponent (1 x cols,
+ * scheme 0) / exmy_encode_blocked / exmy_decode_blocked (ROWS) per entry.
+ * Extra requirement: cols % 8 == 0 (E_SHAPE); meta not 8-byte aligned:
+ * E_ALIGN.  exmy_group_max_exponent on such a plan is one launch. */
+exmy_status exmy_group_plan_rows(const exmy_group_entry *entries, int n, int dtype, int x, int y,
+                                 int out_dtype, void *plan, size_t plan_bytes);
+
 /* meta of every entry := its max biased exponent over finite elements
  * (== exmy_max_exponent / the top histogram bin; 0 for all-zero tensors).
  * Two launches (clear, reduce).  Needs every entry's `in`. */

@@ -89,6 +89,7 @@ def _load():
         "exmy_ckpt_close": ([vp], None),
         "exmy_group_plan_bytes": ([i32], ctypes.c_size_t),
         "exmy_group_plan": ([vp, i32, i32, i32, i32, i32, vp, ctypes.c_size_t], i32),
+        "exmy_group_plan_rows": ([vp, i32, i32, i32, i32, i32, vp, ctypes.c_size_t], i32),
         "exmy_group_max_exponent": ([vp, vp, vp], i32),
         "exmy_group_encode": ([vp, vp, vp], i32),
         "exmy_group_decode": ([vp, vp, vp], i32),
@@ -108,7 +109,7 @@ EXPORTED = ["exmy_version", "exmy_status_string", "exmy_format_valid", "exmy_pac
             "exmy_emax_from_histogram", "exmy_quantize", "exmy_encode", "exmy_decode", "exmy_encode_host",
             "exmy_decode_host", "exmy_block_max_exponent", "exmy_quantize_blocked", "exmy_encode_blocked",
             "exmy_decode_blocked", "exmy_decode_rows", "exmy_max_exponent", "exmy_encode_rowwise",
-            "exmy_group_plan_bytes", "exmy_group_plan", "exmy_group_max_exponent", "exmy_group_encode",
+            "exmy_group_plan_bytes", "exmy_group_plan", "exmy_group_plan_rows", "exmy_group_max_exponent", "exmy_group_encode",
             "exmy_group_decode", "exmy_block_float_scale", "exmy_quantize_fs", "exmy_encode_fs", "exmy_decode_fs",
             "exmy_encode_push", "exmy_decode_pull", "exmy_embedding_bag", "exmy_ckpt_write", "exmy_ckpt_open", "exmy_ckpt_count", "exmy_ckpt_info",
             "exmy_ckpt_find", "exmy_ckpt_read", "exmy_ckpt_verify", "exmy_ckpt_bytes_read", "exmy_ckpt_close"]
@@ -690,9 +691,10 @@ def group_layout(shape) -> tuple[int, int]:
     return _as_2d_shape(shape)
 
 
-def group_plan(entries, dtype, fmt, out_dtype=None) -> bytes:
+def group_plan(entries, dtype, fmt, out_dtype=None, per_row: bool = False) -> bytes:
     """Host plan bytes for a list of dicts with keys of exmy_group_entry
-    (pointers as ints / tensors).  Low-level: see GroupCodec."""
+    (pointers as ints / tensors); per_row: exmy_group_plan_rows (one
+    metadata byte per row).  Low-level: see GroupCodec."""
     x, y = parse_format(fmt)
     n = len(entries)
     arr = (_GroupEntry * max(n, 1))()
@@ -704,8 +706,9 @@ def group_plan(entries, dtype, fmt, out_dtype=None) -> bytes:
             setattr(arr[i], f, v or 0)
     nb = _lib.exmy_group_plan_bytes(n)
     buf = (ctypes.c_uint64 * max(1, (nb + 7) // 8))()
-    _check(_lib.exmy_group_plan(arr if n else None, n, _dtype_code(dtype), x, y,
-                                _dtype_code(out_dtype if out_dtype is not None else dtype), buf, nb), "group_plan")
+    fn = _lib.exmy_group_plan_rows if per_row else _lib.exmy_group_plan
+    _check(fn(arr if n else None, n, _dtype_code(dtype), x, y,
+              _dtype_code(out_dtype if out_dtype is not None else dtype), buf, nb), "group_plan")
     return bytes(buf)[:nb]
 
 
@@ -719,11 +722,17 @@ class GroupCodec:
         packed = g.encode()          # list[Packed]
         outs = g.decode()            # list[Tensor] (out_dtype, default: input dtype)
 
+    per_row=True: one metadata byte per row of each tensor's group_layout
+    (the paper's Llama recipe), bit-identical to encode_blocked /
+    decode with block "row" per tensor; self.meta is then every tensor's
+    row bytes back to back (self.meta_offsets[i] = tensor i's first).
+
     The device buffers (packed bytes, metadata, specials, outputs) are owned
     here and reused by every call; the plan is copied to the device once, so
     the calls can be captured in a CUDA graph."""
 
-    def __init__(self, tensors, fmt, out_dtype=None, specials_capacity: int = 0, decode_outputs: bool = True):
+    def __init__(self, tensors, fmt, out_dtype=None, specials_capacity: int = 0, decode_outputs: bool = True,
+                 per_row: bool = False):
         tensors = [t.contiguous() for t in tensors]
         if not tensors:
             raise ValueError("empty tensor table")
@@ -739,7 +748,12 @@ class GroupCodec:
         self.tensors = tensors
         self.layouts = [group_layout(t.shape) for t in tensors]
         n = len(tensors)
-        self.meta = torch.zeros(n, dtype=torch.uint8, device=dev)
+        self.per_row = bool(per_row)
+        offs = [0]
+        for (R, C) in self.layouts:
+            offs.append(offs[-1] + (max(R, 0) if self.per_row else 1))
+        self.meta_offsets = offs[:-1]
+        self.meta = torch.zeros(max(offs[-1], 1), dtype=torch.uint8, device=dev)
         self.packed = [torch.empty(max(R * C, 0) * self.k // 8, dtype=torch.uint8, device=dev)
                        for R, C in self.layouts]
         cap = int(specials_capacity)
@@ -754,11 +768,12 @@ class GroupCodec:
             if R < 0 or C < 0:
                 raise ValueError(f"tensor {i} of shape {tuple(t.shape)}: a 1-D group member needs n % 32 == 0")
             ents.append({"in": t.data_ptr(), "out": self.outs[i].data_ptr() if self.outs else 0,
-                         "packed": self.packed[i].data_ptr(), "meta": self.meta.data_ptr() + i,
+                         "packed": self.packed[i].data_ptr(), "meta": self.meta.data_ptr() + self.meta_offsets[i],
                          "sp_index": self.spi[i].data_ptr() if cap else 0,
                          "sp_bits": self.spb[i].data_ptr() if cap else 0,
                          "sp_count": self.spc[i].data_ptr(), "sp_capacity": cap, "rows": R, "cols": C})
-        self.plan_host = torch.frombuffer(bytearray(group_plan(ents, self.dtype, (self.x, self.y), self.out_dtype)),
+        self.plan_host = torch.frombuffer(bytearray(group_plan(ents, self.dtype, (self.x, self.y), self.out_dtype,
+                                                               self.per_row)),
                                           dtype=torch.uint8).clone()   # torch allocation: 64-byte aligned
         self.plan_dev = self.plan_host.to(dev)
         self._ph = ctypes.c_void_p(self.plan_host.data_ptr())
@@ -767,7 +782,8 @@ class GroupCodec:
         _check(fn(self._ph, _ptr(self.plan_dev), _stream(self.device)), what)
 
     def max_exponent(self) -> torch.Tensor:
-        """meta[i] := max biased exponent of tensor i (2 launches)."""
+        """meta[i] := max biased exponent of tensor i (2 launches); per-row
+        plans: every row's byte (1 launch)."""
         self._call(_lib.exmy_group_max_exponent, "group_max_exponent")
         return self.meta
 
@@ -783,8 +799,13 @@ class GroupCodec:
     def packed_list(self) -> list:
         res = []
         for i, (t, lay) in enumerate(zip(self.tensors, self.layouts)):
-            res.append(Packed(self.packed[i], self.meta[i:i + 1], self.spi[i], self.spb[i], self.spc[i:i + 1],
-                              tuple(t.shape), self.x, self.y, ROWS, self.dtype, None,
+            o = self.meta_offsets[i]
+            if self.per_row:
+                meta, block = self.meta[o:o + lay[0]].view(lay[0], 1), (1, lay[1])
+            else:
+                meta, block = self.meta[o:o + 1], None
+            res.append(Packed(self.packed[i], meta, self.spi[i], self.spb[i], self.spc[i:i + 1],
+                              tuple(t.shape), self.x, self.y, ROWS, self.dtype, block,
                               lay if t.dim() == 1 else None))
         return res
 

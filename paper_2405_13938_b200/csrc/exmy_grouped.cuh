@@ -24,8 +24,9 @@ struct GroupHeader {   // first 64 bytes of a plan (host and device copies ident
     int64_t tile_chunks;   // encode: CTA chunks of GRP_TILE_CHUNK 8x4 tiles
     int64_t dtile_chunks;  // decode: CTA chunks of GRP_DTILE_CHUNK 8x(4*dec_nh) tiles
     int32_t dec_nh;        // decode tile width / 4: 2 for bf16 output when every cols % 8 == 0, else 1
-    int32_t specials;      // 1 if any entry has a specials counter
-    int64_t pad;
+    int16_t specials;      // 1 if any entry has a specials counter
+    int16_t per_row;       // 1: one metadata byte per row (exmy_group_plan_rows), else one per tensor
+    int64_t row_total;     // per-row plans: rows over all non-empty entries (the row max pass's work)
 };
 static_assert(sizeof(GroupHeader) == 64, "plan header is 64 bytes");
 
@@ -40,7 +41,8 @@ struct GroupEntry {   // one tensor (128 bytes)
     int64_t cap;
     int64_t rows, cols;
     int64_t vec_begin, tile_begin, dtile_begin;   // first chunk of this tensor in each pass
-    int64_t pad[3];
+    int64_t row_begin;                            // per-row plans: first global row of this tensor
+    int64_t pad[2];
 };
 static_assert(sizeof(GroupEntry) == 128, "plan entry is 128 bytes");
 
@@ -92,11 +94,12 @@ constexpr int GRP_DTILE_CHUNK = GRP_THREADS * GRP_DTPC;   // decode: tiles per C
 // entries) so the search costs shared-memory latency, not a chain of
 // dependent global loads in front of every chunk's loads.
 constexpr int GRP_SMEM_TAB = 4096;
-enum GrpKind { GRP_VEC = 0, GRP_TILE = 1, GRP_DTILE = 2 };
+enum GrpKind { GRP_VEC = 0, GRP_TILE = 1, GRP_DTILE = 2, GRP_ROW = 3 };
 
 template <int KIND>
 __device__ __forceinline__ int64_t grp_begin(const GroupEntry &e) {
-    return KIND == GRP_VEC ? e.vec_begin : KIND == GRP_TILE ? e.tile_begin : e.dtile_begin;
+    return KIND == GRP_VEC ? e.vec_begin : KIND == GRP_TILE ? e.tile_begin : KIND == GRP_DTILE ? e.dtile_begin
+                                                                                              : e.row_begin;
 }
 
 inline size_t grp_smem_bytes(int n) { return n <= GRP_SMEM_TAB ? (size_t)n * 8 : 0; }
@@ -278,23 +281,88 @@ __device__ __forceinline__ bool grp_next(GrpCur &u, const GroupEntry *tab, const
     return true;
 }
 
+// ------------------------------------------------ per-row max exponent
+// Per-row plans ("the maximum exponent of each row"): one warp per row,
+// rows numbered across the whole table; consecutive warps of a CTA take
+// consecutive rows, so a CTA streams one contiguous run of the table.  Each
+// row's byte is written by its warp alone (no clear, no atomics).  Host
+// guarantees cols % 8 == 0 (whole 16-byte vectors per row).
+constexpr int GRP_ROW_UNROLL = 4;
+
+template <bool BF16>
+__global__ void __launch_bounds__(GRP_THREADS) k_grouped_rowmax(const GroupEntry *__restrict__ tab, int n,
+                                                                int64_t nrows) {
+    extern __shared__ int64_t grp_sm[];
+    const int64_t *sb = grp_stage<GRP_ROW>(tab, n, grp_sm);
+    const int lane = threadIdx.x & 31;
+    const int64_t wstride = (int64_t)gridDim.x * (GRP_THREADS / 32);
+    int64_t r = (int64_t)blockIdx.x * (GRP_THREADS / 32) + (threadIdx.x >> 5);
+    if (r >= nrows) return;
+    int e = grp_find<GRP_ROW>(tab, sb, n, r);
+    for (; r < nrows; r += wstride) {
+        e = grp_advance<GRP_ROW>(tab, sb, n, e, r);
+        const int64_t lr = r - grp_b<GRP_ROW>(tab, sb, e);
+        const int64_t C = tab[e].cols;
+        const int64_t nv = C * Elem<BF16>::ES / 16;
+        const uint8_t *src = tab[e].in + lr * C * Elem<BF16>::ES;
+        uint32_t amax = 0;
+        for (int64_t v = lane; v < nv; v += 32 * GRP_ROW_UNROLL) {
+            uint4 q[GRP_ROW_UNROLL];
+#pragma unroll
+            for (int u = 0; u < GRP_ROW_UNROLL; ++u) {
+                const int64_t vi = v + 32 * u;
+                q[u] = vi < nv ? ldg_nc_v4(src + vi * 16) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < GRP_ROW_UNROLL; ++u) {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const uint32_t w = word_of(q[u], t);
+                    if (BF16) {
+                        const uint32_t a2 = w & 0x7FFF7FFFu;
+                        const uint32_t sp = (a2 + 0x00800080u) & 0x80008000u;   // lanes with exponent 255
+                        amax = vmax_u16x2(amax, a2 & ~((sp >> 15) * 0xFFFFu));
+                    } else {
+                        const uint32_t a = w & 0x7FFFFFFFu;
+                        amax = max(amax, a < 0x7F800000u ? a : 0u);
+                    }
+                }
+            }
+        }
+        uint32_t m = BF16 ? max((amax & 0xFFFFu) >> 7, amax >> 23) : (amax >> 23);
+        m = __reduce_max_sync(0xFFFFFFFFu, m);
+        if (lane == 0) tab[e].meta[lr] = (uint8_t)(m > 254u ? 254u : m);
+    }
+}
+
 // ------------------------------------------------ encode (ROWS)
 // The lane's next tile is loaded while the current one is converted and
 // packed (software pipeline, as k_enc_rows_fast).
-template <bool BF16, int NW>
-__device__ __forceinline__ void grp_enc_load(const GroupEntry *tab, const GrpCur &u, uint32_t (&nxt)[8][NW]) {
+template <bool BF16, int NW, bool PR>
+__device__ __forceinline__ void grp_enc_load(const GroupEntry *tab, const GrpCur &u, uint32_t (&nxt)[8][NW],
+                                             uint2 &nm) {
     using EL = Elem<BF16>;
     const uint8_t *src = tab[u.e].in + ((int64_t)8 * u.g * u.C + u.c) * EL::ES;
     const int64_t rs = (int64_t)u.C * EL::ES;
 #pragma unroll
     for (int i = 0; i < 8; ++i) load4<BF16>(src + i * rs, nxt[i]);
+    if (PR) nm = __ldg(reinterpret_cast<const uint2 *>(tab[u.e].meta) + u.g);   // the tile's 8 row bytes
 }
 
-template <int K, bool BF16, int MODE>
+// byte i of a tile's 8 per-row metadata bytes, clamped to 254 (D2)
+__device__ __forceinline__ int tile_row_meta(const uint2 &m, int i) {
+    const uint32_t b = ((i < 4 ? m.x : m.y) >> (8 * (i & 3))) & 0xFFu;
+    return b > 254u ? 254 : (int)b;
+}
+
+// PR: per-row metadata (exmy_group_plan_rows): the tile's 8 rows each under
+// their own byte, arithmetic as k_enc_rows_blk (exmy_blocked.cuh)
+template <int K, bool BF16, int MODE, bool PR>
 __global__ void __launch_bounds__(GRP_THREADS, GRP_ENC_MINB) k_grouped_encode(const GroupEntry *__restrict__ tab,
                                                                               int n, int64_t nchunks, int x, int y,
                                                                               int force_generic) {
     constexpr int NW = BF16 ? 2 : 4;
+    constexpr bool SIMD = (MODE == ENC_SIMD || MODE == ENC_SIMD_Y0);
     extern __shared__ int64_t grp_sm[];
     const int64_t *sb = grp_stage<GRP_TILE>(tab, n, grp_sm);
     const int64_t wstride = gridDim.x;
@@ -304,10 +372,15 @@ __global__ void __launch_bounds__(GRP_THREADS, GRP_ENC_MINB) k_grouped_encode(co
     u.e = grp_find<GRP_TILE>(tab, sb, n, u.ch);
     grp_chunk<1, GRP_TILE>(u, tab, sb);
     uint32_t nxt[8][NW];
-    if (u.g < u.G) grp_enc_load<BF16, NW>(tab, u, nxt);
+    uint2 nm = make_uint2(0, 0);
+    if (u.g < u.G) grp_enc_load<BF16, NW, PR>(tab, u, nxt, nm);
     int cur = -1;
     FastP P;            // only the fast path's constants stay live; the integer
     bool fast = false;  // path rebuilds its Fmt from the metadata byte
+    if (PR) {           // e_max-independent constants only (per-row: RowP per tile row)
+        P = make_fast(fmt_of(x, y, 0), BF16, 1);
+        fast = !force_generic;
+    }
     for (bool more = true; more;) {
         const int te = u.e, tg = u.g, tc = u.c;
         const bool ok = u.g < u.G;
@@ -316,9 +389,10 @@ __global__ void __launch_bounds__(GRP_THREADS, GRP_ENC_MINB) k_grouped_encode(co
         for (int i = 0; i < 8; ++i)
 #pragma unroll
             for (int q = 0; q < NW; ++q) w[i][q] = nxt[i][q];
+        const uint2 em = nm;
         more = grp_next<1, GRP_TILE, GRP_ENC_BAR != 0>(u, tab, sb, n, nchunks, wstride);   // warp-uniform
-        if (more && u.g < u.G) grp_enc_load<BF16, NW>(tab, u, nxt);
-        if (te != cur) {   // new tensor: its format constants
+        if (more && u.g < u.G) grp_enc_load<BF16, NW, PR>(tab, u, nxt, nm);
+        if (!PR && te != cur) {   // new tensor: its format constants
             cur = te;
             const Fmt F = load_fmt(x, y, tab[cur].meta);
             P = make_fast(F, BF16, force_generic);
@@ -330,11 +404,20 @@ __global__ void __launch_bounds__(GRP_THREADS, GRP_ENC_MINB) k_grouped_encode(co
         const SegOffsets so = grp_so<K>(E.rows * C);
         uint32_t amax = 0;
         uint32_t cp[8][2];
+        bool tfast = fast;
         if (fast) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) vec_codes<K, BF16, MODE, NW>(w[i], cp[i], P, amax);
+            for (int i = 0; i < 8; ++i) {
+                if (PR) {
+                    const RowP Rp = make_rowp<SIMD>(tile_row_meta(em, i), x, y);
+                    tfast = tfast && Rp.ok;
+                    vec_codes_r<K, BF16, MODE, NW>(w[i], cp[i], P, Rp, amax);
+                } else {
+                    vec_codes<K, BF16, MODE, NW>(w[i], cp[i], P, amax);
+                }
+            }
         }
-        if (fast && !amax_special<BF16, MODE>(amax, P)) {
+        if (tfast && !amax_special<BF16, MODE>(amax, P)) {
             uint32_t RL[1][8], RH[1][8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -342,6 +425,11 @@ __global__ void __launch_bounds__(GRP_THREADS, GRP_ENC_MINB) k_grouped_encode(co
                 RH[0][i] = (K == 9) ? prmt(cp[i][0] >> 1, cp[i][1] >> 1, 0x6420) : 0u;
             }
             rows_fast_store<K, 1, 0>(RL, RH, E.packed, so, tg, C, tc);
+        } else if (PR) {   // NaN/Inf in the tile or a row's metadata outside the fast range
+            const MetaMap M{E.meta, 1, C, 1};
+            for (int v = 0; v < 4; ++v)
+                enc_container_generic_blk<BF16, K>(E.in, C, (int64_t)tg * C + tc + v, 0, x, y, M, E.packed, so,
+                                                   E.spi, E.spb, E.spc, E.cap);
         } else {   // NaN/Inf in the tile or metadata outside the fast range
             const Fmt F = load_fmt(x, y, E.meta);
             for (int v = 0; v < 4; ++v)
@@ -390,14 +478,60 @@ __device__ __forceinline__ void grp_dec_tile(const uint32_t (&raw)[tile_words(K,
     }
 }
 
-template <int K, int NH>
-__device__ __forceinline__ void grp_dec_load(const GroupEntry *tab, const GrpCur &u,
-                                             uint32_t (&nxt)[tile_words(K, NH)]) {
-    rows_load_raw<K, NH, 0>(nxt, tab[u.e].packed, grp_so<K>(tab[u.e].rows * tab[u.e].cols), u.g, u.C, u.c);
+// per-row metadata: row i of the tile scaled by 2^o_i (one multiply, o_i <=
+// 127 checked by the caller), arithmetic as k_dec_rows_blk; GEN: the integer
+// path (dec_code_generic) under each row's own format, inline (a call to the
+// per-container fallback would keep the pipeline registers live across it)
+template <int K, bool OBF16, int NH, bool GEN>
+__device__ __forceinline__ void grp_dec_tile_r(const uint32_t (&raw)[tile_words(K, NH)], uint8_t *out, int64_t C,
+                                               int64_t g, int64_t c0, int x, int y, const uint2 &em) {
+    using EL = Elem<OBF16>;
+    uint32_t RL[NH][8], RH[NH][8];
+#pragma unroll
+    for (int h = 0; h < NH; ++h)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { RL[h][i] = 0; RH[h][i] = 0; }
+    rows_unpack_raw<K, NH, 0>(raw, RL, RH);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const RowD D = make_rowd(tile_row_meta(em, i), x);
+        const Fmt F = fmt_of(x, y, tile_row_meta(em, i));
+        uint8_t *dst = out + ((8 * g + i) * C + c0) * EL::ES;
+        if (OBF16) {
+            uint32_t o[2 * NH];
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const uint32_t cp = pair_from_lanes<K>(RL[h][i], RH[h][i], j ? 0x4342 : 0x4140);
+                    o[2 * h + j] = GEN ? dec_code_generic<8>(cp & 0xFFFFu, F) | (dec_code_generic<8>(cp >> 16, F) << 16)
+                                       : dec_pair_bf16_r<K>(cp, y, D);
+                }
+            }
+            if constexpr (NH == 2) stg_v4(dst, make_uint4(o[0], o[1], o[2], o[3]));
+            else stg_v2(dst, o[0], o[1]);
+        } else {
+            uint32_t o[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                uint32_t code = (RL[0][i] >> (8 * v)) & 0xFFu;
+                if (K == 9) code |= ((RH[0][i] >> (8 * v)) & 0xFFu) << 1;
+                o[v] = GEN ? dec_code_generic<24>(code, F) : dec_f32_r<K>(code, y, D);
+            }
+            stg_v4(dst, make_uint4(o[0], o[1], o[2], o[3]));
+        }
+    }
 }
 
-template <int K, bool OBF16, int MODE, int NH>
-__global__ void __launch_bounds__(GRP_THREADS) k_grouped_decode(const GroupEntry *__restrict__ tab, int n,
+template <int K, int NH, bool PR>
+__device__ __forceinline__ void grp_dec_load(const GroupEntry *tab, const GrpCur &u,
+                                             uint32_t (&nxt)[tile_words(K, NH)], uint2 &nm) {
+    rows_load_raw<K, NH, 0>(nxt, tab[u.e].packed, grp_so<K>(tab[u.e].rows * tab[u.e].cols), u.g, u.C, u.c);
+    if (PR) nm = __ldg(reinterpret_cast<const uint2 *>(tab[u.e].meta) + u.g);
+}
+
+template <int K, bool OBF16, int MODE, int NH, bool PR>
+__global__ void __launch_bounds__(GRP_THREADS, K < 9 ? GRP_DEC_OCC : 2) k_grouped_decode(const GroupEntry *__restrict__ tab, int n,
                                                                 int64_t nchunks, int x, int y) {
     constexpr int TW = tile_words(K, NH);
     static_assert(NH == 1 || OBF16, "fp32 output uses 8x4 tiles");
@@ -410,19 +544,22 @@ __global__ void __launch_bounds__(GRP_THREADS) k_grouped_decode(const GroupEntry
     u.e = grp_find<GRP_DTILE>(tab, sb, n, u.ch);
     grp_chunk<NH, GRP_DTILE>(u, tab, sb);
     uint32_t nxt[TW];
-    if (u.g < u.G) grp_dec_load<K, NH>(tab, u, nxt);
+    uint2 nm = make_uint2(0, 0);
+    if (u.g < u.G) grp_dec_load<K, NH, PR>(tab, u, nxt, nm);
     int cur = -1;
     Fmt F;
     FastP P;
+    const int omax = 127 + (1 << x) - 1;   // per-row fast path: o = e_max - (2^x - 1) <= 127
     for (bool more = true; more;) {
         const int te = u.e, tg = u.g, tc = u.c;
         const bool ok = u.g < u.G;
         uint32_t raw[TW];
 #pragma unroll
         for (int q = 0; q < TW; ++q) raw[q] = nxt[q];
+        const uint2 em = nm;
         more = grp_next<NH, GRP_DTILE, GRP_DEC_BAR != 0>(u, tab, sb, n, nchunks, wstride);
-        if (more && u.g < u.G) grp_dec_load<K, NH>(tab, u, nxt);
-        if (te != cur) {
+        if (more && u.g < u.G) grp_dec_load<K, NH, PR>(tab, u, nxt, nm);
+        if (!PR && te != cur) {
             cur = te;
             F = load_fmt(x, y, tab[cur].meta);
             P = make_fast(F, false, 0);
@@ -430,8 +567,17 @@ __global__ void __launch_bounds__(GRP_THREADS) k_grouped_decode(const GroupEntry
         if (!ok) continue;
         uint8_t *out = tab[te].out;
         const int64_t C = tab[te].cols;
-        if (MODE == DEC_FAST && P.two_mul) grp_dec_tile<K, OBF16, DEC_FAST2, NH>(raw, out, C, tg, tc, F, P);
-        else grp_dec_tile<K, OBF16, MODE, NH>(raw, out, C, tg, tc, F, P);
+        if (PR) {
+            bool tfast = MODE == DEC_FAST;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) tfast = tfast && tile_row_meta(em, i) <= omax;
+            if (tfast) grp_dec_tile_r<K, OBF16, NH, false>(raw, out, C, tg, tc, x, y, em);
+            else grp_dec_tile_r<K, OBF16, NH, true>(raw, out, C, tg, tc, x, y, em);
+        } else if (MODE == DEC_FAST && P.two_mul) {
+            grp_dec_tile<K, OBF16, DEC_FAST2, NH>(raw, out, C, tg, tc, F, P);
+        } else {
+            grp_dec_tile<K, OBF16, MODE, NH>(raw, out, C, tg, tc, F, P);
+        }
     }
 }
 

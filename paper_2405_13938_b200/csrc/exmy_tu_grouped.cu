@@ -41,15 +41,21 @@ unsigned grid_for(KF kernel, int threads, int64_t chunks, size_t sm) {
     return (unsigned)(g < 1 ? 1 : g);
 }
 
-template <int K, bool BF16, int MODE>
-exmy_status launch_genc_km(const GroupEntry *tab, const GroupHeader &h, cudaStream_t st) {
+template <int K, bool BF16, int MODE, bool PR>
+exmy_status launch_genc_kmp(const GroupEntry *tab, const GroupHeader &h, cudaStream_t st) {
     const size_t sm = grp_smem_bytes(h.n);
-    const int occ = occupancy(k_grouped_encode<K, BF16, MODE>, GRP_THREADS, sm);
+    const int occ = occupancy(k_grouped_encode<K, BF16, MODE, PR>, GRP_THREADS, sm);
     int64_t g = (int64_t)num_sms() * occ;
     if (g > h.tile_chunks) g = h.tile_chunks;
-    k_grouped_encode<K, BF16, MODE><<<(unsigned)g, GRP_THREADS, sm, st>>>(tab, h.n, h.tile_chunks, h.x, h.y,
-                                                                           g_force_generic);
+    k_grouped_encode<K, BF16, MODE, PR><<<(unsigned)g, GRP_THREADS, sm, st>>>(tab, h.n, h.tile_chunks, h.x, h.y,
+                                                                               g_force_generic);
     return launch_status();
+}
+
+template <int K, bool BF16, int MODE>
+exmy_status launch_genc_km(const GroupEntry *tab, const GroupHeader &h, cudaStream_t st) {
+    return h.per_row ? launch_genc_kmp<K, BF16, MODE, true>(tab, h, st)
+                     : launch_genc_kmp<K, BF16, MODE, false>(tab, h, st);
 }
 
 template <int K, bool BF16>
@@ -74,15 +80,22 @@ exmy_status launch_genc(int k, const GroupEntry *tab, const GroupHeader &h, cuda
     return EXMY_E_FORMAT;
 }
 
-template <int K, bool OBF16, int MODE, int NH>
-exmy_status launch_gdec_kmn(const GroupEntry *tab, const GroupHeader &h, cudaStream_t st) {
+template <int K, bool OBF16, int MODE, int NH, bool PR>
+exmy_status launch_gdec_kmnp(const GroupEntry *tab, const GroupHeader &h, cudaStream_t st) {
     const size_t sm = grp_smem_bytes(h.n);
-    const int occ = occupancy(k_grouped_decode<K, OBF16, MODE, NH>, GRP_THREADS, sm);
-    // decode is write-bound: 2 CTAs/SM, as the per-tensor ROWS decode
+    const int occ = occupancy(k_grouped_decode<K, OBF16, MODE, NH, PR>, GRP_THREADS, sm);
+    // decode is write-bound: GRP_DEC_OCC CTAs/SM (measured on config 3)
     int64_t g = (int64_t)num_sms() * (occ < GRP_DEC_OCC ? occ : GRP_DEC_OCC);
     if (g > h.dtile_chunks) g = h.dtile_chunks;
-    k_grouped_decode<K, OBF16, MODE, NH><<<(unsigned)g, GRP_THREADS, sm, st>>>(tab, h.n, h.dtile_chunks, h.x, h.y);
+    k_grouped_decode<K, OBF16, MODE, NH, PR><<<(unsigned)g, GRP_THREADS, sm, st>>>(tab, h.n, h.dtile_chunks, h.x,
+                                                                                   h.y);
     return launch_status();
+}
+
+template <int K, bool OBF16, int MODE, int NH>
+exmy_status launch_gdec_kmn(const GroupEntry *tab, const GroupHeader &h, cudaStream_t st) {
+    return h.per_row ? launch_gdec_kmnp<K, OBF16, MODE, NH, true>(tab, h, st)
+                     : launch_gdec_kmnp<K, OBF16, MODE, NH, false>(tab, h, st);
 }
 
 template <int K, bool OBF16, int MODE>
@@ -126,8 +139,12 @@ size_t exmy_group_plan_bytes(int n) {
     return n < 1 ? 0 : sizeof(GroupHeader) + (size_t)n * sizeof(GroupEntry);
 }
 
-exmy_status exmy_group_plan(const exmy_group_entry *entries, int n, int dtype, int x, int y, int out_dtype,
-                            void *plan, size_t plan_bytes) {
+}  // extern "C"
+
+namespace {
+
+exmy_status plan_impl(const exmy_group_entry *entries, int n, int dtype, int x, int y, int out_dtype, int per_row,
+                      void *plan, size_t plan_bytes) {
     if (dtype != EXMY_F32 && dtype != EXMY_BF16) return EXMY_E_DTYPE;
     if (out_dtype != EXMY_F32 && out_dtype != EXMY_BF16) return EXMY_E_DTYPE;
     if (!fmt_ok(x, y)) return EXMY_E_FORMAT;
@@ -143,6 +160,7 @@ exmy_status exmy_group_plan(const exmy_group_entry *entries, int n, int dtype, i
     h.x = x;
     h.y = y;
     h.out_dtype = out_dtype;
+    h.per_row = (int16_t)per_row;
     auto *tab = reinterpret_cast<GroupEntry *>(static_cast<uint8_t *>(plan) + sizeof(GroupHeader));
     // decode tiles 8x8 (16-byte bf16 stores) when every tensor allows them
     h.dec_nh = 1;
@@ -151,7 +169,7 @@ exmy_status exmy_group_plan(const exmy_group_entry *entries, int n, int dtype, i
         for (int i = 0; i < n; ++i)
             if (entries[i].cols % 8) h.dec_nh = 1;
     }
-    int64_t vc = 0, tc = 0, dc = 0;
+    int64_t vc = 0, tc = 0, dc = 0, rc = 0;
     for (int i = 0; i < n; ++i) {
         const exmy_group_entry &a = entries[i];
         if (a.rows < 0 || a.cols < 0 || a.rows % 8 || a.cols % 4) return EXMY_E_SHAPE;
@@ -173,11 +191,14 @@ exmy_status exmy_group_plan(const exmy_group_entry *entries, int n, int dtype, i
         g.vec_begin = vc;
         g.tile_begin = tc;
         g.dtile_begin = dc;
+        g.row_begin = rc;
         const int64_t ne = a.rows * a.cols;
         if (ne > 0) {
             if (!a.packed || !a.meta) return EXMY_E_ARG;
             if ((a.in && !aligned(a.in, 16)) || (a.out && !aligned(a.out, 16)) || !aligned(a.packed, 16))
                 return EXMY_E_ALIGN;
+            if (per_row && (a.cols % 8 || !aligned(a.meta, 8))) return a.cols % 8 ? EXMY_E_SHAPE : EXMY_E_ALIGN;
+            rc += a.rows;
             vc += cdiv(ne / V, GRP_VEC_CHUNK);
             tc += cdiv((a.rows / 8) * (a.cols / 4), GRP_TILE_CHUNK);
             dc += cdiv((a.rows / 8) * (a.cols / (4 * h.dec_nh)), GRP_DTILE_CHUNK);
@@ -188,8 +209,23 @@ exmy_status exmy_group_plan(const exmy_group_entry *entries, int n, int dtype, i
     h.vec_chunks = vc;
     h.tile_chunks = tc;
     h.dtile_chunks = dc;
+    h.row_total = per_row ? rc : 0;
     std::memcpy(plan, &h, sizeof(h));
     return EXMY_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+exmy_status exmy_group_plan(const exmy_group_entry *entries, int n, int dtype, int x, int y, int out_dtype,
+                            void *plan, size_t plan_bytes) {
+    return plan_impl(entries, n, dtype, x, y, out_dtype, 0, plan, plan_bytes);
+}
+
+exmy_status exmy_group_plan_rows(const exmy_group_entry *entries, int n, int dtype, int x, int y, int out_dtype,
+                                 void *plan, size_t plan_bytes) {
+    return plan_impl(entries, n, dtype, x, y, out_dtype, 1, plan, plan_bytes);
 }
 
 exmy_status exmy_group_max_exponent(const void *plan_host, const void *plan_device, void *stream) {
@@ -201,6 +237,19 @@ exmy_status exmy_group_max_exponent(const void *plan_host, const void *plan_devi
         if (e[i].rows * e[i].cols > 0 && !e[i].in) return EXMY_E_ARG;
     cudaStream_t st = S(stream);
     const GroupEntry *tab = dev_table(plan_device);
+    if (h->per_row) {   // every row's byte written by its warp: one launch
+        if (h->row_total == 0) return EXMY_OK;
+        const size_t sm = grp_smem_bytes(h->n);
+        const int64_t wpc = GRP_THREADS / 32;
+        const int64_t cta = cdiv(h->row_total, wpc);
+        if (h->dtype == EXMY_BF16)
+            k_grouped_rowmax<true><<<grid_for(k_grouped_rowmax<true>, GRP_THREADS, cta, sm), GRP_THREADS, sm, st>>>(
+                tab, h->n, h->row_total);
+        else
+            k_grouped_rowmax<false><<<grid_for(k_grouped_rowmax<false>, GRP_THREADS, cta, sm), GRP_THREADS, sm,
+                                      st>>>(tab, h->n, h->row_total);
+        return launch_status();
+    }
     k_grouped_clear<0><<<small_grid(h->n, 256), 256, 0, st>>>(tab, h->n);
     if ((s = launch_status()) != EXMY_OK) return s;
     if (h->vec_chunks == 0) return EXMY_OK;

@@ -163,6 +163,20 @@ def test_group_plan_host(exmy):
         assert ei.value.status == status
     with pytest.raises(exmy.ExmyError):
         exmy.group_plan([], torch.bfloat16, "e3m3")
+    # per-row plans (exmy_group_plan_rows): header flag + row count, each
+    # entry's first global row; cols % 8 and 8-byte aligned row bytes
+    rents = [ent(0, 64, 4096, meta=A * 1000), ent(1, 0, 8, meta=A * 1001), ent(2, 16, 8, meta=A * 1002),
+             ent(3, 8, 512, meta=A * 1003)]
+    b = exmy.group_plan(rents, torch.bfloat16, "e3m3", per_row=True)
+    sp, per_row, row_total = struct.unpack("<hhq", b[52:64])
+    assert (sp, per_row, row_total) == (0, 1, 64 + 16 + 8)
+    for i, rb in enumerate([0, 64, 64, 80]):
+        assert struct.unpack("<q", b[64 + 128 * i + 104:64 + 128 * i + 112])[0] == rb
+    assert struct.unpack("<hh", exmy.group_plan(rents, torch.bfloat16, "e3m3")[52:56]) == (0, 0)
+    for ents, status in [([ent(0, 8, 4, meta=A * 1000)], 3), ([ent(0, 8, 8, meta=A * 1000 + 4)], 5)]:
+        with pytest.raises(exmy.ExmyError) as ei:
+            exmy.group_plan(ents, torch.bfloat16, "e3m3", per_row=True)
+        assert ei.value.status == status
     assert exmy.group_layout((4096,)) == (8, 512)
     assert exmy.group_layout((3, 5, 8)) == (15, 8)
     # the device calls check the plan before launching anything

@@ -106,13 +106,22 @@ def main():
     def group_decode():
         grp.decode()
 
+    grp_rows = exmy.GroupCodec([t for t, _ in tensors], (x, y), per_row=True)   # per-row recipe, grouped
+
+    def group_rows_encode():   # row bytes (1 launch) + encode (1)
+        grp_rows.encode()
+
+    def group_rows_decode():
+        grp_rows.decode()
+
     res = {"tensors": len(tensors), "params": nparams, "fmt": a.fmt}
     nl = {"encode": 3 * len(tensors), "encode_maxexp": 2 * len(tensors), "decode": len(tensors),
           "encode_rowwise": len(tensors), "decode_rowwise": len(tensors),
-          "group_encode": 3, "group_decode": 1}
+          "group_encode": 3, "group_decode": 1, "group_rows_encode": 2, "group_rows_decode": 1}
     for name, fn in (("encode", encode_all), ("encode_maxexp", encode_all_max), ("decode", decode_all),
                      ("encode_rowwise", encode_all_rowwise), ("decode_rowwise", decode_all_rowwise),
-                     ("group_encode", group_encode), ("group_decode", group_decode)):
+                     ("group_encode", group_encode), ("group_decode", group_decode),
+                     ("group_rows_encode", group_rows_encode), ("group_rows_decode", group_rows_decode)):
         if a.only and name not in a.only.split(","):
             continue
         ms = time(fn)
