@@ -179,9 +179,13 @@ exmy_status exmy_decode(const uint8_t *packed, int64_t rows, int64_t cols, int a
  * counter-update variant (0: lane-private read-modify-write, 1: lane-private
  * shared-memory atomics, 2 (default): the same atomics with both bf16
  * elements' counter offsets from one shift+mask and red.shared on 32-bit
- * shared addresses).  Pass -1 to query.  Return the previous value. */
+ * shared addresses).
+ * exmy_debug_hist_blocks(b) caps the histogram grid at b CTAs (0: auto) so
+ * tests reach the counter-overflow flushes with small inputs.  Pass -1 to
+ * query.  Return the previous value. */
 int exmy_debug_force_generic(int on);
 int exmy_debug_hist_mode(int mode);
+int exmy_debug_hist_blocks(int blocks);
 
 /* ------------------------------------------------------- block metadata */
 /* Blocks ("a tensor, a row, a column, a sub row or even a 2D

@@ -57,6 +57,7 @@ def _load():
         "exmy_choose_x": ([vp, dbl, vp], i32),
         "exmy_debug_force_generic": ([i32], i32),
         "exmy_debug_hist_mode": ([i32], i32),
+        "exmy_debug_hist_blocks": ([i32], i32),
         "exmy_exponent_histogram": ([vp, i32, i64, vp, vp], i32),
         "exmy_emax_from_histogram": ([vp, vp, vp], i32),
         "exmy_max_exponent": ([vp, i32, i64, vp, vp], i32),
@@ -105,7 +106,7 @@ _lib = _load()
 LIB_PATH = _LIB_PATH
 EXPORTED = ["exmy_version", "exmy_status_string", "exmy_format_valid", "exmy_packed_bytes", "exmy_segments",
             "exmy_bias_from_emax", "exmy_emax_from_bias", "exmy_emax_from_histogram_host", "exmy_choose_x",
-            "exmy_debug_force_generic", "exmy_debug_hist_mode", "exmy_exponent_histogram",
+            "exmy_debug_force_generic", "exmy_debug_hist_mode", "exmy_debug_hist_blocks", "exmy_exponent_histogram",
             "exmy_emax_from_histogram", "exmy_quantize", "exmy_encode", "exmy_decode", "exmy_encode_host",
             "exmy_decode_host", "exmy_block_max_exponent", "exmy_quantize_blocked", "exmy_encode_blocked",
             "exmy_decode_blocked", "exmy_decode_rows", "exmy_max_exponent", "exmy_encode_rowwise",
@@ -192,6 +193,11 @@ def force_generic(on: bool | None = None) -> bool:
 
 def hist_mode(mode: int | None = None) -> int:
     return _lib.exmy_debug_hist_mode(-1 if mode is None else int(mode))
+
+
+def hist_blocks(blocks: int | None = None) -> int:
+    """test knob: cap the histogram grid (0 = auto); returns the previous cap"""
+    return _lib.exmy_debug_hist_blocks(-1 if blocks is None else int(blocks))
 
 
 def _check(status: int, what: str):

@@ -10,6 +10,7 @@
 namespace exmy {
 int g_force_generic = 0;
 int g_hist_mode = 2;
+int g_hist_blocks = 0;
 }  // namespace exmy
 
 using namespace exmy;
@@ -129,6 +130,12 @@ int exmy_debug_force_generic(int on) {
 int exmy_debug_hist_mode(int mode) {
     int prev = g_hist_mode;
     if (mode >= 0) g_hist_mode = mode;
+    return prev;
+}
+
+int exmy_debug_hist_blocks(int blocks) {
+    int prev = g_hist_blocks;
+    if (blocks >= 0) g_hist_blocks = blocks;
     return prev;
 }
 

@@ -12,6 +12,7 @@ namespace exmy {
 
 extern int g_force_generic;   // exmy_debug_force_generic
 extern int g_hist_mode;       // exmy_debug_hist_mode
+extern int g_hist_blocks;     // exmy_debug_hist_blocks
 
 inline int num_sms() {
     static int cache[64] = {0};

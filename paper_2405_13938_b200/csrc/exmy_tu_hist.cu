@@ -17,13 +17,15 @@ exmy_status launch_hist_vec(const uint8_t *in, int64_t n, unsigned long long *hi
         if (dev >= 0 && dev < 64) configured |= 1ull << dev;
     }
     const int64_t nvec = n / Elem<BF16>::V;
-    int64_t blocks = cdiv(cdiv(nvec, 128), HIST_WARPS);
+    int64_t blocks = cdiv(cdiv(nvec, 32 * HIST_U), HIST_WARPS);
     if (blocks < 1) blocks = 1;
     int64_t maxb = (int64_t)num_sms() * occ;
     if (blocks > maxb) blocks = maxb;
+    if (g_hist_blocks > 0 && blocks > g_hist_blocks) blocks = g_hist_blocks;   // test knob: long per-lane runs
     k_hist<BF16, MODE><<<(unsigned)blocks, HIST_THREADS, HIST_SMEM, st>>>(in, n, hist);
     return launch_status();
 }
+
 }  // namespace
 
 exmy_status launch_histogram(const uint8_t *in, bool bf16, int64_t n, unsigned long long *hist, cudaStream_t st) {

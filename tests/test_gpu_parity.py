@@ -86,6 +86,44 @@ def test_histogram_peaked_and_misaligned(exmy, orc, dt):
     np.testing.assert_array_equal(h.cpu().numpy().astype(np.uint64), 2 * orc.histogram(bits))
 
 
+def peaked_mix(n, seed, dt="bf16"):
+    """bf16 weights-like values (peaked exponents) with far
+    clusters, exact zeros, subnormals and NaN/Inf sprinkled in"""
+    rng = np.random.default_rng(seed)
+    v = (rng.standard_normal(n) * 0.02).astype(np.float32)
+    blk = rng.integers(0, 4, size=(n + 4095) // 4096).repeat(4096)[:n]
+    v = np.where(blk == 1, v * np.float32(2.0 ** 60), v)       # whole 4K runs in another window
+    v = np.where(blk == 2, v * np.float32(2.0 ** -100), v)     # runs near the subnormal range
+    m = rng.random(n)
+    v = np.where(m < 0.01, np.float32(0), v)
+    v = np.where((m > 0.01) & (m < 0.012), v * np.float32(2.0 ** 30), v)   # single far elements
+    bits = (v.view(np.uint32) >> 16).astype(np.uint16) if dt == "bf16" else v.view(np.uint32).copy()
+    k = rng.choice(n, size=min(n, 50), replace=False)
+    bits[k[:25]] = 0x7FC0 if dt == "bf16" else 0x7FC00000
+    bits[k[25:]] = 0xFF80 if dt == "bf16" else 0xFF800000
+    return bits
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("blocks", [0, 1, 3])
+@pytest.mark.parametrize("n", [8 * 1000 + 5, (1 << 22) + 3, 20_000_011])
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+def test_histogram_peaked_epochs(exmy, orc, mode, blocks, n, dt):
+    """peaked bf16 data (most elements in a few bins: the lane-private 16-bit
+    counters fill fastest), far clusters, zeros, specials; a grid capped at
+    1 / 3 CTAs makes every lane run past the counter epoch, so the flush
+    before overflow is exercised at test sizes"""
+    exmy.hist_mode(mode)
+    exmy.hist_blocks(blocks)
+    try:
+        bits = peaked_mix(n, n % 97, dt)
+        h = exmy.histogram(dev_bits(bits)).cpu().numpy().astype(np.uint64)
+        np.testing.assert_array_equal(h, orc.histogram(bits))
+    finally:
+        exmy.hist_mode(2)
+        exmy.hist_blocks(0)
+
+
 def test_emax_parity(exmy, orc):
     rng = np.random.default_rng(1)
     for trial in range(50):
