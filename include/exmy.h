@@ -187,6 +187,13 @@ int exmy_debug_force_generic(int on);
 int exmy_debug_hist_mode(int mode);
 int exmy_debug_hist_blocks(int blocks);
 
+/* Roofline probe, not part of the codec: reads in_bytes
+ * (a multiple of 16 KB, 16-byte aligned) and writes out_bytes (a multiple of
+ * 16; each 16 KB input chunk's CTA writes its share) with the codec kernels' access shape and no
+ * arithmetic, so read 2 B / write 0.875 B per element times the HBM limit of
+ * an e3m3 bf16 encode's traffic mix.  Errors: E_SHAPE, E_ARG, E_ALIGN. */
+exmy_status exmy_debug_probe(const void *in, int64_t in_bytes, void *out, int64_t out_bytes, void *stream);
+
 /* ------------------------------------------------------- block metadata */
 /* Blocks ("a tensor, a row, a column, a sub row or even a 2D
  * tile"; per-row metadata is the paper's quality recipe): the

@@ -58,6 +58,7 @@ def _load():
         "exmy_debug_force_generic": ([i32], i32),
         "exmy_debug_hist_mode": ([i32], i32),
         "exmy_debug_hist_blocks": ([i32], i32),
+        "exmy_debug_probe": ([vp, i64, vp, i64, vp], i32),
         "exmy_exponent_histogram": ([vp, i32, i64, vp, vp], i32),
         "exmy_emax_from_histogram": ([vp, vp, vp], i32),
         "exmy_max_exponent": ([vp, i32, i64, vp, vp], i32),
@@ -106,7 +107,8 @@ _lib = _load()
 LIB_PATH = _LIB_PATH
 EXPORTED = ["exmy_version", "exmy_status_string", "exmy_format_valid", "exmy_packed_bytes", "exmy_segments",
             "exmy_bias_from_emax", "exmy_emax_from_bias", "exmy_emax_from_histogram_host", "exmy_choose_x",
-            "exmy_debug_force_generic", "exmy_debug_hist_mode", "exmy_debug_hist_blocks", "exmy_exponent_histogram",
+            "exmy_debug_force_generic", "exmy_debug_hist_mode", "exmy_debug_hist_blocks", "exmy_debug_probe",
+            "exmy_exponent_histogram",
             "exmy_emax_from_histogram", "exmy_quantize", "exmy_encode", "exmy_decode", "exmy_encode_host",
             "exmy_decode_host", "exmy_block_max_exponent", "exmy_quantize_blocked", "exmy_encode_blocked",
             "exmy_decode_blocked", "exmy_decode_rows", "exmy_max_exponent", "exmy_encode_rowwise",
@@ -193,6 +195,17 @@ def force_generic(on: bool | None = None) -> bool:
 
 def hist_mode(mode: int | None = None) -> int:
     return _lib.exmy_debug_hist_mode(-1 if mode is None else int(mode))
+
+
+def roofline_probe(src: torch.Tensor, out_bytes: int, out: torch.Tensor | None = None) -> torch.Tensor:
+    """diagnostic (exmy_debug_probe): stream src's bytes in and out_bytes out
+    with the codec's access shape; time it for a read:write mix's HBM limit"""
+    _require_cuda(src)
+    if out is None:
+        out = torch.empty(max(int(out_bytes), 16), dtype=torch.uint8, device=src.device)
+    _check(_lib.exmy_debug_probe(_ptr(src), src.numel() * src.element_size(), _ptr(out), int(out_bytes),
+                                 _stream(src.device)), "roofline_probe")
+    return out
 
 
 def hist_blocks(blocks: int | None = None) -> int:

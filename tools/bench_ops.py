@@ -42,6 +42,7 @@ def main():
     ap.add_argument("--fmts", default="e0m6,e1m5,e2m4,e3m3,e4m2,e5m1,e6m0")
     ap.add_argument("--axis", default="rows")
     ap.add_argument("--hist-modes", default="2")
+    ap.add_argument("--probe", action="store_true", help="also time the roofline probe for each op's byte mix")
     ap.add_argument("--fs", action="store_true", help="with --block: also time the float-scaling scheme")
     ap.add_argument("--block", default=None, help="row | col | tensor | BRxBC: time the block-metadata path")
     a = ap.parse_args()
@@ -112,6 +113,25 @@ def main():
                 ms = timeit(lambda: exmy.decode(pf, out=d))
                 res[f"fsdecode_{f}"] = {"ms": ms, "gbs": n * (es + k / 8) / ms / 1e6,
                                         "frac": n * (es + k / 8) / ms / 1e6 / peak}
+    if a.probe:   # roofline probe: the same read:write bytes with no arithmetic
+        src = t.reshape(-1).view(torch.uint8)
+        mixes = {"hist": 0.0, "quantize": float(es)}
+        for f in a.fmts.split(","):
+            k = 1 + sum(exmy.parse_format(f))
+            mixes[f"encode_{f}"] = k / 8
+        for name, wpe in mixes.items():   # write bytes per element
+            ob = int(n * wpe)
+            o = torch.empty(max(ob, 16), dtype=torch.uint8, device=dev)
+            ms = timeit(lambda: exmy.roofline_probe(src, ob, out=o))
+            tot = n * es + ob
+            res[f"probe_{name}"] = {"ms": ms, "gbs": tot / ms / 1e6, "frac": tot / ms / 1e6 / peak}
+        for f in a.fmts.split(","):   # decode's mix: read k/8, write es (probe reads the packed bytes' size)
+            k = 1 + sum(exmy.parse_format(f))
+            pk = torch.empty(n * k // 8, dtype=torch.uint8, device=dev)
+            o = torch.empty(n * es, dtype=torch.uint8, device=dev)
+            ms = timeit(lambda: exmy.roofline_probe(pk, n * es, out=o))
+            tot = n * k // 8 + n * es
+            res[f"probe_decode_{f}"] = {"ms": ms, "gbs": tot / ms / 1e6, "frac": tot / ms / 1e6 / peak}
     for k_, v in res.items():
         print(f"{k_:16s} {v['ms']*1e3:9.1f} us {v['gbs']:8.1f} GB/s  {v['frac']*100:5.1f}%")
     print(json.dumps(res))
