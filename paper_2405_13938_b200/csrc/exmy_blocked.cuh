@@ -972,7 +972,13 @@ __device__ __forceinline__ uint32_t vec_max_mag(const uint4 &v, uint32_t m) {
     return m;
 }
 
-constexpr int RW_THREADS = 512;
+#ifndef RW_THREADS_N
+#define RW_THREADS_N 512
+#endif
+constexpr int RW_THREADS = RW_THREADS_N;
+#ifndef RW_HINT
+#define RW_HINT 1   // L2 eviction priorities: pass 1 evict_last, pass 2 evict_first
+#endif
 
 template <int K, bool BF16, int MODE>
 __global__ void __launch_bounds__(RW_THREADS) k_enc_rowwise_rows(const uint8_t *__restrict__ in, int64_t R, int64_t C,
@@ -990,6 +996,7 @@ __global__ void __launch_bounds__(RW_THREADS) k_enc_rowwise_rows(const uint8_t *
     const int64_t G = R / 8, CV16 = C / EL::V, CV4 = C / 4;
     const int64_t rstride = C * EL::ES;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t pol_keep = RW_HINT ? l2_policy_evict_last() : 0, pol_drop = RW_HINT ? l2_policy_evict_first() : 0;
     for (int64_t g = blockIdx.x; g < G; g += gridDim.x) {
         // ---- pass 1: row maxima
         uint32_t m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -997,7 +1004,8 @@ __global__ void __launch_bounds__(RW_THREADS) k_enc_rowwise_rows(const uint8_t *
         for (int64_t j = tid; j < CV16; j += RW_THREADS) {
             uint4 v[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) v[i] = ldg_nc_v4(rg + i * rstride + j * 16);
+            for (int i = 0; i < 8; ++i)
+                v[i] = RW_HINT ? ldg_nc_v4_pol(rg + i * rstride + j * 16, pol_keep) : ldg_nc_v4(rg + i * rstride + j * 16);
 #pragma unroll
             for (int i = 0; i < 8; ++i) m[i] = vec_max_mag<BF16>(v[i], m[i]);
         }
@@ -1032,7 +1040,19 @@ __global__ void __launch_bounds__(RW_THREADS) k_enc_rowwise_rows(const uint8_t *
             const int64_t c0 = jj * 4;
             uint32_t w[8][NW];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) load4<BF16>(rg + i * rstride + c0 * EL::ES, w[i]);
+            for (int i = 0; i < 8; ++i) {
+                if constexpr (RW_HINT) {   // second read of the row group: last use
+                    if constexpr (BF16) {
+                        const uint2 t = ldg_nc_v2_pol(rg + i * rstride + c0 * EL::ES, pol_drop);
+                        w[i][0] = t.x; w[i][1] = t.y;
+                    } else {
+                        const uint4 t = ldg_nc_v4_pol(rg + i * rstride + c0 * EL::ES, pol_drop);
+                        w[i][0] = t.x; w[i][1] = t.y; w[i][2] = t.z; w[i][3] = t.w;
+                    }
+                } else {
+                    load4<BF16>(rg + i * rstride + c0 * EL::ES, w[i]);
+                }
+            }
             uint32_t cp[8][2];
             uint32_t amax = 0;
 #pragma unroll
@@ -1051,6 +1071,138 @@ __global__ void __launch_bounds__(RW_THREADS) k_enc_rowwise_rows(const uint8_t *
             }
         }
         __syncthreads();   // s_e / s_m reused by the next row group
+    }
+}
+
+// ------------------- fused per-row metadata + encode, TMA-staged (ROWS)
+// Rows up to RWS_MAX_ROW_BYTES: the CTA's row group (8 rows) is copied into
+// shared memory by bulk asynchronous copies (cp.async.bulk, one per row,
+// completion counted on an mbarrier), so pass 1 (the 8 row maxima) and pass 2
+// (the encode) both read shared memory: HBM is read exactly once and no L2
+// residency is assumed.  Several CTAs per SM overlap one CTA's copy with
+// another's passes.
+constexpr int RWS_THREADS = 256;
+constexpr int64_t RWS_MAX_ROW_BYTES = 9216;   // 8 rows <= 72 KB of shared memory: 3 CTAs per SM
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "RWS_WAIT%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra RWS_WAIT%=;\n\t}" ::"r"(bar), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+
+template <int K, bool BF16, int MODE>
+__global__ void __launch_bounds__(RWS_THREADS) k_enc_rowwise_smem(const uint8_t *__restrict__ in, int64_t R, int64_t C,
+                                                                 int x, int y, int scheme, uint8_t *__restrict__ meta,
+                                                                 uint8_t *__restrict__ packed, SegOffsets so,
+                                                                 int64_t *spi, uint32_t *spb,
+                                                                 unsigned long long *spc, int64_t cap,
+                                                                 int force_generic) {
+    using EL = Elem<BF16>;
+    constexpr int NW = BF16 ? 2 : 4;
+    constexpr bool SIMD = (MODE == ENC_SIMD || MODE == ENC_SIMD_Y0);
+    extern __shared__ __align__(16) uint8_t rws_sm[];   // 8 rows of C elements
+    __shared__ __align__(8) unsigned long long s_bar;
+    __shared__ uint32_t s_m[RWS_THREADS / 32][8];
+    __shared__ int s_e[8];
+    const FastP P = make_fast(fmt_of(x, y, 0), BF16, 1);
+    const int64_t G = R / 8;
+    const uint32_t rowb = (uint32_t)(C * EL::ES);
+    const int CV16 = (int)(rowb / 16), CV4 = (int)(C / 4);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(rws_sm);
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t phase = 0;
+    for (int64_t g = blockIdx.x; g < G; g += gridDim.x, phase ^= 1u) {
+        if (tid == 0) {   // the row group's 8 rows -> shared memory (async proxy)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior generic reads of the buffer
+            mbar_expect_tx(bar, 8u * rowb);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) bulk_g2s(sbase + i * rowb, in + (8 * g + i) * (int64_t)rowb, rowb, bar);
+        }
+        mbar_wait(bar, phase);
+        // ---- pass 1: row maxima from shared memory
+        uint32_t m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int j = tid; j < CV16; j += RWS_THREADS) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const uint4 v = *reinterpret_cast<const uint4 *>(rws_sm + i * rowb + j * 16);
+                m[i] = vec_max_mag<BF16>(v, m[i]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t mm = BF16 ? max((m[i] & 0xFFFFu) << 16, m[i] & 0xFFFF0000u) : m[i];
+            const uint32_t r = __reduce_max_sync(0xFFFFFFFFu, mm);
+            if (lane == 0) s_m[warp][i] = r;
+        }
+        __syncthreads();
+        if (tid < 8) {
+            uint32_t r = 0;
+#pragma unroll
+            for (int w = 0; w < RWS_THREADS / 32; ++w) r = max(r, s_m[w][tid]);
+            int e = scheme == 0 ? (int)(r >> 23) : exp_after_rounding(r, y);
+            e = e > 254 ? 254 : e;
+            s_e[tid] = e;
+            meta[8 * g + tid] = (uint8_t)e;
+        }
+        __syncthreads();
+        int e8[8];
+        bool ok = !force_generic;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            e8[i] = s_e[i];
+            ok = ok && make_rowp<SIMD>(e8[i], x, y).ok;
+        }
+        // ---- pass 2: encode the row group (8 x 4 tiles) from shared memory
+        for (int jj = tid; jj < CV4; jj += RWS_THREADS) {
+            const int c0 = jj * 4;
+            uint32_t w[8][NW];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const uint8_t *sp = rws_sm + i * rowb + c0 * EL::ES;
+                if constexpr (BF16) {
+                    const uint2 t = *reinterpret_cast<const uint2 *>(sp);
+                    w[i][0] = t.x; w[i][1] = t.y;
+                } else {
+                    const uint4 t = *reinterpret_cast<const uint4 *>(sp);
+                    w[i][0] = t.x; w[i][1] = t.y; w[i][2] = t.z; w[i][3] = t.w;
+                }
+            }
+            uint32_t cp[8][2];
+            uint32_t amax = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) vec_codes_r<K, BF16, MODE, NW>(w[i], cp[i], P, make_rowp<SIMD>(e8[i], x, y), amax);
+            if (ok && !amax_special<BF16, MODE>(amax, P)) {
+                uint32_t RL[1][8], RH[1][8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    RL[0][i] = prmt(cp[i][0], cp[i][1], 0x6420);
+                    RH[0][i] = (K == 9) ? prmt(cp[i][0] >> 1, cp[i][1] >> 1, 0x6420) : 0u;
+                }
+                rows_fast_store<K, 1, 0>(RL, RH, packed, so, g, C, c0);
+            } else {
+                for (int v = 0; v < 4; ++v)
+                    enc_container_generic_rows8<BF16, K>(in, C, g, c0 + v, x, y, e8, packed, so, spi, spb, spc, cap);
+            }
+        }
+        __syncthreads();   // buffer, s_e and s_m are reused by the next row group
     }
 }
 

@@ -1,6 +1,10 @@
 // exmy_tu_blk_encode.cu -- encode with block metadata launchers.
 #include "exmy_launch.cuh"
 
+#ifndef RWS_ENABLE
+#define RWS_ENABLE 1   // TMA-staged fused per-row encode for rows <= RWS_MAX_ROW_BYTES
+#endif
+
 namespace exmy {
 
 namespace {
@@ -86,6 +90,29 @@ template <int K, bool BF16, int MODE>
 exmy_status launch_rowwise_km(const uint8_t *in, int64_t R, int64_t C, int x, int y, int scheme, uint8_t *meta,
                               uint8_t *packed, const Plan &p, int64_t *spi, uint32_t *spb, unsigned long long *spc,
                               int64_t cap, cudaStream_t st) {
+#if RWS_ENABLE
+    const int64_t rowb = C * Elem<BF16>::ES;
+    if (rowb % 16 == 0 && rowb <= RWS_MAX_ROW_BYTES) {   // TMA-staged: each row group read from HBM once
+        const size_t sm = (size_t)(8 * rowb);
+        static unsigned long long configured = 0;
+        static int occ_s = 0;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 0 || dev >= 64 || !(configured & (1ull << dev))) {
+            cudaFuncSetAttribute(k_enc_rowwise_smem<K, BF16, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(8 * RWS_MAX_ROW_BYTES));
+            occ_s = occupancy(k_enc_rowwise_smem<K, BF16, MODE>, RWS_THREADS, 8 * RWS_MAX_ROW_BYTES);
+            if (dev >= 0 && dev < 64) configured |= 1ull << dev;
+        }
+        const int occ_now = occupancy(k_enc_rowwise_smem<K, BF16, MODE>, RWS_THREADS, sm);
+        int64_t blocks = (int64_t)num_sms() * (occ_now > 0 ? occ_now : (occ_s > 0 ? occ_s : 1));
+        if (blocks > R / 8) blocks = R / 8;
+        if (blocks < 1) blocks = 1;
+        k_enc_rowwise_smem<K, BF16, MODE><<<(unsigned)blocks, RWS_THREADS, sm, st>>>(
+            in, R, C, x, y, scheme, meta, packed, p.so, spi, spb, spc, cap, g_force_generic);
+        return launch_status();
+    }
+#endif
     static int occ = 0;
     if (!occ) occ = occupancy(k_enc_rowwise_rows<K, BF16, MODE>, RW_THREADS, 0);
     // the two passes of a row group must meet in L2: bound the CTAs in flight

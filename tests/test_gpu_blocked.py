@@ -172,7 +172,9 @@ def test_row_gather_decode(exmy, orc, fmt, dt, per_row):
 @pytest.mark.parametrize("dt", ["bf16", "f32"])
 def test_encode_rowwise_fused(exmy, orc, fmt, dt):
     """fused per-row metadata + encode == block max (row) + blocked encode"""
-    for shape in [(64, 192), (24, 40), (8, 4104)]:
+    # (4096, 264): more row groups than CTAs (each CTA reuses its staging buffer);
+    # (16, 2304): fp32 rows of exactly the shared-memory staging limit (9216 B)
+    for shape in [(64, 192), (24, 40), (8, 4104), (4096, 264), (16, 2304)]:
         bits = rowscaled_bits(shape, shape[1] + fmt[1], dt)
         d = W.from_bits(bits).to(DEV)
         for scheme in (0, 1):
