@@ -388,6 +388,15 @@ exmy_status exmy_group_max_exponent(const void *plan_host, const void *plan_devi
  * exmy_encode (counts cleared, list sorted by index).  Three launches. */
 exmy_status exmy_group_encode(const void *plan_host, const void *plan_device, void *stream);
 
+/* Per-row plans only (else E_ARG): every row's byte (max before rounding)
+ * AND the encode in one call, == exmy_group_max_exponent + exmy_group_encode
+ * on the same plan.  Entries whose rows are <= 9216 bytes (bf16 <= 4608
+ * columns, fp32 <= 2304) and a multiple of 16 bytes are read from HBM once:
+ * each row group is staged in shared memory by bulk asynchronous copies,
+ * its 8 maxima and its codes computed from there (like exmy_encode_rowwise);
+ * the other entries take the two passes.  Two to five launches. */
+exmy_status exmy_group_encode_rowwise(const void *plan_host, const void *plan_device, void *stream);
+
 /* Decode every entry into its `out` (+ out-of-band specials).  Two launches. */
 exmy_status exmy_group_decode(const void *plan_host, const void *plan_device, void *stream);
 

@@ -94,6 +94,7 @@ def _load():
         "exmy_group_plan_rows": ([vp, i32, i32, i32, i32, i32, vp, ctypes.c_size_t], i32),
         "exmy_group_max_exponent": ([vp, vp, vp], i32),
         "exmy_group_encode": ([vp, vp, vp], i32),
+        "exmy_group_encode_rowwise": ([vp, vp, vp], i32),
         "exmy_group_decode": ([vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
@@ -112,7 +113,7 @@ EXPORTED = ["exmy_version", "exmy_status_string", "exmy_format_valid", "exmy_pac
             "exmy_emax_from_histogram", "exmy_quantize", "exmy_encode", "exmy_decode", "exmy_encode_host",
             "exmy_decode_host", "exmy_block_max_exponent", "exmy_quantize_blocked", "exmy_encode_blocked",
             "exmy_decode_blocked", "exmy_decode_rows", "exmy_max_exponent", "exmy_encode_rowwise",
-            "exmy_group_plan_bytes", "exmy_group_plan", "exmy_group_plan_rows", "exmy_group_max_exponent", "exmy_group_encode",
+            "exmy_group_plan_bytes", "exmy_group_plan", "exmy_group_plan_rows", "exmy_group_max_exponent", "exmy_group_encode", "exmy_group_encode_rowwise",
             "exmy_group_decode", "exmy_block_float_scale", "exmy_quantize_fs", "exmy_encode_fs", "exmy_decode_fs",
             "exmy_encode_push", "exmy_decode_pull", "exmy_embedding_bag", "exmy_ckpt_write", "exmy_ckpt_open", "exmy_ckpt_count", "exmy_ckpt_info",
             "exmy_ckpt_find", "exmy_ckpt_read", "exmy_ckpt_verify", "exmy_ckpt_bytes_read", "exmy_ckpt_close"]
@@ -807,8 +808,12 @@ class GroupCodec:
         return self.meta
 
     def encode(self, meta: torch.Tensor | None = None) -> list:
-        """Encode every tensor; meta=None derives the per-tensor metadata first."""
+        """Encode every tensor; meta=None derives the metadata first (per-row
+        plans: in the same pass, exmy_group_encode_rowwise)."""
         if meta is None:
+            if self.per_row:
+                self._call(_lib.exmy_group_encode_rowwise, "group_encode_rowwise")
+                return self.packed_list()
             self.max_exponent()
         else:
             self.meta.copy_(meta)

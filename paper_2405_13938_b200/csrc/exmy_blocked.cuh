@@ -1102,6 +1102,97 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
                  ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
 
+// one row group (8 rows starting at row 8g of a C-column tensor `in`):
+// stage, row maxima -> meta[8g..8g+7], encode.  Called by every thread of the
+// CTA with the same arguments; `phase` is the mbarrier parity of this use.
+template <int K, bool BF16, int MODE>
+__device__ __forceinline__ void rws_row_group(const uint8_t *__restrict__ in, int64_t C, int64_t g, int x, int y,
+                                              int scheme, uint8_t *__restrict__ meta, uint8_t *__restrict__ packed,
+                                              const SegOffsets &so, int64_t *spi, uint32_t *spb,
+                                              unsigned long long *spc, int64_t cap, int force_generic,
+                                              const FastP &P, uint8_t *rws_sm, uint32_t sbase, uint32_t bar,
+                                              uint32_t phase, uint32_t (*s_m)[8], int *s_e) {
+    using EL = Elem<BF16>;
+    constexpr int NW = BF16 ? 2 : 4;
+    constexpr bool SIMD = (MODE == ENC_SIMD || MODE == ENC_SIMD_Y0);
+    const uint32_t rowb = (uint32_t)(C * EL::ES);
+    const int CV16 = (int)(rowb / 16), CV4 = (int)(C / 4);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {   // the row group's 8 rows -> shared memory (async proxy)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior generic reads of the buffer
+        mbar_expect_tx(bar, 8u * rowb);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) bulk_g2s(sbase + i * rowb, in + (8 * g + i) * (int64_t)rowb, rowb, bar);
+    }
+    mbar_wait(bar, phase);
+    // ---- pass 1: row maxima from shared memory
+    uint32_t m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int j = tid; j < CV16; j += RWS_THREADS) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint4 v = *reinterpret_cast<const uint4 *>(rws_sm + i * rowb + j * 16);
+            m[i] = vec_max_mag<BF16>(v, m[i]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t mm = BF16 ? max((m[i] & 0xFFFFu) << 16, m[i] & 0xFFFF0000u) : m[i];
+        const uint32_t r = __reduce_max_sync(0xFFFFFFFFu, mm);
+        if (lane == 0) s_m[warp][i] = r;
+    }
+    __syncthreads();
+    if (tid < 8) {
+        uint32_t r = 0;
+#pragma unroll
+        for (int w = 0; w < RWS_THREADS / 32; ++w) r = max(r, s_m[w][tid]);
+        int e = scheme == 0 ? (int)(r >> 23) : exp_after_rounding(r, y);
+        e = e > 254 ? 254 : e;
+        s_e[tid] = e;
+        meta[8 * g + tid] = (uint8_t)e;
+    }
+    __syncthreads();
+    int e8[8];
+    bool ok = !force_generic;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        e8[i] = s_e[i];
+        ok = ok && make_rowp<SIMD>(e8[i], x, y).ok;
+    }
+    // ---- pass 2: encode the row group (8 x 4 tiles) from shared memory
+    for (int jj = tid; jj < CV4; jj += RWS_THREADS) {
+        const int c0 = jj * 4;
+        uint32_t w[8][NW];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint8_t *sp = rws_sm + i * rowb + c0 * EL::ES;
+            if constexpr (BF16) {
+                const uint2 t = *reinterpret_cast<const uint2 *>(sp);
+                w[i][0] = t.x; w[i][1] = t.y;
+            } else {
+                const uint4 t = *reinterpret_cast<const uint4 *>(sp);
+                w[i][0] = t.x; w[i][1] = t.y; w[i][2] = t.z; w[i][3] = t.w;
+            }
+        }
+        uint32_t cp[8][2];
+        uint32_t amax = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) vec_codes_r<K, BF16, MODE, NW>(w[i], cp[i], P, make_rowp<SIMD>(e8[i], x, y), amax);
+        if (ok && !amax_special<BF16, MODE>(amax, P)) {
+            uint32_t RL[1][8], RH[1][8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                RL[0][i] = prmt(cp[i][0], cp[i][1], 0x6420);
+                RH[0][i] = (K == 9) ? prmt(cp[i][0] >> 1, cp[i][1] >> 1, 0x6420) : 0u;
+            }
+            rows_fast_store<K, 1, 0>(RL, RH, packed, so, g, C, c0);
+        } else {
+            for (int v = 0; v < 4; ++v)
+                enc_container_generic_rows8<BF16, K>(in, C, g, c0 + v, x, y, e8, packed, so, spi, spb, spc, cap);
+        }
+    }
+    __syncthreads();   // buffer, s_e and s_m are reused by the next row group
+}
+
 template <int K, bool BF16, int MODE>
 __global__ void __launch_bounds__(RWS_THREADS) k_enc_rowwise_smem(const uint8_t *__restrict__ in, int64_t R, int64_t C,
                                                                  int x, int y, int scheme, uint8_t *__restrict__ meta,
@@ -1109,101 +1200,22 @@ __global__ void __launch_bounds__(RWS_THREADS) k_enc_rowwise_smem(const uint8_t 
                                                                  int64_t *spi, uint32_t *spb,
                                                                  unsigned long long *spc, int64_t cap,
                                                                  int force_generic) {
-    using EL = Elem<BF16>;
-    constexpr int NW = BF16 ? 2 : 4;
-    constexpr bool SIMD = (MODE == ENC_SIMD || MODE == ENC_SIMD_Y0);
     extern __shared__ __align__(16) uint8_t rws_sm[];   // 8 rows of C elements
     __shared__ __align__(8) unsigned long long s_bar;
     __shared__ uint32_t s_m[RWS_THREADS / 32][8];
     __shared__ int s_e[8];
     const FastP P = make_fast(fmt_of(x, y, 0), BF16, 1);
-    const int64_t G = R / 8;
-    const uint32_t rowb = (uint32_t)(C * EL::ES);
-    const int CV16 = (int)(rowb / 16), CV4 = (int)(C / 4);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(rws_sm);
-    if (tid == 0) {
+    if (threadIdx.x == 0) {
         mbar_init(bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     uint32_t phase = 0;
-    for (int64_t g = blockIdx.x; g < G; g += gridDim.x, phase ^= 1u) {
-        if (tid == 0) {   // the row group's 8 rows -> shared memory (async proxy)
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior generic reads of the buffer
-            mbar_expect_tx(bar, 8u * rowb);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) bulk_g2s(sbase + i * rowb, in + (8 * g + i) * (int64_t)rowb, rowb, bar);
-        }
-        mbar_wait(bar, phase);
-        // ---- pass 1: row maxima from shared memory
-        uint32_t m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int j = tid; j < CV16; j += RWS_THREADS) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const uint4 v = *reinterpret_cast<const uint4 *>(rws_sm + i * rowb + j * 16);
-                m[i] = vec_max_mag<BF16>(v, m[i]);
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const uint32_t mm = BF16 ? max((m[i] & 0xFFFFu) << 16, m[i] & 0xFFFF0000u) : m[i];
-            const uint32_t r = __reduce_max_sync(0xFFFFFFFFu, mm);
-            if (lane == 0) s_m[warp][i] = r;
-        }
-        __syncthreads();
-        if (tid < 8) {
-            uint32_t r = 0;
-#pragma unroll
-            for (int w = 0; w < RWS_THREADS / 32; ++w) r = max(r, s_m[w][tid]);
-            int e = scheme == 0 ? (int)(r >> 23) : exp_after_rounding(r, y);
-            e = e > 254 ? 254 : e;
-            s_e[tid] = e;
-            meta[8 * g + tid] = (uint8_t)e;
-        }
-        __syncthreads();
-        int e8[8];
-        bool ok = !force_generic;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            e8[i] = s_e[i];
-            ok = ok && make_rowp<SIMD>(e8[i], x, y).ok;
-        }
-        // ---- pass 2: encode the row group (8 x 4 tiles) from shared memory
-        for (int jj = tid; jj < CV4; jj += RWS_THREADS) {
-            const int c0 = jj * 4;
-            uint32_t w[8][NW];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const uint8_t *sp = rws_sm + i * rowb + c0 * EL::ES;
-                if constexpr (BF16) {
-                    const uint2 t = *reinterpret_cast<const uint2 *>(sp);
-                    w[i][0] = t.x; w[i][1] = t.y;
-                } else {
-                    const uint4 t = *reinterpret_cast<const uint4 *>(sp);
-                    w[i][0] = t.x; w[i][1] = t.y; w[i][2] = t.z; w[i][3] = t.w;
-                }
-            }
-            uint32_t cp[8][2];
-            uint32_t amax = 0;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) vec_codes_r<K, BF16, MODE, NW>(w[i], cp[i], P, make_rowp<SIMD>(e8[i], x, y), amax);
-            if (ok && !amax_special<BF16, MODE>(amax, P)) {
-                uint32_t RL[1][8], RH[1][8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    RL[0][i] = prmt(cp[i][0], cp[i][1], 0x6420);
-                    RH[0][i] = (K == 9) ? prmt(cp[i][0] >> 1, cp[i][1] >> 1, 0x6420) : 0u;
-                }
-                rows_fast_store<K, 1, 0>(RL, RH, packed, so, g, C, c0);
-            } else {
-                for (int v = 0; v < 4; ++v)
-                    enc_container_generic_rows8<BF16, K>(in, C, g, c0 + v, x, y, e8, packed, so, spi, spb, spc, cap);
-            }
-        }
-        __syncthreads();   // buffer, s_e and s_m are reused by the next row group
-    }
+    for (int64_t g = blockIdx.x; g < R / 8; g += gridDim.x, phase ^= 1u)
+        rws_row_group<K, BF16, MODE>(in, C, g, x, y, scheme, meta, packed, so, spi, spb, spc, cap, force_generic, P,
+                                     rws_sm, sbase, bar, phase, s_m, s_e);
 }
 
 }  // namespace exmy

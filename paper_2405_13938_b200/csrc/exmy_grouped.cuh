@@ -42,7 +42,8 @@ struct GroupEntry {   // one tensor (128 bytes)
     int64_t rows, cols;
     int64_t vec_begin, tile_begin, dtile_begin;   // first chunk of this tensor in each pass
     int64_t row_begin;                            // per-row plans: first global row of this tensor
-    int64_t pad[2];
+    int64_t frg_begin;                            // per-row plans: first staged row group (fused entries)
+    int64_t fused;                                // per-row plans: rows fit the TMA-staged fused encode
 };
 static_assert(sizeof(GroupEntry) == 128, "plan entry is 128 bytes");
 
@@ -94,15 +95,18 @@ constexpr int GRP_DTILE_CHUNK = GRP_THREADS * GRP_DTPC;   // decode: tiles per C
 // entries) so the search costs shared-memory latency, not a chain of
 // dependent global loads in front of every chunk's loads.
 constexpr int GRP_SMEM_TAB = 4096;
-enum GrpKind { GRP_VEC = 0, GRP_TILE = 1, GRP_DTILE = 2, GRP_ROW = 3 };
+enum GrpKind { GRP_VEC = 0, GRP_TILE = 1, GRP_DTILE = 2, GRP_ROW = 3, GRP_FRG = 4 };
 
 template <int KIND>
 __device__ __forceinline__ int64_t grp_begin(const GroupEntry &e) {
-    return KIND == GRP_VEC ? e.vec_begin : KIND == GRP_TILE ? e.tile_begin : KIND == GRP_DTILE ? e.dtile_begin
-                                                                                              : e.row_begin;
+    return KIND == GRP_VEC     ? e.vec_begin
+           : KIND == GRP_TILE  ? e.tile_begin
+           : KIND == GRP_DTILE ? e.dtile_begin
+           : KIND == GRP_ROW   ? e.row_begin
+                               : e.frg_begin;
 }
 
-inline size_t grp_smem_bytes(int n) { return n <= GRP_SMEM_TAB ? (size_t)n * 8 : 0; }
+__host__ __device__ inline size_t grp_smem_bytes(int n) { return n <= GRP_SMEM_TAB ? (size_t)n * 8 : 0; }
 
 template <int KIND>
 __device__ __forceinline__ const int64_t *grp_stage(const GroupEntry *tab, int n, int64_t *sm) {
@@ -242,7 +246,7 @@ struct GrpCur {
     int dq, dc;    // step to the thread's next tile of the chunk (+256 tiles): +dq row groups, +dc columns
 };
 
-template <int NH, int KIND>
+template <int NH, int KIND, bool SKIPF = false>   // SKIPF: fused entries' chunks do no work
 __device__ __forceinline__ void grp_chunk(GrpCur &u, const GroupEntry *tab, const int64_t *sb) {
     const int C = (int)tab[u.e].cols;
     const uint32_t CV = (uint32_t)C / (4 * NH);
@@ -250,7 +254,7 @@ __device__ __forceinline__ void grp_chunk(GrpCur &u, const GroupEntry *tab, cons
                       threadIdx.x;
     const int64_t q = ((j >> 32) == 0) ? (int64_t)((uint32_t)j / CV) : j / CV;   // 32-bit division when it fits
     u.C = C;
-    u.G = (int)(tab[u.e].rows >> 3);
+    u.G = (SKIPF && tab[u.e].fused) ? 0 : (int)(tab[u.e].rows >> 3);
     u.g = (int)q;
     u.c = (int)(j - q * CV) * (4 * NH);
     u.dq = (int)((uint32_t)GRP_THREADS / CV);
@@ -261,7 +265,7 @@ __device__ __forceinline__ void grp_chunk(GrpCur &u, const GroupEntry *tab, cons
 // next tile of this thread; false when the CTA has no more chunks.  BAR: a
 // CTA barrier at each chunk boundary (uniform: every warp takes GRP_TPC
 // steps per chunk), which keeps the CTA's warps on the same chunk
-template <int NH, int KIND, bool BAR = false>
+template <int NH, int KIND, bool BAR = false, bool SKIPF = false>
 __device__ __forceinline__ bool grp_next(GrpCur &u, const GroupEntry *tab, const int64_t *sb, int n,
                                          int64_t nchunks, int64_t wstride) {
     if (++u.sub < (KIND == GRP_DTILE ? GRP_DTPC : GRP_TPC)) {
@@ -277,7 +281,7 @@ __device__ __forceinline__ bool grp_next(GrpCur &u, const GroupEntry *tab, const
     if (u.ch >= nchunks) return false;
     if (BAR) __syncthreads();
     u.e = grp_advance<KIND>(tab, sb, n, u.e, u.ch);
-    grp_chunk<NH, KIND>(u, tab, sb);
+    grp_chunk<NH, KIND, SKIPF>(u, tab, sb);
     return true;
 }
 
@@ -289,7 +293,7 @@ __device__ __forceinline__ bool grp_next(GrpCur &u, const GroupEntry *tab, const
 // guarantees cols % 8 == 0 (whole 16-byte vectors per row).
 constexpr int GRP_ROW_UNROLL = 4;
 
-template <bool BF16>
+template <bool BF16, bool SKIPF = false>   // SKIPF: leave the fused entries' rows to k_grouped_rowwise_smem
 __global__ void __launch_bounds__(GRP_THREADS) k_grouped_rowmax(const GroupEntry *__restrict__ tab, int n,
                                                                 int64_t nrows) {
     extern __shared__ int64_t grp_sm[];
@@ -301,6 +305,7 @@ __global__ void __launch_bounds__(GRP_THREADS) k_grouped_rowmax(const GroupEntry
     int e = grp_find<GRP_ROW>(tab, sb, n, r);
     for (; r < nrows; r += wstride) {
         e = grp_advance<GRP_ROW>(tab, sb, n, e, r);
+        if (SKIPF && tab[e].fused) continue;
         const int64_t lr = r - grp_b<GRP_ROW>(tab, sb, e);
         const int64_t C = tab[e].cols;
         const int64_t nv = C * Elem<BF16>::ES / 16;
@@ -357,7 +362,7 @@ __device__ __forceinline__ int tile_row_meta(const uint2 &m, int i) {
 
 // PR: per-row metadata (exmy_group_plan_rows): the tile's 8 rows each under
 // their own byte, arithmetic as k_enc_rows_blk (exmy_blocked.cuh)
-template <int K, bool BF16, int MODE, bool PR>
+template <int K, bool BF16, int MODE, bool PR, bool SKIPF = false>
 __global__ void __launch_bounds__(GRP_THREADS, GRP_ENC_MINB) k_grouped_encode(const GroupEntry *__restrict__ tab,
                                                                               int n, int64_t nchunks, int x, int y,
                                                                               int force_generic) {
@@ -370,7 +375,7 @@ __global__ void __launch_bounds__(GRP_THREADS, GRP_ENC_MINB) k_grouped_encode(co
     u.ch = blockIdx.x;
     if (u.ch >= nchunks) return;
     u.e = grp_find<GRP_TILE>(tab, sb, n, u.ch);
-    grp_chunk<1, GRP_TILE>(u, tab, sb);
+    grp_chunk<1, GRP_TILE, SKIPF>(u, tab, sb);
     uint32_t nxt[8][NW];
     uint2 nm = make_uint2(0, 0);
     if (u.g < u.G) grp_enc_load<BF16, NW, PR>(tab, u, nxt, nm);
@@ -390,7 +395,7 @@ __global__ void __launch_bounds__(GRP_THREADS, GRP_ENC_MINB) k_grouped_encode(co
 #pragma unroll
             for (int q = 0; q < NW; ++q) w[i][q] = nxt[i][q];
         const uint2 em = nm;
-        more = grp_next<1, GRP_TILE, GRP_ENC_BAR != 0>(u, tab, sb, n, nchunks, wstride);   // warp-uniform
+        more = grp_next<1, GRP_TILE, GRP_ENC_BAR != 0, SKIPF>(u, tab, sb, n, nchunks, wstride);   // warp-uniform
         if (more && u.g < u.G) grp_enc_load<BF16, NW, PR>(tab, u, nxt, nm);
         if (!PR && te != cur) {   // new tensor: its format constants
             cur = te;
@@ -578,6 +583,43 @@ __global__ void __launch_bounds__(GRP_THREADS, K < 9 ? GRP_DEC_OCC : 2) k_groupe
         } else {
             grp_dec_tile<K, OBF16, MODE, NH>(raw, out, C, tg, tc, F, P);
         }
+    }
+}
+
+// ------------------------------------------------ fused per-row max + encode
+// Per-row plans, entries whose rows fit the staging limit (`fused`): one CTA
+// per row group at a time, the rows staged in shared memory by bulk async
+// copies, row maxima and encode from shared memory (rws_row_group,
+// exmy_blocked.cuh): each such tensor is read from HBM once.  Units are row
+// groups numbered across the fused entries (frg_begin).
+__host__ __device__ inline size_t grws_tab_bytes(int n) { return (grp_smem_bytes(n) + 15) & ~(size_t)15; }
+
+template <int K, bool BF16, int MODE>
+__global__ void __launch_bounds__(RWS_THREADS) k_grouped_rowwise_smem(const GroupEntry *__restrict__ tab, int n,
+                                                                     int64_t nunits, int x, int y,
+                                                                     int force_generic) {
+    extern __shared__ __align__(16) uint8_t grws_sm[];   // [table begins][8 staged rows]
+    __shared__ __align__(8) unsigned long long s_bar;
+    __shared__ uint32_t s_m[RWS_THREADS / 32][8];
+    __shared__ int s_e[8];
+    const int64_t *sb = grp_stage<GRP_FRG>(tab, n, reinterpret_cast<int64_t *>(grws_sm));
+    uint8_t *buf = grws_sm + grws_tab_bytes(n);
+    const FastP P = make_fast(fmt_of(x, y, 0), BF16, 1);
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(buf);
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t phase = 0;
+    int e = -1;
+    for (int64_t unit = blockIdx.x; unit < nunits; unit += gridDim.x, phase ^= 1u) {
+        e = e < 0 ? grp_find<GRP_FRG>(tab, sb, n, unit) : grp_advance<GRP_FRG>(tab, sb, n, e, unit);
+        const GroupEntry &E = tab[e];
+        rws_row_group<K, BF16, MODE>(E.in, E.cols, unit - grp_b<GRP_FRG>(tab, sb, e), x, y, 0, E.meta, E.packed,
+                                     grp_so<K>(E.rows * E.cols), E.spi, E.spb, E.spc, E.cap, force_generic, P, buf,
+                                     sbase, bar, phase, s_m, s_e);
     }
 }
 

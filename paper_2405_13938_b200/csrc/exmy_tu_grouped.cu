@@ -126,6 +126,76 @@ exmy_status launch_gdec(int k, const GroupEntry *tab, const GroupHeader &h, cuda
     return EXMY_E_FORMAT;
 }
 
+template <int K, bool BF16, int MODE>
+exmy_status launch_grws_km(const GroupEntry *tab, const GroupHeader &h, const GroupEntry *host_e, cudaStream_t st) {
+    int64_t units = 0, maxrowb = 0, rest = 0;
+    for (int i = 0; i < h.n; ++i) {
+        const GroupEntry &E = host_e[i];
+        if (E.rows * E.cols == 0) continue;
+        if (E.fused) {
+            units += E.rows / 8;
+            maxrowb = E.cols * (BF16 ? 2 : 4) > maxrowb ? E.cols * (BF16 ? 2 : 4) : maxrowb;
+        } else {
+            rest += E.rows;
+        }
+    }
+    exmy_status s = EXMY_OK;
+    if (units) {
+        const size_t smax = grws_tab_bytes(GRP_SMEM_TAB) + 8 * (size_t)RWS_MAX_ROW_BYTES;
+        static unsigned long long configured = 0;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 0 || dev >= 64 || !(configured & (1ull << dev))) {
+            cudaFuncSetAttribute(k_grouped_rowwise_smem<K, BF16, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smax);
+            if (dev >= 0 && dev < 64) configured |= 1ull << dev;
+        }
+        const size_t sm = grws_tab_bytes(h.n) + 8 * (size_t)maxrowb;
+        const int occ = occupancy(k_grouped_rowwise_smem<K, BF16, MODE>, RWS_THREADS, sm);
+        int64_t g = (int64_t)num_sms() * (occ > 0 ? occ : 1);
+        if (g > units) g = units;
+        k_grouped_rowwise_smem<K, BF16, MODE><<<(unsigned)g, RWS_THREADS, sm, st>>>(tab, h.n, units, h.x, h.y,
+                                                                                      g_force_generic);
+        if ((s = launch_status()) != EXMY_OK) return s;
+    }
+    if (rest) {   // entries with wider rows: row bytes pass + encode, skipping the fused ones
+        const size_t sm = grp_smem_bytes(h.n);
+        const int64_t cta = cdiv(h.row_total, (int64_t)(GRP_THREADS / 32));
+        k_grouped_rowmax<BF16, true><<<grid_for(k_grouped_rowmax<BF16, true>, GRP_THREADS, cta, sm), GRP_THREADS, sm,
+                                        st>>>(tab, h.n, h.row_total);
+        if ((s = launch_status()) != EXMY_OK) return s;
+        const int occ = occupancy(k_grouped_encode<K, BF16, MODE, true, true>, GRP_THREADS, sm);
+        int64_t g = (int64_t)num_sms() * occ;
+        if (g > h.tile_chunks) g = h.tile_chunks;
+        k_grouped_encode<K, BF16, MODE, true, true><<<(unsigned)g, GRP_THREADS, sm, st>>>(tab, h.n, h.tile_chunks,
+                                                                                          h.x, h.y, g_force_generic);
+        s = launch_status();
+    }
+    return s;
+}
+
+template <int K, bool BF16>
+exmy_status launch_grws_k(const GroupEntry *tab, const GroupHeader &h, const GroupEntry *he, cudaStream_t st) {
+    if (BF16 && h.y <= 6)   // same mode choice as exmy_encode_rowwise
+        return h.y == 0 ? launch_grws_km<K, BF16, (BF16 ? ENC_SIMD_Y0 : ENC_F32_Y0)>(tab, h, he, st)
+                        : launch_grws_km<K, BF16, (BF16 ? ENC_SIMD : ENC_F32)>(tab, h, he, st);
+    return h.y == 0 ? launch_grws_km<K, BF16, ENC_F32_Y0>(tab, h, he, st) : launch_grws_km<K, BF16, ENC_F32>(tab, h, he, st);
+}
+
+template <bool BF16>
+exmy_status launch_grws(int k, const GroupEntry *tab, const GroupHeader &h, const GroupEntry *he, cudaStream_t st) {
+    switch (k) {
+        case 3: return launch_grws_k<3, BF16>(tab, h, he, st);
+        case 4: return launch_grws_k<4, BF16>(tab, h, he, st);
+        case 5: return launch_grws_k<5, BF16>(tab, h, he, st);
+        case 6: return launch_grws_k<6, BF16>(tab, h, he, st);
+        case 7: return launch_grws_k<7, BF16>(tab, h, he, st);
+        case 8: return launch_grws_k<8, BF16>(tab, h, he, st);
+        case 9: return launch_grws_k<9, BF16>(tab, h, he, st);
+    }
+    return EXMY_E_FORMAT;
+}
+
 inline unsigned small_grid(int n, int per) {
     int64_t g = cdiv(n, per);
     return (unsigned)(g < 1 ? 1 : (g > 65535 ? 65535 : g));
@@ -169,7 +239,8 @@ exmy_status plan_impl(const exmy_group_entry *entries, int n, int dtype, int x, 
         for (int i = 0; i < n; ++i)
             if (entries[i].cols % 8) h.dec_nh = 1;
     }
-    int64_t vc = 0, tc = 0, dc = 0, rc = 0;
+    int64_t vc = 0, tc = 0, dc = 0, rc = 0, fc = 0;
+    const int64_t es = dtype == EXMY_BF16 ? 2 : 4;
     for (int i = 0; i < n; ++i) {
         const exmy_group_entry &a = entries[i];
         if (a.rows < 0 || a.cols < 0 || a.rows % 8 || a.cols % 4) return EXMY_E_SHAPE;
@@ -192,6 +263,8 @@ exmy_status plan_impl(const exmy_group_entry *entries, int n, int dtype, int x, 
         g.tile_begin = tc;
         g.dtile_begin = dc;
         g.row_begin = rc;
+        g.frg_begin = fc;
+        g.fused = 0;
         const int64_t ne = a.rows * a.cols;
         if (ne > 0) {
             if (!a.packed || !a.meta) return EXMY_E_ARG;
@@ -199,6 +272,10 @@ exmy_status plan_impl(const exmy_group_entry *entries, int n, int dtype, int x, 
                 return EXMY_E_ALIGN;
             if (per_row && (a.cols % 8 || !aligned(a.meta, 8))) return a.cols % 8 ? EXMY_E_SHAPE : EXMY_E_ALIGN;
             rc += a.rows;
+            if (per_row && (a.cols * es) % 16 == 0 && a.cols * es <= RWS_MAX_ROW_BYTES) {
+                g.fused = 1;
+                fc += a.rows / 8;
+            }
             vc += cdiv(ne / V, GRP_VEC_CHUNK);
             tc += cdiv((a.rows / 8) * (a.cols / 4), GRP_TILE_CHUNK);
             dc += cdiv((a.rows / 8) * (a.cols / (4 * h.dec_nh)), GRP_DTILE_CHUNK);
@@ -279,6 +356,28 @@ exmy_status exmy_group_encode(const void *plan_host, const void *plan_device, vo
     if (h->tile_chunks == 0) return EXMY_OK;
     const int k = 1 + h->x + h->y;
     s = h->dtype == EXMY_BF16 ? launch_genc<true>(k, tab, *h, st) : launch_genc<false>(k, tab, *h, st);
+    if (s != EXMY_OK || !h->specials) return s;
+    k_grouped_sort<<<small_grid(h->n, 1), 1024, 0, st>>>(tab, h->n);
+    return launch_status();
+}
+
+exmy_status exmy_group_encode_rowwise(const void *plan_host, const void *plan_device, void *stream) {
+    const GroupHeader *h;
+    const GroupEntry *e;
+    exmy_status s = open_plan(plan_host, plan_device, &h, &e);
+    if (s != EXMY_OK) return s;
+    if (!h->per_row) return EXMY_E_ARG;
+    for (int i = 0; i < h->n; ++i)
+        if (e[i].rows * e[i].cols > 0 && !e[i].in) return EXMY_E_ARG;
+    cudaStream_t st = S(stream);
+    const GroupEntry *tab = dev_table(plan_device);
+    if (h->specials) {
+        k_grouped_clear<1><<<small_grid(h->n, 256), 256, 0, st>>>(tab, h->n);
+        if ((s = launch_status()) != EXMY_OK) return s;
+    }
+    if (h->row_total == 0) return EXMY_OK;
+    const int k = 1 + h->x + h->y;
+    s = h->dtype == EXMY_BF16 ? launch_grws<true>(k, tab, *h, e, st) : launch_grws<false>(k, tab, *h, e, st);
     if (s != EXMY_OK || !h->specials) return s;
     k_grouped_sort<<<small_grid(h->n, 1), 1024, 0, st>>>(tab, h->n);
     return launch_status();

@@ -170,8 +170,11 @@ def test_group_plan_host(exmy):
     b = exmy.group_plan(rents, torch.bfloat16, "e3m3", per_row=True)
     sp, per_row, row_total = struct.unpack("<hhq", b[52:64])
     assert (sp, per_row, row_total) == (0, 1, 64 + 16 + 8)
-    for i, rb in enumerate([0, 64, 64, 80]):
-        assert struct.unpack("<q", b[64 + 128 * i + 104:64 + 128 * i + 112])[0] == rb
+    for i, (rb, fb, fused) in enumerate([(0, 0, 1), (64, 8, 0), (64, 8, 1), (80, 10, 1)]):
+        # first global row; first TMA-staged row group and the "rows <= 9216 B" flag
+        assert struct.unpack("<qqq", b[64 + 128 * i + 104:64 + 128 * i + 128]) == (rb, fb, fused)
+    wide = exmy.group_plan([ent(0, 8, 4616, meta=A * 1000)], torch.bfloat16, "e3m3", per_row=True)
+    assert struct.unpack("<q", wide[64 + 120:64 + 128])[0] == 0      # 9232-byte rows: two-pass entry
     assert struct.unpack("<hh", exmy.group_plan(rents, torch.bfloat16, "e3m3")[52:56]) == (0, 0)
     for ents, status in [([ent(0, 8, 4, meta=A * 1000)], 3), ([ent(0, 8, 8, meta=A * 1000 + 4)], 5)]:
         with pytest.raises(exmy.ExmyError) as ei:
