@@ -102,3 +102,16 @@ def test_gather_bag_push_pull_in_bounds(exmy, fmt):
     o = Guarded((R, C), torch.float32)
     exmy.decode_pull(shards, 16, C, fmt, m, out=o.t)
     assert o.intact() and torch.equal(o.t, exmy.decode(exmy.encode(t, fmt, m), torch.float32))
+
+
+def test_roofline_probe_runs_and_validates(exmy):
+    """exmy_debug_probe (SURVEY 8(d) roofline probe): streams the bytes it is
+    given; the output share of each chunk lands inside the output buffer"""
+    src = torch.zeros(64 * 1024, dtype=torch.uint8, device=DEV)
+    o = Guarded((7 * 1024 + 16 * 5,), torch.uint8)
+    exmy.roofline_probe(src, o.nbytes, out=o.t)
+    assert o.intact()
+    with pytest.raises(exmy.ExmyError):
+        exmy.roofline_probe(src[:1000], 16)          # input not a multiple of 16 KB
+    with pytest.raises(exmy.ExmyError):
+        exmy.roofline_probe(src, 17)                 # output not a multiple of 16 B
