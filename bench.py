@@ -268,6 +268,11 @@ def run_ours(args):
                      "hbm_gbs": alg_bytes[k] / (ms * 1e-3) / 1e9,
                      "frac_of_measured": alg_bytes[k] / (ms * 1e-3) / 1e9 / peak,
                      "frac_of_8tbs": alg_bytes[k] / (ms * 1e-3) / 1e9 / 8000.0}
+        # per-launch distribution over the timed steps (median, p10 / p90)
+        us = sorted(1e3 * a.elapsed_time(b) for a, b in ev[k])
+        pct = lambda q: us[min(len(us) - 1, int(round(q * (len(us) - 1))))]
+        per_op[k]["launch_us"] = {"p10": round(pct(0.1), 2), "median": round(pct(0.5), 2),
+                                  "p90": round(pct(0.9), 2), "n": len(us)}
     dom = max(("quantize", "encode", "decode", "hist"), key=lambda k: per_op_ms[k])
     traffic = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
