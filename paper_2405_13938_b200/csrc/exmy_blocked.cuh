@@ -642,6 +642,66 @@ __global__ void __launch_bounds__(256) k_quant_blk(const uint8_t *__restrict__ i
     }
 }
 
+// Narrow rows (C / V < 256 vectors, e.g. 128-column embedding tables): the
+// 2D mapping above would leave most of a CTA's threads without a column.
+// Here vectors are numbered over the whole tensor (row-major), a CTA takes
+// one contiguous chunk of 4 x 256 vectors per iteration, and each vector
+// finds its row by one 32-bit division (64-bit beyond 2^32 vectors).
+template <bool BF16>
+__global__ void __launch_bounds__(256) k_quant_blk_flat(const uint8_t *__restrict__ in, uint8_t *__restrict__ out,
+                                                        int64_t R, int64_t C, int x, int y, MetaMap M,
+                                                        int force_generic) {
+    using EL = Elem<BF16>;
+    constexpr int U = 4;
+    const int64_t CV = C / EL::V, nvec = R * CV;
+    const bool small = nvec < (1ll << 32);
+    const int64_t cstep = (int64_t)gridDim.x * blockDim.x * U;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x * U + threadIdx.x; base < nvec; base += cstep) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t vi = base + (int64_t)u * blockDim.x;
+            v[u] = vi < nvec ? ldg_nc_v4(in + vi * 16) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t vi = base + (int64_t)u * blockDim.x;
+            if (vi >= nvec) continue;
+            const int64_t r = small ? (int64_t)((uint32_t)vi / (uint32_t)CV) : vi / CV;
+            const int64_t c0 = (vi - r * CV) * EL::V;
+            const int64_t rb = M.br == 1 ? r : r / M.br;
+            const int64_t cb = M.nbc == 1 ? 0 : c0 / M.bc;
+            const int em = __ldg(M.meta + rb * M.nbc + cb);
+            const Fmt F = fmt_of(x, y, em > 254 ? 254 : em);
+            const FastP P = make_fast(F, BF16, force_generic);
+            uint32_t o[4];
+            uint32_t flag = 0;
+            const bool fast = BF16 ? P.enc_simd : P.enc_f32;
+            if (fast) {
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    o[t] = BF16 ? quant_pair_bf16(word_of(v[u], t), P, flag) : quant_f32_fast(word_of(v[u], t), P, flag);
+                flag &= 0x80008000u;
+            }
+            if (!fast || flag) {
+                const DecPath DP = make_dec_path(F, force_generic);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const uint32_t w = word_of(v[u], t);
+                    if (BF16) {
+                        const uint32_t lo = quantize_elem<true>(w << 16, F, DP);
+                        const uint32_t hi = quantize_elem<true>(w & 0xFFFF0000u, F, DP);
+                        o[t] = (lo & 0xFFFFu) | (hi << 16);
+                    } else {
+                        o[t] = quantize_elem<false>(w, F, DP);
+                    }
+                }
+            }
+            stg_v4(out + vi * 16, make_uint4(o[0], o[1], o[2], o[3]));
+        }
+    }
+}
+
 template <bool BF16>
 __global__ void k_quant_blk_scalar(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, int64_t R, int64_t C,
                                    int x, int y, MetaMap M, int force_generic) {

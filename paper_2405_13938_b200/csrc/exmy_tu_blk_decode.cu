@@ -131,6 +131,15 @@ exmy_status launch_quantize_blocked(const uint8_t *in, uint8_t *out, bool bf16, 
     if (aligned(in, 16) && aligned(out, 16) && C % V == 0 && bc % V == 0) {
         const int threads = 256;
         const int64_t CV = C / V;
+        if (CV < threads) {   // narrow rows: flat vector numbering (k_quant_blk_flat)
+            int64_t blocks = cdiv(R * CV, (int64_t)threads * 4);
+            const int64_t maxb = (int64_t)num_sms() * 8;
+            if (blocks > maxb) blocks = maxb;
+            if (blocks < 1) blocks = 1;
+            if (bf16) k_quant_blk_flat<true><<<(unsigned)blocks, threads, 0, st>>>(in, out, R, C, x, y, M, g_force_generic);
+            else k_quant_blk_flat<false><<<(unsigned)blocks, threads, 0, st>>>(in, out, R, C, x, y, M, g_force_generic);
+            return launch_status();
+        }
         int64_t gx = cdiv(CV, threads);
         int64_t gy = (int64_t)num_sms() * 8 / gx;
         if (gy < 1) gy = 1;
