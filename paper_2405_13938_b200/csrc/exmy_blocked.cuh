@@ -755,9 +755,12 @@ __global__ void __launch_bounds__(256) k_block_max_small(const uint8_t *__restri
                                                          int y, uint8_t *__restrict__ meta, float *__restrict__ amax_out) {
     constexpr int U = 4;
     const int lane = threadIdx.x & 31;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t v0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x - lane; v0 < nvec; v0 += stride * U) {
-        // warp-uniform: this warp's 32 consecutive vectors, then the next 3 strides
+    // a CTA reads one contiguous chunk of U x 256 vectors per iteration (as
+    // k_quant_fast); a warp's 32 consecutive vectors per u hold whole blocks
+    const int64_t stride = blockDim.x;
+    const int gshift = __ffs(gsz) - 1;   // gsz is a power of two
+    for (int64_t v0 = (int64_t)blockIdx.x * blockDim.x * U + (threadIdx.x - lane); v0 < nvec;
+         v0 += (int64_t)gridDim.x * blockDim.x * U) {
         uint4 r[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -784,7 +787,7 @@ __global__ void __launch_bounds__(256) k_block_max_small(const uint8_t *__restri
             for (int o = 1; o < gsz; o <<= 1) am = max(am, __shfl_xor_sync(0xFFFFFFFFu, am, o));
             const int64_t vi = vb + lane;
             if ((lane & (gsz - 1)) == 0 && vi < nvec) {
-                const int64_t b = vi / gsz;
+                const int64_t b = vi >> gshift;
                 if (MODE == 2) {
                     amax_out[b] = __uint_as_float(am);
                 } else {
