@@ -257,9 +257,11 @@ __device__ __forceinline__ int64_t div_rcp(int64_t q, int64_t d, double inv) {
 struct GroupMeta {
     int64_t gpr, bc8;
     double inv_gpr, inv_br, inv_bc8;
+    int gpr_shift;   // log2(gpr) when gpr is a power of two (e.g. 128-column tables), else -1
     __device__ __forceinline__ GroupMeta(const MetaMap &M, int64_t C) {
         gpr = C / 8;
         bc8 = M.bc / 8;
+        gpr_shift = (gpr > 0 && (gpr & (gpr - 1)) == 0) ? __ffsll(gpr) - 1 : -1;
         inv_gpr = 1.0 / (double)gpr;
         inv_br = 1.0 / (double)M.br;
         inv_bc8 = 1.0 / (double)bc8;
@@ -271,7 +273,7 @@ struct GroupMeta {
         return e > 254 ? 254 : e;
     }
     __device__ __forceinline__ int at(const MetaMap &M, int64_t q) const {
-        const int64_t row = div_rcp(q, gpr, inv_gpr);
+        const int64_t row = gpr_shift >= 0 ? (q >> gpr_shift) : div_rcp(q, gpr, inv_gpr);
         return at_row(M, row, q - row * gpr);
     }
     // blocks spanning whole rows (bc == C) and rows of >= 128 groups: a warp
