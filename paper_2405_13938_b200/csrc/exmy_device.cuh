@@ -217,11 +217,23 @@ __device__ __forceinline__ uint2 ldg_nc_v2_pol(const void *p, uint64_t pol) {
                  : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(pol));
     return r;
 }
+// EXMY_ST_HINT (A/B builds only, default 0): 1 = st.global.cs (evict-first
+// streaming stores), 2 = st.global.L1::no_allocate
+#ifndef EXMY_ST_HINT
+#define EXMY_ST_HINT 0
+#endif
+#if EXMY_ST_HINT == 1
+#define EXMY_ST_OP "st.global.cs"
+#elif EXMY_ST_HINT == 2
+#define EXMY_ST_OP "st.global.L1::no_allocate"
+#else
+#define EXMY_ST_OP "st.global"
+#endif
 __device__ __forceinline__ void stg_v4(void *p, uint4 v) {
-    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+    asm volatile(EXMY_ST_OP ".v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
 __device__ __forceinline__ void stg_v2(void *p, uint32_t a, uint32_t b) {
-    asm volatile("st.global.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(a), "r"(b) : "memory");
+    asm volatile(EXMY_ST_OP ".v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(a), "r"(b) : "memory");
 }
 
 }  // namespace exmy

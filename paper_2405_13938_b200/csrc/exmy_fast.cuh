@@ -371,7 +371,16 @@ template <bool BF16>
 __device__ __forceinline__ void load4(const uint8_t *p, uint32_t (&w)[BF16 ? 2 : 4]) {
     if constexpr (BF16) {
         uint2 t;
+#if defined(EXMY_LD_HINT) && EXMY_LD_HINT == 1   // A/B builds only: 256-byte L2 prefetch
+        asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v2.u32 {%0,%1}, [%2];" : "=r"(t.x), "=r"(t.y) : "l"(p));
+#elif defined(EXMY_LD_HINT) && EXMY_LD_HINT == 2   // A/B builds only: L2 evict_first policy
+        uint64_t pol;
+        asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+                     : "=r"(t.x), "=r"(t.y) : "l"(p), "l"(pol));
+#else
         asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(t.x), "=r"(t.y) : "l"(p));
+#endif
         w[0] = t.x; w[1] = t.y;
     } else {
         uint4 t = ldg_nc_v4(p);
