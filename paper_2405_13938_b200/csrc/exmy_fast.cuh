@@ -462,7 +462,13 @@ template <int K, bool BF16>
 __host__ __device__ constexpr bool enc_rows_bar() { return BF16 && K >= 8; }
 
 template <int K, bool BF16, int MODE>
-__global__ void __launch_bounds__(256, BF16 ? 3 : 2) k_enc_rows_fast(const uint8_t *__restrict__ in, int64_t R, int64_t C, int x,
+#ifndef EXMY_ENC_ROWS_MINB   // A/B builds only: bf16 ROWS encode CTAs per SM, CTA size
+#define EXMY_ENC_ROWS_MINB 3
+#endif
+#ifndef EXMY_ENC_ROWS_THREADS
+#define EXMY_ENC_ROWS_THREADS 256
+#endif
+__global__ void __launch_bounds__(BF16 ? EXMY_ENC_ROWS_THREADS : 256, BF16 ? EXMY_ENC_ROWS_MINB : 2) k_enc_rows_fast(const uint8_t *__restrict__ in, int64_t R, int64_t C, int x,
                                                        int y, const uint8_t *__restrict__ meta,
                                                        uint8_t *__restrict__ packed, SegOffsets so, int64_t *spi,
                                                        uint32_t *spb, unsigned long long *spc, int64_t cap,

@@ -15,7 +15,7 @@ exmy_status launch_encode_km(const uint8_t *in, int64_t R, int64_t C, int axis, 
         vec = aligned(in, 4 * Elem<BF16>::ES) && (C % 4 == 0);
         for (int s = 0; s < p.nseg; ++s) vec = vec && aligned(packed + p.so.off[s], p.w[s] == 8 ? 4 : 4 * p.w[s]);
         if (vec) {
-            const int threads = 256;
+            const int threads = BF16 ? EXMY_ENC_ROWS_THREADS : 256;
             static int occ = 0;
             if (!occ) occ = occupancy(k_enc_rows_fast<K, BF16, MODE>, threads, 0);
             const int64_t CV = C / 4, G = R / 8;
