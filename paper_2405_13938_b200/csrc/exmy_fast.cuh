@@ -485,6 +485,7 @@ __global__ void __launch_bounds__(BF16 ? EXMY_ENC_ROWS_THREADS : 256, BF16 ? EXM
     const int64_t c0 = j * 4;
     const uint8_t *src = in + c0 * EL::ES;
     const int64_t rstride = C * EL::ES;
+    const uint32_t rs32 = (uint32_t)rstride;
     if (!enc_fast_ok<BF16, MODE>(F, force_generic)) {   // metadata outside the fast preconditions
         if (!act) return;
         for (int64_t g = blockIdx.y; g < G; g += gridDim.y)
@@ -509,8 +510,18 @@ __global__ void __launch_bounds__(BF16 ? EXMY_ENC_ROWS_THREADS : 256, BF16 ? EXM
         if constexpr (BAR) __syncthreads();
         const int64_t gn = g + gridDim.y;
         if (gn < G && act) {
+            if constexpr (BF16) {
+                // one 64-bit base and 32-bit row offsets (the launcher guarantees
+                // 8 * rstride < 2^32): no local-memory reloads at the 80-register
+                // cap, e3m3 139.0 -> 137.9 us, e6m0 160.7 -> 150.3 us (fp32 input
+                // does not spill and measured 1 % slower this way)
+                const uint8_t *pb = src + 8 * gn * rstride;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) load4<BF16>(src + (8 * gn + i) * rstride, nxt[i]);
+                for (int i = 0; i < 8; ++i) load4<BF16>(pb + (uint32_t)i * rs32, nxt[i]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) load4<BF16>(src + (8 * gn + i) * rstride, nxt[i]);
+            }
         }
         if (!act) continue;
         uint32_t cp[8][2];

@@ -12,7 +12,8 @@ exmy_status launch_encode_km(const uint8_t *in, int64_t R, int64_t C, int axis, 
     bool vec = aligned(in, 16);
     if (axis == EXMY_AXIS_ROWS) {
         // thread tile = 8 rows x 4 columns: 4-element row chunks, 4*w-byte segment stores
-        vec = aligned(in, 4 * Elem<BF16>::ES) && (C % 4 == 0);
+        // (8 rows of one row group must span < 4 GiB: the kernel uses 32-bit row offsets)
+        vec = aligned(in, 4 * Elem<BF16>::ES) && (C % 4 == 0) && (8 * C * Elem<BF16>::ES <= (int64_t)UINT32_MAX);
         for (int s = 0; s < p.nseg; ++s) vec = vec && aligned(packed + p.so.off[s], p.w[s] == 8 ? 4 : 4 * p.w[s]);
         if (vec) {
             const int threads = BF16 ? EXMY_ENC_ROWS_THREADS : 256;
