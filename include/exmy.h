@@ -403,7 +403,7 @@ exmy_status exmy_group_decode(const void *plan_host, const void *plan_device, vo
 /* ------------------------------------------------ checkpoint container
  * "encoding and decoding tensors and checkpoints"
  * (P:17-18); file layout after S:369-378 (little-endian):
- *   "EXMY" | version u8 = 1 | entry_count u32, then per tensor
+ *   "EXMY" | version u8 = 2 | entry_count u32, then per tensor
  *   name_len u16 | name | rank u8 | dims u32 x rank | x u8 | y u8 | scheme u8
  *   (0 max-before, 1 max-after, 2 float-scale) | block_kind u8 (0 tensor,
  *   1 row, 2 col, 3 sub-row + L u32, 4 tile + r u32, c u32) | flags u8 (bit0
@@ -411,8 +411,10 @@ exmy_status exmy_group_decode(const void *plan_host, const void *plan_device, vo
  *   length u64) of metadata, each packed segment (descending width), scale
  *   array, specials | crc32 u32 (IEEE) of the tensor's payload bytes;
  *   payloads follow the manifest, one tensor's sections contiguous.
- * Specials are stored as count u64 indices then count u32 fp32 patterns.
- * Host code (pread / pwrite); every buffer here is HOST memory. */
+ * Specials are stored as count (u64 index, u32 fp32 pattern) records
+ * (version 2; version-1 files stored the indices, then the patterns, and
+ * are still read).  Host code (pread / pwrite); every buffer here is HOST
+ * memory. */
 typedef struct exmy_ckpt_tensor {
     const char *name;              /* unique, <= 65535 bytes */
     int rank;                      /* 0..8 */
@@ -440,7 +442,9 @@ typedef struct exmy_ckpt exmy_ckpt;   /* opaque reader */
 int64_t exmy_ckpt_write(const char *path, const exmy_ckpt_tensor *tensors, int n);
 
 /* Open: reads the header and manifest only (E_IO, E_CONTAINER for bad
- * magic / version / truncated manifest / sections outside the file). */
+ * magic / version / truncated manifest / sections outside the file or
+ * overlapping / segment lengths != prod(dims)*w/8 / metadata or scale
+ * lengths that do not match the block grid / allocation failure). */
 exmy_status exmy_ckpt_open(const char *path, exmy_ckpt **out);
 int exmy_ckpt_count(const exmy_ckpt *h);
 /* Tensor i's manifest entry: sizes filled, data pointers NULL; `name` stays
@@ -450,7 +454,8 @@ exmy_status exmy_ckpt_info(const exmy_ckpt *h, int i, exmy_ckpt_tensor *info);
 int exmy_ckpt_find(const exmy_ckpt *h, const char *name);
 /* Lazy read of tensor i: each non-NULL destination (host) receives exactly
  * that section (sizes from exmy_ckpt_info); no other tensor's bytes are
- * touched.  No CRC check (see exmy_ckpt_verify). */
+ * touched.  No CRC check (see exmy_ckpt_verify); a specials index outside
+ * [0, prod(dims)) returns E_CONTAINER. */
 exmy_status exmy_ckpt_read(exmy_ckpt *h, int i, void *meta, void *packed, void *scale,
                            int64_t *sp_index, uint32_t *sp_bits);
 /* Recompute tensor i's CRC32 over its payload: EXMY_OK or E_CHECKSUM. */

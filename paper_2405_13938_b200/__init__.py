@@ -325,6 +325,13 @@ class Packed:
     block: tuple | None = None   # (block_rows, block_cols) when meta is per block
     layout: tuple | None = None  # (rows, cols) packed when not the 2-D view of shape (grouped 1-D tensors)
     scale: torch.Tensor | None = None   # float-scaling metadata: per-block fp32 amax (reading D23)
+    sp_capacity: int | None = None   # specials capacity the encode ran with (entries written); None: sp_index.numel()
+    scheme: int = 0              # block metadata scheme: 0 max-before, 1 max-after, 2 float scaling
+
+    @property
+    def capacity(self) -> int:
+        """entries the encode could write: decode scatters min(count, capacity)"""
+        return self.sp_index.numel() if self.sp_capacity is None else int(self.sp_capacity)
 
     @property
     def k(self) -> int:
@@ -345,9 +352,21 @@ class Packed:
         return [(w, self.data[o:o + n * w // 8]) for w, o in zip(ws, offs)]
 
     def specials(self):
-        cnt = int(self.sp_count.item())
-        c = min(cnt, self.sp_index.numel())
+        """(index, bits, total count) of the out-of-band NaN/Inf (D9); the lists
+        hold min(count, capacity) entries."""
+        cnt = int(self.sp_count.item()) if self.sp_count is not None else 0
+        c = min(cnt, self.capacity)
         return self.sp_index[:c], self.sp_bits[:c], cnt
+
+    def check_specials(self):
+        """Raise E_CAPACITY if the encode saw more NaN/Inf than its specials
+        capacity (the extra ones would decode as their in-band code 0).
+        Synchronises the stream."""
+        cnt = int(self.sp_count.item()) if self.sp_count is not None else 0
+        if cnt > self.capacity:
+            raise ExmyError(6, f"encode: {cnt} NaN/Inf elements but specials capacity {self.capacity}; "
+                               f"re-encode with specials_capacity >= {cnt}")
+        return self
 
 
 def _as_2d_shape(shape):
@@ -360,9 +379,12 @@ def _as_2d_shape(shape):
 
 
 def encode(t: torch.Tensor, fmt, meta=None, axis="rows", specials_capacity: int = 4096,
-           out: torch.Tensor | None = None) -> Packed:
+           out: torch.Tensor | None = None, strict: bool = True) -> Packed:
     """Type conversion + power-of-2 bit packing.  meta=None derives
-    the per-tensor max biased exponent from the histogram."""
+    the per-tensor max biased exponent.  strict: synchronise and
+    raise E_CAPACITY when the tensor holds more NaN/Inf than
+    specials_capacity (strict=False keeps the call asynchronous; check later
+    with Packed.check_specials())."""
     _require_cuda(t)
     x, y = parse_format(fmt)
     ax = _AXES[axis]
@@ -380,7 +402,11 @@ def encode(t: torch.Tensor, fmt, meta=None, axis="rows", specials_capacity: int 
     spc = torch.zeros(1, dtype=torch.int64, device=dev)
     _check(_lib.exmy_encode(_ptr(t), _dtype_code(t.dtype), R, C, ax, x, y, _ptr(m), _ptr(out), _ptr(spi), _ptr(spb),
                             _ptr(spc), cap, _stream(dev)), "encode")
-    return Packed(out, m, spi, spb, spc, tuple(t.shape), x, y, ax, t.dtype)
+    return _finish(Packed(out, m, spi, spb, spc, tuple(t.shape), x, y, ax, t.dtype, sp_capacity=cap), strict)
+
+
+def _finish(p: Packed, strict: bool) -> Packed:
+    return p.check_specials() if strict else p
 
 
 def decode(p: Packed, dtype: torch.dtype | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
@@ -390,7 +416,7 @@ def decode(p: Packed, dtype: torch.dtype | None = None, out: torch.Tensor | None
     R, C = p.rows, p.cols
     if out is None:
         out = torch.empty(p.shape, dtype=dtype, device=dev)
-    cap = p.sp_index.numel() if p.sp_count is not None else 0
+    cap = p.capacity if p.sp_count is not None else 0
     if p.scale is not None:
         _check(_lib.exmy_decode_fs(_ptr(p.data), R, C, p.axis, p.block[0], p.block[1], p.x, p.y, _ptr(p.scale),
                                    _ptr(p.sp_index), _ptr(p.sp_bits), _ptr(p.sp_count), cap, _ptr(out),
@@ -452,7 +478,7 @@ def quantize_blocked(t: torch.Tensor, fmt, meta: torch.Tensor, block, out: torch
 
 
 def encode_blocked(t: torch.Tensor, fmt, meta: torch.Tensor | None, block, axis="rows", scheme="before",
-                   specials_capacity: int = 4096, out: torch.Tensor | None = None) -> Packed:
+                   specials_capacity: int = 4096, out: torch.Tensor | None = None, strict: bool = True) -> Packed:
     """Encode with one metadata byte per block; meta=None computes it with
     the given scheme."""
     _require_cuda(t)
@@ -475,11 +501,13 @@ def encode_blocked(t: torch.Tensor, fmt, meta: torch.Tensor | None, block, axis=
     spc = torch.zeros(1, dtype=torch.int64, device=dev)
     _check(_lib.exmy_encode_blocked(_ptr(t), _dtype_code(t.dtype), R, C, ax, br, bc, x, y, _ptr(meta), _ptr(out),
                                     _ptr(spi), _ptr(spb), _ptr(spc), cap, _stream(dev)), "encode_blocked")
-    return Packed(out, meta, spi, spb, spc, tuple(t.shape), x, y, ax, t.dtype, (br, bc))
+    return _finish(Packed(out, meta, spi, spb, spc, tuple(t.shape), x, y, ax, t.dtype, (br, bc), sp_capacity=cap,
+                          scheme=SCHEMES[scheme]), strict)
 
 
 def encode_rowwise(t: torch.Tensor, fmt, axis="rows", scheme="before", specials_capacity: int = 4096,
-                   out: torch.Tensor | None = None, meta_out: torch.Tensor | None = None) -> Packed:
+                   out: torch.Tensor | None = None, meta_out: torch.Tensor | None = None,
+                   strict: bool = True) -> Packed:
     """Per-row metadata + encode in one call (fused single-pass kernel for ROWS)."""
     _require_cuda(t)
     x, y = parse_format(fmt)
@@ -498,16 +526,30 @@ def encode_rowwise(t: torch.Tensor, fmt, axis="rows", scheme="before", specials_
     spc = torch.zeros(1, dtype=torch.int64, device=dev)
     _check(_lib.exmy_encode_rowwise(_ptr(t), _dtype_code(t.dtype), R, C, ax, x, y, SCHEMES[scheme], _ptr(meta),
                                     _ptr(out), _ptr(spi), _ptr(spb), _ptr(spc), cap, _stream(dev)), "encode_rowwise")
-    return Packed(out, meta, spi, spb, spc, tuple(t.shape), x, y, ax, t.dtype, (1, C))
+    return _finish(Packed(out, meta, spi, spb, spc, tuple(t.shape), x, y, ax, t.dtype, (1, C), sp_capacity=cap,
+                          scheme=SCHEMES[scheme]), strict)
+
+
+def _check_indices(idx: torch.Tensor, rows: int, what: str):
+    """host-side validation (synchronises): every row index in [0, rows)"""
+    if idx.numel():
+        lo, hi = torch.aminmax(idx)
+        lo, hi = int(lo), int(hi)
+        if lo < 0 or hi >= rows:
+            raise IndexError(f"{what}: row index out of range [0, {rows}): min {lo}, max {hi}")
 
 
 def decode_rows(p: Packed, row_index: torch.Tensor, dtype: torch.dtype | None = None,
-                out: torch.Tensor | None = None) -> torch.Tensor:
-    """Gather-decode rows of a COLS-packed tensor (embedding lookup)."""
+                out: torch.Tensor | None = None, check: bool = True) -> torch.Tensor:
+    """Gather-decode rows of a COLS-packed tensor (embedding lookup).
+    check: validate the indices first (one host sync; check=False for
+    graph capture with trusted indices)."""
     if p.axis != COLS:
         raise ValueError("row gather needs the COLS layout (rows are contiguous byte ranges)")
     dtype = p.dtype if dtype is None else dtype
     idx = row_index.to(device=p.data.device, dtype=torch.int64).contiguous()
+    if check:
+        _check_indices(idx, p.rows, "decode_rows")
     if out is None:
         out = torch.empty((idx.numel(), p.cols), dtype=dtype, device=p.data.device)
     per_row = 0
@@ -521,7 +563,7 @@ def decode_rows(p: Packed, row_index: torch.Tensor, dtype: torch.dtype | None = 
 
 
 def embedding_bag(p: Packed, indices: torch.Tensor, offsets: torch.Tensor, per_sample_weights=None, mode="sum",
-                  out: torch.Tensor | None = None) -> torch.Tensor:
+                  out: torch.Tensor | None = None, check: bool = True) -> torch.Tensor:
     """Pooled decode of rows of a COLS-packed table (reading D25): fp32
     (nbags, cols), like torch.nn.functional.embedding_bag with offsets of
     length nbags + 1; the decoded rows never reach HBM."""
@@ -531,6 +573,14 @@ def embedding_bag(p: Packed, indices: torch.Tensor, offsets: torch.Tensor, per_s
     idx = indices.to(device=dev, dtype=torch.int64).contiguous()
     off = offsets.to(device=dev, dtype=torch.int64).contiguous()
     nb = off.numel() - 1
+    if nb < 0:
+        raise ValueError("offsets needs nbags + 1 entries")
+    if check:
+        _check_indices(idx, p.rows, "embedding_bag")
+        if nb > 0:
+            o = off.cpu()
+            if int(o[0]) != 0 or int(o[-1]) != idx.numel() or bool((o[1:] < o[:-1]).any()):
+                raise ValueError("embedding_bag offsets must start at 0, be non-decreasing and end at len(indices)")
     w = None if per_sample_weights is None else per_sample_weights.to(device=dev, dtype=torch.float32).contiguous()
     per_row = 0
     if p.block is not None:
@@ -545,15 +595,21 @@ def embedding_bag(p: Packed, indices: torch.Tensor, offsets: torch.Tensor, per_s
 
 
 def decode_raw(data: torch.Tensor, rows: int, cols: int, fmt, meta, axis="rows", dtype=torch.bfloat16,
-               out: torch.Tensor | None = None) -> torch.Tensor:
-    """Decode bare packed bytes (e.g. one row shard) without specials."""
+               out: torch.Tensor | None = None, specials=None) -> torch.Tensor:
+    """Decode bare packed bytes (e.g. one row shard).  specials:
+    optional (sp_index, sp_bits, sp_count, capacity) of this (rows, cols)
+    tensor, restored after the decode (D9)."""
     x, y = parse_format(fmt)
     dev = data.device
     m = _meta_tensor(meta, dev)
     if out is None:
         out = torch.empty((rows, cols), dtype=dtype, device=dev)
-    _check(_lib.exmy_decode(_ptr(data), rows, cols, _AXES[axis], x, y, _ptr(m), None, None, None, 0, _ptr(out),
-                            _dtype_code(dtype), _stream(dev)), "decode")
+    spi = spb = spc = None
+    cap = 0
+    if specials is not None:
+        spi, spb, spc, cap = specials
+    _check(_lib.exmy_decode(_ptr(data), rows, cols, _AXES[axis], x, y, _ptr(m), _ptr(spi), _ptr(spb), _ptr(spc),
+                            int(cap), _ptr(out), _dtype_code(dtype), _stream(dev)), "decode")
     return out
 
 
@@ -630,7 +686,7 @@ def quantize_fs(t: torch.Tensor, fmt, scale: torch.Tensor | None, block, out: to
 
 
 def encode_fs(t: torch.Tensor, fmt, scale: torch.Tensor | None, block, axis="rows", specials_capacity: int = 4096,
-              out: torch.Tensor | None = None) -> Packed:
+              out: torch.Tensor | None = None, strict: bool = True) -> Packed:
     """Encode with float-scaling metadata (reading D23); Packed.scale holds it."""
     _require_cuda(t)
     x, y = parse_format(fmt)
@@ -651,7 +707,8 @@ def encode_fs(t: torch.Tensor, fmt, scale: torch.Tensor | None, block, axis="row
     _check(_lib.exmy_encode_fs(_ptr(t), _dtype_code(t.dtype), R, C, ax, br, bc, x, y, _ptr(scale), _ptr(out),
                                _ptr(spi), _ptr(spb), _ptr(spc), cap, _stream(dev)), "encode_fs")
     meta = torch.full((1,), 127, dtype=torch.uint8, device=dev)
-    return Packed(out, meta, spi, spb, spc, tuple(t.shape), x, y, ax, t.dtype, (br, bc), None, scale)
+    return _finish(Packed(out, meta, spi, spb, spc, tuple(t.shape), x, y, ax, t.dtype, (br, bc), None, scale,
+                          sp_capacity=cap, scheme=2), strict)
 
 
 # ------------------------------------------------------- host-buffer path
@@ -830,7 +887,7 @@ class GroupCodec:
                 meta, block = self.meta[o:o + 1], None
             res.append(Packed(self.packed[i], meta, self.spi[i], self.spb[i], self.spc[i:i + 1],
                               tuple(t.shape), self.x, self.y, ROWS, self.dtype, block,
-                              lay if t.dim() == 1 else None))
+                              lay if t.dim() == 1 else None, sp_capacity=self.cap))
         return res
 
     def decode(self) -> list:
@@ -881,7 +938,7 @@ def save_checkpoint(path: str, tensors: dict) -> int:
         meta = p.meta.detach().cpu().contiguous()
         scale = p.scale.detach().cpu().contiguous() if p.scale is not None else None
         cnt = int(p.sp_count.item()) if p.sp_count is not None else 0
-        cnt = min(cnt, p.sp_index.numel()) if cnt else 0
+        cnt = min(cnt, p.capacity) if cnt else 0
         spi = p.sp_index[:cnt].detach().cpu().contiguous() if cnt else None
         spb = p.sp_bits[:cnt].detach().cpu().contiguous() if cnt else None
         nm = name.encode()
@@ -892,7 +949,7 @@ def save_checkpoint(path: str, tensors: dict) -> int:
         for d, v in enumerate(dims):
             e.dims[d] = int(v)
         e.x, e.y = p.x, p.y
-        e.scheme = 2 if p.scale is not None else 0
+        e.scheme = 2 if p.scale is not None else int(p.scheme)
         e.block_kind, e.block_p0, e.block_p1 = _block_kind(p)
         e.axis = p.axis
         e.src_dtype = _dtype_code(p.dtype)
@@ -985,4 +1042,5 @@ class Checkpoint:
         spc = torch.tensor([cnt], dtype=torch.int64)
         dt = torch.bfloat16 if e.src_dtype == BF16 else torch.float32
         return Packed(to(data), to(meta), to(spi), to(spb), to(spc), dims, int(e.x), int(e.y), int(e.axis), dt,
-                      block, None, to(scale.reshape(R // block[0], C // block[1])) if scale is not None else None)
+                      block, None, to(scale.reshape(R // block[0], C // block[1])) if scale is not None else None,
+                      sp_capacity=cnt, scheme=int(e.scheme))

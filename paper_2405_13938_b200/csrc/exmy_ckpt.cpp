@@ -4,7 +4,7 @@
 // manifest + per-tensor CRC32 + lazy byte-range reads with pread, so loading
 // one tensor touches only its own bytes.
 //
-//   header   "EXMY" | version u8 = 1 | entry_count u32
+//   header   "EXMY" | version u8 = 2 | entry_count u32
 //   entry    name_len u16 | name | rank u8 | dims u32 x rank | x u8 | y u8 |
 //            scheme u8 | block_kind u8 [+ L u32 | + r u32, c u32] | flags u8 |
 //            (offset u64, length u64) for: metadata, each segment (descending
@@ -13,8 +13,15 @@
 //            of one tensor contiguous, in that order)
 // flags: bit0 scale present, bit1 specials present, bit2 COLS packing
 // (extension: the packing axis), bit3 source dtype bf16 (extension).
-// Specials: count x (u64 index) then count x (u32 fp32 bits).  CRC32 (IEEE,
-// reflected 0xEDB88320) over the tensor's payload bytes in section order.
+// Specials: count x (u64 index, u32 fp32 bits) records, as SPEC's
+// "(u64 index, u32 bits) pairs" (version 2; version-1 files, which stored all
+// indices then all bits, are still read).  CRC32 (IEEE, reflected
+// 0xEDB88320) over the tensor's payload bytes in section order.
+//
+// The reader trusts nothing in the file: section ranges are checked without
+// wrap-around, segment lengths against prod(dims) * w / 8, metadata / scale
+// lengths against the block grid, specials indices against the element count;
+// allocation failures return E_CONTAINER instead of throwing across the C ABI.
 #include <fcntl.h>
 #include <sys/stat.h>
 #include <unistd.h>
@@ -61,6 +68,7 @@ struct Entry {
     int nseg = 0;
     Section meta, seg[4], scale, specials;
     uint32_t crc = 0;
+    uint64_t nel = 0;   // prod(dims) (reader)
 };
 
 int popcount_k(int k) {
@@ -135,6 +143,63 @@ void put_entry(std::vector<uint8_t> &b, const Entry &e) {
     put_le<uint32_t>(b, e.crc);
 }
 
+constexpr uint8_t kVersion = 2;
+
+// (u64 index, u32 bits) records of a tensor's specials list
+std::vector<uint8_t> specials_records(const exmy_ckpt_tensor &a) {
+    std::vector<uint8_t> sp;
+    sp.reserve((size_t)a.specials_count * 12u);
+    for (int64_t j = 0; j < a.specials_count; ++j) {
+        put_le<uint64_t>(sp, (uint64_t)a.sp_index[j]);
+        put_le<uint32_t>(sp, a.sp_bits[j]);
+    }
+    return sp;
+}
+
+// number of metadata blocks of an entry, or -1 if the block shape does not
+// tile the (R, C) view (R = prod(dims[:-1]), C = dims[-1])
+int64_t block_count(const Entry &e, uint64_t nel) {
+    const uint64_t C = e.rank ? e.dims[e.rank - 1] : 1;
+    const uint64_t R = C ? nel / C : 0;
+    switch (e.block_kind) {
+    case 0: return 1;
+    case 1: return (int64_t)R;
+    case 2: return (int64_t)C;
+    case 3:
+        if (e.bp0 == 0 || C % e.bp0) return -1;
+        return (int64_t)(R * (C / e.bp0));
+    case 4:
+        if (e.bp0 == 0 || e.bp1 == 0 || R % e.bp0 || C % e.bp1) return -1;
+        return (int64_t)((R / e.bp0) * (C / e.bp1));
+    default: return -1;
+    }
+}
+
+// structural checks of one manifest entry against its own shape
+bool entry_consistent(const Entry &e) {
+    if (e.x > 8 || 1 + e.x + e.y > 15 || e.scheme > 2 || e.block_kind > 4) return false;
+    uint64_t nel = 1;
+    for (int d = 0; d < e.rank; ++d)
+        if (__builtin_mul_overflow(nel, (uint64_t)e.dims[d], &nel)) return false;
+    if (nel % 8) return false;
+    const int k = 1 + e.x + e.y;
+    int si = 0;
+    for (int w = 8; w >= 1; w >>= 1)
+        if (k & w) {
+            if (e.seg[si].len != nel / 8 * (uint64_t)w) return false;
+            ++si;
+        }
+    const int64_t nb = block_count(e, nel);
+    if (nb < 0) return false;
+    if (e.scheme == 2) {   // float scaling: one fp32 per block, a fixed metadata byte
+        if (e.scale.len != 4u * (uint64_t)nb || e.meta.len > 1) return false;
+    } else if (e.meta.len != (uint64_t)nb || e.scale.len != 0) {
+        return false;
+    }
+    if (e.specials.len % 12 || e.specials.len / 12 > nel) return false;
+    return true;
+}
+
 struct Reader {
     const uint8_t *p, *end;
     bool ok = true;
@@ -155,6 +220,7 @@ struct Reader {
 
 struct exmy_ckpt {
     int fd = -1;
+    int version = 0;
     uint64_t file_size = 0;
     std::vector<Entry> entries;
     uint64_t bytes_read = 0;   // payload bytes read (lazy-read instrumentation)
@@ -223,14 +289,12 @@ int64_t exmy_ckpt_write(const char *path, const exmy_ckpt_tensor *t, int n) {
         uint32_t c = crc_update(0, static_cast<const uint8_t *>(a.meta), (size_t)a.meta_bytes);
         c = crc_update(c, static_cast<const uint8_t *>(a.packed), (size_t)a.packed_bytes);
         c = crc_update(c, static_cast<const uint8_t *>(a.scale), (size_t)a.scale_bytes);
-        std::vector<uint8_t> sp;
-        for (int64_t j = 0; j < a.specials_count; ++j) put_le<uint64_t>(sp, (uint64_t)a.sp_index[j]);
-        for (int64_t j = 0; j < a.specials_count; ++j) put_le<uint32_t>(sp, a.sp_bits[j]);
+        const std::vector<uint8_t> sp = specials_records(a);
         e.crc = crc_update(c, sp.data(), sp.size());
     }
     std::vector<uint8_t> head;
     put(head, "EXMY", 4);
-    put_le<uint8_t>(head, 1);
+    put_le<uint8_t>(head, kVersion);
     put_le<uint32_t>(head, (uint32_t)n);
     for (auto &e : es) put_entry(head, e);
     const int fd = open(path, O_CREAT | O_TRUNC | O_WRONLY, 0644);
@@ -242,18 +306,14 @@ int64_t exmy_ckpt_write(const char *path, const exmy_ckpt_tensor *t, int n) {
         ok = ok && write_all(fd, a.meta, (size_t)e.meta.len, e.meta.off);
         ok = ok && write_all(fd, a.packed, (size_t)a.packed_bytes, e.seg[0].off);
         ok = ok && write_all(fd, a.scale, (size_t)e.scale.len, e.scale.off);
-        std::vector<uint8_t> sp;
-        for (int64_t j = 0; j < a.specials_count; ++j) put_le<uint64_t>(sp, (uint64_t)a.sp_index[j]);
-        for (int64_t j = 0; j < a.specials_count; ++j) put_le<uint32_t>(sp, a.sp_bits[j]);
+        const std::vector<uint8_t> sp = specials_records(a);
         ok = ok && write_all(fd, sp.data(), sp.size(), e.specials.off);
     }
     if (close(fd) != 0) ok = false;
     return ok ? (int64_t)off : -(int64_t)EXMY_E_IO;
 }
 
-exmy_status exmy_ckpt_open(const char *path, exmy_ckpt **out) {
-    if (!path || !out) return EXMY_E_ARG;
-    *out = nullptr;
+static exmy_status ckpt_open_impl(const char *path, exmy_ckpt **out) {
     const int fd = open(path, O_RDONLY);
     if (fd < 0) return EXMY_E_IO;
     struct stat st;
@@ -264,16 +324,18 @@ exmy_status exmy_ckpt_open(const char *path, exmy_ckpt **out) {
     auto *h = new exmy_ckpt;
     h->fd = fd;
     h->file_size = (uint64_t)st.st_size;
+    auto fail = [&](exmy_status s) {
+        exmy_ckpt_close(h);
+        return s;
+    };
     uint8_t hd[9];
-    if (!read_all(fd, hd, 9, 0)) {
-        exmy_ckpt_close(h);
-        return EXMY_E_CONTAINER;
-    }
-    if (std::memcmp(hd, "EXMY", 4) != 0 || hd[4] != 1) {
-        exmy_ckpt_close(h);
-        return EXMY_E_CONTAINER;
-    }
+    if (!read_all(fd, hd, 9, 0)) return fail(EXMY_E_CONTAINER);
+    if (std::memcmp(hd, "EXMY", 4) != 0 || hd[4] < 1 || hd[4] > kVersion) return fail(EXMY_E_CONTAINER);
+    h->version = hd[4];
     const uint32_t n = (uint32_t)hd[5] | ((uint32_t)hd[6] << 8) | ((uint32_t)hd[7] << 16) | ((uint32_t)hd[8] << 24);
+    // every entry takes at least 2+1+4+1+16*3+4 manifest bytes: a count the
+    // file cannot hold is a malformed container, not an allocation to try
+    if ((uint64_t)n * 60u > h->file_size) return fail(EXMY_E_CONTAINER);
     // the manifest lies before the first payload byte; read it in growing chunks
     std::vector<uint8_t> man;
     uint64_t want = 4096;
@@ -281,10 +343,7 @@ exmy_status exmy_ckpt_open(const char *path, exmy_ckpt **out) {
         const uint64_t avail = h->file_size > 9 ? h->file_size - 9 : 0;
         const uint64_t len = want < avail ? want : avail;
         man.resize((size_t)len);
-        if (len && !read_all(fd, man.data(), (size_t)len, 9)) {
-            exmy_ckpt_close(h);
-            return EXMY_E_IO;
-        }
+        if (len && !read_all(fd, man.data(), (size_t)len, 9)) return fail(EXMY_E_IO);
         Reader r{man.data(), man.data() + man.size()};
         h->entries.clear();
         for (uint32_t i = 0; i < n && r.ok; ++i) {
@@ -297,10 +356,7 @@ exmy_status exmy_ckpt_open(const char *path, exmy_ckpt **out) {
             e.name.assign(reinterpret_cast<const char *>(r.p), nl);
             r.p += nl;
             e.rank = r.get<uint8_t>();
-            if (e.rank > 8) {
-                exmy_ckpt_close(h);
-                return EXMY_E_CONTAINER;
-            }
+            if (e.rank > 8) return fail(EXMY_E_CONTAINER);
             for (int d = 0; d < e.rank; ++d) e.dims[d] = r.get<uint32_t>();
             e.x = r.get<uint8_t>();
             e.y = r.get<uint8_t>();
@@ -314,10 +370,7 @@ exmy_status exmy_ckpt_open(const char *path, exmy_ckpt **out) {
             const uint8_t flags = r.get<uint8_t>();
             e.axis = (flags >> 2) & 1;
             e.bf16 = (flags >> 3) & 1;
-            if (e.x > 8 || 1 + e.x + e.y > 15) {
-                exmy_ckpt_close(h);
-                return EXMY_E_CONTAINER;
-            }
+            if (e.x > 8 || 1 + e.x + e.y > 15) return fail(EXMY_E_CONTAINER);
             e.nseg = popcount_k(1 + e.x + e.y);
             auto sec = [&](Section &s) {
                 s.off = r.get<uint64_t>();
@@ -331,14 +384,15 @@ exmy_status exmy_ckpt_open(const char *path, exmy_ckpt **out) {
             h->entries.push_back(e);
         }
         if (r.ok) break;
-        if (len == avail) {   // truncated manifest
-            exmy_ckpt_close(h);
-            return EXMY_E_CONTAINER;
-        }
+        if (len == avail) return fail(EXMY_E_CONTAINER);   // truncated manifest
         want *= 4;
     }
-    // sections inside the file, contiguous per tensor, non-overlapping
     for (auto &e : h->entries) {
+        // shape, segment, metadata and specials sizes consistent with the entry
+        if (!entry_consistent(e)) return fail(EXMY_E_CONTAINER);
+        e.nel = 1;
+        for (int d = 0; d < e.rank; ++d) e.nel *= e.dims[d];
+        // sections inside the file (no wrap-around), contiguous per tensor
         uint64_t pos = e.meta.off;
         Section *ss[7] = {&e.meta, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
         int ns = 1;
@@ -346,15 +400,23 @@ exmy_status exmy_ckpt_open(const char *path, exmy_ckpt **out) {
         ss[ns++] = &e.scale;
         ss[ns++] = &e.specials;
         for (int s = 0; s < ns; ++s) {
-            if (ss[s]->off != pos || ss[s]->off + ss[s]->len > h->file_size) {
-                exmy_ckpt_close(h);
-                return EXMY_E_CONTAINER;
-            }
-            pos += ss[s]->len;
+            const Section &q = *ss[s];
+            if (q.off != pos || q.len > h->file_size || q.off > h->file_size - q.len) return fail(EXMY_E_CONTAINER);
+            pos += q.len;
         }
     }
     *out = h;
     return EXMY_OK;
+}
+
+exmy_status exmy_ckpt_open(const char *path, exmy_ckpt **out) {
+    if (!path || !out) return EXMY_E_ARG;
+    *out = nullptr;
+    try {
+        return ckpt_open_impl(path, out);
+    } catch (...) {   // std::bad_alloc and friends never cross the C ABI
+        return EXMY_E_CONTAINER;
+    }
 }
 
 int exmy_ckpt_count(const exmy_ckpt *h) { return h ? (int)h->entries.size() : -1; }
@@ -390,9 +452,8 @@ int exmy_ckpt_find(const exmy_ckpt *h, const char *name) {
     return -1;
 }
 
-exmy_status exmy_ckpt_read(exmy_ckpt *h, int i, void *meta, void *packed, void *scale, int64_t *sp_index,
-                           uint32_t *sp_bits) {
-    if (!h || i < 0 || i >= (int)h->entries.size()) return EXMY_E_ARG;
+static exmy_status ckpt_read_impl(exmy_ckpt *h, int i, void *meta, void *packed, void *scale, int64_t *sp_index,
+                                  uint32_t *sp_bits) {
     const Entry &e = h->entries[(size_t)i];
     uint64_t pk = 0;
     for (int s = 0; s < e.nseg; ++s) pk += e.seg[s].len;
@@ -406,10 +467,14 @@ exmy_status exmy_ckpt_read(exmy_ckpt *h, int i, void *meta, void *packed, void *
         if (!read_all(h->fd, sp.data(), sp.size(), e.specials.off)) return EXMY_E_IO;
         h->bytes_read += e.specials.len;
         for (int64_t j = 0; j < cnt; ++j) {
+            // version 2: (u64, u32) records; version 1: all indices, then all bits
+            const size_t io = h->version >= 2 ? (size_t)(12 * j) : (size_t)(8 * j);
+            const size_t bo = h->version >= 2 ? (size_t)(12 * j + 8) : (size_t)(8 * cnt + 4 * j);
             uint64_t v = 0;
-            for (int b = 0; b < 8; ++b) v |= (uint64_t)sp[(size_t)(8 * j + b)] << (8 * b);
+            for (int b = 0; b < 8; ++b) v |= (uint64_t)sp[io + (size_t)b] << (8 * b);
             uint32_t u = 0;
-            for (int b = 0; b < 4; ++b) u |= (uint32_t)sp[(size_t)(8 * cnt + 4 * j + b)] << (8 * b);
+            for (int b = 0; b < 4; ++b) u |= (uint32_t)sp[bo + (size_t)b] << (8 * b);
+            if (v >= e.nel) return EXMY_E_CONTAINER;   // an index outside the tensor
             if (sp_index) sp_index[j] = (int64_t)v;
             if (sp_bits) sp_bits[j] = u;
         }
@@ -417,12 +482,27 @@ exmy_status exmy_ckpt_read(exmy_ckpt *h, int i, void *meta, void *packed, void *
     return EXMY_OK;
 }
 
+exmy_status exmy_ckpt_read(exmy_ckpt *h, int i, void *meta, void *packed, void *scale, int64_t *sp_index,
+                           uint32_t *sp_bits) {
+    if (!h || i < 0 || i >= (int)h->entries.size()) return EXMY_E_ARG;
+    try {
+        return ckpt_read_impl(h, i, meta, packed, scale, sp_index, sp_bits);
+    } catch (...) {
+        return EXMY_E_CONTAINER;
+    }
+}
+
 exmy_status exmy_ckpt_verify(exmy_ckpt *h, int i) {
     if (!h || i < 0 || i >= (int)h->entries.size()) return EXMY_E_ARG;
     crc_init();
     const Entry &e = h->entries[(size_t)i];
     const uint64_t len = e.specials.off + e.specials.len - e.meta.off;
-    std::vector<uint8_t> buf(1u << 20);
+    std::vector<uint8_t> buf;
+    try {
+        buf.resize(1u << 20);
+    } catch (...) {
+        return EXMY_E_CONTAINER;
+    }
     uint32_t c = 0;
     for (uint64_t done = 0; done < len;) {
         const size_t n = (size_t)((len - done) < buf.size() ? (len - done) : buf.size());

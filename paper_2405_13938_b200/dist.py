@@ -91,12 +91,56 @@ def sharded_encode(shard: torch.Tensor, fmt, axis="rows", group=None, codec=None
     hist = codec.histogram(shard)
     allreduce_histogram(hist, group)
     meta = codec.emax(hist)
-    return codec.encode(shard, fmt, meta, axis=axis), meta
+    return codec.encode(shard, fmt, meta, axis=axis, strict=False), meta
 
 
-def sharded_roundtrip(shard: torch.Tensor, fmt, axis="rows", group=None, codec=None, gather=True):
-    """Encode own shard -> all-gather packed shards -> decode every shard.
-    Returns (global packed bytes in single-GPU layout, decoded full tensor)."""
+def _allgather_stack(t: torch.Tensor, group=None) -> torch.Tensor:
+    """[G, *t.shape] of every rank's equal-shape tensor (rank order)."""
+    G = dist.get_world_size(group)
+    t = t.contiguous()
+    if dist.get_backend(group) == "gloo":
+        parts = [torch.empty_like(t, device="cpu") for _ in range(G)]
+        dist.all_gather(parts, t.cpu(), group=group)
+        return torch.stack(parts).to(t.device)
+    out = torch.empty((G,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+    dist.all_gather_into_tensor(out, t, group=group)
+    return out
+
+
+def allgather_specials(p, group=None):
+    """Every rank's out-of-band NaN/Inf list (D9): (index[G, cap],
+    bits[G, cap], count[G]) with shard-local indices, and the capacity.
+    Raises E_CAPACITY (synchronising) if any rank overflowed its list, so no
+    NaN/Inf is ever dropped silently."""
+    cap = int(p.capacity)
+    n = max(cap, 1)
+    idx = _allgather_stack(p.sp_index[:n], group)
+    bits = _allgather_stack(p.sp_bits[:n], group)
+    cnt = _allgather_stack(p.sp_count.reshape(1).to(torch.int64), group).reshape(-1)
+    worst = int(cnt.max())
+    if worst > cap:
+        import paper_2405_13938_b200 as exmy
+        raise exmy.ExmyError(6, f"sharded encode: a shard holds {worst} NaN/Inf but the specials capacity is {cap}")
+    return idx, bits, cnt, cap
+
+
+def global_specials(idx, bits, cnt, elems_per_rank: int):
+    """Concatenate the per-rank lists into the single-GPU list: indices offset
+    by r * elems_per_rank (row-major shards), ascending."""
+    gi, gb = [], []
+    for r in range(idx.shape[0]):
+        c = int(cnt[r])
+        gi.append(idx[r, :c] + r * elems_per_rank)
+        gb.append(bits[r, :c])
+    return torch.cat(gi), torch.cat(gb)
+
+
+def sharded_roundtrip(shard: torch.Tensor, fmt, axis="rows", group=None, codec=None, gather=True,
+                      return_specials=False):
+    """Encode own shard -> all-gather packed shards and specials lists ->
+    decode every shard with its own specials (NaN/Inf restored, D9).
+    Returns (global packed bytes in single-GPU layout, decoded full tensor)
+    [, (global specials index, bits)]."""
     codec = codec or _default_codec()
     G = dist.get_world_size(group)
     p, meta = sharded_encode(shard, fmt, axis, group, codec)
@@ -104,13 +148,18 @@ def sharded_roundtrip(shard: torch.Tensor, fmt, axis="rows", group=None, codec=N
     nb = p.data.numel()
     out = torch.empty(G * nb, dtype=torch.uint8, device=p.data.device)
     allgather_bytes(p.data, out, group)
+    sidx, sbits, scnt, cap = allgather_specials(p, group)
     k = 1 + p.x + p.y
     glob = to_global_layout(out, G, R_local, C, k, codec)
-    if not gather:
-        return glob, None
-    dec = [codec.decode_raw(out[r * nb:(r + 1) * nb], R_local, C, (p.x, p.y), meta, axis=axis, dtype=shard.dtype)
-           for r in range(G)]
-    return glob, torch.cat(dec, 0)
+    dec = None
+    if gather:
+        dec = torch.cat([codec.decode_raw(out[r * nb:(r + 1) * nb], R_local, C, (p.x, p.y), meta, axis=axis,
+                                          dtype=shard.dtype,
+                                          specials=(sidx[r], sbits[r], scnt[r:r + 1], cap))
+                         for r in range(G)], 0)
+    if return_specials:
+        return glob, dec, global_specials(sidx, sbits, scnt, R_local * C)
+    return glob, dec
 
 
 # --------------------------------------------- fused encode + all-gather (push)

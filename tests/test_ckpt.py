@@ -94,7 +94,7 @@ def test_crc_is_zlib_crc32(exmy, orc, tmp_path):
     payload = p.meta.numpy().tobytes() + p.data.numpy().tobytes()
     crc = struct.unpack("<I", raw[len(raw) - len(payload) - 4:len(raw) - len(payload)])[0]
     assert crc == zlib.crc32(payload)
-    assert raw[:4] == b"EXMY" and raw[4] == 1 and struct.unpack("<I", raw[5:9])[0] == 1
+    assert raw[:4] == b"EXMY" and raw[4] == 2 and struct.unpack("<I", raw[5:9])[0] == 1
 
 
 def test_file_size_is_perfect_compression(exmy, orc, tmp_path):
@@ -122,7 +122,7 @@ def test_empty_and_malformed(exmy, tmp_path):
     with pytest.raises(exmy.ExmyError) as ei:
         exmy.Checkpoint(bad)
     assert ei.value.status == 10
-    open(bad, "wb").write(b"EXMY\x02\x00\x00\x00\x00")     # version 2
+    open(bad, "wb").write(b"EXMY\x03\x00\x00\x00\x00")     # version 3 (unknown)
     with pytest.raises(exmy.ExmyError):
         exmy.Checkpoint(bad)
     open(bad, "wb").write(b"EXMY\x01\x05\x00\x00\x00abc")  # 5 entries, truncated manifest
@@ -153,3 +153,127 @@ def test_gpu_decode_of_loaded(exmy, orc, tmp_path):
             assert torch.equal(q.data, p.data), name
             assert torch.equal(exmy.decode(q).reshape(-1), exmy.decode(p).reshape(-1)), name
             assert ck.verify(name)
+
+
+def _one_tensor_file(exmy, orc, tmp_path, specials=True):
+    path = str(tmp_path / "v.exmy")
+    p, _ = packed_from_oracle(exmy, orc, (32, 48), "e4m4", 3, dt="f32", specials=specials)
+    exmy.save_checkpoint(path, {"w": p})
+    return path, p
+
+
+def _manifest_fields(raw):
+    """offsets of the single entry's fields: (name 'w', rank 2, e4m4: k = 9 ->
+    segments w8, w1) -> dict of byte positions"""
+    pos = 9 + 2 + 1 + 1 + 8 + 4 + 1            # header, name_len, name, rank, dims, x y scheme kind, flags
+    secs = {}
+    for name in ("meta", "seg8", "seg1", "scale", "specials"):
+        secs[name] = pos
+        pos += 16
+    return secs
+
+
+def test_specials_are_interleaved_records(exmy, orc, tmp_path):
+    """version 2 stores (u64 index, u32 bits) pairs, as SPEC's container says"""
+    path, p = _one_tensor_file(exmy, orc, tmp_path)
+    raw = open(path, "rb").read()
+    f = _manifest_fields(raw)
+    off, ln = struct.unpack("<QQ", raw[f["specials"]:f["specials"] + 16])
+    assert ln == 24
+    recs = [struct.unpack("<QI", raw[off + 12 * j: off + 12 * j + 12]) for j in range(2)]
+    idx, bits, cnt = p.specials()
+    assert recs == [(int(idx[j]), int(bits[j]) & 0xFFFFFFFF) for j in range(cnt)]
+
+
+def test_version1_layout_still_reads(exmy, orc, tmp_path):
+    """a version-1 file (indices then bits) loads to the same specials"""
+    path, p = _one_tensor_file(exmy, orc, tmp_path)
+    raw = bytearray(open(path, "rb").read())
+    f = _manifest_fields(raw)
+    off, ln = struct.unpack("<QQ", raw[f["specials"]:f["specials"] + 16])
+    recs = [struct.unpack("<QI", raw[off + 12 * j: off + 12 * j + 12]) for j in range(ln // 12)]
+    v1 = b"".join(struct.pack("<Q", i) for i, _ in recs) + b"".join(struct.pack("<I", b) for _, b in recs)
+    raw[off:off + ln] = v1
+    raw[4] = 1
+    open(path, "wb").write(bytes(raw))
+    with exmy.Checkpoint(path) as ck:
+        q = ck.load("w", device="cpu")
+    a, b, c = q.specials()
+    a0, b0, c0 = p.specials()
+    assert c == c0 and torch.equal(a, a0) and torch.equal(b, b0)
+
+
+@pytest.mark.parametrize("field,value", [
+    ("seg8", "len+8"),            # segment length != prod(dims) * w / 8
+    ("meta", "len+1"),            # metadata length != block count
+    ("specials", "len+5"),        # not a whole number of 12-byte records
+    ("specials", "wrap"),         # offset + length wraps around 2^64
+    ("seg1", "off-1"),            # sections not contiguous
+])
+def test_malformed_manifest_rejected(exmy, orc, tmp_path, field, value):
+    path, _ = _one_tensor_file(exmy, orc, tmp_path)
+    raw = bytearray(open(path, "rb").read())
+    at = _manifest_fields(raw)[field]
+    off, ln = struct.unpack("<QQ", raw[at:at + 16])
+    if value == "len+8":
+        ln += 8
+    elif value == "len+1":
+        ln += 1
+    elif value == "len+5":
+        ln += 5
+    elif value == "wrap":
+        off, ln = 2 ** 64 - 8, 16
+    elif value == "off-1":
+        off -= 1
+    raw[at:at + 16] = struct.pack("<QQ", off, ln)
+    open(path, "wb").write(bytes(raw))
+    with pytest.raises(exmy.ExmyError) as ei:
+        exmy.Checkpoint(path)
+    assert ei.value.status == 10
+
+
+def test_specials_index_out_of_range_rejected(exmy, orc, tmp_path):
+    """a crafted index past the tensor would make the GPU scatter write out of
+    bounds: the reader refuses it"""
+    path, _ = _one_tensor_file(exmy, orc, tmp_path)
+    raw = bytearray(open(path, "rb").read())
+    at = _manifest_fields(raw)["specials"]
+    off, ln = struct.unpack("<QQ", raw[at:at + 16])
+    raw[off:off + 8] = struct.pack("<Q", 32 * 48)     # == numel: one past the end
+    open(path, "wb").write(bytes(raw))
+    with exmy.Checkpoint(path) as ck:                  # the manifest is fine ...
+        with pytest.raises(exmy.ExmyError) as ei:      # ... the read is not
+            ck.load("w", device="cpu")
+        assert ei.value.status == 10
+        assert not ck.verify("w")                     # and the CRC disagrees too
+
+
+def test_huge_entry_count_rejected(exmy, tmp_path):
+    """an entry count the file cannot hold is E_CONTAINER, not an allocation"""
+    bad = str(tmp_path / "n.exmy")
+    open(bad, "wb").write(b"EXMY\x02\xff\xff\xff\xff" + bytes(64))
+    with pytest.raises(exmy.ExmyError) as ei:
+        exmy.Checkpoint(bad)
+    assert ei.value.status == 10
+
+
+def test_scheme_is_recorded(exmy, orc, tmp_path):
+    """the block scheme (max-before 0 / max-after 1) travels with the tensor"""
+    path = str(tmp_path / "s.exmy")
+    p, _ = packed_from_oracle(exmy, orc, (16, 32), "e2m1", 6, per_row=True)
+    p.scheme = 1
+    exmy.save_checkpoint(path, {"t": p})
+    with exmy.Checkpoint(path) as ck:
+        assert ck.info("t").scheme == 1
+        assert ck.load("t", device="cpu").scheme == 1
+
+
+def test_capacity_zero_packed_writes_no_specials(exmy, orc, tmp_path):
+    """a Packed whose encode had capacity 0 but counted NaN/Inf stores no
+    (garbage) specials records"""
+    path = str(tmp_path / "z.exmy")
+    p, _ = packed_from_oracle(exmy, orc, (32, 48), "e4m4", 3, dt="f32", specials=True)
+    p.sp_capacity = 0
+    exmy.save_checkpoint(path, {"w": p})
+    with exmy.Checkpoint(path) as ck:
+        assert ck.info("w").specials_count == 0

@@ -35,19 +35,33 @@ class OracleCodec:
     def emax(self, hist):
         return torch.tensor([self.o.emax(hist.numpy().astype(np.uint64))], dtype=torch.uint8)
 
-    def encode(self, t, fmt, meta, axis="rows"):
+    CAP = 16
+
+    def encode(self, t, fmt, meta, axis="rows", strict=True):
         import workloads as W
         x, y = self.o.parse_format(fmt)
         bits = W.to_bits(t)
         ax = self.o.ROWS if axis == "rows" else self.o.COLS
-        packed, _, _, _ = self.o.encode(bits, (x, y), int(meta.item()), ax)
-        return types.SimpleNamespace(data=torch.from_numpy(packed), x=x, y=y)
+        packed, idx, sb, ns = self.o.encode(bits, (x, y), int(meta.item()), ax)
+        spi = torch.zeros(self.CAP, dtype=torch.int64)
+        spb = torch.zeros(self.CAP, dtype=torch.int32)
+        c = min(ns, self.CAP)
+        spi[:c] = torch.from_numpy(np.asarray(idx[:c], np.int64))
+        spb[:c] = torch.from_numpy(np.asarray(sb[:c]).astype(np.uint32).view(np.int32))
+        return types.SimpleNamespace(data=torch.from_numpy(packed), x=x, y=y, sp_index=spi, sp_bits=spb,
+                                     sp_count=torch.tensor([ns], dtype=torch.int64), capacity=self.CAP)
 
-    def decode_raw(self, data, rows, cols, fmt, meta, axis="rows", dtype=torch.bfloat16):
+    def decode_raw(self, data, rows, cols, fmt, meta, axis="rows", dtype=torch.bfloat16, specials=None):
         import workloads as W
         ax = self.o.ROWS if axis == "rows" else self.o.COLS
+        idx = sb = None
+        if specials is not None:
+            spi, spb, spc, cap = specials
+            c = min(int(spc.reshape(-1)[0]), cap)
+            idx = spi[:c].numpy().astype(np.int64)
+            sb = spb[:c].numpy().view(np.uint32)
         out = self.o.decode(data.numpy(), (rows, cols), fmt, int(meta.item()) if torch.is_tensor(meta) else meta,
-                            ax, out_dtype=np.uint16 if dtype == torch.bfloat16 else np.uint32)
+                            ax, idx, sb, out_dtype=np.uint16 if dtype == torch.bfloat16 else np.uint32)
         return W.from_bits(out)
 
 
@@ -87,6 +101,19 @@ def _free_port():
     return p
 
 
+def _specials_tensor():
+    """NaN/Inf in every quarter of the rows, so every rank (up to 4) carries a
+    list; specials don't disturb the byte layout and decode restores them"""
+    import workloads as W
+    full = W.bf16_weights((64, 48), seed=11, std=0.05)
+    flat = full.view(-1)
+    flat[5] = float("inf")
+    flat[48 * 20 + 3] = float("-inf")
+    flat[48 * 33] = float("nan")
+    flat[48 * 63 + 47] = float("nan")
+    return full
+
+
 def _worker(rank, ws, port, fmt, axis, results):
     import sys
     sys.path.insert(0, ROOT)
@@ -94,12 +121,13 @@ def _worker(rank, ws, port, fmt, axis, results):
     from paper_2405_13938_b200 import dist as xdist
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=ws)
     try:
-        full = W.bf16_weights((64, 48), seed=11, std=0.05)
-        full.view(-1)[5] = float("inf")  # specials don't disturb the byte layout
+        full = _specials_tensor()
         r0, r1 = xdist.shard_rows(64, ws, rank, axis == "rows")
         codec = OracleCodec()
-        glob, dec = xdist.sharded_roundtrip(full[r0:r1].contiguous(), fmt, axis=axis, codec=codec)
-        results[rank] = (glob.numpy().tobytes(), W.to_bits(dec).tobytes())
+        glob, dec, (gi, gb) = xdist.sharded_roundtrip(full[r0:r1].contiguous(), fmt, axis=axis, codec=codec,
+                                                      return_specials=True)
+        results[rank] = (glob.numpy().tobytes(), W.to_bits(dec).tobytes(), gi.numpy().tolist(),
+                         gb.numpy().view(np.uint32).tolist())
     finally:
         dist.destroy_process_group()
 
@@ -118,18 +146,17 @@ def test_sharded_roundtrip_gloo(orc, ws, fmt, axis):
     for p in procs:
         p.join(120)
         assert p.exitcode == 0
-    full = W.bf16_weights((64, 48), seed=11, std=0.05)
-    full.view(-1)[5] = float("inf")
-    bits = W.to_bits(full)
+    bits = W.to_bits(_specials_tensor())
     e = orc.emax(orc.histogram(bits))
     ax = orc.ROWS if axis == "rows" else orc.COLS
-    ref_packed = orc.encode(bits, fmt, e, ax)[0]
-    q = orc.quantize(bits, fmt, e)
-    q.reshape(-1)[5] = 0  # decode_raw carries no specials list: code 0 -> +0
+    ref_packed, ref_idx, ref_bits, ref_n = orc.encode(bits, fmt, e, ax)
+    assert ref_n == 4
+    q = orc.quantize(bits, fmt, e)     # NaN/Inf pass through quantize; decode restores them from the lists
     for r in range(ws):
-        glob, dec = results[r]
+        glob, dec, gi, gb = results[r]
         assert np.frombuffer(glob, np.uint8).tolist() == ref_packed.tolist()
         np.testing.assert_array_equal(np.frombuffer(dec, np.uint16).reshape(64, 48), q)
+        assert gi == list(ref_idx) and gb == [int(b) for b in ref_bits]
 
 
 def test_shard_rows_validation():

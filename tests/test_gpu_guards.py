@@ -115,3 +115,55 @@ def test_roofline_probe_runs_and_validates(exmy):
         exmy.roofline_probe(src[:1000], 16)          # input not a multiple of 16 KB
     with pytest.raises(exmy.ExmyError):
         exmy.roofline_probe(src, 17)                 # output not a multiple of 16 B
+
+
+def test_capacity_zero_specials_never_scatter(exmy):
+    """ADVICE r1 (high): an encode with specials capacity 0 still counts NaN/Inf;
+    the decode must scatter min(count, capacity) = 0 entries (no write through
+    an unwritten index), and strict encodes refuse the overflow."""
+    t = W.bf16_weights((64, 256), seed=3, device=DEV)
+    t.view(-1)[[7, 300, 5000]] = torch.tensor([float("nan"), float("inf"), float("-inf")], dtype=torch.bfloat16,
+                                               device=DEV)
+    p = exmy.encode(t, "e3m3", specials_capacity=0, strict=False)
+    assert int(p.sp_count.item()) == 3 and p.capacity == 0
+    p.sp_index.fill_(1 << 40)      # garbage an unguarded scatter would write through
+    g = Guarded(t.shape, torch.bfloat16)
+    exmy.decode(p, out=g.t)
+    assert g.intact()
+    ref = exmy.decode(exmy.encode(t, "e3m3", p.meta))          # with the lists
+    keep = torch.ones(t.numel(), dtype=torch.bool, device=DEV)
+    keep[[7, 300, 5000]] = False
+    assert torch.equal(g.t.reshape(-1)[keep].view(torch.int16), ref.reshape(-1)[keep].view(torch.int16))
+    assert int(g.t.reshape(-1)[7].view(torch.int16)) == 0      # in-band code 0 -> +0
+    with pytest.raises(exmy.ExmyError) as ei:
+        exmy.encode(t, "e3m3", specials_capacity=2)
+    assert ei.value.status == 6
+    q = exmy.encode(t, "e3m3", specials_capacity=3)            # exactly enough
+    idx, bits, cnt = q.specials()
+    assert cnt == 3 and idx.tolist() == [7, 300, 5000]
+
+
+def test_group_codec_default_capacity_zero(exmy):
+    """GroupCodec's default capacity 0 with NaN in a member: decode stays in bounds"""
+    a = W.bf16_weights((64, 128), seed=4, device=DEV)
+    a.view(-1)[11] = float("nan")
+    g = exmy.GroupCodec([a, W.bf16_weights((32, 64), seed=5, device=DEV)], "e2m4")
+    ps = g.encode()
+    assert ps[0].capacity == 0 and int(ps[0].sp_count.item()) == 1
+    outs = g.decode()
+    torch.cuda.synchronize()
+    d = exmy.decode(ps[0])
+    assert int(d.reshape(-1)[11].view(torch.int16)) == 0 and torch.equal(d, outs[0])
+
+
+def test_gather_index_validation(exmy):
+    t = W.f32_embedding(100, 128, seed=9).to(DEV)
+    p = exmy.encode(t, "e4m2", axis="cols")
+    with pytest.raises(IndexError):
+        exmy.decode_rows(p, torch.tensor([0, 100]))
+    with pytest.raises(IndexError):
+        exmy.decode_rows(p, torch.tensor([-1]))
+    with pytest.raises(IndexError):
+        exmy.embedding_bag(p, torch.tensor([3, 1000]), torch.tensor([0, 2]))
+    with pytest.raises(ValueError):
+        exmy.embedding_bag(p, torch.tensor([3, 4]), torch.tensor([0, 3]))
