@@ -76,6 +76,8 @@ def lib():
         L.oracle_fs_grid_top.argtypes = [i32, i32]
         L.oracle_fs_grid_top.restype = dbl
         L.oracle_block_float_scale.argtypes = [vp, i32, i64, i64, i64, i64, vp]
+        L.oracle_fs_factor.argtypes = [u32, i32, i32]
+        L.oracle_fs_factor.restype = u32
         L.oracle_fs_scale_in.argtypes = [u32, u32, i32, i32]
         L.oracle_fs_scale_in.restype = u32
         L.oracle_fs_scale_out.argtypes = [u32, u32, i32, i32]
@@ -316,6 +318,12 @@ def block_float_scale(bits: np.ndarray, block) -> np.ndarray:
     if lib().oracle_block_float_scale(_p(bits), _dtype_code(bits), rows, cols, br, bc, _p(amax)):
         raise ValueError("bad block shape")
     return amax.reshape(rows // br, cols // bc)
+
+
+def fs_factor(amax_bits: int, fmt) -> int:
+    """fp32 bits of the block's encode factor RN32(G / A1) (amax != 0)"""
+    x, y = parse_format(fmt)
+    return lib().oracle_fs_factor(amax_bits, x, y)
 
 
 def fs_scale_in(v_bits: int, amax_bits: int, fmt) -> int:

@@ -11,8 +11,9 @@
  * reading numbered Dn in DESIGN.md "Readings".  No blocking, no bit tricks:
  *
  *   quantize  = the grid point nearest to the exact input value, ties to the
- *               code whose LSB is 0, saturating at the largest magnitude
- *               (D5-D8).  Implemented as: enumerate all
+ *               code whose LSB is 0 (y = 0: to the even fp32 exponent),
+ *               saturating at the largest magnitude (
+ *               D5-D8).  Implemented as: enumerate all
  *               2^(k-1) magnitude codes, compute their exact values in fp64,
  *               sort them (qsort, a library primitive), binary-search the two
  *               neighbours of |v| and compare |v| with their exact midpoint.
@@ -127,7 +128,19 @@ static uint32_t grid_nearest(const grid *g, double a)
     double midpoint = (below->v + above->v) / 2.0;   /* exact, see header */
     if (a < midpoint) return below->mag;
     if (a > midpoint) return above->mag;
-    /* tie: the code with LSB 0 (D6) */
+    /* tie (D6): for y >= 1 the code whose LSB -- the mantissa LSB -- is 0
+     * (round-to-nearest-even).  For y = 0 there is no mantissa bit: the
+     * paper's Eigen RTNE extended to zero mantissa bits keeps the
+     * fp32 pattern whose last kept bit, the exponent LSB, is 0, i.e. the
+     * neighbour whose fp32 biased exponent is even (the same rule as D22's
+     * "after rounding" exponent).  Zero (exponent field 0) wins the tie with
+     * the smallest non-zero value (D8). */
+    if (g->y == 0) {
+        if (below->v == 0.0) return below->mag;
+        int e;
+        (void)frexp(below->v, &e);                       /* below = 2^(e-1) */
+        return ((e - 1 + 127) & 1) ? above->mag : below->mag;
+    }
     return (below->mag & 1u) ? above->mag : below->mag;
 }
 
@@ -623,18 +636,18 @@ int oracle_decode_blocked(const uint8_t *packed, int64_t rows, int64_t cols, int
  * Reading D23: every block stores one fp32 metadata value, its
  * largest finite magnitude amax, and uses e_max = 127, whose grid top is
  * G = the largest magnitude code's value at e_max 127.  The block is mapped
- * onto that grid by the factor G/amax and decoded with amax/G, so its maximum
- * lands on G and comes back as amax ("captures the largest value in the
- * block accurately").  Step by step, with amax = A1 * 2^p, A1 in [1, 2):
- *   encode  r  = RN32(G / A1)                      (exact quotient, rounded once)
- *           u  = RN32(v * r * 2^-p)                (exact product, rounded once)
- *           code = the e_max-127 code of u         (as oracle_encode)
- *   decode  g  = RN32(the code's value at e_max 127)   (the plain decode)
- *           s_hi = RN32(amax / G), s_lo = RN32((amax - s_hi G) / G)
- *           out = sign(g) * RN32(|g| s_hi + RN32(|g| s_lo))   (one FMA on the GPU;
- *           a zero result keeps the code's sign);
+ * onto that grid by the fp32 factor RN32(G/amax) and mapped back by amax/G,
+ * so its maximum lands on G and comes back as amax ("captures the largest
+ * value in the block accurately").  With amax = A1 * 2^p, A1 in [1, 2):
+ *   encode  r  = RN32(G / A1)                 (the fp32 scaling factor)
+ *           u  = RN32(v * r * 2^-p)           (exact product, rounded once)
+ *           code = the e_max-127 code of u    (as oracle_encode)
+ *   decode  out = RN32(g * amax / G)          (g = the code's exact value at
+ *           e_max 127; the exact product and quotient, rounded once, fp32
+ *           subnormals included; a zero result keeps the code's sign)
  *           bf16 output = RN16 of that fp32 value  (reading D24)
- * amax = 0 (no finite non-zero element): u = v * 0, codes are signed zeros. */
+ * amax = 0 (no finite non-zero element): u = v * 0, codes are signed zeros,
+ * and they decode to signed zeros. */
 
 double oracle_fs_grid_top(int x, int y)
 {
@@ -651,24 +664,31 @@ static void fs_split(uint32_t amax_bits, double *A1, int *p)
     *p = e - 1;
 }
 
-/* RN32 of the exact quotient n / d of two positive doubles holding at most
- * 25 significant bits each: long division of their integer significands. */
-static uint32_t rn32_div(double n, double d)
+/* The fp32 value nearest to the exact quotient num / den of two positive
+ * doubles (ties to the even pattern, fp32 subnormals included), where den has
+ * at most 26 significant bits.  No division result is trusted: starting from
+ * a guess, the answer is the fp32 t with
+ *     den * (t - ulp/2)  <=  num  <=  den * (t + ulp/2),
+ * checked with exact products -- every midpoint between neighbouring fp32
+ * values has at most 25 significant bits, so den * midpoint is an exact
+ * double (<= 51 bits) and each comparison below is exact. */
+static uint32_t rn32_quotient(double num, double den)
 {
-    int en, ed;
-    double fn = frexp(n, &en), fd = frexp(d, &ed);
-    uint64_t N = (uint64_t)ldexp(fn, 30), D = (uint64_t)ldexp(fd, 30);   /* exact integers < 2^30 */
-    /* n/d = (N/D) * 2^(en-ed); N/D in (1/2, 2) */
-    unsigned __int128 num = (unsigned __int128)N << 60;
-    uint64_t q = (uint64_t)(num / D), rem = (uint64_t)(num % D);
-    /* q has 60..61 significant bits; fold the remainder into a sticky bit and
-     * keep 52 bits so that the value is exact in a double */
-    int sh = 0;
-    while ((q >> sh) >= (1ull << 52)) ++sh;
-    uint64_t lost = q & ((1ull << sh) - 1ull);
-    uint64_t qs = (q >> sh) | ((lost | rem) ? 1ull : 0ull);
-    /* qs's last bit is a sticky bit 28+ bits below fp32's rounding position */
-    return oracle_round_f32(ldexp((double)qs, sh - 60 + en - ed));
+    uint32_t t = oracle_round_f32(num / den);         /* a guess: within one step */
+    for (;;) {
+        double vt = f32_value(t);
+        if (t < 0x7F7FFFFFu) {                        /* compare with the midpoint above */
+            double mid = (vt + f32_value(t + 1u)) / 2.0;
+            double dm = den * mid;
+            if (num > dm || (num == dm && (t & 1u))) { t += 1u; continue; }
+        }
+        if (t > 0u) {                                 /* and with the midpoint below */
+            double mid = (vt + f32_value(t - 1u)) / 2.0;
+            double dm = den * mid;
+            if (num < dm || (num == dm && (t & 1u))) { t -= 1u; continue; }
+        }
+        return t;
+    }
 }
 
 /* fp32 bits of the per-block float-scale metadata: the largest finite |v| */
@@ -687,6 +707,15 @@ int oracle_block_float_scale(const void *in, int dtype, int64_t rows, int64_t co
     return 0;
 }
 
+/* the fp32 encode factor RN32(G / A1) of a block (amax != 0) */
+uint32_t oracle_fs_factor(uint32_t amax, int x, int y)
+{
+    double A1;
+    int p;
+    fs_split(amax, &A1, &p);
+    return rn32_quotient(oracle_fs_grid_top(x, y), A1);   /* A1: <= 24 significant bits */
+}
+
 /* scaled fp32 value u of the finite element v (bits) under block max amax */
 uint32_t oracle_fs_scale_in(uint32_t v, uint32_t amax, int x, int y)
 {
@@ -694,61 +723,22 @@ uint32_t oracle_fs_scale_in(uint32_t v, uint32_t amax, int x, int y)
     double A1;
     int p;
     fs_split(amax, &A1, &p);
-    uint32_t r = rn32_div(oracle_fs_grid_top(x, y), A1);
+    uint32_t r = oracle_fs_factor(amax, x, y);
     double prod = f32_value(v) * f32_value(r);                  /* exact: 24 x 24 bits */
-    return oracle_round_f32(ldexp(prod, -p));
-}
-
-/* RN32 of the exact quotient n / G for any double n (sign kept, 0 -> +0) */
-static uint32_t rn32_div_signed(double n, double G)
-{
-    if (n == 0.0) return 0u;
-    uint32_t q = rn32_div(fabs(n), G);
-    return n < 0 ? (q | 0x80000000u) : q;
-}
-
-/* fp32 neighbour of the positive fp32 pattern t toward +inf (up) or 0 (down) */
-static double f32_step(uint32_t t, int up) { return f32_value(up ? t + 1u : t - 1u); }
-
-/* RN32 of the exact value S + e, where (S, e) is an exact two-double sum with
- * |e| <= ulp64(S)/2: RN32(S) unless S is exactly an fp32 midpoint, then e
- * decides the direction. */
-static uint32_t rn32_twosum(double S, double e)
-{
-    uint32_t sign = 0;
-    if (S < 0 || (S == 0 && e < 0)) { S = -S; e = -e; sign = 0x80000000u; }
-    uint32_t t = oracle_round_f32(S);                 /* positive pattern */
-    double vt = f32_value(t);
-    if (e != 0.0 && vt != S) {
-        double other = vt < S ? f32_step(t, 1) : f32_step(t, 0);
-        if ((vt + other) / 2.0 == S) {                 /* a tie in fp32: S+e lies off it */
-            double lo = vt < other ? vt : other, hi = vt < other ? other : vt;
-            t = oracle_round_f32(e > 0 ? hi : lo);
-        }
-    }
-    return t | sign;
+    return oracle_round_f32(ldexp(prod, -p));                   /* exact scaling, one rounding */
 }
 
 /* decoded fp32 bits of code under block max amax (reading D23):
- *   g    = RN32(value of the code at e_max 127)      (the plain decode)
- *   s_hi = RN32(amax / G), s_lo = RN32((amax - s_hi G) / G)
- *   out  = sign(g) RN32(|g| s_hi + RN32(|g| s_lo))    (one FMA on the GPU) */
+ * RN32(g * amax / G), g the exact value of the code at e_max 127 */
 uint32_t oracle_fs_scale_out(uint32_t code, uint32_t amax, int x, int y)
 {
-    uint32_t gb = oracle_round_f32(oracle_code_value(code, x, y, 127));
-    double g = fabs(f32_value(gb));                   /* |g|; the code's sign is attached last */
+    int k = 1 + x + y;
+    uint32_t sign = ((code >> (k - 1)) & 1u) << 31;
+    double g = fabs(oracle_code_value(code, x, y, 127));   /* exact, a normal fp64 */
     double a = f32_value(amax & 0x7FFFFFFFu);
-    double G = oracle_fs_grid_top(x, y);
-    uint32_t shi = (a == 0.0) ? 0u : rn32_div(a, G);
-    double s_hi = f32_value(shi);
-    double r = a - s_hi * G;                          /* exact: 24-bit x (y+1)-bit product */
-    double s_lo = f32_value(rn32_div_signed(r, G));
-    double t = f32_value(oracle_round_f32(g * s_lo)); /* exact product, one rounding */
-    double p = g * s_hi;                              /* exact */
-    volatile double S = p + t;                        /* TwoSum (Knuth): S + e == p + t exactly */
-    volatile double bp = S - p;
-    volatile double e = (p - (S - bp)) + (t - bp);
-    return rn32_twosum(S, e) | (gb & 0x80000000u);  /* s_hi + s_lo >= 0: result >= 0, then the sign */
+    if (g == 0.0 || a == 0.0) return sign;                 /* signed zero */
+    /* g * a is exact (<= 24 + 24 significant bits); G has <= 24 */
+    return rn32_quotient(g * a, oracle_fs_grid_top(x, y)) | sign;
 }
 
 static uint32_t fs_encode_code(const grid *g127, uint32_t u_in, uint32_t amax)

@@ -13,28 +13,6 @@
 
 #ifdef __cplusplus
 extern "C" {
-/* float scaling (reading D23) */
-double oracle_fs_grid_top(int x, int y);
-int oracle_block_float_scale(const void *in, int dtype, int64_t rows, int64_t cols,
-                             int64_t br, int64_t bc, uint32_t *amax);
-uint32_t oracle_fs_scale_in(uint32_t v, uint32_t amax, int x, int y);
-uint32_t oracle_fs_scale_out(uint32_t code, uint32_t amax, int x, int y);
-int oracle_quantize_fs(const void *in, void *out, int dtype, int64_t rows, int64_t cols,
-                       int64_t br, int64_t bc, int x, int y, const uint32_t *amax);
-int64_t oracle_encode_fs(const void *in, int dtype, int64_t rows, int64_t cols, int axis,
-                         int64_t br, int64_t bc, int x, int y, const uint32_t *amax, uint8_t *packed,
-                         int64_t *sp_index, uint32_t *sp_bits, int64_t sp_capacity);
-int oracle_decode_fs(const uint8_t *packed, int64_t rows, int64_t cols, int axis,
-                     int64_t br, int64_t bc, int x, int y, const uint32_t *amax,
-                     const int64_t *sp_index, const uint32_t *sp_bits, int64_t sp_count,
-                     void *out, int out_dtype);
-
-/* embedding bag over a COLS-packed table (reading D25) */
-int oracle_embedding_bag(const uint8_t *packed, int64_t rows, int64_t cols, int x, int y,
-                         const uint8_t *meta, int meta_per_row, const int64_t *indices,
-                         const int64_t *offsets, int64_t nbags, const float *weights, int mode,
-                         float *out);
-
 #endif
 int oracle_format_valid(int x, int y, int e_max);
 int oracle_bias(int x, int e_max);
@@ -72,51 +50,30 @@ int oracle_decode_blocked(const uint8_t *packed, int64_t rows, int64_t cols, int
                           int64_t br, int64_t bc, int x, int y, const uint8_t *meta,
                           const int64_t *sp_index, const uint32_t *sp_bits, int64_t sp_count,
                           void *out, int out_dtype);
+/* float scaling (reading D23) */
+double oracle_fs_grid_top(int x, int y);
+int oracle_block_float_scale(const void *in, int dtype, int64_t rows, int64_t cols,
+                             int64_t br, int64_t bc, uint32_t *amax);
+uint32_t oracle_fs_factor(uint32_t amax, int x, int y);
+uint32_t oracle_fs_scale_in(uint32_t v, uint32_t amax, int x, int y);
+uint32_t oracle_fs_scale_out(uint32_t code, uint32_t amax, int x, int y);
+int oracle_quantize_fs(const void *in, void *out, int dtype, int64_t rows, int64_t cols,
+                       int64_t br, int64_t bc, int x, int y, const uint32_t *amax);
+int64_t oracle_encode_fs(const void *in, int dtype, int64_t rows, int64_t cols, int axis,
+                         int64_t br, int64_t bc, int x, int y, const uint32_t *amax, uint8_t *packed,
+                         int64_t *sp_index, uint32_t *sp_bits, int64_t sp_capacity);
+int oracle_decode_fs(const uint8_t *packed, int64_t rows, int64_t cols, int axis,
+                     int64_t br, int64_t bc, int x, int y, const uint32_t *amax,
+                     const int64_t *sp_index, const uint32_t *sp_bits, int64_t sp_count,
+                     void *out, int out_dtype);
+
+/* embedding bag over a COLS-packed table (reading D25) */
+int oracle_embedding_bag(const uint8_t *packed, int64_t rows, int64_t cols, int x, int y,
+                         const uint8_t *meta, int meta_per_row, const int64_t *indices,
+                         const int64_t *offsets, int64_t nbags, const float *weights, int mode,
+                         float *out);
+
 #ifdef __cplusplus
 }
-/* float scaling (reading D23) */
-double oracle_fs_grid_top(int x, int y);
-int oracle_block_float_scale(const void *in, int dtype, int64_t rows, int64_t cols,
-                             int64_t br, int64_t bc, uint32_t *amax);
-uint32_t oracle_fs_scale_in(uint32_t v, uint32_t amax, int x, int y);
-uint32_t oracle_fs_scale_out(uint32_t code, uint32_t amax, int x, int y);
-int oracle_quantize_fs(const void *in, void *out, int dtype, int64_t rows, int64_t cols,
-                       int64_t br, int64_t bc, int x, int y, const uint32_t *amax);
-int64_t oracle_encode_fs(const void *in, int dtype, int64_t rows, int64_t cols, int axis,
-                         int64_t br, int64_t bc, int x, int y, const uint32_t *amax, uint8_t *packed,
-                         int64_t *sp_index, uint32_t *sp_bits, int64_t sp_capacity);
-int oracle_decode_fs(const uint8_t *packed, int64_t rows, int64_t cols, int axis,
-                     int64_t br, int64_t bc, int x, int y, const uint32_t *amax,
-                     const int64_t *sp_index, const uint32_t *sp_bits, int64_t sp_count,
-                     void *out, int out_dtype);
-
-/* embedding bag over a COLS-packed table (reading D25) */
-int oracle_embedding_bag(const uint8_t *packed, int64_t rows, int64_t cols, int x, int y,
-                         const uint8_t *meta, int meta_per_row, const int64_t *indices,
-                         const int64_t *offsets, int64_t nbags, const float *weights, int mode,
-                         float *out);
-
 #endif
-/* float scaling (reading D23) */
-double oracle_fs_grid_top(int x, int y);
-int oracle_block_float_scale(const void *in, int dtype, int64_t rows, int64_t cols,
-                             int64_t br, int64_t bc, uint32_t *amax);
-uint32_t oracle_fs_scale_in(uint32_t v, uint32_t amax, int x, int y);
-uint32_t oracle_fs_scale_out(uint32_t code, uint32_t amax, int x, int y);
-int oracle_quantize_fs(const void *in, void *out, int dtype, int64_t rows, int64_t cols,
-                       int64_t br, int64_t bc, int x, int y, const uint32_t *amax);
-int64_t oracle_encode_fs(const void *in, int dtype, int64_t rows, int64_t cols, int axis,
-                         int64_t br, int64_t bc, int x, int y, const uint32_t *amax, uint8_t *packed,
-                         int64_t *sp_index, uint32_t *sp_bits, int64_t sp_capacity);
-int oracle_decode_fs(const uint8_t *packed, int64_t rows, int64_t cols, int axis,
-                     int64_t br, int64_t bc, int x, int y, const uint32_t *amax,
-                     const int64_t *sp_index, const uint32_t *sp_bits, int64_t sp_count,
-                     void *out, int out_dtype);
-
-/* embedding bag over a COLS-packed table (reading D25) */
-int oracle_embedding_bag(const uint8_t *packed, int64_t rows, int64_t cols, int x, int y,
-                         const uint8_t *meta, int meta_per_row, const int64_t *indices,
-                         const int64_t *offsets, int64_t nbags, const float *weights, int mode,
-                         float *out);
-
 #endif

@@ -123,3 +123,41 @@ def test_block_shape_validation(orc):
     with pytest.raises(ValueError):
         orc.block_max_exponent(np.zeros((8, 8), np.uint32), (3, 8))
     assert orc.lib().oracle_block_shape_ok(8, 8, 8, 8) == 1
+
+
+@pytest.mark.parametrize("y", [0, 1, 2, 5])
+def test_after_rounding_exponent_fractions(orc, y):
+    """Reading D22 with Fractions, every y incl. y = 0: the 'after rounding'
+    exponent of a normal fp32 value a in [2^E, 2^(E+1)) is E, or E + 1 when a
+    rounds (RTNE with y mantissa bits) up to 2^(E+1); a tie goes to the
+    representation whose last kept bit is 0 -- the mantissa LSB for y >= 1,
+    the exponent LSB for y = 0 (the same rule as quantize's D6).  Every exact
+    tie and its fp32 neighbours are included; a second check uses the paper's
+    Eigen procedure on the bits (the exponent field of the rounded pattern)."""
+    from fractions import Fraction as F
+    rng = np.random.default_rng(70 + y)
+    E = rng.integers(1, 250, 3000)
+    mant = rng.integers(0, 1 << 23, 3000)
+    sh = 23 - y
+    mant[::3] = (mant[::3] & ~((1 << sh) - 1)) | (1 << (sh - 1))            # exact ties
+    mant[1::3] = (mant[1::3] & ~((1 << sh) - 1)) | ((1 << (sh - 1)) - 1)    # one ulp below a tie
+    mant[:40] = (1 << 23) - 1                                             # carries into the next binade
+    bits = ((E << 23) | mant).astype(np.uint32)
+    got = orc.block_max_exponent(bits.reshape(-1, 1), (1, 1), y=y, scheme=orc.SCHEME_MAX_AFTER).reshape(-1)
+    for b, g, e, m in zip(bits.tolist(), got.tolist(), E.tolist(), mant.tolist()):
+        frac = F(m, 1 << 23) * (1 << y)               # mantissa in units of the kept LSB
+        n, r = divmod(frac, 1)
+        n = int(n)
+        last_odd = (n & 1) if y >= 1 else (e & 1)     # the last kept bit: mantissa LSB / exponent LSB
+        up = r > F(1, 2) or (r == F(1, 2) and last_odd)
+        want = e + 1 if (up and n + 1 == 1 << y) else e
+        assert g == min(want, 254), (hex(b), g, want)
+    eig = eigen_round(bits, y)
+    np.testing.assert_array_equal(got, np.minimum((eig >> 23) & 0xFF, 254).astype(np.uint8))
+
+
+def eigen_round(u, y):
+    sh = 23 - y
+    u = u.astype(np.uint64)
+    r = u + ((1 << (sh - 1)) - 1) + ((u >> sh) & 1)
+    return (r & ~np.uint64((1 << sh) - 1)).astype(np.uint64)

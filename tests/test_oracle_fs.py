@@ -141,36 +141,134 @@ def test_scale_in_is_exact_rounding(orc, fmt):
             assert orc.fs_scale_in(vb, ab, fmt) == want
 
 
+def code_value_fr(code: int, x: int, y: int) -> Fraction:
+    """exact value of a k-bit code at e_max 127 (bias 2^x - 1, D1), written
+    from Table 1 / P:172-175 in Fractions (the oracle's grid is pinned to
+    ml_dtypes in test_oracle_pins)"""
+    k = 1 + x + y
+    s = -1 if (code >> (k - 1)) & 1 else 1
+    mag = code & ((1 << (k - 1)) - 1)
+    bias = (1 << x) - 1
+    e = 0 if x == 0 else mag >> y
+    m = mag & ((1 << y) - 1)
+    if e == 0:
+        return s * Fraction(m) * Fraction(2) ** (1 - bias - y)
+    return s * Fraction((1 << y) + m) * Fraction(2) ** (e - bias - y)
+
+
+def numpy_rn32(fr: Fraction) -> int:
+    """RN32 by numpy's float64 -> float32 conversion of RN64(fr).  Exact here:
+    for fr = g * amax / G the double rounding could only go wrong if RN64(fr)
+    landed on an fp32 midpoint while fr did not; fr's distance from any fp32
+    midpoint is either 0 or >= 2^-42 relative (normal results) / >= 2^-33 of
+    the value (subnormal results), both far above RN64's 2^-53."""
+    return int(np.array([float(fr)], np.float64).astype(np.float32).view(np.uint32)[0])
+
+
+def amax_sample(rng, fmt, n=48):
+    """random maxima over the whole fp32 range (subnormal ones included) plus
+    maxima whose significand is divisible by the odd part of G's (so that
+    g * amax / G is an exact binary fraction, possibly an fp32 midpoint) and
+    the extremes"""
+    x, y = fmt
+    MG = (2 << y) - 1 if x >= 1 else (1 << y) - 1
+    a = list((rng.random(n) * 2.0 ** rng.integers(-149, 128, n)).astype(np.float32).view(np.uint32))
+    for _ in range(n // 2):
+        q = int(rng.integers(1, (1 << 24) // max(MG, 1)))
+        sig = q * max(MG, 1)
+        if sig >= 1 << 24:
+            continue
+        e = int(rng.integers(-149, 104))
+        v = np.float32(np.ldexp(float(sig), e))
+        if np.isfinite(v) and v > 0:
+            a.append(int(np.array([v], np.float32).view(np.uint32)[0]))
+    a += [0x00000001, 0x007FFFFF, 0x00800000, 0x7F7FFFFF, 0x3F800000,
+          int(np.array([3.9], np.float32).view(np.uint32)[0])]
+    return [int(v) for v in a if v != 0]      # amax = 0 is its own case (test_zero_and_special_blocks)
+
+
 @pytest.mark.parametrize("fmt", FMTS, ids=lambda f: f"e{f[0]}m{f[1]}")
-def test_scale_out_is_correctly_rounded(orc, fmt):
-    """The decode RN32(g s_hi + RN32(g s_lo)), s_hi + s_lo ~ amax/G, equals the
-    correctly rounded exact value g * amax / G for normal fp32 results (its
-    relative error <= 2^-47 is below the distance >= 2^-42 of g*amax/G from a
-    rounding boundary, D23), whenever the grid value g is itself an
-    fp32 value (always for x <= 7)."""
+def test_scale_out_is_the_plain_definition(orc, fmt):
+    """Decode (reading D23) = RN32(g * amax / G) exactly, g the code's exact
+    value at e_max 127: for EVERY code (incl. e8m0 values below the fp32
+    range and fp32-subnormal results) under maxima spanning the fp32 range,
+    against (a) round-to-nearest-even of the exact Fraction, written here from
+    the IEEE definition, and (b) numpy's float32 conversion (see numpy_rn32).
+    Zero results keep the code's sign."""
     x, y = fmt
     k = 1 + x + y
-    rng = np.random.default_rng(k)
-    G = Fraction(orc.fs_grid_top(fmt))
-    amaxs = (rng.random(60) * 2.0 ** rng.integers(-60, 60, 60)).astype(np.float32)
-    amaxs[0] = 3.9
-    for a in amaxs:
-        ab = int(np.array([a], np.float32).view(np.uint32)[0])
-        for code in rng.integers(0, 1 << k, 24):
-            g = Fraction(orc.code_value(int(code), fmt, 127))
-            if g != Fraction(float(np.float32(float(g)))):
-                continue                       # e8m0 values below the fp32 range: g rounds first
-            exact = g * frac_of_f32(ab) / G
-            got = orc.fs_scale_out(int(code), ab, fmt)
-            if exact != 0 and abs(exact) < Fraction(2) ** -126:
-                continue                   # subnormal results: formula value, not claimed exact
-            want = rn32(exact) if exact != 0 else (0x80000000 if code >> (k - 1) else 0)   # signed zero code
-            assert got == want, (code, a)
-    # the top code returns amax itself
-    top = (1 << (k - 1)) - 1
-    for a in amaxs:
-        ab = int(np.array([a], np.float32).view(np.uint32)[0])
-        assert orc.fs_scale_out(top, ab, fmt) == ab
+    rng = np.random.default_rng(100 + k + 10 * x)
+    G = code_value_fr((1 << (k - 1)) - 1, x, y)
+    assert G == Fraction(orc.fs_grid_top(fmt))
+    for ab in amax_sample(rng, fmt):
+        A = frac_of_f32(ab)
+        for code in range(1 << k):
+            g = code_value_fr(code, x, y)
+            exact = g * A / G
+            got = orc.fs_scale_out(code, ab, fmt)
+            sign = 0x80000000 if (code >> (k - 1)) & 1 else 0
+            want = rn32(exact) if exact != 0 else sign
+            if want & 0x7FFFFFFF == 0:
+                want = sign                       # a zero result keeps the code's sign
+            assert got == want, (code, hex(ab))
+            assert (got & 0x7FFFFFFF) == (numpy_rn32(abs(exact)) if exact != 0 else 0), (code, hex(ab))
+        assert orc.fs_scale_out((1 << (k - 1)) - 1, ab, fmt) == ab        # the block max comes back
+
+
+@pytest.mark.parametrize("fmt", [(2, 3), (3, 3), (1, 5), (3, 5), (0, 6), (2, 1), (4, 3), (7, 1)],
+                         ids=lambda f: f"e{f[0]}m{f[1]}")
+def test_scale_out_ties_only_in_the_subnormal_range(orc, fmt):
+    """Where can g * amax / G sit exactly halfway between two fp32 values?
+    With g = M_g 2^a, amax = M_a 2^b, G = M_G 2^c (M_* odd-free integers,
+    M_g <= M_G, M_a < 2^24), an exact binary fraction needs M_G | M_g M_a and
+    then has the integer significand M_g M_a / M_G < 2^24: it is an fp32
+    value in the normal range, never a midpoint.  Ties therefore only occur
+    among fp32-subnormal results (quantum 2^-149): there the plain definition
+    sends them to the even pattern, as numpy's RTNE conversion of the (exactly
+    representable) double midpoint does.  (For x <= 1 every code shares G's
+    quantum, so even subnormal exact results are fp32 values: no ties.)"""
+    x, y = fmt
+    k = 1 + x + y
+    MG = (2 << y) - 1 if x >= 1 else (1 << y) - 1
+    G = code_value_fr((1 << (k - 1)) - 1, x, y)
+    rng = np.random.default_rng(7 * k + x)
+    ties = 0
+    for it in range(3000):
+        if it % 2:       # an fp32-subnormal maximum whose significand M_G divides
+            ab = MG * int(rng.integers(1, (1 << 23) // MG))
+        else:            # a normal one (biased exponent 1..40: small results)
+            sig = MG * int(rng.integers(((1 << 23) + MG - 1) // MG, (1 << 24) // MG))
+            ab = (int(rng.integers(1, 41)) << 23) | (sig - (1 << 23))
+        A = frac_of_f32(ab)
+        for code in rng.integers(1, 1 << (k - 1), 6):
+            exact = code_value_fr(int(code), x, y) * A / G
+            scaled = exact * Fraction(2) ** 150                   # in units of half the subnormal quantum
+            if exact >= Fraction(2) ** -126:
+                # normal range: exact binary fractions are fp32 values
+                if exact.denominator & (exact.denominator - 1) == 0:
+                    assert rn32(exact) == numpy_rn32(exact) and frac_of_f32(rn32(exact)) == exact
+                continue
+            if scaled.denominator == 1 and scaled.numerator % 2 == 1:   # an odd multiple of 2^-150: a tie
+                got = orc.fs_scale_out(int(code), ab, fmt)
+                assert got == rn32(exact) == numpy_rn32(exact)
+                assert got & 1 == 0
+                ties += 1
+    assert ties >= 3 if x >= 2 else ties == 0, ties
+
+
+def test_factor_is_correctly_rounded(orc):
+    """the encode factor RN32(G / A1) vs numpy (G / A1 is never within 2^-53
+    of an fp32 midpoint unless exactly on it) and Fractions"""
+    rng = np.random.default_rng(11)
+    for fmt in FMTS:
+        G = code_value_fr((1 << (fmt[0] + fmt[1])) - 1, *fmt)
+        for ab in amax_sample(rng, fmt, 16):
+            A = frac_of_f32(ab)
+            while A >= 2:
+                A /= 2
+            while A < 1:
+                A *= 2
+            assert orc.fs_factor(ab, fmt) == rn32(G / A) == numpy_rn32(G / A), (fmt, hex(ab))
 
 
 @pytest.mark.parametrize("fmt", [(2, 1), (3, 3), (4, 2), (1, 4), (5, 0), (6, 1)], ids=lambda f: f"e{f[0]}m{f[1]}")

@@ -415,7 +415,8 @@ def test_fractions_brute_force_tiny(orc):
         a = F(f, 1 << 149) if E == 0 else F(f | 0x800000) * F(2) ** (int(E) - 150)
         return -a if bits >> 31 else a
 
-    for fmt, e_max in [("e2m1", 129), ("e3m0", 127), ("e0m3", 120), ("e1m2", 126), ("e6m0", 124)]:
+    for fmt, e_max in [("e2m1", 129), ("e3m0", 127), ("e0m3", 120), ("e1m2", 126), ("e6m0", 124), ("e6m0", 123),
+                       ("e2m0", 130), ("e2m0", 131), ("e4m0", 200)]:
         x, y = orc.parse_format(fmt)
         k = 1 + x + y
         g = [F(orc.code_value(c, fmt, e_max)) for c in range(1 << (k - 1))]
@@ -430,6 +431,56 @@ def test_fractions_brute_force_tiny(orc):
         codes = orc.encode_codes(b, fmt, e_max)
         for bits, code in zip(b.tolist(), codes.tolist()):
             a = abs(exact(bits))
-            best = min(range(len(g)), key=lambda c: (abs(g[c] - a), c & 1))
+
+            def tie_key(c):
+                # D6: ties to the even code for y >= 1; for y = 0 to the value whose
+                # fp32 biased exponent is even, zero (exponent field 0) first
+                if y >= 1:
+                    return c & 1
+                if g[c] == 0:
+                    return 0
+                e = g[c].numerator.bit_length() - g[c].denominator.bit_length()   # g = 2^e exactly
+                return (e + 127) & 1
+
+            best = min(range(len(g)), key=lambda c: (abs(g[c] - a), tie_key(c), g[c]))
             assert code & ((1 << (k - 1)) - 1) == best, (fmt, bits)
             assert code >> (k - 1) == bits >> 31
+
+
+def eigen_round_bits(u: np.ndarray, y: int) -> np.ndarray:
+    """The paper's rounding procedure: Eigen's float32 -> bfloat16
+    round-to-nearest-even -- add 0x7FFF + (the lowest kept bit), then truncate
+    -- extended to y kept mantissa bits, on fp32 bit patterns (uint32)."""
+    sh = 23 - y
+    lsb = (u >> np.uint32(sh)) & np.uint32(1)
+    r = u + np.uint32((1 << (sh - 1)) - 1) + lsb
+    return r & np.uint32(~((1 << sh) - 1) & 0xFFFFFFFF)
+
+
+@pytest.mark.parametrize("y", range(0, 8))
+def test_eigen_procedure_in_the_normal_range(orc, y):
+    """Inside a format's normal range its grid is the fp32 values with y
+    mantissa bits, so quantize must equal the paper's own rounding procedure
+    (Eigen RTNE on the fp32 bits, extended to y mantissa bits) wherever that
+    result stays in the normal range -- including every exact tie.  For
+    y = 0 this pins reading D6's tie rule (even fp32 exponent), which no
+    library implements."""
+    rng = np.random.default_rng(40 + y)
+    for x in sorted({1, 2, 3, 8 - y} & set(range(1, 9 - y))):
+        for e_max in (100, 127, 131, 254 - y if y else 250):
+            o = e_max - ((1 << x) - 1)
+            if o + 1 < 1:
+                continue
+            lo_e, hi_e = o + 1, e_max                      # normal binades of the grid
+            E = rng.integers(lo_e, hi_e + 1, 20000).astype(np.uint32)
+            f = rng.integers(0, 1 << 23, 20000).astype(np.uint32)
+            sh = 23 - y
+            if sh >= 1:                                    # half of the inputs are exact ties
+                f[::2] = (f[::2] & np.uint32(~((1 << sh) - 1) & 0x7FFFFF)) | np.uint32(1 << (sh - 1))
+            s = rng.integers(0, 2, 20000).astype(np.uint32) << np.uint32(31)
+            u = s | (E << np.uint32(23)) | f
+            want = eigen_round_bits(u, y)
+            ok = ((want >> np.uint32(23)) & np.uint32(0xFF)) <= e_max      # no rounding past the top binade
+            q = orc.quantize(u, (x, y), e_max)
+            np.testing.assert_array_equal(q[ok], want[ok], err_msg=f"e{x}m{y} e_max {e_max}")
+            assert ok.sum() > 4000
