@@ -11,13 +11,23 @@ histogram all-reduce and the all-gather of packed shards (A8).
 value = input GB/s of the step: sum over the codec calls of the bytes of each
 call's input buffer (histogram 2n, quantize 2n, encode 2n, decode n*k/8 per
 format), divided by the device time of the step; at N>1 summed over ranks
-(weak scaling: every rank owns one 16384^2 shard) over the max rank time.
+over the max rank time.
+
+N > 1 (one process per GPU, NCCL, call stack 4): every rank owns
+one 16384^2 shard (weak scaling of the encode side), histograms it, the
+histograms are all-reduced into the global e_max, and per format the rank
+quantizes and encodes its shard, all-gathers the packed shards (the
+compressed exchange, P:298 / P:536) and decodes every received shard, each
+one independently -- so each rank's decode input grows with N.
+`python bench.py --gpus N` without a launcher re-executes itself under
+torch.distributed.run; the driver's own torchrun launch is used as is.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -162,6 +172,26 @@ def device_index(local):
     return local % n if n else local
 
 
+def self_launch(args) -> int:
+    """`bench.py --gpus N` run directly: re-execute under torch.distributed.run
+    with N ranks (127.0.0.1 rendezvous).  NCCL needs N visible GPUs."""
+    n_dev = torch.cuda.device_count()
+    if args.dist_backend == "nccl" and n_dev < args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus}: only {n_dev} CUDA device(s) visible "
+                         "(one process per GPU; --dist-backend gloo shares one GPU for a host-logic smoke run)")
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")            # rank / channel / NVLS lines for the driver's logs
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 # --------------------------------------------------------------- our arm
 def run_ours(args):
     import paper_2405_13938_b200 as exmy
@@ -185,8 +215,11 @@ def run_ours(args):
     cap = 4096
     spi = torch.empty(cap, dtype=torch.int64, device=dev)
     spb = torch.empty(cap, dtype=torch.int32, device=dev)
-    spc = torch.zeros(1, dtype=torch.int64, device=dev)
-    gathered = torch.empty(ws * n * K_BITS // 8, dtype=torch.uint8, device=dev) if ws > 1 else None
+    spc = exmy.specials_workspace(dev)
+    packed_b = n * K_BITS // 8
+    gathered = torch.empty(ws * packed_b, dtype=torch.uint8, device=dev) if ws > 1 else None
+    # at N > 1 every received shard is decoded (into its rows of the full tensor)
+    dout_all = torch.empty((ws * R, C), dtype=torch.bfloat16, device=dev) if ws > 1 else None
     L = exmy.lib()
     st = torch.cuda.current_stream(dev)
     sp = exmy._stream(dev)
@@ -219,8 +252,16 @@ def run_ours(args):
                                                   P(spi), P(spb), P(spc), cap, sp)))
             if ws > 1:
                 f("allgather", lambda: xdist.allgather_bytes(packed[i], gathered, group))
-            f("decode", lambda: chk(L.exmy_decode(P(packed[i]), R, C, exmy.ROWS, x, y, P(meta), P(spi), P(spb),
-                                                  P(spc), cap, P(dout), exmy.BF16, sp)))
+
+                def dec_all():
+                    for r in range(ws):      # shards decode independently; no specials in the data
+                        chk(L.exmy_decode(ctypes.c_void_p(gathered.data_ptr() + r * packed_b), R, C, exmy.ROWS, x,
+                                          y, P(meta), None, None, None, 0,
+                                          ctypes.c_void_p(dout_all.data_ptr() + r * n * 2), exmy.BF16, sp))
+                f("decode", dec_all)
+            else:
+                f("decode", lambda: chk(L.exmy_decode(P(packed[i]), R, C, exmy.ROWS, x, y, P(meta), P(spi), P(spb),
+                                                      P(spc), cap, P(dout), exmy.BF16, sp)))
 
     for _ in range(args.warmup):
         step(False)
@@ -250,12 +291,11 @@ def run_ours(args):
     per_op_ms = {k: sum(a.elapsed_time(b) for a, b in v) / args.steps for k, v in ev.items() if v}
     launches = {k: len(v) / args.steps for k, v in ev.items() if v}
 
-    # bytes per step (one rank)
+    # bytes per step (one rank); at N > 1 the rank decodes all ws received shards
     nf = len(FORMATS)
-    packed_b = n * K_BITS // 8
-    in_bytes = {"hist": 2 * n, "quantize": nf * 2 * n, "encode": nf * 2 * n, "decode": nf * packed_b}
+    in_bytes = {"hist": 2 * n, "quantize": nf * 2 * n, "encode": nf * 2 * n, "decode": nf * ws * packed_b}
     alg_bytes = {"hist": 2 * n, "emax": 2048, "quantize": nf * 4 * n, "encode": nf * (2 * n + packed_b),
-                 "decode": nf * (packed_b + 2 * n)}
+                 "decode": nf * ws * (packed_b + 2 * n)}
     step_in = sum(in_bytes.values())
     value = ws * step_in / (ms_step * 1e-3) / 1e9
 
@@ -287,8 +327,9 @@ def run_ours(args):
                 "algorithmic_bytes_per_launch": alg_bytes[dom] / launches[dom], "peak_source": peak_src}
 
     # gpu launches of OUR kernels per step: hist 1, emax 1; per format quantize 1,
-    # encode 2 (encode + specials sort), decode 2 (decode + specials scatter)
-    gpu_launches = args.steps * (2 + nf * 5)
+    # encode 2 (encode + specials sort), decode 2 (decode + specials scatter) or,
+    # at N > 1, one decode per received shard
+    gpu_launches = args.steps * (2 + nf * (3 + (2 if ws == 1 else ws)))
 
     result = {
         "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
@@ -299,12 +340,19 @@ def run_ours(args):
                                + (", + hist all-reduce and packed all-gather (NCCL)" if ws > 1 else ""),
                    "elements_per_gpu": n, "formats": [f"e{x}m{y}" for x, y in FORMATS], "axis": "rows",
                    "l2": "inputs (512 MiB) larger than L2 (126 MB); no flush needed",
-                   "parallelism": f"shard-per-rank x{ws}" if ws > 1 else "single GPU",
+                   "parallelism": f"shard-per-rank x{ws}, all-gather of packed shards + decode of all {ws}"
+                                  if ws > 1 else "single GPU",
                    "value_definition": "sum of codec-call input bytes per step / device step time"},
+        # the metric's own per-codec numbers (input bytes of the call / its device time)
+        "encode_input_gbs": round(per_op["encode"]["input_gbs"], 1),
+        "decode_input_gbs": round(per_op["decode"]["input_gbs"], 1),
         "per_op": per_op, "per_op_ms_per_step": {k: round(v, 4) for k, v in per_op_ms.items()},
         "roofline": roofline, "gpu_launches": gpu_launches,
     }
     result["clocks"] = clk.summary()
+    if ws > 1:
+        result["multi_gpu"] = multi_gpu_report(dist, dev, t, packed[0], gathered, ev, per_op_ms, ms_total, args, ws,
+                                               rank, nf, packed_b)
 
     # ---------------- block metadata: per-row e_max, e3m3,
     # same tensor; timed separately (not part of `value`)
@@ -325,6 +373,8 @@ def run_ours(args):
     e2e_streams = [torch.cuda.Stream(dev) for _ in range(NS)]
     for x, y in FORMATS:
         hc[(x, y)] = exmy.HostCodec((R, C), torch.bfloat16, (x, y), device=dev, specials_capacity=cap)
+    parity = parity_of_timed_outputs(exmy, t, packed, qout, dout if ws == 1 else dout_all[rank * R:(rank + 1) * R],
+                                     packed_b) if rank == 0 else None
     del qout, packed
     torch.cuda.empty_cache()
 
@@ -359,13 +409,17 @@ def run_ours(args):
         tt = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt.item())
-    e2e_in = nf * (2 * n + 2 * n + packed_b)     # histogram + encode inputs, decode input per format
+    e2e_in = nf * (2 * n + packed_b)     # per format: the encode call's host input, the decode call's host input
     result["e2e"] = {"value": round(ws * e2e_in / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
                      "h2d_bytes_per_step": nf * (2 * n + packed_b), "d2h_bytes_per_step": nf * (packed_b + 1 + 2 * n),
                      "ms_per_step": round(e2e_ms, 3), "steps": e2e_steps,
-                     "path": "exmy_encode_host + exmy_decode_host (pinned host buffers) per format, "
-                             "formats alternating over 2 streams (H2D and D2H copies overlap)"}
+                     "path": "exmy_encode_host (H2D, histogram, e_max, encode, D2H) + exmy_decode_host (H2D, decode, "
+                             "D2H) per format, pinned host buffers, formats alternating over 2 streams (H2D and D2H "
+                             "copies overlap); value = the two calls' host input bytes / time"}
 
+    if rank == 0:
+        result["parity"] = parity
+        result["config1_latency_us"] = config1_latency(exmy, dev)
     if rank == 0 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(t[:args.cpu_rows].cpu())
     if rank == 0:
@@ -373,6 +427,128 @@ def run_ours(args):
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def parity_of_timed_outputs(exmy, t, packed, qout, dout, packed_b, windows=(0, 6144, 12000, 16376)):
+    """parity checked on the timed outputs.  After the timed
+    steps every format's packed buffer, and the last format's quantize and
+    decode outputs, are still in device memory: 8-row windows of them (a row
+    shard's bytes are, per segment, one contiguous range) are
+    compared bit for bit with the CPU oracle run on the same rows."""
+    import numpy as np
+    import oracle as orc
+    import workloads as W
+    orc.lib()
+    n = R * C
+    e = int(exmy.max_exponent(t).item())
+    ok = True
+    checked = 0
+    for r0 in windows:
+        rows = W.to_bits(t[r0:r0 + 8])
+        for i, (x, y) in enumerate(FORMATS):
+            k = 1 + x + y
+            ws, offs = exmy.segments(k, n)
+            got = torch.cat([packed[i][o + r0 * C * w // 8: o + (r0 + 8) * C * w // 8] for w, o in zip(ws, offs)])
+            ref = orc.encode(rows, (x, y), e, orc.ROWS)[0]
+            ok = ok and bool(np.array_equal(got.cpu().numpy(), ref))
+            checked += ref.size
+        x, y = FORMATS[-1]
+        q = orc.quantize(rows, (x, y), e)
+        ok = ok and bool(np.array_equal(W.to_bits(qout[r0:r0 + 8]), q))
+        ok = ok and bool(np.array_equal(W.to_bits(dout[r0:r0 + 8]), q))
+    return {"ok": ok, "e_max": e, "windows": [f"rows {r}..{r + 7}" for r in windows],
+            "packed_bytes_compared": checked,
+            "what": "every format's packed bytes of 8-row windows (row-shard byte ranges) and the last format's "
+                    "quantize / decode rows, vs the CPU oracle on the same rows"}
+
+
+def config1_latency(exmy, dev, reps: int = 30):
+    """BASELINE configs[0] ("config 1"): a 65,536-element fp32 tensor (256 x
+    256), e3m2 -- L2-resident and launch-bound, so per-call latency (median
+    us of CUDA events around one call, L2 flushed by a 256 MB write between
+    calls) through the Python binding, histogram -> e_max -> quantize ->
+    encode -> decode."""
+    import workloads as W
+    t = W.f32_wide((256, 256), seed=0).to(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    hist = torch.zeros(256, dtype=torch.int64, device=dev)
+    meta = exmy.emax(exmy.histogram(t))
+    q = torch.empty_like(t)
+    d = torch.empty_like(t)
+    pk = torch.empty(65536 * 6 // 8, dtype=torch.uint8, device=dev)
+    p = exmy.encode(t, "e3m2", meta, out=pk, strict=False)
+    ops = {"histogram": lambda: exmy.histogram(t, out=hist), "emax": lambda: exmy.emax(hist, out=meta),
+           "quantize": lambda: exmy.quantize(t, "e3m2", meta, out=q),
+           "encode": lambda: exmy.encode(t, "e3m2", meta, out=pk, strict=False),
+           "decode": lambda: exmy.decode(p, out=d)}
+    res = {}
+    for name, fn in ops.items():
+        ts = []
+        for i in range(reps + 3):
+            flush.fill_(i & 0xFF)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            if i >= 3:
+                ts.append(a.elapsed_time(b) * 1e3)
+        ts.sort()
+        res[name] = round(ts[len(ts) // 2], 2)
+    res["workload"] = "config1: 256x256 fp32 N(0,1)*2^U{-12..12}, e3m2, per-call median, L2 flushed between calls"
+    return res
+
+
+def multi_gpu_report(dist, dev, t, pk, gathered, ev, per_op_ms, ms_total, args, ws, rank, nf, packed_b):
+    """Per-rank step times, the all-gather's algbw / busbw (NCCL convention:
+    busbw = algbw (G-1)/G), the same all-gather of the bf16 shard (the wire
+    the codec saves: 16/k), and how many distinct GPUs the ranks ran on."""
+    import torch.distributed as tdist
+    mine = torch.tensor([ms_total / args.steps], dtype=torch.float64, device=dev)
+    times = [torch.zeros_like(mine) for _ in range(ws)]
+    tdist.all_gather(times, mine)
+    ag_ms = per_op_ms.get("allgather", 0.0) / nf           # per all-gather (one per format)
+    # the uncompressed exchange for comparison: all-gather of the bf16 shard
+    full = torch.empty(ws * t.numel(), dtype=torch.bfloat16, device=dev)
+    st = torch.cuda.current_stream(dev)
+    for _ in range(2):
+        tdist.all_gather_into_tensor(full, t.reshape(-1)) if args.dist_backend == "nccl" else None
+    reps = max(3, min(args.steps, 10))
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    tdist.barrier()
+    a.record(st)
+    for _ in range(reps):
+        if args.dist_backend == "nccl":
+            tdist.all_gather_into_tensor(full, t.reshape(-1))
+        else:
+            parts = [torch.empty_like(t.reshape(-1), device="cpu") for _ in range(ws)]
+            tdist.all_gather(parts, t.reshape(-1).cpu())
+    b.record(st)
+    torch.cuda.synchronize(dev)
+    bf_ms = torch.tensor([a.elapsed_time(b) / reps], dtype=torch.float64, device=dev)
+    tdist.all_reduce(bf_ms, op=tdist.ReduceOp.MAX)
+    bf_ms = float(bf_ms.item())
+    del full
+    # distinct physical GPUs behind the ranks
+    try:
+        uuid = str(torch.cuda.get_device_properties(dev).uuid)
+    except Exception:
+        uuid = f"cuda:{dev.index}"
+    uuids = [None] * ws
+    tdist.all_gather_object(uuids, uuid)
+    ag_bytes = ws * packed_b
+    bf_bytes = ws * t.numel() * 2
+
+    def bw(nbytes, ms):
+        alg = nbytes / (ms * 1e-3) / 1e9 if ms > 0 else None
+        return {"ms": round(ms, 4), "bytes": nbytes, "algbw_gbs": round(alg, 1) if alg else None,
+                "busbw_gbs": round(alg * (ws - 1) / ws, 1) if alg else None}
+    return {"ranks": ws, "gpus_active": len(set(uuids)), "backend": args.dist_backend,
+            "rank_ms_per_step": [round(float(x.item()), 4) for x in times],
+            "allgather_packed": bw(ag_bytes, ag_ms), "allgather_bf16": bw(bf_bytes, bf_ms),
+            "wire_ratio_bf16_over_packed": round(bf_bytes / ag_bytes, 4),
+            "time_ratio_bf16_over_packed": round(bf_ms / ag_ms, 3) if ag_ms > 0 else None}
 
 
 def bench_blocked(exmy, t, args, peak, st):
@@ -389,7 +565,8 @@ def bench_blocked(exmy, t, args, peak, st):
     ops = {
         "block_max": (lambda: exmy.block_max_exponent(t, "row", y, "before", out=meta), 2 * n, 2 * n),
         "quantize": (lambda: exmy.quantize_blocked(t, (x, y), meta, "row", out=q), 2 * n, 4 * n),
-        "encode": (lambda: exmy.encode_blocked(t, (x, y), meta, "row", out=buf), 2 * n, 2 * n + n * k // 8),
+        "encode": (lambda: exmy.encode_blocked(t, (x, y), meta, "row", out=buf, strict=False), 2 * n,
+                   2 * n + n * k // 8),
     }
     res = {}
     reps = max(args.steps, 5)
@@ -406,7 +583,7 @@ def bench_blocked(exmy, t, args, peak, st):
         ms = a.elapsed_time(b) / reps
         res[name] = {"us_per_call": round(ms * 1e3, 2), "hbm_gbs": round(alg_b / ms / 1e6, 1),
                      "frac_of_measured": round(alg_b / ms / 1e6 / peak, 4)}
-    p = exmy.encode_blocked(t, (x, y), meta, "row", out=buf)
+    p = exmy.encode_blocked(t, (x, y), meta, "row", out=buf, strict=False)
     for _ in range(3):
         exmy.decode(p, out=d)
     a = torch.cuda.Event(enable_timing=True)
@@ -426,32 +603,86 @@ def bench_blocked(exmy, t, args, peak, st):
 
 
 # ------------------------------------------------------ the oracle arm
-def oracle_step(bits, orc):
-    """One hot-path pass of the CPU oracle over a (rows, C) bf16 sample."""
-    h = orc.histogram(bits)
-    e = orc.emax(h)
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_step(bits, orc, threads: int = 1):
+    """One hot-path pass of the CPU oracle over a (rows, C) bf16 sample:
+    histogram -> e_max -> 7 x (quantize, encode, decode).  threads > 1 splits
+    the rows into contiguous 8-row-aligned chunks, one per thread (the oracle
+    is plain single-threaded C; ctypes releases the GIL), with the histogram
+    summed across chunks before e_max.  Returns the codec-call input bytes."""
+    from concurrent.futures import ThreadPoolExecutor
+    rows = bits.shape[0]
+    per = max(8, (rows // threads) // 8 * 8)
+    chunks = [bits[r:r + per] for r in range(0, rows, per)]
     nbytes = bits.size * 2
-    in_bytes = nbytes
-    for x, y in FORMATS:
-        orc.quantize(bits, (x, y), e)
-        p, idx, sb, ns = orc.encode(bits, (x, y), e, orc.ROWS)
-        orc.decode(p, bits.shape, (x, y), e, orc.ROWS, idx, sb, bits.dtype)
-        in_bytes += nbytes + nbytes + p.size
+    with ThreadPoolExecutor(max_workers=len(chunks)) as ex:
+        hists = list(ex.map(orc.histogram, chunks))
+        e = orc.emax(sum(hists))
+        in_bytes = nbytes
+
+        def one(ch, x, y):
+            orc.quantize(ch, (x, y), e)
+            p, idx, sb, ns = orc.encode(ch, (x, y), e, orc.ROWS)
+            orc.decode(p, ch.shape, (x, y), e, orc.ROWS, idx, sb, ch.dtype)
+            return p.size
+
+        for x, y in FORMATS:
+            packed = sum(ex.map(lambda ch: one(ch, x, y), chunks))
+            in_bytes += nbytes + nbytes + packed
     return in_bytes
 
 
+def time_oracle(bits, orc, threads: int, reps: int = 3):
+    """median wall time of `reps` oracle passes (GB/s of codec-call input)"""
+    vals = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        nb = oracle_step(bits, orc, threads)
+        vals.append(nb / (time.perf_counter() - t0) / 1e9)
+    return statistics.median(vals), vals
+
+
 def cpu_baseline(sample: torch.Tensor):
+    """The oracle as it stands (SURVEY 8(d) "Oracle baseline"): one thread and
+    all host cores, median of 3 passes each, on a bounded sample of the bench
+    tensor (its first rows)."""
     import oracle as orc
     import workloads as W
     bits = W.to_bits(sample)
     orc.lib()
-    t0 = time.perf_counter()
-    in_bytes = oracle_step(bits, orc)
-    dt = time.perf_counter() - t0
-    return {"value": round(in_bytes / dt / 1e9, 5), "unit": "GB/s", "cores": 1, "kind": "oracle",
+    cores = host_cores()
+    one, one_all = time_oracle(bits, orc, 1)
+    many, many_all = time_oracle(bits, orc, cores)
+    return {"value": round(many, 5), "unit": "GB/s", "cores": cores, "kind": "oracle",
+            "cpu_model": cpu_model(), "single_thread": {"value": round(one, 5), "runs": [round(v, 5) for v in one_all]},
+            "all_cores": {"value": round(many, 5), "threads": cores, "runs": [round(v, 5) for v in many_all]},
             "sample": f"rows 0..{bits.shape[0]} of the same 16384x16384 bf16 tensor ({bits.size} elements, "
                       f"{bits.shape[0] / R * 100:.3g}% of it): histogram + 7 x (quantize, encode, decode), "
-                      f"single-threaded scalar C oracle, {dt:.2f} s"}
+                      f"scalar C oracle (gcc -O2 -fno-tree-vectorize), median of 3 passes on 1 thread and on "
+                      f"{cores} threads (contiguous 8-row chunks)"}
 
 
 def run_reference(args):
@@ -464,12 +695,13 @@ def run_reference(args):
     rows = args.cpu_rows
     bits = W.to_bits(t[:rows])
     orc.lib()
+    cores = host_cores()
     for _ in range(args.warmup):
-        oracle_step(bits, orc)
+        oracle_step(bits, orc, cores)
     t0 = time.perf_counter()
     in_bytes = 0
     for _ in range(args.steps):
-        in_bytes += oracle_step(bits, orc)
+        in_bytes += oracle_step(bits, orc, cores)
     dt = time.perf_counter() - t0
     v = in_bytes / dt / 1e9
     print(json.dumps({
@@ -479,8 +711,9 @@ def run_reference(args):
         "config": {"workload": "config2 sample: rows of the 16384x16384 bf16 ~N(0,0.02^2) tensor, ROWS, "
                                "7-bit formats; step = histogram, e_max, 7x(quantize, encode, decode)",
                    "rows": rows, "elements": int(bits.size)},
-        "cpu_baseline": {"value": round(v, 5), "unit": "GB/s", "cores": 1, "kind": "oracle",
-                         "sample": f"{rows} of {R} rows per step (bounded sample), scalar C oracle"},
+        "cpu_baseline": {"value": round(v, 5), "unit": "GB/s", "cores": cores, "kind": "oracle",
+                         "cpu_model": cpu_model(),
+                         "sample": f"{rows} of {R} rows per step (bounded sample), scalar C oracle on {cores} threads"},
         "e2e": {"value": round(v, 5), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -498,6 +731,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     else:
         run_ours(args)
 

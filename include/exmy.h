@@ -148,13 +148,22 @@ exmy_status exmy_quantize(const void *in, void *out, int dtype, int64_t n,
 /* Encode = type conversion (A4) + power-of-2 bit packing
  * (A5), fused: codes never touch HBM.
  *   in: (rows, cols) row-major fp32/bf16; packed: n*k/8 bytes (layout above).
- *   NaN/Inf (D9): code 0 in the packed stream; (index, fp32 bits) appended to
- *   sp_index[]/sp_bits[] (device, capacity entries) in ascending index order;
- *   *sp_count (device uint64) is SET to the total number of specials, even
- *   when it exceeds capacity (extra entries are dropped; check after the
- *   stream syncs).  The histogram's bin 255 is that count.  sp_index/sp_bits
- *   may be NULL iff sp_capacity == 0; sp_count may be NULL only if the input
- *   is known to hold no NaN/Inf. */
+ *   NaN/Inf (D9): code 0 in the packed stream; (index, fp32 bits) of the
+ *   first sp_capacity of them in ascending index order in sp_index[] /
+ *   sp_bits[] (device); sp_count[0] (device uint64) is SET to the total
+ *   number of specials, even when it exceeds capacity (the entries past the
+ *   capacity are not written; check after the stream syncs).  The
+ *   histogram's bin 255 is that count.  The list is built after the encode
+ *   kernel by ordered stream compaction (no sort): with sp_capacity > 0,
+ *   sp_count must point to EXMY_SPECIALS_WORDS uint64 of device workspace
+ *   (word 0 = the count, the rest per-range counts); with sp_capacity == 0
+ *   one word is enough.  Without NaN/Inf (word 0 == 0) the two compaction
+ *   launches return at once.  sp_index/sp_bits may be NULL iff
+ *   sp_capacity == 0; sp_count may be NULL only if the input is known to
+ *   hold no NaN/Inf.  The same convention holds for every *_encode* call
+ *   below except the grouped ones (per-entry lists of one count word). */
+#define EXMY_SPECIALS_WORDS 1025
+int exmy_specials_words(void);   /* == EXMY_SPECIALS_WORDS */
 exmy_status exmy_encode(const void *in, int dtype, int64_t rows, int64_t cols, int axis,
                         int x, int y, const uint8_t *meta, uint8_t *packed,
                         int64_t *sp_index, uint32_t *sp_bits, uint64_t *sp_count,
@@ -185,6 +194,10 @@ exmy_status exmy_decode(const uint8_t *packed, int64_t rows, int64_t cols, int a
  * query.  Return the previous value. */
 int exmy_debug_force_generic(int on);
 int exmy_debug_hist_mode(int mode);
+/* ROWS encode kernel choice: 1 = TMA-staged persistent kernel (bulk copies
+ * into a shared-memory ring), 0 = register-pipelined tiles; -1 queries.
+ * Returns the previous value. */
+int exmy_debug_enc_tma(int on);
 int exmy_debug_hist_blocks(int blocks);
 
 /* Roofline probe, not part of the codec: reads in_bytes
@@ -269,7 +282,12 @@ exmy_status exmy_decode_rows(const uint8_t *packed, int64_t rows, int64_t cols, 
  * e_max = 127 grid, whose top is G (2 - 2^-y for x >= 1).  With amax =
  * A1 * 2^p, A1 in [1,2):
  *   encode  u = RN32(v * RN32(G/A1) * 2^-p), code = the e_max-127 code of u
- *   decode  out = RN32(RN64(g * RN64(A1 * RN64(1/G)) * 2^p)); bf16 = RN16(out)
+ *           (the fp32 scaling factor RN32(G/A1))
+ *   decode  out = RN32(g * amax / G), g the code's exact value at e_max 127
+ *           (exact product and quotient rounded once, fp32 subnormals
+ *           included; a zero result keeps the code's sign); bf16 = RN16(out)
+ *           (reading D24).  Kernels: FMUL + FFMA with a two-term amax/G for
+ *           results >= 2^-100, integer evaluation below that and for x = 8.
  * so each block's maximum decodes to exactly amax ("captures the largest
  * value in the block accurately").  Layout, specials and error codes
  * as exmy_encode_blocked / exmy_decode_blocked; scale is device memory,
@@ -316,6 +334,19 @@ exmy_status exmy_encode_push(const void *in, int dtype, int64_t rows, int64_t co
                              int64_t total_rows, int x, int y, const uint8_t *meta,
                              uint8_t *const *dst, int ndst, int64_t *sp_index, uint32_t *sp_bits,
                              uint64_t *sp_count, int64_t sp_capacity, void *stream);
+
+/* NVLS multicast form of exmy_encode_push (P:298,
+ * P:536): identical arguments except one destination, `mc_dst`, a multicast
+ * address of the gathered packed buffer (e.g. torch symmetric memory's
+ * multicast_ptr) bound on every GPU of the node.  Each 4 / 8 / 16-byte
+ * segment store is one multimem.st, replicated to every bound GPU by the
+ * NVSwitch, instead of one store per peer.  Same bytes as exmy_encode_push
+ * into every bound buffer; the caller synchronises (stream + barrier) before
+ * peers read.  E_ALIGN as exmy_encode_push. */
+exmy_status exmy_encode_push_multicast(const void *in, int dtype, int64_t rows, int64_t cols,
+                                       int64_t row0, int64_t total_rows, int x, int y, const uint8_t *meta,
+                                       uint8_t *mc_dst, int64_t *sp_index, uint32_t *sp_bits,
+                                       uint64_t *sp_count, int64_t sp_capacity, void *stream);
 
 /* Pull decode, the mirror of exmy_encode_push ("decode
  * reads peers' packed shards over NVLink"): decodes the whole

@@ -47,6 +47,7 @@ def _load():
     i64, i32, vp, dbl = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_double
     sig = {
         "exmy_version": ([], ctypes.c_char_p),
+        "exmy_specials_words": ([], i32),
         "exmy_status_string": ([i32], ctypes.c_char_p),
         "exmy_format_valid": ([i32, i32], i32),
         "exmy_packed_bytes": ([i64, i32, i32], i64),
@@ -58,6 +59,7 @@ def _load():
         "exmy_debug_force_generic": ([i32], i32),
         "exmy_debug_hist_mode": ([i32], i32),
         "exmy_debug_hist_blocks": ([i32], i32),
+        "exmy_debug_enc_tma": ([i32], i32),
         "exmy_debug_probe": ([vp, i64, vp, i64, vp], i32),
         "exmy_exponent_histogram": ([vp, i32, i64, vp, vp], i32),
         "exmy_emax_from_histogram": ([vp, vp, vp], i32),
@@ -78,6 +80,7 @@ def _load():
         "exmy_encode_fs": ([vp, i32, i64, i64, i32, i64, i64, i32, i32, vp, vp, vp, vp, vp, i64, vp], i32),
         "exmy_decode_fs": ([vp, i64, i64, i32, i64, i64, i32, i32, vp, vp, vp, vp, i64, vp, i32, vp], i32),
         "exmy_encode_push": ([vp, i32, i64, i64, i64, i64, i32, i32, vp, vp, i32, vp, vp, vp, i64, vp], i32),
+        "exmy_encode_push_multicast": ([vp, i32, i64, i64, i64, i64, i32, i32, vp, vp, vp, vp, vp, i64, vp], i32),
         "exmy_embedding_bag": ([vp, i64, i64, i32, i32, vp, i32, vp, vp, i64, vp, i32, vp, vp], i32),
         "exmy_decode_pull": ([vp, i32, i64, i64, i32, i32, vp, vp, i32, vp], i32),
         "exmy_ckpt_write": ([ctypes.c_char_p, vp, i32], i64),
@@ -106,21 +109,29 @@ def _load():
 
 _lib = _load()
 LIB_PATH = _LIB_PATH
-EXPORTED = ["exmy_version", "exmy_status_string", "exmy_format_valid", "exmy_packed_bytes", "exmy_segments",
+EXPORTED = ["exmy_version", "exmy_specials_words", "exmy_status_string", "exmy_format_valid", "exmy_packed_bytes", "exmy_segments",
             "exmy_bias_from_emax", "exmy_emax_from_bias", "exmy_emax_from_histogram_host", "exmy_choose_x",
-            "exmy_debug_force_generic", "exmy_debug_hist_mode", "exmy_debug_hist_blocks", "exmy_debug_probe",
+            "exmy_debug_force_generic", "exmy_debug_hist_mode", "exmy_debug_hist_blocks", "exmy_debug_enc_tma", "exmy_debug_probe",
             "exmy_exponent_histogram",
             "exmy_emax_from_histogram", "exmy_quantize", "exmy_encode", "exmy_decode", "exmy_encode_host",
             "exmy_decode_host", "exmy_block_max_exponent", "exmy_quantize_blocked", "exmy_encode_blocked",
             "exmy_decode_blocked", "exmy_decode_rows", "exmy_max_exponent", "exmy_encode_rowwise",
             "exmy_group_plan_bytes", "exmy_group_plan", "exmy_group_plan_rows", "exmy_group_max_exponent", "exmy_group_encode", "exmy_group_encode_rowwise",
             "exmy_group_decode", "exmy_block_float_scale", "exmy_quantize_fs", "exmy_encode_fs", "exmy_decode_fs",
-            "exmy_encode_push", "exmy_decode_pull", "exmy_embedding_bag", "exmy_ckpt_write", "exmy_ckpt_open", "exmy_ckpt_count", "exmy_ckpt_info",
+            "exmy_encode_push", "exmy_encode_push_multicast", "exmy_decode_pull", "exmy_embedding_bag", "exmy_ckpt_write", "exmy_ckpt_open", "exmy_ckpt_count", "exmy_ckpt_info",
             "exmy_ckpt_find", "exmy_ckpt_read", "exmy_ckpt_verify", "exmy_ckpt_bytes_read", "exmy_ckpt_close"]
 
 
 def lib():
     return _lib
+
+
+SPECIALS_WORDS = _lib.exmy_specials_words()   # the sp_count workspace (include/exmy.h)
+
+
+def specials_workspace(device) -> torch.Tensor:
+    """device int64[SPECIALS_WORDS]: word 0 = the specials count (uint64)"""
+    return torch.zeros(SPECIALS_WORDS, dtype=torch.int64, device=device)
 
 
 def version() -> str:
@@ -207,6 +218,12 @@ def roofline_probe(src: torch.Tensor, out_bytes: int, out: torch.Tensor | None =
     _check(_lib.exmy_debug_probe(_ptr(src), src.numel() * src.element_size(), _ptr(out), int(out_bytes),
                                  _stream(src.device)), "roofline_probe")
     return out
+
+
+def enc_tma(on: bool | None = None) -> int:
+    """knob: ROWS encode through the TMA-staged kernel (1) or the register
+    pipeline (0); returns the previous setting"""
+    return _lib.exmy_debug_enc_tma(-1 if on is None else int(on))
 
 
 def hist_blocks(blocks: int | None = None) -> int:
@@ -354,7 +371,7 @@ class Packed:
     def specials(self):
         """(index, bits, total count) of the out-of-band NaN/Inf (D9); the lists
         hold min(count, capacity) entries."""
-        cnt = int(self.sp_count.item()) if self.sp_count is not None else 0
+        cnt = int(self.sp_count[0].item()) if self.sp_count is not None else 0
         c = min(cnt, self.capacity)
         return self.sp_index[:c], self.sp_bits[:c], cnt
 
@@ -362,7 +379,7 @@ class Packed:
         """Raise E_CAPACITY if the encode saw more NaN/Inf than its specials
         capacity (the extra ones would decode as their in-band code 0).
         Synchronises the stream."""
-        cnt = int(self.sp_count.item()) if self.sp_count is not None else 0
+        cnt = int(self.sp_count[0].item()) if self.sp_count is not None else 0
         if cnt > self.capacity:
             raise ExmyError(6, f"encode: {cnt} NaN/Inf elements but specials capacity {self.capacity}; "
                                f"re-encode with specials_capacity >= {cnt}")
@@ -399,7 +416,7 @@ def encode(t: torch.Tensor, fmt, meta=None, axis="rows", specials_capacity: int 
     cap = int(specials_capacity)
     spi = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
     spb = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
-    spc = torch.zeros(1, dtype=torch.int64, device=dev)
+    spc = specials_workspace(dev)
     _check(_lib.exmy_encode(_ptr(t), _dtype_code(t.dtype), R, C, ax, x, y, _ptr(m), _ptr(out), _ptr(spi), _ptr(spb),
                             _ptr(spc), cap, _stream(dev)), "encode")
     return _finish(Packed(out, m, spi, spb, spc, tuple(t.shape), x, y, ax, t.dtype, sp_capacity=cap), strict)
@@ -498,7 +515,7 @@ def encode_blocked(t: torch.Tensor, fmt, meta: torch.Tensor | None, block, axis=
     cap = int(specials_capacity)
     spi = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
     spb = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
-    spc = torch.zeros(1, dtype=torch.int64, device=dev)
+    spc = specials_workspace(dev)
     _check(_lib.exmy_encode_blocked(_ptr(t), _dtype_code(t.dtype), R, C, ax, br, bc, x, y, _ptr(meta), _ptr(out),
                                     _ptr(spi), _ptr(spb), _ptr(spc), cap, _stream(dev)), "encode_blocked")
     return _finish(Packed(out, meta, spi, spb, spc, tuple(t.shape), x, y, ax, t.dtype, (br, bc), sp_capacity=cap,
@@ -523,7 +540,7 @@ def encode_rowwise(t: torch.Tensor, fmt, axis="rows", scheme="before", specials_
     cap = int(specials_capacity)
     spi = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
     spb = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
-    spc = torch.zeros(1, dtype=torch.int64, device=dev)
+    spc = specials_workspace(dev)
     _check(_lib.exmy_encode_rowwise(_ptr(t), _dtype_code(t.dtype), R, C, ax, x, y, SCHEMES[scheme], _ptr(meta),
                                     _ptr(out), _ptr(spi), _ptr(spb), _ptr(spc), cap, _stream(dev)), "encode_rowwise")
     return _finish(Packed(out, meta, spi, spb, spc, tuple(t.shape), x, y, ax, t.dtype, (1, C), sp_capacity=cap,
@@ -630,10 +647,30 @@ def encode_push(shard: torch.Tensor, fmt, meta: torch.Tensor, row0: int, total_r
     cap = int(specials_capacity)
     spi = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
     spb = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
-    spc = torch.zeros(1, dtype=torch.int64, device=dev)
+    spc = specials_workspace(dev)
     _check(_lib.exmy_encode_push(_ptr(shard), _dtype_code(shard.dtype), R, C, int(row0), int(total_rows), x, y,
                                  _ptr(_meta_tensor(meta, dev)), ptrs, len(dsts), _ptr(spi), _ptr(spb), _ptr(spc), cap,
                                  _stream(dev)), "encode_push")
+    return spi, spb, spc
+
+
+def encode_push_multicast(shard: torch.Tensor, fmt, meta: torch.Tensor, row0: int, total_rows: int, mc_ptr: int,
+                          specials_capacity: int = 4096):
+    """encode_push with ONE destination: a multicast address (NVLS,
+    multimem.st) of the gathered buffer bound on every GPU -- each store
+    reaches all of them.  Returns the shard's (sp_index, sp_bits, sp_count)."""
+    _require_cuda(shard)
+    x, y = parse_format(fmt)
+    shard = shard.contiguous()
+    R, C = _as_2d(shard)
+    dev = shard.device
+    cap = int(specials_capacity)
+    spi = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
+    spb = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    spc = specials_workspace(dev)
+    _check(_lib.exmy_encode_push_multicast(_ptr(shard), _dtype_code(shard.dtype), R, C, int(row0), int(total_rows), x,
+                                           y, _ptr(_meta_tensor(meta, dev)), ctypes.c_void_p(int(mc_ptr)), _ptr(spi),
+                                           _ptr(spb), _ptr(spc), cap, _stream(dev)), "encode_push_multicast")
     return spi, spb, spc
 
 
@@ -703,7 +740,7 @@ def encode_fs(t: torch.Tensor, fmt, scale: torch.Tensor | None, block, axis="row
     cap = int(specials_capacity)
     spi = torch.empty(max(cap, 1), dtype=torch.int64, device=dev)
     spb = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
-    spc = torch.zeros(1, dtype=torch.int64, device=dev)
+    spc = specials_workspace(dev)
     _check(_lib.exmy_encode_fs(_ptr(t), _dtype_code(t.dtype), R, C, ax, br, bc, x, y, _ptr(scale), _ptr(out),
                                _ptr(spi), _ptr(spb), _ptr(spc), cap, _stream(dev)), "encode_fs")
     meta = torch.full((1,), 127, dtype=torch.uint8, device=dev)
@@ -734,7 +771,7 @@ class HostCodec:
         self.cap = specials_capacity
         self.spi = torch.empty(max(self.cap, 1), dtype=torch.int64, device=device)
         self.spb = torch.empty(max(self.cap, 1), dtype=torch.int32, device=device)
-        self.spc = torch.zeros(1, dtype=torch.int64, device=device)
+        self.spc = specials_workspace(device)
 
     def encode(self, host_in: torch.Tensor, host_packed: torch.Tensor, host_meta: torch.Tensor | None = None):
         _check(_lib.exmy_encode_host(_ptr(host_in), _dtype_code(self.dtype), self.R, self.C, self.axis, self.x,
@@ -937,7 +974,7 @@ def save_checkpoint(path: str, tensors: dict) -> int:
         data = p.data.detach().cpu().contiguous()
         meta = p.meta.detach().cpu().contiguous()
         scale = p.scale.detach().cpu().contiguous() if p.scale is not None else None
-        cnt = int(p.sp_count.item()) if p.sp_count is not None else 0
+        cnt = int(p.sp_count[0].item()) if p.sp_count is not None else 0
         cnt = min(cnt, p.capacity) if cnt else 0
         spi = p.sp_index[:cnt].detach().cpu().contiguous() if cnt else None
         spb = p.sp_bits[:cnt].detach().cpu().contiguous() if cnt else None

@@ -9,8 +9,9 @@
 
 namespace exmy {
 int g_force_generic = 0;
-int g_hist_mode = 2;
+int g_hist_mode = 3;
 int g_hist_blocks = 0;
+int g_enc_tma = 0;
 }  // namespace exmy
 
 using namespace exmy;
@@ -44,7 +45,12 @@ bool block_ok(int64_t rows, int64_t cols, int64_t br, int64_t bc) {
 // ====================================================================== ABI
 extern "C" {
 
-const char *exmy_version(void) { return "exmy-b200 0.1 (sm_100a)"; }
+const char *exmy_version(void) { return "exmy-b200 0.2 (sm_100a)"; }
+
+int exmy_specials_words(void) {
+    static_assert(EXMY_SPECIALS_WORDS == 1 + SPECIALS_RANGES, "workspace = count + one word per range");
+    return EXMY_SPECIALS_WORDS;
+}
 
 const char *exmy_status_string(int s) {
     switch (s) {
@@ -133,6 +139,12 @@ int exmy_debug_hist_mode(int mode) {
     return prev;
 }
 
+int exmy_debug_enc_tma(int on) {
+    int prev = g_enc_tma;
+    if (on >= 0) g_enc_tma = on;
+    return prev;
+}
+
 int exmy_debug_hist_blocks(int blocks) {
     int prev = g_hist_blocks;
     if (blocks >= 0) g_hist_blocks = blocks;
@@ -191,11 +203,12 @@ exmy_status exmy_encode(const void *in, int dtype, int64_t rows, int64_t cols, i
     if (spc && cudaMemsetAsync(spc, 0, sizeof(unsigned long long), st) != cudaSuccess) return EXMY_E_CUDA;
     if (n == 0) return EXMY_OK;
     if (!in || !packed || !meta) return EXMY_E_ARG;
+    // the kernel counts the NaN/Inf (ws[0]); the ordered list is written after it
     s = launch_encode(static_cast<const uint8_t *>(in), dtype == EXMY_BF16, rows, cols, axis, x, y, meta, packed,
-                      sp_index, sp_bits, spc, sp_capacity, st);
+                      nullptr, nullptr, spc, 0, st);
     if (s != EXMY_OK) return s;
-    if (spc && sp_capacity > 1) s = launch_specials_sort(sp_index, sp_bits, spc, sp_capacity, st);
-    return s;
+    return launch_specials_compact(static_cast<const uint8_t *>(in), dtype == EXMY_BF16, n, 0, sp_index, sp_bits, spc,
+                                   sp_capacity, st);
 }
 
 exmy_status exmy_decode(const uint8_t *packed, int64_t rows, int64_t cols, int axis, int x, int y,
@@ -261,10 +274,10 @@ exmy_status exmy_encode_blocked(const void *in, int dtype, int64_t rows, int64_t
     if (n == 0) return EXMY_OK;
     if (!in || !packed || !meta) return EXMY_E_ARG;
     s = launch_encode_blocked(static_cast<const uint8_t *>(in), dtype == EXMY_BF16, rows, cols, axis, block_rows,
-                              block_cols, x, y, meta, packed, sp_index, sp_bits, spc, sp_capacity, st);
+                              block_cols, x, y, meta, packed, nullptr, nullptr, spc, 0, st);
     if (s != EXMY_OK) return s;
-    if (spc && sp_capacity > 1) s = launch_specials_sort(sp_index, sp_bits, spc, sp_capacity, st);
-    return s;
+    return launch_specials_compact(static_cast<const uint8_t *>(in), dtype == EXMY_BF16, n, 0, sp_index, sp_bits, spc,
+                                   sp_capacity, st);
 }
 
 exmy_status exmy_decode_blocked(const uint8_t *packed, int64_t rows, int64_t cols, int axis, int64_t block_rows,
@@ -311,17 +324,14 @@ exmy_status exmy_encode_rowwise(const void *in, int dtype, int64_t rows, int64_t
     const bool bf = dtype == EXMY_BF16;
     s = EXMY_E_ALIGN;
     if (axis == EXMY_AXIS_ROWS && !g_force_generic)
-        s = launch_encode_rowwise(pin, bf, rows, cols, x, y, scheme, meta, packed, sp_index, sp_bits, spc,
-                                  sp_capacity, st);
+        s = launch_encode_rowwise(pin, bf, rows, cols, x, y, scheme, meta, packed, nullptr, nullptr, spc, 0, st);
     if (s == EXMY_E_ALIGN) {   // two launches: row maxima, then the blocked encode
         s = launch_block_max(pin, bf, rows, cols, 1, cols, y, scheme, meta, st);
         if (s != EXMY_OK) return s;
-        s = launch_encode_blocked(pin, bf, rows, cols, axis, 1, cols, x, y, meta, packed, sp_index, sp_bits, spc,
-                                  sp_capacity, st);
+        s = launch_encode_blocked(pin, bf, rows, cols, axis, 1, cols, x, y, meta, packed, nullptr, nullptr, spc, 0, st);
     }
     if (s != EXMY_OK) return s;
-    if (spc && sp_capacity > 1) s = launch_specials_sort(sp_index, sp_bits, spc, sp_capacity, st);
-    return s;
+    return launch_specials_compact(pin, bf, n, 0, sp_index, sp_bits, spc, sp_capacity, st);
 }
 
 exmy_status exmy_decode_rows(const uint8_t *packed, int64_t rows, int64_t cols, int x, int y, const uint8_t *meta,

@@ -32,8 +32,8 @@ __device__ __forceinline__ Fmt fmt_of(int x, int y, int e) {
 // ------------------------------------------------------- per-row params
 // The e_max-dependent constants of the encode fast paths (see FastP).
 struct RowP {
-    uint32_t lo2, k3, par2;     // bf16 lanes
-    uint32_t lo, k3f, parf;     // fp32
+    uint32_t lo2, k3;           // bf16 lanes
+    uint32_t lo, k3f;           // fp32
     bool ok;                    // fast preconditions hold for this e_max
 };
 
@@ -46,13 +46,11 @@ __device__ __forceinline__ RowP make_rowp(int e, int x, int y) {
     if (SIMD) {
         R.lo2 = u1 * (0x80u * 0x00010001u);
         R.k3 = u1 * ((1u << y) * 0x00010001u);
-        R.par2 = (u1 & 1u) * 0x00010001u;
-        R.lo = R.k3f = R.parf = 0;
+        R.lo = R.k3f = 0;
     } else {
         R.lo = u1 << 23;
         R.k3f = u1 << y;
-        R.parf = u1 & 1u;
-        R.lo2 = R.k3 = R.par2 = 0;
+        R.lo2 = R.k3 = 0;
     }
     return R;
 }
@@ -60,11 +58,12 @@ __device__ __forceinline__ RowP make_rowp(int e, int x, int y) {
 template <int K, bool Y0>
 __device__ __forceinline__ uint32_t enc_pair_bf16_r(uint32_t w, const FastP &P, const RowP &R, uint32_t &amax) {
     const uint32_t a2 = w & 0x7FFF7FFFu;
-    const uint32_t ecl = vmax_u16x2(w & 0x7F807F80u, R.lo2);
+    const uint32_t ev = w & 0x7F807F80u;
+    const uint32_t ecl = vmax_u16x2(ev, R.lo2);
     uint32_t c, t;
-    if (Y0) {
+    if (Y0) {   // D6: y = 0 ties to the even fp32 exponent (see exmy_fast.cuh)
         t = ecl >> 7;
-        c = ecl + P.k2 + ((t ^ R.par2) & 0x00010001u);
+        c = ecl + P.k2 + ((~(t | (ev >> 7))) & 0x00010001u);
     } else {
         t = ecl >> P.sh_b;
         c = ecl + P.k2;
@@ -80,9 +79,10 @@ __device__ __forceinline__ uint32_t enc_pair_bf16_r(uint32_t w, const FastP &P, 
 template <int K, bool Y0>
 __device__ __forceinline__ uint32_t enc_f32_fast_r(uint32_t u, const FastP &P, const RowP &R, uint32_t &amax) {
     const uint32_t a = u & 0x7FFFFFFFu;
-    const uint32_t ecl = max(u & 0x7F800000u, R.lo);
+    const uint32_t ev = u & 0x7F800000u;
+    const uint32_t ecl = max(ev, R.lo);
     uint32_t c = ecl + P.k2f;
-    if (Y0) c += ((ecl >> 23) ^ R.parf) & 1u;
+    if (Y0) c += (~((ecl | ev) >> 23)) & 1u;
     const uint32_t s = __float_as_uint(__fadd_rn(__uint_as_float(a), __uint_as_float(c)));
     uint32_t code = s - c + (ecl >> P.sh_f) - R.k3f;
     code = min(code, (1u << (K - 1)) - 1u);

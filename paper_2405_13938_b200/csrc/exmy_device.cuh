@@ -36,11 +36,12 @@ __device__ __forceinline__ Fmt load_fmt(int x, int y, const uint8_t *meta) {
 
 // ---------------------------------------------------------------- rounding
 // round-to-nearest-even of X / 2^sh, 1 <= sh <= 31
-__device__ __forceinline__ uint32_t rtne_shr(uint32_t X, int sh) {
+__device__ __forceinline__ uint32_t rtne_shr(uint32_t X, int sh, uint32_t flip = 0u) {
+    // ties go up when (q ^ flip) is odd: flip = 0 is ties-to-even on q
     uint32_t q = X >> sh;
     uint32_t r = X & ((1u << sh) - 1u);
     uint32_t h = 1u << (sh - 1);
-    return q + (uint32_t)((r > h) | ((r == h) & (q & 1u)));
+    return q + (uint32_t)((r > h) | ((r == h) & ((q ^ flip) & 1u)));
 }
 
 __device__ __forceinline__ bool is_special_f32(uint32_t u) {
@@ -76,14 +77,18 @@ __device__ __forceinline__ uint32_t enc_code_generic(uint32_t u, const Fmt &F) {
     } else {
         uint32_t X;
         int sh;
+        uint32_t flip = 0u;
         if (F.x > 0 && Ep >= 1) {       // normal target code
             X = ((uint32_t)(Ep - 1) << 23) + sig;
             sh = 23 - F.y;
+            // y = 0 (D6): a tie goes to the even fp32 exponent, i.e. up iff
+            // Ep + o is odd (q = Ep here); y >= 1: the even code
+            if (F.y == 0) flip = (uint32_t)F.o & 1u;
         } else {                        // subnormal target (every code when x=0)
             X = sig;
             sh = 24 - F.y - Ep;
         }
-        mag = sh >= 32 ? 0u : rtne_shr(X, sh);
+        mag = sh >= 32 ? 0u : rtne_shr(X, sh, flip);
         mag = min(mag, F.M);
     }
     return (s << (F.x + F.y)) | mag;

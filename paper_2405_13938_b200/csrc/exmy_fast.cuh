@@ -11,10 +11,14 @@
 // count of quanta is bits(RN(|v|+C)) - bits(C).  The code is that count
 // plus (Ecl-o-1) << y (the implicit bit is in the count).  A carry out of
 // the binade lands on the next exponent code; saturation is one min.
-// For y = 0 the tie parity of the count and of the code differ when
-// Ecl-o-1 is odd; C is then moved by one quantum so the hardware's "even
-// significand" is the even code.  bf16 inputs run two elements per 32-bit
-// register (16-bit SIMD lanes, HADD2.BF16) for y <= 6.
+// For y = 0 (reading D6) a tie goes to the even fp32 exponent (the paper's
+// Eigen RTNE extended to zero mantissa bits): without help the addition
+// sends every y = 0 tie up (count 2 is the even significand), so C is moved
+// by one quantum where the binade's exponent is even; taking that parity
+// from (clamped | unclamped) exponent keeps the flush tie (half the smallest
+// non-zero value, one binade below the clamp) at zero (D8).  bf16 inputs run
+// two elements per 32-bit register (16-bit SIMD lanes, HADD2.BF16) for
+// y <= 6.
 //
 // Decode: the magnitude code shifted into a bf16/fp32 bit pattern is the
 // value scaled by 2^-o (code exponent 0 lands on subnormals); one
@@ -72,8 +76,7 @@ struct FastP {
     uint32_t lo2, hi2;  // clamp bounds on the exponent field (bf16 lanes)
     uint32_t k2, k3;    // (7-y)<<7, (o+1)<<y per lane (bf16 lanes)
     uint32_t m2;        // M per lane
-    uint32_t par2;      // parity constant per lane (y = 0)
-    uint32_t lo, hi, k2f, k3f, parf;   // fp32 variants
+    uint32_t lo, hi, k2f, k3f;   // fp32 variants
     int sh_b, sh_f;     // 7-y, 23-y
     // decode
     bool dec_fast;      // fp32 out: x <= 7
@@ -103,12 +106,10 @@ __device__ __forceinline__ FastP make_fast(const Fmt &F, bool bf16_in, int force
     P.k2 = ((uint32_t)(7 - (y > 7 ? 7 : y)) << 7) * 0x00010001u;
     P.k3 = ((uint32_t)(o + 1) << y) * 0x00010001u;
     P.m2 = F.M * 0x00010001u;
-    P.par2 = ((uint32_t)((o + 1) & 1)) * 0x00010001u;
     P.lo = (uint32_t)(o + 1) << 23;
     P.hi = (uint32_t)(e + 1) << 23;
     P.k2f = (uint32_t)(23 - y) << 23;
     P.k3f = (uint32_t)(o + 1) << y;
-    P.parf = (uint32_t)((o + 1) & 1);
     P.sh_b = 7 - (y > 7 ? 7 : y);
     // Without an upper clamp on the exponent, C = 2^(E-127+7-y) overflows only
     // for E > 247+y (bf16) / 231+y (fp32); tiles holding such magnitudes (or
@@ -157,11 +158,12 @@ enum EncMode { ENC_SIMD = 0, ENC_SIMD_Y0 = 1, ENC_F32 = 2, ENC_F32_Y0 = 3 };
 template <int K, bool Y0>
 __device__ __forceinline__ uint32_t enc_pair_bf16(uint32_t w, const FastP &P, uint32_t &amax) {
     const uint32_t a2 = w & 0x7FFF7FFFu;
-    uint32_t ecl = vmax_u16x2(w & 0x7F807F80u, P.lo2);   // subnormal region -> binade o+1
+    const uint32_t ev = w & 0x7F807F80u;
+    uint32_t ecl = vmax_u16x2(ev, P.lo2);   // subnormal region -> binade o+1
     uint32_t c, t;
-    if (Y0) {   // y = 0: shift is 7; move C by one quantum where Ecl-o-1 is odd (even code, not even count)
+    if (Y0) {   // y = 0: shift is 7; move C by one quantum where the binade's exponent is even (D6)
         t = ecl >> 7;
-        c = ecl + P.k2 + ((t ^ P.par2) & 0x00010001u);
+        c = ecl + P.k2 + ((~(t | (ev >> 7))) & 0x00010001u);
     } else {
         t = ecl >> P.sh_b;
         c = ecl + P.k2;
@@ -182,9 +184,10 @@ __device__ __forceinline__ bool amax_special_bf16(uint32_t amax, const FastP &P)
 template <int K, bool Y0>
 __device__ __forceinline__ uint32_t enc_f32_fast(uint32_t u, const FastP &P, uint32_t &amax) {
     const uint32_t a = u & 0x7FFFFFFFu;
-    const uint32_t ecl = max(u & 0x7F800000u, P.lo);
+    const uint32_t ev = u & 0x7F800000u;
+    const uint32_t ecl = max(ev, P.lo);
     uint32_t c = ecl + P.k2f;
-    if (Y0) c += ((ecl >> 23) ^ P.parf) & 1u;
+    if (Y0) c += (~((ecl | ev) >> 23)) & 1u;   // D6: y = 0 ties to the even fp32 exponent
     const uint32_t s = __float_as_uint(__fadd_rn(__uint_as_float(a), __uint_as_float(c)));
     uint32_t code = s - c + (ecl >> P.sh_f) - P.k3f;
     code = min(code, (1u << (K - 1)) - 1u);
@@ -196,9 +199,10 @@ __device__ __forceinline__ uint32_t enc_f32_fast(uint32_t u, const FastP &P, uin
 // quantize two bf16 elements directly in bf16 arithmetic (value, not code)
 __device__ __forceinline__ uint32_t quant_pair_bf16(uint32_t w, const FastP &P, uint32_t &flag) {
     const uint32_t a2 = w & 0x7FFF7FFFu;
-    const uint32_t ecl = vmax_u16x2(w & 0x7F807F80u, P.lo2);
+    const uint32_t ev = w & 0x7F807F80u;
+    const uint32_t ecl = vmax_u16x2(ev, P.lo2);
     uint32_t c = ecl + P.k2;
-    if (P.y0) c += ((ecl >> 7) ^ P.par2) & 0x00010001u;
+    if (P.y0) c += (~((ecl | ev) >> 7)) & 0x00010001u;
     const uint32_t s = hadd2_bf16(a2, c);
     uint32_t q = hsub2_bf16(s, c);            // exact (Sterbenz): RTNE_q(|v|)
     q = vmin_u16x2(q, P.maxv2);
@@ -313,9 +317,10 @@ namespace exmy {
 
 __device__ __forceinline__ uint32_t quant_f32_fast(uint32_t u, const FastP &P, uint32_t &flag) {
     const uint32_t a = u & 0x7FFFFFFFu;
-    const uint32_t ecl = max(u & 0x7F800000u, P.lo);
+    const uint32_t ev = u & 0x7F800000u;
+    const uint32_t ecl = max(ev, P.lo);
     uint32_t c = ecl + P.k2f;
-    if (P.y0) c += ((ecl >> 23) ^ P.parf) & 1u;
+    if (P.y0) c += (~((ecl | ev) >> 23)) & 1u;
     const float s = __fadd_rn(__uint_as_float(a), __uint_as_float(c));
     uint32_t q = __float_as_uint(__fsub_rn(s, __uint_as_float(c)));   // exact
     q = min(q, P.maxvf);
@@ -358,6 +363,55 @@ template <bool BF16, int MODE>
 __device__ __forceinline__ bool amax_special(uint32_t amax, const FastP &P) {
     if constexpr (MODE == ENC_SIMD || MODE == ENC_SIMD_Y0) return amax_special_bf16(amax, P);
     else return amax >= P.bigf;
+}
+
+// A tile whose fast-path flag fired because of NaN/Inf only (no finite
+// magnitude in the C-overflow range): its codes are the fast ones with the
+// special lanes set to 0 (D9's in-band placeholder), so NaN-heavy tensors
+// keep the vector path; returns the number of specials (the ordered list is
+// written afterwards by the compaction kernels), or -1 if the tile needs the
+// integer path.  cp as from vec_codes (16-bit lanes: codes 2t, 2t+1).
+template <int K, bool BF16, int MODE, int NW>
+__device__ __forceinline__ int mask_special_codes(const uint32_t (&w)[NW], uint32_t (&cp)[BF16 ? NW : NW / 2],
+                                                  const FastP &P) {
+    constexpr int NP = BF16 ? NW : NW / 2;
+    int n = 0;
+    bool bad = false;
+#pragma unroll
+    for (int t = 0; t < NP; ++t) {
+        uint32_t sp;   // bit 15 / 31: element 2t / 2t+1 is NaN/Inf
+        if (BF16) {
+            const uint32_t a2 = w[t] & 0x7FFF7FFFu;
+            sp = (a2 + 0x00800080u) & 0x80008000u;
+            if constexpr (MODE == ENC_SIMD || MODE == ENC_SIMD_Y0) {
+                bad = bad || (((a2 + P.big2) & 0x80008000u) & ~sp) != 0u;
+                // a NaN/Inf lane's arithmetic can borrow across the 16-bit lane
+                // boundary: recompute the pair with that lane zeroed
+                if (sp) {
+                    const uint32_t keep = ~((sp >> 15) * 0xFFFFu);
+                    uint32_t am = 0;
+                    cp[t] = enc_pair_bf16<K, MODE == ENC_SIMD_Y0>(w[t] & keep, P, am);
+                }
+            } else   // y >= 7: per-element fp32 path on the widened elements
+                bad = bad || (!(sp & 0x8000u) && (a2 << 16) >= P.bigf) ||
+                      (!(sp & 0x80000000u) && (a2 & 0xFFFF0000u) >= P.bigf);
+        } else {
+            const uint32_t a0 = w[2 * t] & 0x7FFFFFFFu, a1 = w[2 * t + 1] & 0x7FFFFFFFu;
+            const bool s0 = a0 >= 0x7F800000u, s1 = a1 >= 0x7F800000u;
+            sp = (s0 ? 0x8000u : 0u) | (s1 ? 0x80000000u : 0u);
+            bad = bad || (!s0 && a0 >= P.bigf) || (!s1 && a1 >= P.bigf);
+        }
+        cp[t] &= ~((sp >> 15) * 0xFFFFu);
+        n += __popc(sp);
+    }
+    return bad ? -1 : n;
+}
+
+// add a thread's count of specials to *spc once per warp (kernel end)
+__device__ __forceinline__ void flush_special_count(unsigned long long *spc, unsigned long long nsp) {
+    const unsigned m = __activemask();
+    const unsigned long long t = __reduce_add_sync(m, (unsigned)nsp);
+    if (spc && t && (threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(spc, t);
 }
 
 template <bool BF16, int MODE>
@@ -495,6 +549,7 @@ __global__ void __launch_bounds__(BF16 ? EXMY_ENC_ROWS_THREADS : 256, BF16 ? EXM
     }
     // software pipeline: the next tile's 8 row chunks are in flight while
     // this tile is converted and packed
+    unsigned nsp = 0;   // NaN/Inf seen on the masked fast path
     uint32_t nxt[8][NW];
     int64_t g = blockIdx.y;
     if (g < G && act) {
@@ -536,11 +591,29 @@ __global__ void __launch_bounds__(BF16 ? EXMY_ENC_ROWS_THREADS : 256, BF16 ? EXM
                 RH[0][i] = (K == 9) ? prmt(cp[i][0] >> 1, cp[i][1] >> 1, 0x6420) : 0u;
             }
             rows_fast_store<K, 1, 0>(RL, RH, packed, so, g, C, c0);
-        } else {   // NaN/Inf in the tile (rare): integer path, records the specials
-            for (int v = 0; v < 4; ++v)
-                enc_container_generic<BF16, K>(in, C, g * C + c0 + v, 0, F, packed, so, spi, spb, spc, cap);
+        } else {   // NaN/Inf in the tile: masked fast codes, or the integer path for huge finite values
+            int ns = 0;
+#pragma unroll
+            for (int i = 0; i < 8 && ns >= 0; ++i) {
+                const int m = mask_special_codes<K, BF16, MODE, NW>(w[i], cp[i], P);
+                ns = m < 0 ? -1 : ns + m;
+            }
+            if (ns >= 0) {
+                nsp += (unsigned)ns;
+                uint32_t RL[1][8], RH[1][8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    RL[0][i] = prmt(cp[i][0], cp[i][1], 0x6420);
+                    RH[0][i] = (K == 9) ? prmt(cp[i][0] >> 1, cp[i][1] >> 1, 0x6420) : 0u;
+                }
+                rows_fast_store<K, 1, 0>(RL, RH, packed, so, g, C, c0);
+            } else {
+                for (int v = 0; v < 4; ++v)
+                    enc_container_generic<BF16, K>(in, C, g * C + c0 + v, 0, F, packed, so, spi, spb, spc, cap);
+            }
         }
     }
+    flush_special_count(spc, nsp);
 }
 
 // ---------------------------------------------------------- encode COLS
@@ -601,6 +674,7 @@ __global__ void __launch_bounds__(256) k_enc_cols_fast(const uint8_t *__restrict
             }
         return;
     }
+    unsigned nsp = 0;   // NaN/Inf seen on the masked fast path
     uint4 nxt[4][NV];
     int64_t base = gw * 128;
 #pragma unroll
@@ -650,12 +724,48 @@ __global__ void __launch_bounds__(256) k_enc_cols_fast(const uint8_t *__restrict
             }
             cols_fast_store<K, 0>(RL, RH, cp, packed, so, base + lane, NG);
         } else {
-            for (int u = 0; u < 4; ++u) {
-                const int64_t q = base + 32 * u + lane;
-                if (q < NG) enc_container_generic<BF16, K>(in, 0, q, 1, F, packed, so, spi, spb, spc, cap);
+            // NaN/Inf: masked fast codes per group, or the integer path (huge finite values)
+            int ns = 0;
+#pragma unroll
+            for (int u = 0; u < 4 && ns >= 0; ++u) {
+#pragma unroll
+                for (int t = 0; t < NV && ns >= 0; ++t) {
+                    const uint32_t ww[4] = {r[u][t].x, r[u][t].y, r[u][t].z, r[u][t].w};
+                    uint32_t c2[NP];
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) c2[p] = cp[u][t * NP + p];
+                    const int m = mask_special_codes<K, BF16, MODE, 4>(ww, c2, P);
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) cp[u][t * NP + p] = c2[p];
+                    ns = m < 0 ? -1 : ns + m;
+                }
+            }
+            if (ns >= 0) {
+                // groups past the end were loaded as zeros: no specials counted there
+                nsp += (unsigned)ns;
+                uint32_t RL[8], RH[8];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const uint32_t y01 = prmt(cp[0][t], cp[1][t], 0x6420), y23 = prmt(cp[2][t], cp[3][t], 0x6420);
+                    RL[2 * t] = prmt(y01, y23, 0x6420);
+                    RL[2 * t + 1] = prmt(y01, y23, 0x7531);
+                    if (K == 9) {
+                        const uint32_t h01 = prmt(cp[0][t] >> 1, cp[1][t] >> 1, 0x6420);
+                        const uint32_t h23 = prmt(cp[2][t] >> 1, cp[3][t] >> 1, 0x6420);
+                        RH[2 * t] = prmt(h01, h23, 0x6420);
+                        RH[2 * t + 1] = prmt(h01, h23, 0x7531);
+                    }
+                }
+                cols_fast_store<K, 0>(RL, RH, cp, packed, so, base + lane, NG);
+            } else {
+                for (int u = 0; u < 4; ++u) {
+                    const int64_t q = base + 32 * u + lane;
+                    if (q < NG) enc_container_generic<BF16, K>(in, 0, q, 1, F, packed, so, spi, spb, spc, cap);
+                }
             }
         }
     }
+    flush_special_count(spc, nsp);
 }
 
 }  // namespace exmy

@@ -5,9 +5,16 @@
 // whose top is G.
 //   encode: u = RN32(v * RN32(G / A1) * 2^-p)         (FMUL when the factor is
 //           a normal fp32, else one fp64 product), code = e_max-127 code of u
-//   decode: g = RN32(code value at e_max 127), s_hi = RN32(amax / G),
-//           s_lo = RN32((amax - s_hi G) / G), out = RN32(g s_hi + RN32(g s_lo))
-//           (one FMUL + one FFMA per element)
+//   decode: out = RN32(g amax / G), g the code's exact value at e_max 127.
+//           Computed as RN32(g s_hi + RN32(g s_lo)) with s_hi = RN32(amax/G),
+//           s_lo = RN32((amax - s_hi G) / G) (one FMUL + one FFMA per
+//           element): its relative error <= 2^-47 cannot move a result
+//           >= 2^-100 across a rounding boundary, because g amax / G is either
+//           an fp32 value (an exact binary fraction has the integer
+//           significand M_g M_a / M_G < 2^24) or >= 2^-34 (relative) away
+//           from every fp32 midpoint.  Smaller results (fp32 subnormals, tiny
+//           maxima) and x = 8 codes below the fp32 range take fs_out_exact,
+//           the integer evaluation of the definition.
 // so the block maximum decodes to exactly amax.
 #pragma once
 #include "exmy_blocked.cuh"
@@ -18,7 +25,55 @@ namespace exmy {
 struct FsMap {
     const float *amax;
     int64_t br, bc, nbc;
+    float tchk;   // rows / blocks with s_hi < tchk may produce results < 2^-100: per-element check
+    int x8;       // x = 8: codes below the fp32 range, every element takes fs_out_exact
 };
+
+// RN32(g * amax / G) evaluated with integers (reading D23's definition), for
+// the results the FMUL + FFMA decode cannot guarantee.  mag = the code's
+// magnitude bits, amax = the block's fp32 maximum (bits, positive).  Returns
+// the result's magnitude bits; the caller attaches the code's sign.
+//   g = M_g 2^eg, amax = M_a 2^ea, G = M_G 2^eG  ->  (M_g M_a / M_G) 2^(eg+ea-eG),
+// the quotient taken to >= 54 bits plus a sticky remainder, then rounded once
+// at the fp32 quantum (2^-149 in the subnormal range), ties to even.
+__device__ __noinline__ uint32_t fs_out_exact(uint32_t mag, uint32_t amax, int x, int y) {
+    if (mag == 0u || amax == 0u) return 0u;
+    const int bias = (1 << x) - 1;                               // e_max 127 (D1)
+    const uint32_t e = x == 0 ? 0u : (mag >> y), m = mag & ((1u << y) - 1u);
+    const uint32_t Mg = e ? ((1u << y) | m) : m;
+    const int eg = e ? (int)e - bias - y : 1 - bias - y;
+    const uint32_t MG = x >= 1 ? (2u << y) - 1u : (1u << y) - 1u;   // G's integer significand
+    const int eG = x >= 1 ? -y : 1 - y;
+    const uint32_t Ea = amax >> 23, fa = amax & 0x7FFFFFu;
+    const uint32_t Ma = Ea ? (fa | 0x800000u) : fa;
+    const int ea = Ea ? (int)Ea - 150 : -149;
+    const unsigned long long N = (unsigned long long)Mg * Ma;    // < 2^33, > 0
+    const int L = __clzll((long long)N) - 1;                     // N << L in [2^62, 2^63)
+    const unsigned long long num = N << L;
+    const unsigned long long q = num / MG, rem = num - q * MG;   // q >= 2^53
+    const int E0 = eg + ea - eG - L;                             // value = (q + rem / MG) 2^E0
+    const int b = 64 - __clzll((long long)q);
+    int qe = E0 + b - 24;                                        // quantum of a 24-bit significand
+    if (qe < -149) qe = -149;
+    const int sh = qe - E0;                                      // >= b - 24
+    if (sh > b) return 0u;                                       // below half the quantum
+    unsigned long long kept, r;
+    if (sh >= 64) {
+        kept = 0ull;
+        r = q;
+    } else {
+        kept = q >> sh;
+        r = q & ((1ull << sh) - 1ull);
+    }
+    const unsigned long long half = 1ull << (sh - 1);
+    if (r > half || (r == half && (rem != 0ull || (kept & 1ull)))) ++kept;
+    if (kept >= (1ull << 24)) {                                  // carry into the next binade
+        kept >>= 1;
+        ++qe;
+    }
+    if (kept >= (1ull << 23)) return ((uint32_t)(qe + 150) << 23) | ((uint32_t)kept - 0x800000u);
+    return (uint32_t)kept;                                       // fp32 subnormal (qe = -149)
+}
 
 __device__ __forceinline__ uint32_t fs_amax_at(const FsMap &S, int64_t r, int64_t c) {
     return __float_as_uint(__ldg(S.amax + (r / S.br) * S.nbc + c / S.bc)) & 0x7FFFFFFFu;
@@ -222,7 +277,11 @@ __device__ __noinline__ void fs_dec_container(const uint8_t *__restrict__ packed
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const uint32_t o = fs_out(dec_code_generic<24>(c[i], F), fs_dec(fs_amax_at(S, e[i] / C, e[i] % C), G));
+        const uint32_t am = fs_amax_at(S, e[i] / C, e[i] % C);
+        uint32_t o = fs_out(dec_code_generic<24>(c[i], F), fs_dec(am, G));
+        const uint32_t mag = c[i] & F.M;
+        if (mag != 0u && (S.x8 || (o & 0x7FFFFFFFu) < 0x0D800000u))   // results < 2^-100: the definition itself
+            o = fs_out_exact(mag, am, x, y) | (o & 0x80000000u);
         if (OBF16) {
             const uint16_t h = (uint16_t)f32_to_bf16_bits(o);
             memcpy(out + 2 * e[i], &h, 2);
@@ -248,7 +307,7 @@ __global__ void k_fs_decode_generic(const uint8_t *__restrict__ packed, int64_t 
 // integer code path.
 template <bool BF16, bool FAST>
 __device__ __forceinline__ uint32_t fs_quant_elem(uint32_t u, const FsE &fe, const FsD &fd, const Fmt &F,
-                                                  const FastP &P) {
+                                                  const FastP &P, const FsMap &S, uint32_t am) {
     if (is_special_f32(u)) return u;
     const uint32_t us = fs_in(u, fe);
     uint32_t g;
@@ -258,7 +317,11 @@ __device__ __forceinline__ uint32_t fs_quant_elem(uint32_t u, const FsE &fe, con
     } else {
         g = dec_code_generic<24>(enc_code_generic(us, F), F);
     }
-    const uint32_t o = fs_out(g, fd);
+    uint32_t o = fs_out(g, fd);
+    if ((o & 0x7FFFFFFFu) < 0x0D800000u || S.x8) {   // tiny results / x = 8: the definition itself
+        const uint32_t mag = enc_code_generic(us, F) & F.M;
+        if (mag != 0u) o = fs_out_exact(mag, am, F.x, F.y) | (o & 0x80000000u);
+    }
     return BF16 ? (f32_to_bf16_bits(o) << 16) : o;
 }
 
@@ -292,9 +355,9 @@ __global__ void __launch_bounds__(256) k_fs_quant(const uint8_t *__restrict__ in
         const int lane = threadIdx.x & 31;
         const float *scol = S.amax + ((act ? j : 0) * V) / S.bc;
         for (int64_t g = blockIdx.y; g < R / 8; g += gridDim.y) {
-            const uint32_t am = __float_as_uint(__ldg(scol + fs_rb(S, 8 * g + (lane & 7)) * S.nbc)) & 0x7FFFFFFFu;
-            const FsE fe0 = fs_enc(am, G);
-            const FsD fd0 = fs_dec(am, G);
+            const uint32_t am0 = __float_as_uint(__ldg(scol + fs_rb(S, 8 * g + (lane & 7)) * S.nbc)) & 0x7FFFFFFFu;
+            const FsE fe0 = fs_enc(am0, G);
+            const FsD fd0 = fs_dec(am0, G);
             uint4 q[8];
             if (act) {
 #pragma unroll
@@ -310,11 +373,12 @@ __global__ void __launch_bounds__(256) k_fs_quant(const uint8_t *__restrict__ in
                 FsD fd;
                 fd.hi = __shfl_sync(0xFFFFFFFFu, fd0.hi, i);
                 fd.lo = __shfl_sync(0xFFFFFFFFu, fd0.lo, i);
+                const uint32_t am = __shfl_sync(0xFFFFFFFFu, am0, i);
                 if (!act) continue;
                 uint32_t w[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
 #pragma unroll
                 for (int v = 0; v < V; ++v)
-                    fs_put<BF16>(w, v, fs_quant_elem<BF16, FAST>(vec_elem<BF16>(q[i], v), fe, fd, F, P));
+                    fs_put<BF16>(w, v, fs_quant_elem<BF16, FAST>(vec_elem<BF16>(q[i], v), fe, fd, F, P, S, am));
                 stg_v4(out + ((8 * g + i) * C + j * V) * EL::ES, make_uint4(w[0], w[1], w[2], w[3]));
             }
         }
@@ -331,7 +395,8 @@ __global__ void __launch_bounds__(256) k_fs_quant(const uint8_t *__restrict__ in
             const FsD fd = fs_dec(am, G);
             uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-            for (int v = 0; v < V; ++v) fs_put<BF16>(w, v, fs_quant_elem<BF16, FAST>(vec_elem<BF16>(q, v), fe, fd, F, P));
+            for (int v = 0; v < V; ++v)
+                fs_put<BF16>(w, v, fs_quant_elem<BF16, FAST>(vec_elem<BF16>(q, v), fe, fd, F, P, S, am));
             stg_v4(out + off, make_uint4(w[0], w[1], w[2], w[3]));
         }
     } else {
@@ -344,7 +409,7 @@ __global__ void __launch_bounds__(256) k_fs_quant(const uint8_t *__restrict__ in
             for (int v = 0; v < V; ++v) {
                 const int64_t e = vi * V + v;
                 const uint32_t am = fs_amax_at(S, e / C, e % C);
-                fs_put<BF16>(w, v, fs_quant_elem<BF16, FAST>(vec_elem<BF16>(q, v), fs_enc(am, G), fs_dec(am, G), F, P));
+                fs_put<BF16>(w, v, fs_quant_elem<BF16, FAST>(vec_elem<BF16>(q, v), fs_enc(am, G), fs_dec(am, G), F, P, S, am));
             }
             stg_v4(out + vi * 16, make_uint4(w[0], w[1], w[2], w[3]));
         }
@@ -500,6 +565,11 @@ __global__ void __launch_bounds__(256) k_fs_dec_rows(const uint8_t *__restrict__
 #pragma unroll
         for (int i = 0; i < 8; ++i) { RL[0][i] = 0; RH[0][i] = 0; }
         rows_unpack_raw<K, 1, 0>(raw, RL, RH);
+        // rows whose smallest non-zero result could fall below 2^-100 (or x = 8)
+        // take the checked variant: results < 2^-100 from the definition itself
+        bool chk = S.x8 != 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) chk = chk || hi[i] < S.tchk;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             uint32_t o[4];
@@ -509,7 +579,13 @@ __global__ void __launch_bounds__(256) k_fs_dec_rows(const uint8_t *__restrict__
                 if (K == 9) code |= ((RH[0][i] >> (8 * v)) & 0xFFu) << 1;
                 const uint32_t gb = FAST ? dec_f32_fast<K, false>(code, P, y) : dec_code_generic<24>(code, F);
                 const float gf = __uint_as_float(gb & 0x7FFFFFFFu);
-                o[v] = __float_as_uint(__fmaf_rn(gf, hi[i], __fmul_rn(gf, lo[i]))) | (gb & 0x80000000u);
+                uint32_t r = __float_as_uint(__fmaf_rn(gf, hi[i], __fmul_rn(gf, lo[i])));
+                if (chk) {
+                    const uint32_t mag = code & F.M;
+                    if (mag != 0u && (S.x8 || r < 0x0D800000u))
+                        r = fs_out_exact(mag, fs_amax_at(S, 8 * g + i, c0), x, y);
+                }
+                o[v] = r | ((code << (32 - K)) & 0x80000000u);
             }
             uint8_t *dst = out + ((8 * g + i) * C + c0) * EL::ES;
             if (OBF16)

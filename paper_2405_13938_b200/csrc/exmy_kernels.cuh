@@ -9,6 +9,8 @@
 //   K4  k_decode_rows / k_decode_cols / k_decode_generic
 //   K5  k_specials_sort / k_specials_scatter   out-of-band NaN/Inf (D9)
 #pragma once
+#include <cooperative_groups.h>
+
 #include "exmy_device.cuh"
 
 namespace exmy {
@@ -29,10 +31,22 @@ __device__ __forceinline__ uint32_t vec_elem(const uint4 &r, int v) {
     return w[v];
 }
 
+// Out-of-band NaN/Inf (D9).  The per-tensor encode kernels only COUNT them
+// here (sp_index == NULL: one warp-aggregated atomic per call site and warp,
+// not one per element) and the index-ordered list is written afterwards by
+// k_specials_count + k_specials_write (deterministic stream compaction, no
+// sort).  The grouped kernels pass their per-entry lists and append directly
+// (then k_grouped_sort orders them).
 __device__ __forceinline__ void push_special(int64_t idx, uint32_t bits, int64_t *sp_index,
                                              uint32_t *sp_bits, unsigned long long *sp_count,
                                              int64_t cap) {
     if (!sp_count) return;
+    if (!sp_index) {
+        const unsigned m = __activemask();
+        const int lane = threadIdx.x & 31;
+        if (lane == __ffs(m) - 1) atomicAdd(sp_count, (unsigned long long)__popc(m));
+        return;
+    }
     unsigned long long slot = atomicAdd(sp_count, 1ull);
     if ((long long)slot < cap) {
         sp_index[slot] = idx;
@@ -103,6 +117,33 @@ __device__ __forceinline__ void red_shared_add(uint32_t addr, uint32_t v) {
                     // counters per 4 warps) need ~2x12 vectors in flight per lane to cover HBM latency
                     // (config 2 bf16: U=4 114.0 us, 8 105.2, 12 103.1; fp32 200.9 -> 156.6 us)
 #endif
+// MODE 3 (default): LANE-PAIR counters.  Lanes 2j and 2j+1 share the 32-bit
+// word [bin][j] of their warp's 16 KB (256 bins x 16 words), lane 2j counting
+// in the low half and 2j+1 in the high half, so each lane's increment is a
+// constant (1 or 0x10000) and an element costs only the bin's byte offset
+// (bin * 64: one shift + mask, both bf16 elements of a word at once) and
+// its reduction -- MODE 2 spent two more ALU ops per element choosing the
+// half by the exponent's LSB and was ALU-bound (ncu: ALU pipe 78 %, issue
+// 65 %).  The price: the two lanes of a pair hit the same bank when their
+// bins have equal parity (at most 2-way).  Counters stay lane-private, so
+// the 16-bit epochs and flushes are MODE 2's.
+__device__ __forceinline__ void hist3_flush_warp(uint32_t *warpbase, int lane, unsigned long long *hist) {
+    __syncwarp();
+#pragma unroll 1
+    for (int b = lane; b < 256; b += 32) {
+        uint32_t c = 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const uint32_t v = warpbase[b * 16 + j];
+            c += (v & 0xFFFFu) + (v >> 16);
+        }
+        if (c) atomicAdd(hist + b, (unsigned long long)c);
+    }
+    __syncwarp();
+    for (int i = lane; i < HIST_WORDS_PER_WARP; i += 32) warpbase[i] = 0;
+    __syncwarp();
+}
+
 template <bool BF16, int MODE>
 __global__ void __launch_bounds__(HIST_THREADS) k_hist(const uint8_t *__restrict__ in, int64_t n,
                                                        unsigned long long *__restrict__ hist) {
@@ -111,7 +152,10 @@ __global__ void __launch_bounds__(HIST_THREADS) k_hist(const uint8_t *__restrict
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t *warpbase = hsm + warp * HIST_WORDS_PER_WARP;
     uint32_t *lanebase = warpbase + lane;
-    const uint32_t lane_sa = (uint32_t)__cvta_generic_to_shared(lanebase);   // shared-window byte address
+    // MODE 3: this lane's word of each bin row and its constant half increment
+    const uint32_t lane_sa = MODE == 3 ? (uint32_t)__cvta_generic_to_shared(warpbase + (lane >> 1))
+                                       : (uint32_t)__cvta_generic_to_shared(lanebase);   // shared-window byte address
+    const uint32_t inc3 = (lane & 1) ? 0x10000u : 1u;
     for (int i = threadIdx.x; i < HIST_WARPS * HIST_WORDS_PER_WARP; i += HIST_THREADS) hsm[i] = 0;
     __syncthreads();
 
@@ -146,7 +190,15 @@ __global__ void __launch_bounds__(HIST_THREADS) k_hist(const uint8_t *__restrict
                 const uint32_t w[4] = {r[u].x, r[u].y, r[u].z, r[u].w};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    if (BF16 && MODE == 2) {
+                    if (MODE == 3) {
+                        if (BF16) {   // both elements' bin * 64 from one shift + mask
+                            const uint32_t off = (w[q] >> 1) & 0x3FC03FC0u;
+                            red_shared_add(lane_sa + (off & 0xFFFFu), inc3);
+                            red_shared_add(lane_sa + (off >> 16), inc3);
+                        } else {
+                            red_shared_add(lane_sa + ((w[q] >> 17) & 0x3FC0u), inc3);
+                        }
+                    } else if (BF16 && MODE == 2) {
                         const uint32_t off = (w[q] >> 1) & 0x3F803F80u;   // both elements' word offsets (bytes)
                         const uint32_t inc_lo = (w[q] & 0x80u) ? 0x10000u : 1u;
                         const uint32_t inc_hi = (w[q] & 0x800000u) ? 0x10000u : 1u;
@@ -165,7 +217,8 @@ __global__ void __launch_bounds__(HIST_THREADS) k_hist(const uint8_t *__restrict
             }
         }
         if (++epoch == EPOCH_VECS) {
-            hist_flush_warp(warpbase, lane, hist);
+            if (MODE == 3) hist3_flush_warp(warpbase, lane, hist);
+            else hist_flush_warp(warpbase, lane, hist);
             epoch = 0;
         }
     }
@@ -174,16 +227,25 @@ __global__ void __launch_bounds__(HIST_THREADS) k_hist(const uint8_t *__restrict
         int64_t t0 = nvec * EL::V;
         for (int64_t i = t0 + lane; i < n; i += 32) {
             uint32_t u = BF16 ? ((uint32_t)((const uint16_t *)in)[i] << 16) : ((const uint32_t *)in)[i];
-            hist_bump(lanebase, (u >> 23) & 0xFFu, 1);
+            if (MODE == 3) atomicAdd(warpbase + ((u >> 23) & 0xFFu) * 16 + (lane >> 1), inc3);
+            else hist_bump(lanebase, (u >> 23) & 0xFFu, 1);
         }
     }
     __syncthreads();
     // block-level reduction: thread t owns bins t and t+128
     for (int b = threadIdx.x; b < 256; b += HIST_THREADS) {
-        uint32_t wd = b >> 1, sh = (b & 1) << 4;
         unsigned long long s = 0;
-        for (int w = 0; w < HIST_WARPS; ++w)
-            for (int l = 0; l < 32; ++l) s += (hsm[w * HIST_WORDS_PER_WARP + wd * 32 + l] >> sh) & 0xFFFFu;
+        if (MODE == 3) {
+            for (int w = 0; w < HIST_WARPS; ++w)
+                for (int j = 0; j < 16; ++j) {
+                    const uint32_t v = hsm[w * HIST_WORDS_PER_WARP + b * 16 + j];
+                    s += (v & 0xFFFFu) + (v >> 16);
+                }
+        } else {
+            const uint32_t wd = b >> 1, sh = (b & 1) << 4;
+            for (int w = 0; w < HIST_WARPS; ++w)
+                for (int l = 0; l < 32; ++l) s += (hsm[w * HIST_WORDS_PER_WARP + wd * 32 + l] >> sh) & 0xFFFFu;
+        }
         if (s) atomicAdd(hist + b, s);
     }
 }
@@ -807,6 +869,141 @@ static __global__ void __launch_bounds__(1024) k_specials_sort(int64_t *idx, uin
         return;
     }
     flip_bitonic((volatile long long *)idx, (volatile uint32_t *)bits, cnt);
+}
+
+// ------------------------------------------- K5 ordered specials list
+// Deterministic stream compaction of the NaN/Inf elements into (index,
+// fp32 bits) in ascending index order, after an encode counted them in
+// ws[0] (include/exmy.h: sp_count is a workspace of EXMY_SPECIALS_WORDS
+// words).  The tensor is cut into nr <= SPECIALS_RANGES contiguous ranges of
+// L elements (L % 8 == 0), one CTA each:
+//   k_specials_count  ws[1 + b] := number of specials in range b
+//   k_specials_write  CTA b writes its specials at positions
+//                     sum_{j<b} ws[1+j] + (rank inside the range), the rank
+//                     from a CTA-wide exclusive scan, only those < capacity.
+// Both phases run in one cooperative launch (k_specials_compact) that returns
+// at once when ws[0] == 0 (the usual case: no re-read), and a range whose
+// first position is past the capacity is never re-read.
+constexpr int SPECIALS_RANGES = 1024;
+
+template <bool BF16>
+__device__ __forceinline__ uint32_t elem_bits(const uint8_t *in, int64_t e) {
+    return BF16 ? ((uint32_t)((const uint16_t *)in)[e] << 16) : ((const uint32_t *)in)[e];
+}
+
+// 8-bit mask of the specials among elements e .. e + 7 (all < n)
+template <bool BF16>
+__device__ __forceinline__ uint32_t special_mask8(const uint8_t *in, int64_t e, bool vec) {
+    uint32_t m = 0;
+    if (vec) {
+        if (BF16) {
+            const uint4 q = ldg_nc_v4(in + e * 2);
+            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const uint32_t h = ((w[t] & 0x7F807F80u) + 0x00800080u) & 0x80008000u;   // bit 15 / 31: exponent 255
+                m |= ((h >> 15) & 1u) << (2 * t) | ((h >> 31) & 1u) << (2 * t + 1);
+            }
+        } else {
+            const uint4 a = ldg_nc_v4(in + e * 4), b = ldg_nc_v4(in + e * 4 + 16);
+            const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int t = 0; t < 8; ++t) m |= (uint32_t)((w[t] & 0x7F800000u) == 0x7F800000u) << t;
+        }
+    } else {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) m |= (uint32_t)is_special_f32(elem_bits<BF16>(in, e + t)) << t;
+    }
+    return m;
+}
+
+// one cooperative launch of <= nr CTAs (grid-stride over the ranges):
+// phase 1 counts every range, a grid-wide barrier, phase 2 writes.  With no
+// NaN/Inf (ws[0] == 0) every CTA returns at once: a single short launch.
+template <bool BF16>
+__global__ void __launch_bounds__(256) k_specials_compact(const uint8_t *__restrict__ in, int64_t n, int64_t L,
+                                                          int nr, int64_t elem_offset,
+                                                          unsigned long long *__restrict__ ws,
+                                                          int64_t *__restrict__ spi, uint32_t *__restrict__ spb,
+                                                          int64_t cap) {
+    if (ws[0] == 0ull) return;                       // uniform over the grid
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
+    const bool vec = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+    __shared__ uint32_t wsum[8];
+    __shared__ unsigned long long s_prefix;
+    // ---- phase 1: ws[1 + b] := specials in range b
+    for (int b = blockIdx.x; b < nr; b += gridDim.x) {
+        const int64_t e0 = (int64_t)b * L, e1 = min(n, e0 + L);
+        uint32_t c = 0;
+        const int64_t full = e0 + ((e1 - e0) / 8) * 8;
+        for (int64_t e = e0 + 8 * (int64_t)threadIdx.x; e < full; e += 8 * (int64_t)blockDim.x)
+            c += __popc(special_mask8<BF16>(in, e, vec));
+        for (int64_t e = full + threadIdx.x; e < e1; e += blockDim.x) c += is_special_f32(elem_bits<BF16>(in, e));
+        c = __reduce_add_sync(0xFFFFFFFFu, c);
+        if (lane == 0) wsum[warp] = c;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long t = 0;
+            for (int w = 0; w < nw; ++w) t += wsum[w];
+            ws[1 + b] = t;
+        }
+        __syncthreads();
+    }
+    cooperative_groups::this_grid().sync();
+    // ---- phase 2: each range's specials at sum_{j<b} ws[1+j] + rank, up to the capacity
+    for (int b = blockIdx.x; b < nr; b += gridDim.x) {
+        if (warp == 0) {
+            unsigned long long p = 0;
+            for (int j = lane; j < b; j += 32) p += ws[1 + j];
+#pragma unroll
+            for (int o = 16; o; o >>= 1) p += __shfl_xor_sync(0xFFFFFFFFu, p, o);
+            if (lane == 0) s_prefix = p;
+        }
+        __syncthreads();
+        const unsigned long long prefix = s_prefix;
+        __syncthreads();
+        if ((long long)prefix >= cap) break;          // later ranges start even further on
+        if (ws[1 + b] == 0ull) continue;
+        const int64_t e0 = (int64_t)b * L, e1 = min(n, e0 + L);
+        unsigned long long run = prefix;   // position of the chunk's first special
+        for (int64_t c0 = e0; c0 < e1; c0 += 8 * (int64_t)blockDim.x) {
+            const int64_t e = c0 + 8 * (int64_t)threadIdx.x;
+            uint32_t m = 0;
+            if (e + 8 <= e1) {
+                m = special_mask8<BF16>(in, e, vec);
+            } else {
+                for (int t = 0; t < 8 && e + t < e1; ++t) m |= (uint32_t)is_special_f32(elem_bits<BF16>(in, e + t)) << t;
+            }
+            const uint32_t cnt = __popc(m);
+            // CTA-wide exclusive scan of cnt (thread order = element order)
+            uint32_t incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            if (lane == 31) wsum[warp] = incl;
+            __syncthreads();
+            uint32_t before = 0, total = 0;
+            for (int w = 0; w < nw; ++w) {
+                before += (w < warp) ? wsum[w] : 0u;
+                total += wsum[w];
+            }
+            unsigned long long pos = run + before + (incl - cnt);
+            while (m) {
+                const int t = __ffs(m) - 1;
+                m &= m - 1;
+                if ((long long)pos < cap) {
+                    spi[pos] = elem_offset + e + t;
+                    spb[pos] = elem_bits<BF16>(in, e + t);
+                }
+                ++pos;
+            }
+            run += total;
+            __syncthreads();   // wsum reuse
+            if ((long long)run >= cap) break;
+        }
+    }
 }
 
 template <bool OBF16>

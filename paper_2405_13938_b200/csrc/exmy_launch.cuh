@@ -13,6 +13,7 @@ namespace exmy {
 extern int g_force_generic;   // exmy_debug_force_generic
 extern int g_hist_mode;       // exmy_debug_hist_mode
 extern int g_hist_blocks;     // exmy_debug_hist_blocks
+extern int g_enc_tma;         // exmy_debug_enc_tma: ROWS encode through the TMA-staged kernel
 
 inline int num_sms() {
     static int cache[64] = {0};
@@ -73,6 +74,8 @@ exmy_status launch_encode(const uint8_t *in, bool bf16, int64_t R, int64_t C, in
                           unsigned long long *spc, int64_t cap, cudaStream_t st);
 exmy_status launch_specials_sort(int64_t *spi, uint32_t *spb, const unsigned long long *spc, int64_t cap,
                                  cudaStream_t st);
+exmy_status launch_specials_compact(const uint8_t *in, bool bf16, int64_t n, int64_t elem_offset, int64_t *spi,
+                                    uint32_t *spb, unsigned long long *ws, int64_t cap, cudaStream_t st);
 exmy_status launch_decode(const uint8_t *packed, int64_t R, int64_t C, int axis, int x, int y,
                           const uint8_t *meta, uint8_t *out, bool obf16, cudaStream_t st);
 exmy_status launch_specials_scatter(const int64_t *spi, const uint32_t *spb, const unsigned long long *spc,

@@ -1,5 +1,6 @@
-// exmy_tu_encode.cu -- K3 encode launchers (+ K5 specials sort).
+// exmy_tu_encode.cu -- K3 encode launchers (+ K5 specials list).
 #include "exmy_launch.cuh"
+#include "exmy_tma.cuh"
 
 namespace exmy {
 
@@ -15,6 +16,22 @@ exmy_status launch_encode_km(const uint8_t *in, int64_t R, int64_t C, int axis, 
         // (8 rows of one row group must span < 4 GiB: the kernel uses 32-bit row offsets)
         vec = aligned(in, 4 * Elem<BF16>::ES) && (C % 4 == 0) && (8 * C * Elem<BF16>::ES <= (int64_t)UINT32_MAX);
         for (int s = 0; s < p.nseg; ++s) vec = vec && aligned(packed + p.so.off[s], p.w[s] == 8 ? 4 : 4 * p.w[s]);
+        if (vec && g_enc_tma && aligned(in, 16) && (C % 8 == 0)) {
+            // TMA-staged persistent kernel (exmy_tma.cuh): bulk copies need 16-byte rows / offsets
+            constexpr int smem = etma_smem<BF16>();
+            static int occ = 0;
+            if (!occ) {
+                cudaFuncSetAttribute(k_enc_rows_tma<K, BF16, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                occ = occupancy(k_enc_rows_tma<K, BF16, MODE>, ETMA_THREADS, smem);
+            }
+            const int64_t T = (R / 8) * cdiv(C, ETMA_TC);
+            int64_t blocks = (int64_t)num_sms() * (occ > 0 ? occ : 1);
+            if (blocks > T) blocks = T;
+            if (blocks < 1) blocks = 1;
+            k_enc_rows_tma<K, BF16, MODE><<<(unsigned)blocks, ETMA_THREADS, smem, st>>>(
+                in, R, C, x, y, meta, packed, p.so, spi, spb, spc, cap, g_force_generic);
+            return launch_status();
+        }
         if (vec) {
             const int threads = BF16 ? EXMY_ENC_ROWS_THREADS : 256;
             static int occ = 0;
@@ -108,6 +125,32 @@ exmy_status launch_specials_sort(int64_t *spi, uint32_t *spb, const unsigned lon
                                  cudaStream_t st) {
     k_specials_sort<<<1, 1024, 0, st>>>(spi, spb, spc, cap);
     return launch_status();
+}
+
+// the index-ordered specials list of a tensor of n elements (see
+// k_specials_count / k_specials_write); ws = the sp_count workspace whose
+// word 0 the encode kernel filled with the total count
+exmy_status launch_specials_compact(const uint8_t *in, bool bf16, int64_t n, int64_t elem_offset, int64_t *spi,
+                                    uint32_t *spb, unsigned long long *ws, int64_t cap, cudaStream_t st) {
+    if (n <= 0 || cap <= 0 || !spi || !spb || !ws) return EXMY_OK;
+    int64_t nr = cdiv(n, 8192);
+    if (nr > SPECIALS_RANGES) nr = SPECIALS_RANGES;
+    if (nr < 1) nr = 1;
+    const int64_t L = cdiv(cdiv(n, nr), 8) * 8;
+    nr = cdiv(n, L);
+    static int occ_b = 0, occ_f = 0;
+    if (!occ_b) occ_b = occupancy(k_specials_compact<true>, 256, 0);
+    if (!occ_f) occ_f = occupancy(k_specials_compact<false>, 256, 0);
+    int64_t grid = (int64_t)num_sms() * (bf16 ? occ_b : occ_f);   // co-resident: the grid barrier needs it
+    if (grid > nr) grid = nr;
+    if (grid < 1) grid = 1;
+    int nri = (int)nr;
+    void *args[] = {(void *)&in, (void *)&n, (void *)&L, (void *)&nri, (void *)&elem_offset, (void *)&ws,
+                    (void *)&spi, (void *)&spb, (void *)&cap};
+    const void *fn = bf16 ? (const void *)k_specials_compact<true> : (const void *)k_specials_compact<false>;
+    if (cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(256), args, 0, st) != cudaSuccess)
+        return EXMY_E_CUDA;
+    return EXMY_OK;
 }
 
 }  // namespace exmy

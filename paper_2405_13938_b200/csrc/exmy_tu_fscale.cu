@@ -27,6 +27,16 @@ float grid_top(int x, int y) {
     return x >= 1 ? (float)(2.0 - std::ldexp(1.0, -y)) : (float)(std::ldexp((double)((1 << y) - 1), 1 - y));
 }
 
+// the float-scale map of a call: rows / blocks with s_hi = amax / G below
+// tchk = 2^-99 / g_min (g_min = the smallest non-zero grid value at e_max 127)
+// can produce results below 2^-100, which the kernels evaluate exactly
+FsMap fs_map(const float *scale, int64_t rows, int64_t cols, int64_t br, int64_t bc, int x, int y) {
+    (void)rows;
+    const int lg_gmin = x >= 1 ? 2 - (1 << x) - y : 1 - y;
+    const double t = std::ldexp(1.0, -99 - lg_gmin);
+    return FsMap{scale, br, bc, cols / bc, t > 3.0e38 ? INFINITY : (float)t, x == 8 ? 1 : 0};
+}
+
 unsigned grid1(int64_t work, int per_sm) {
     int64_t b = cdiv(work, 256);
     const int64_t m = (int64_t)num_sms() * per_sm;
@@ -175,7 +185,7 @@ exmy_status exmy_quantize_fs(const void *in, void *out, int dtype, int64_t rows,
     if (!in || !out || !scale) return EXMY_E_ARG;
     const int V = dtype == EXMY_BF16 ? 8 : 4;
     if (!aligned(in, 16) || !aligned(out, 16) || (rows * cols) % V) return EXMY_E_ALIGN;
-    const FsMap M{scale, block_rows, block_cols, cols / block_cols};
+    const FsMap M = fs_map(scale, rows, cols, block_rows, block_cols, x, y);
     const float G = grid_top(x, y);
     const int mode = (cols % V == 0 && block_cols % V == 0) ? ((rows % 8 == 0 && block_cols % (32 * V) == 0) ? 2 : 1) : 0;
     const auto *pi = static_cast<const uint8_t *>(in);
@@ -230,17 +240,16 @@ exmy_status exmy_encode_fs(const void *in, int dtype, int64_t rows, int64_t cols
     if (!in || !packed || !scale) return EXMY_E_ARG;
     const int k = 1 + x + y;
     const Plan p = make_plan(k, rows * cols);
-    const FsMap M{scale, block_rows, block_cols, cols / block_cols};
+    const FsMap M = fs_map(scale, rows, cols, block_rows, block_cols, x, y);
     const float G = grid_top(x, y);
     const auto *pi = static_cast<const uint8_t *>(in);
     exmy_status s = dtype == EXMY_BF16
-                        ? enc_dispatch<true>(k, pi, rows, cols, axis, x, y, M, G, packed, p, sp_index, sp_bits, spc,
-                                             sp_capacity, st)
-                        : enc_dispatch<false>(k, pi, rows, cols, axis, x, y, M, G, packed, p, sp_index, sp_bits, spc,
-                                              sp_capacity, st);
+                        ? enc_dispatch<true>(k, pi, rows, cols, axis, x, y, M, G, packed, p, nullptr, nullptr, spc, 0,
+                                             st)
+                        : enc_dispatch<false>(k, pi, rows, cols, axis, x, y, M, G, packed, p, nullptr, nullptr, spc, 0,
+                                              st);
     if (s != EXMY_OK) return s;
-    if (spc && sp_capacity > 1) s = launch_specials_sort(sp_index, sp_bits, spc, sp_capacity, st);
-    return s;
+    return launch_specials_compact(pi, dtype == EXMY_BF16, rows * cols, 0, sp_index, sp_bits, spc, sp_capacity, st);
 }
 
 exmy_status exmy_decode_fs(const uint8_t *packed, int64_t rows, int64_t cols, int axis, int64_t block_rows,
@@ -257,7 +266,7 @@ exmy_status exmy_decode_fs(const uint8_t *packed, int64_t rows, int64_t cols, in
     if (!packed || !out || !scale) return EXMY_E_ARG;
     const int k = 1 + x + y;
     const Plan p = make_plan(k, rows * cols);
-    const FsMap M{scale, block_rows, block_cols, cols / block_cols};
+    const FsMap M = fs_map(scale, rows, cols, block_rows, block_cols, x, y);
     const float G = grid_top(x, y);
     cudaStream_t st = S_(stream);
     auto *po = static_cast<uint8_t *>(out);

@@ -37,6 +37,7 @@ exmy_status launch_histogram(const uint8_t *in, bool bf16, int64_t n, unsigned l
         return launch_status();
     }
     switch (g_hist_mode) {
+        case 3: return bf16 ? launch_hist_vec<true, 3>(in, n, hist, st) : launch_hist_vec<false, 3>(in, n, hist, st);
         case 0: return bf16 ? launch_hist_vec<true, 0>(in, n, hist, st) : launch_hist_vec<false, 0>(in, n, hist, st);
         case 2: return bf16 ? launch_hist_vec<true, 2>(in, n, hist, st) : launch_hist_vec<false, 2>(in, n, hist, st);
         default: return bf16 ? launch_hist_vec<true, 1>(in, n, hist, st) : launch_hist_vec<false, 1>(in, n, hist, st);

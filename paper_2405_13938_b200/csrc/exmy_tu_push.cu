@@ -53,9 +53,78 @@ __device__ __noinline__ void push_container_generic(const uint8_t *__restrict__ 
     }
 }
 
+// ---- NVLS multicast stores: `mc` is a multicast
+// address of the symmetric packed buffer (torch symmetric memory's
+// multicast_ptr); one multimem.st reaches every GPU bound to the multicast
+// object, the NVSwitch replicating it -- instead of one store per peer.
+// multimem.st has no byte or half-word form, so every store here is 4, 8 or
+// 16 bytes: a tile's 4 containers of a segment (4w bytes) or a w8 row chunk.
+__device__ __forceinline__ void mc_st(uint8_t *p, uint32_t a) {
+    asm volatile("multimem.st.relaxed.sys.global.b32 [%0], %1;" ::"l"(p), "r"(a) : "memory");
+}
+__device__ __forceinline__ void mc_st(uint8_t *p, uint32_t a, uint32_t b) {
+    asm volatile("multimem.st.relaxed.sys.global.v2.f32 [%0], {%1, %2};" ::"l"(p), "r"(a), "r"(b) : "memory");
+}
+__device__ __forceinline__ void mc_st(uint8_t *p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c),
+                 "r"(d)
+                 : "memory");
+}
+
+template <int W>
+__device__ __forceinline__ void mc_store_words(uint8_t *p, const uint32_t (&w)[W]) {
+    if constexpr (W == 1) mc_st(p, w[0]);
+    else if constexpr (W == 2) mc_st(p, w[0], w[1]);
+    else mc_st(p, w[0], w[1], w[2], w[3]);
+}
+
+// rows_fast_store (exmy_fast.cuh) with multicast stores: one tile (8 rows x
+// 4 columns) of byte-lane codes RL (low 8 code bits) / RH (bits 8..1, k = 9)
+template <int K, int S>
+__device__ __forceinline__ void rows_mc_store(const uint32_t (&RL)[1][8], const uint32_t (&RH)[1][8], uint8_t *mc,
+                                              const SegOffsets &so, int64_t g, int64_t C, int64_t c0) {
+    if constexpr (S < seg_count(K)) {
+        constexpr int W = seg_width(K, S), LO = seg_lo(K, S);
+        uint8_t *seg = mc + so.off[S];
+        if constexpr (W == 8) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) mc_st(seg + (8 * g + i) * C + c0, (K == 9) ? RH[0][i] : RL[0][i]);
+        } else {
+            uint32_t out[W];
+            swar_pack4<W, LO>(RL[0], out);
+            mc_store_words<W>(seg + (g * C + c0) * W, out);
+        }
+        rows_mc_store<K, S + 1>(RL, RH, mc, so, g, C, c0);
+    }
+}
+
+// the integer path of one tile for multicast destinations: codes element by
+// element (specials recorded with global indices), then the same SWAR packing
+// and 4w-byte multicast stores
+template <bool BF16, int K>
+__device__ __noinline__ void push_tile_generic_mc(const uint8_t *__restrict__ in, int64_t C, int64_t g, int64_t c0,
+                                                  int64_t g0, const Fmt F, uint8_t *mc, const SegOffsets so,
+                                                  int64_t *spi, uint32_t *spb, unsigned long long *spc, int64_t cap) {
+    const int64_t eoff = g0 * 8 * C;
+    uint32_t RL[1][8], RH[1][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        uint32_t cd[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int64_t e = (8 * g + i) * C + c0 + v;
+            cd[v] = enc_elem(load_elem_scalar<BF16>(in, e), F, eoff + e, spi, spb, spc, cap);
+        }
+        const uint32_t p0 = cd[0] | (cd[1] << 16), p1 = cd[2] | (cd[3] << 16);
+        RL[0][i] = prmt(p0, p1, 0x6420);
+        RH[0][i] = (K == 9) ? prmt(p0 >> 1, p1 >> 1, 0x6420) : 0u;
+    }
+    rows_mc_store<K, 0>(RL, RH, mc, so, g + g0, C, c0);
+}
+
 // k_enc_rows_fast's tiles (8 rows x 4 columns, one tile ahead in flight);
 // every segment store is issued once per destination
-template <int K, bool BF16, int MODE>
+template <int K, bool BF16, int MODE, bool MC>
 __global__ void __launch_bounds__(256, 2) k_enc_push(const uint8_t *__restrict__ in, int64_t R, int64_t C, int64_t g0,
                                                      int x, int y, const uint8_t *__restrict__ meta, PushDst D,
                                                      SegOffsets so, int64_t *spi, uint32_t *spb,
@@ -71,9 +140,14 @@ __global__ void __launch_bounds__(256, 2) k_enc_push(const uint8_t *__restrict__
     const uint8_t *src = in + c0 * EL::ES;
     const int64_t rstride = C * EL::ES;
     if (!enc_fast_ok<BF16, MODE>(F, force_generic)) {
-        for (int64_t g = blockIdx.y; g < G; g += gridDim.y)
-            for (int v = 0; v < 4; ++v)
-                push_container_generic<BF16, K>(in, C, g * C + c0 + v, g0, F, D, so, spi, spb, spc, cap);
+        for (int64_t g = blockIdx.y; g < G; g += gridDim.y) {
+            if (MC) {
+                push_tile_generic_mc<BF16, K>(in, C, g, c0, g0, F, D.p[0], so, spi, spb, spc, cap);
+            } else {
+                for (int v = 0; v < 4; ++v)
+                    push_container_generic<BF16, K>(in, C, g * C + c0 + v, g0, F, D, so, spi, spb, spc, cap);
+            }
+        }
         return;
     }
     uint32_t nxt[8][NW];
@@ -104,7 +178,13 @@ __global__ void __launch_bounds__(256, 2) k_enc_push(const uint8_t *__restrict__
                 RL[0][i] = prmt(cp[i][0], cp[i][1], 0x6420);
                 RH[0][i] = (K == 9) ? prmt(cp[i][0] >> 1, cp[i][1] >> 1, 0x6420) : 0u;
             }
-            for (int d = 0; d < D.n; ++d) rows_fast_store<K, 1, 0>(RL, RH, D.p[d], so, g + g0, C, c0);
+            if (MC) {
+                rows_mc_store<K, 0>(RL, RH, D.p[0], so, g + g0, C, c0);   // one store reaches every GPU
+            } else {
+                for (int d = 0; d < D.n; ++d) rows_fast_store<K, 1, 0>(RL, RH, D.p[d], so, g + g0, C, c0);
+            }
+        } else if (MC) {
+            push_tile_generic_mc<BF16, K>(in, C, g, c0, g0, F, D.p[0], so, spi, spb, spc, cap);
         } else {
             for (int v = 0; v < 4; ++v)
                 push_container_generic<BF16, K>(in, C, g * C + c0 + v, g0, F, D, so, spi, spb, spc, cap);
@@ -115,10 +195,10 @@ __global__ void __launch_bounds__(256, 2) k_enc_push(const uint8_t *__restrict__
 template <int K, bool BF16, int MODE>
 exmy_status launch_push_km(const uint8_t *in, int64_t R, int64_t C, int64_t g0, int x, int y, const uint8_t *meta,
                            const PushDst &D, const SegOffsets &so, int64_t *spi, uint32_t *spb,
-                           unsigned long long *spc, int64_t cap, cudaStream_t st) {
+                           unsigned long long *spc, int64_t cap, cudaStream_t st, bool mc) {
     const int threads = 256;
     static int occ = 0;
-    if (!occ) occ = occupancy(k_enc_push<K, BF16, MODE>, threads, 0);
+    if (!occ) occ = occupancy(k_enc_push<K, BF16, MODE, false>, threads, 0);
     const int64_t CV = C / 4, G = R / 8;
     const int64_t gx = cdiv(CV, threads);
     int64_t gy = (int64_t)num_sms() * occ / gx;
@@ -126,36 +206,41 @@ exmy_status launch_push_km(const uint8_t *in, int64_t R, int64_t C, int64_t g0, 
     if (gy > G) gy = G;
     if (gy > 65535) gy = 65535;
     if (gx > INT_MAX) return EXMY_E_SHAPE;
-    k_enc_push<K, BF16, MODE><<<dim3((unsigned)gx, (unsigned)gy), threads, 0, st>>>(in, R, C, g0, x, y, meta, D, so, spi,
-                                                                                   spb, spc, cap, g_force_generic);
+    const dim3 grid((unsigned)gx, (unsigned)gy);
+    if (mc)
+        k_enc_push<K, BF16, MODE, true><<<grid, threads, 0, st>>>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap,
+                                                                  g_force_generic);
+    else
+        k_enc_push<K, BF16, MODE, false><<<grid, threads, 0, st>>>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap,
+                                                                   g_force_generic);
     return launch_status();
 }
 
 template <int K, bool BF16>
 exmy_status launch_push_k(const uint8_t *in, int64_t R, int64_t C, int64_t g0, int x, int y, const uint8_t *meta,
                           const PushDst &D, const SegOffsets &so, int64_t *spi, uint32_t *spb,
-                          unsigned long long *spc, int64_t cap, cudaStream_t st) {
+                          unsigned long long *spc, int64_t cap, cudaStream_t st, bool mc) {
     if (BF16 && y <= 6)   // mode choice as exmy_encode
         return y == 0 ? launch_push_km<K, BF16, (BF16 ? ENC_SIMD_Y0 : ENC_F32_Y0)>(in, R, C, g0, x, y, meta, D, so, spi,
-                                                                                   spb, spc, cap, st)
+                                                                                   spb, spc, cap, st, mc)
                       : launch_push_km<K, BF16, (BF16 ? ENC_SIMD : ENC_F32)>(in, R, C, g0, x, y, meta, D, so, spi, spb,
-                                                                             spc, cap, st);
-    return y == 0 ? launch_push_km<K, BF16, ENC_F32_Y0>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st)
-                  : launch_push_km<K, BF16, ENC_F32>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st);
+                                                                             spc, cap, st, mc);
+    return y == 0 ? launch_push_km<K, BF16, ENC_F32_Y0>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st, mc)
+                  : launch_push_km<K, BF16, ENC_F32>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st, mc);
 }
 
 template <bool BF16>
 exmy_status push_dispatch(int k, const uint8_t *in, int64_t R, int64_t C, int64_t g0, int x, int y,
                           const uint8_t *meta, const PushDst &D, const SegOffsets &so, int64_t *spi, uint32_t *spb,
-                          unsigned long long *spc, int64_t cap, cudaStream_t st) {
+                          unsigned long long *spc, int64_t cap, cudaStream_t st, bool mc) {
     switch (k) {
-        case 3: return launch_push_k<3, BF16>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st);
-        case 4: return launch_push_k<4, BF16>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st);
-        case 5: return launch_push_k<5, BF16>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st);
-        case 6: return launch_push_k<6, BF16>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st);
-        case 7: return launch_push_k<7, BF16>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st);
-        case 8: return launch_push_k<8, BF16>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st);
-        case 9: return launch_push_k<9, BF16>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st);
+        case 3: return launch_push_k<3, BF16>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st, mc);
+        case 4: return launch_push_k<4, BF16>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st, mc);
+        case 5: return launch_push_k<5, BF16>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st, mc);
+        case 6: return launch_push_k<6, BF16>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st, mc);
+        case 7: return launch_push_k<7, BF16>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st, mc);
+        case 8: return launch_push_k<8, BF16>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st, mc);
+        case 9: return launch_push_k<9, BF16>(in, R, C, g0, x, y, meta, D, so, spi, spb, spc, cap, st, mc);
     }
     return EXMY_E_FORMAT;
 }
@@ -168,10 +253,10 @@ bool fmt_ok(int x, int y) {
 
 }  // namespace
 
-extern "C" exmy_status exmy_encode_push(const void *in, int dtype, int64_t rows, int64_t cols, int64_t row0,
-                                        int64_t total_rows, int x, int y, const uint8_t *meta, uint8_t *const *dst,
-                                        int ndst, int64_t *sp_index, uint32_t *sp_bits, uint64_t *sp_count,
-                                        int64_t sp_capacity, void *stream) {
+static exmy_status encode_push_impl(const void *in, int dtype, int64_t rows, int64_t cols, int64_t row0,
+                                    int64_t total_rows, int x, int y, const uint8_t *meta, uint8_t *const *dst,
+                                    int ndst, int64_t *sp_index, uint32_t *sp_bits, uint64_t *sp_count,
+                                    int64_t sp_capacity, void *stream, bool mc) {
     if (dtype != EXMY_F32 && dtype != EXMY_BF16) return EXMY_E_DTYPE;
     if (!fmt_ok(x, y)) return EXMY_E_FORMAT;
     if (rows < 0 || cols < 0 || row0 < 0 || total_rows < 0 || row0 + rows > total_rows) return EXMY_E_SHAPE;
@@ -198,13 +283,31 @@ extern "C" exmy_status exmy_encode_push(const void *in, int dtype, int64_t rows,
     const auto *pi = static_cast<const uint8_t *>(in);
     if (!aligned(pi, 4 * (dtype == EXMY_BF16 ? 2 : 4)) || cols % 4) return EXMY_E_ALIGN;
     exmy_status s = dtype == EXMY_BF16
-                        ? push_dispatch<true>(k, pi, rows, cols, row0 / 8, x, y, meta, D, p.so, sp_index, sp_bits, spc,
-                                              sp_capacity, st)
-                        : push_dispatch<false>(k, pi, rows, cols, row0 / 8, x, y, meta, D, p.so, sp_index, sp_bits, spc,
-                                               sp_capacity, st);
+                        ? push_dispatch<true>(k, pi, rows, cols, row0 / 8, x, y, meta, D, p.so, nullptr, nullptr, spc,
+                                              0, st, mc)
+                        : push_dispatch<false>(k, pi, rows, cols, row0 / 8, x, y, meta, D, p.so, nullptr, nullptr, spc,
+                                               0, st, mc);
     if (s != EXMY_OK) return s;
-    if (spc && sp_capacity > 1) s = launch_specials_sort(sp_index, sp_bits, spc, sp_capacity, st);
-    return s;
+    // the shard's list, with global element indices (row0 * cols offset)
+    return launch_specials_compact(pi, dtype == EXMY_BF16, rows * cols, row0 * cols, sp_index, sp_bits, spc,
+                                   sp_capacity, st);
+}
+
+extern "C" exmy_status exmy_encode_push(const void *in, int dtype, int64_t rows, int64_t cols, int64_t row0,
+                                        int64_t total_rows, int x, int y, const uint8_t *meta, uint8_t *const *dst,
+                                        int ndst, int64_t *sp_index, uint32_t *sp_bits, uint64_t *sp_count,
+                                        int64_t sp_capacity, void *stream) {
+    return encode_push_impl(in, dtype, rows, cols, row0, total_rows, x, y, meta, dst, ndst, sp_index, sp_bits,
+                            sp_count, sp_capacity, stream, false);
+}
+
+extern "C" exmy_status exmy_encode_push_multicast(const void *in, int dtype, int64_t rows, int64_t cols,
+                                                  int64_t row0, int64_t total_rows, int x, int y, const uint8_t *meta,
+                                                  uint8_t *mc_dst, int64_t *sp_index, uint32_t *sp_bits,
+                                                  uint64_t *sp_count, int64_t sp_capacity, void *stream) {
+    uint8_t *const d[1] = {mc_dst};
+    return encode_push_impl(in, dtype, rows, cols, row0, total_rows, x, y, meta, d, 1, sp_index, sp_bits, sp_count,
+                            sp_capacity, stream, true);
 }
 
 // ------------------------------------------------- pull decode (gather on read)

@@ -116,7 +116,7 @@ def allgather_specials(p, group=None):
     n = max(cap, 1)
     idx = _allgather_stack(p.sp_index[:n], group)
     bits = _allgather_stack(p.sp_bits[:n], group)
-    cnt = _allgather_stack(p.sp_count.reshape(1).to(torch.int64), group).reshape(-1)
+    cnt = _allgather_stack(p.sp_count.reshape(-1)[:1].to(torch.int64), group).reshape(-1)
     worst = int(cnt.max())
     if worst > cap:
         import paper_2405_13938_b200 as exmy
@@ -163,32 +163,60 @@ def sharded_roundtrip(shard: torch.Tensor, fmt, axis="rows", group=None, codec=N
 
 
 # --------------------------------------------- fused encode + all-gather (push)
+_SYMM_HANDLES = {}
+
+
 def symmetric_packed_buffers(nbytes: int, group=None):
     """This rank's gathered packed buffer plus every rank's, mapped into this
     process (NVLink peer memory through torch symmetric memory): the
-    destinations of `pushed_encode`.  Needs CUDA peers (NCCL group)."""
+    destinations of `pushed_encode`.  Needs CUDA peers (NCCL group).  The
+    rendezvous handle is kept (multicast_status / multicast pushes)."""
     from torch.distributed import _symmetric_memory as symm_mem
     buf = symm_mem.empty(nbytes, dtype=torch.uint8, device=torch.device("cuda", torch.cuda.current_device()))
     h = symm_mem.rendezvous(buf, group=dist.group.WORLD if group is None else group)
     peers = [h.get_buffer(r, (nbytes,), torch.uint8) for r in range(h.world_size)]
+    _SYMM_HANDLES[buf.data_ptr()] = h
     return buf, peers
 
 
+def multicast_ptr(buf) -> int:
+    """The NVLS multicast address bound to `buf` (from symmetric_packed_buffers)
+    on every rank, or 0 when this node / driver offers no multicast."""
+    h = _SYMM_HANDLES.get(buf.data_ptr())
+    if h is None:
+        return 0
+    try:
+        return int(getattr(h, "multicast_ptr", 0) or 0)
+    except Exception:
+        return 0
+
+
+def multicast_status(buf) -> dict:
+    h = _SYMM_HANDLES.get(buf.data_ptr())
+    return {"symmetric": h is not None, "world_size": getattr(h, "world_size", None),
+            "multicast": multicast_ptr(buf) != 0}
+
+
 def pushed_encode(shard: torch.Tensor, fmt, total_rows: int, row0: int, peer_buffers, group=None, codec=None,
-                  meta=None):
+                  meta=None, multicast: int = 0):
     """Fused encode + all-gather: the global metadata from
     the 2 KiB histogram all-reduce (unless given), then ONE kernel encodes this
     rank's row shard and stores its bytes at their global offsets into every
     rank's buffer (peer_buffers), then a barrier.  Afterwards every rank's
     buffer holds the single-GPU encode of the whole tensor -- no NCCL
     all-gather, no staging copy, the transfer overlaps the conversion.
-    Returns (meta, specials of the shard with global indices)."""
+    multicast: a multicast address of the gathered buffer (multicast_ptr):
+    one multimem.st per store reaches every rank (NVLS) instead of one store
+    per peer.  Returns (meta, specials of the shard with global indices)."""
     codec = codec or _default_codec()
     if meta is None:
         hist = codec.histogram(shard)
         allreduce_histogram(hist, group)
         meta = codec.emax(hist)
-    sp = codec.encode_push(shard, fmt, meta, row0, total_rows, peer_buffers)
+    if multicast:
+        sp = codec.encode_push_multicast(shard, fmt, meta, row0, total_rows, multicast)
+    else:
+        sp = codec.encode_push(shard, fmt, meta, row0, total_rows, peer_buffers)
     if shard.is_cuda:
         torch.cuda.current_stream(shard.device).synchronize()   # the stores have landed before peers read
     dist.barrier(group)

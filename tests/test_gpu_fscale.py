@@ -149,3 +149,45 @@ def test_fs_config2_shape_sampled(exmy, orc):
         got = torch.cat([p.data[o + r0 * C * w // 8: o + (r0 + 8) * C * w // 8] for w, o in zip(ws, offs)])
         np.testing.assert_array_equal(got.cpu().numpy(), ref)
         np.testing.assert_array_equal(W.to_bits(q[r0:r0 + 8]), orc.quantize_fs(rows, "e3m3", amax, (1, C)))
+
+
+def amax_rows(k, seed):
+    """per-row maxima over the whole fp32 range: fp32-subnormal, tiny, normal,
+    huge, and significands divisible by G's odd part (exact binary results)"""
+    rng = np.random.default_rng(seed)
+    a = list((rng.random(40) * 2.0 ** rng.integers(-149, 128, 40)).astype(np.float32).view(np.uint32))
+    a += [1, 3, 0x7FFFFF, 0x00800000, 0x7F7FFFFF, 0x3F800000, 15 * 12345, 0x0D800000, 0x0C000001]
+    for _ in range(16):
+        e = int(rng.integers(1, 255))
+        sig = int(rng.integers(1 << 23, 1 << 24))
+        sig -= sig % 7
+        a.append((e << 23) | (sig & 0x7FFFFF) if sig >= 1 << 23 else sig)
+    a = [int(v) for v in a if v != 0]
+    return np.array(a[:64] + [a[0]] * (64 - len(a[:64])), np.uint32)
+
+
+@pytest.mark.parametrize("fmt", [(3, 3), (2, 1), (4, 2), (0, 6), (6, 0), (1, 5), (8, 0), (7, 1), (2, 5), (5, 3),
+                                 (4, 4), (3, 2)], ids=lambda f: f"e{f[0]}m{f[1]}")
+@pytest.mark.parametrize("od", ["f32", "bf16"])
+def test_fs_decode_every_code_every_range(exmy, orc, fmt, od):
+    """decode = RN32(g amax / G) (reading D23's plain definition): every code
+    of the format in every row, rows with maxima across the whole fp32 range
+    (results down to fp32 subnormals and zero), ROWS fast kernel and the
+    generic (COLS) kernel, both output dtypes -- == the oracle bit for bit."""
+    x, y = fmt
+    k = 1 + x + y
+    C = max(1 << k, 64)
+    R = 64
+    codes = np.tile(np.arange(C, dtype=np.uint16) % (1 << k), (R, 1))
+    amax = amax_rows(k, 100 * k + x)[:, None]
+    for axis, ax in (("rows", orc.ROWS), ("cols", orc.COLS)):
+        packed = orc.pack(codes, (R, C), ax, k)
+        p = exmy.Packed(torch.from_numpy(packed).to(DEV), torch.full((1,), 127, dtype=torch.uint8, device=DEV),
+                        torch.zeros(1, dtype=torch.int64, device=DEV), torch.zeros(1, dtype=torch.int32, device=DEV),
+                        torch.zeros(1, dtype=torch.int64, device=DEV), (R, C), x, y, exmy.ROWS if ax == orc.ROWS
+                        else exmy.COLS, torch.float32, (1, C), None,
+                        torch.from_numpy(amax.view(np.float32).copy()).to(DEV), sp_capacity=0, scheme=2)
+        dt = torch.float32 if od == "f32" else torch.bfloat16
+        got = W.to_bits(exmy.decode(p, dt))
+        ref = orc.decode_fs(packed, (R, C), fmt, amax, (1, C), ax, out_dtype=np.uint32 if od == "f32" else np.uint16)
+        np.testing.assert_array_equal(got, ref, err_msg=axis)

@@ -58,17 +58,17 @@ def oracle_boundary_f32(orc, fmt, e_max):
 
 
 # ----------------------------------------------------------------- K1 / K1b
-@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
 @pytest.mark.parametrize("dt", ["bf16", "f32"])
 @pytest.mark.parametrize("n", [0, 1, 7, 8 * 1000 + 5, 1 << 20, (1 << 22) + 3])
 def test_histogram_parity(exmy, orc, dt, n, mode):
-    exmy.hist_mode(mode)
+    prev = exmy.hist_mode(mode)
     try:
         bits = W.random_bits_bf16(n, n) if dt == "bf16" else W.random_bits_f32(n, n)
         h = exmy.histogram(dev_bits(bits)).cpu().numpy().astype(np.uint64)
         np.testing.assert_array_equal(h, orc.histogram(bits))
     finally:
-        exmy.hist_mode(2)
+        exmy.hist_mode(prev)
 
 
 @pytest.mark.parametrize("dt", ["bf16", "f32"])
@@ -104,7 +104,7 @@ def peaked_mix(n, seed, dt="bf16"):
     return bits
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
 @pytest.mark.parametrize("blocks", [0, 1, 3])
 @pytest.mark.parametrize("n", [8 * 1000 + 5, (1 << 22) + 3, 20_000_011])
 @pytest.mark.parametrize("dt", ["bf16", "f32"])
@@ -113,15 +113,34 @@ def test_histogram_peaked_epochs(exmy, orc, mode, blocks, n, dt):
     counters fill fastest), far clusters, zeros, specials; a grid capped at
     1 / 3 CTAs makes every lane run past the counter epoch, so the flush
     before overflow is exercised at test sizes"""
-    exmy.hist_mode(mode)
+    prev = exmy.hist_mode(mode)
     exmy.hist_blocks(blocks)
     try:
         bits = peaked_mix(n, n % 97, dt)
         h = exmy.histogram(dev_bits(bits)).cpu().numpy().astype(np.uint64)
         np.testing.assert_array_equal(h, orc.histogram(bits))
     finally:
-        exmy.hist_mode(2)
+        exmy.hist_mode(prev)
         exmy.hist_blocks(0)
+
+
+def test_histogram_wide_and_shifting_exponents(exmy, orc):
+    """17+ distinct exponents per warp in the first half, any bin (zeros,
+    subnormals, bin 255) in the second, both orders: the lane-pair counters
+    (MODE 3: bins of equal parity from a lane pair share a bank) count
+    exactly"""
+    prev = exmy.hist_mode(3)
+    try:
+        rng = np.random.default_rng(5)
+        n = 1 << 22
+        e = rng.integers(100, 117, n).astype(np.uint16)        # 17 distinct exponents: one always outside
+        e[n // 2:] = rng.integers(0, 256, n // 2).astype(np.uint16)   # second half: anything
+        bits = (e << 7) | rng.integers(0, 1 << 7, n).astype(np.uint16) | (rng.integers(0, 2, n).astype(np.uint16) << 15)
+        for b in (bits, bits[::-1].copy()):
+            h = exmy.histogram(dev_bits(b)).cpu().numpy().astype(np.uint64)
+            np.testing.assert_array_equal(h, orc.histogram(b))
+    finally:
+        exmy.hist_mode(prev)
 
 
 def test_emax_parity(exmy, orc):
@@ -295,9 +314,12 @@ def test_specials_sorted_and_capacity(exmy, orc):
     _check_roundtrip(exmy, orc, bits, (4, 4), 130, "rows", ("same", "bf16"))
     # more specials than capacity: count still total, first entries dropped
     d = dev_bits(bits)
-    p = exmy.encode(d, "e4m4", 130, specials_capacity=10)
+    p = exmy.encode(d, "e4m4", 130, specials_capacity=10, strict=False)
     spi, spb, cnt = p.specials()
     assert cnt == 3000 and spi.numel() == 10
+    # the list is index-ordered compaction: exactly the FIRST 10 specials by index
+    assert spi.cpu().numpy().tolist() == sorted(pos.tolist())[:10]
+    assert spb.cpu().numpy().view(np.uint32).tolist() == flat[sorted(pos.tolist())[:10]].tolist()
     # > 4096 specials: global-memory sort path
     flat[:] = 0x7FC00000
     flat[::3] = 0x3F800000
@@ -421,3 +443,46 @@ def test_max_exponent_preserves_neighbour_bytes(exmy):
     m2 = torch.tensor([1, 2, 3, 4], dtype=torch.uint8, device=DEV)
     exmy.max_exponent(t, out=m2[2:3])
     assert m2.tolist() == [1, 2, ref, 4]
+
+
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+def test_all_nan_tensor_is_fast_and_ordered(exmy, dt):
+    """a NaN-heavy tensor (a diverged gradient) encodes in
+    under 2x the clean tensor's time -- the fast kernels mask NaN/Inf lanes
+    to code 0 and count them per warp, the ordered list is a stream
+    compaction (no sort) that stops re-reading at the capacity -- and the
+    list holds the first `capacity` specials by index."""
+    n_rows, cols = (16384, 16384) if dt == "bf16" else (8192, 16384)
+    clean = W.bf16_weights((n_rows, cols), seed=1, device=DEV) if dt == "bf16" else \
+        W.f32_gradients(n_rows * cols, device=DEV).view(n_rows, cols)
+    nan = torch.full_like(clean, float("nan"))
+    nan.view(-1)[1::7] = float("-inf")
+    meta = exmy.max_exponent(clean)
+    cap = 4096
+
+    def t_enc(x):
+        for _ in range(2):
+            exmy.encode(x, "e3m3", meta, specials_capacity=cap, strict=False)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            p = exmy.encode(x, "e3m3", meta, specials_capacity=cap, strict=False)
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return sorted(ts)[2], p
+
+    t_clean, pc = t_enc(clean)
+    t_nan, pn = t_enc(nan)
+    idx, bits, cnt = pn.specials()
+    assert cnt == clean.numel()
+    assert idx.cpu().numpy().tolist() == list(range(cap))
+    want = [0xFF800000 if i % 7 == 1 else int(W.to_bits(nan.view(-1)[i:i + 1].cpu())[0]) << (16 if dt == "bf16" else 0)
+            for i in range(cap)]
+    assert bits.cpu().numpy().view(np.uint32).tolist() == [w & 0xFFFFFFFF for w in want]
+    assert int(pc.sp_count[0].item()) == 0
+    assert t_nan < 2.0 * t_clean, (t_nan, t_clean)
+    # the packed stream holds code 0 for every special; decode restores the listed ones
+    assert int(pn.data.max().item()) == 0

@@ -53,7 +53,7 @@ def test_push_equals_whole_encode(exmy, orc, fmt, dt, G):
     for r in range(G):
         spi, spb, spc = exmy.encode_push(t[r * per:(r + 1) * per], fmt, e, r * per, R, bufs,
                                          specials_capacity=R * C)
-        cnt = int(spc.item())
+        cnt = int(spc[0].item())
         idxs.append(spi[:cnt].cpu().numpy())
     torch.cuda.synchronize()
     pref, idx, sb, ns = orc.encode(bits, fmt, e, orc.ROWS)

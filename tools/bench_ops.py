@@ -41,7 +41,7 @@ def main():
     ap.add_argument("--cols", type=int, default=16384)
     ap.add_argument("--fmts", default="e0m6,e1m5,e2m4,e3m3,e4m2,e5m1,e6m0")
     ap.add_argument("--axis", default="rows")
-    ap.add_argument("--hist-modes", default="2")
+    ap.add_argument("--hist-modes", default="3")
     ap.add_argument("--probe", action="store_true", help="also time the roofline probe for each op's byte mix")
     ap.add_argument("--fs", action="store_true", help="with --block: also time the float-scaling scheme")
     ap.add_argument("--block", default=None, help="row | col | tensor | BRxBC: time the block-metadata path")
@@ -62,7 +62,7 @@ def main():
         exmy.hist_mode(m)
         ms = timeit(lambda: exmy.histogram(t, out=h))
         res[f"hist_mode{m}"] = {"ms": ms, "gbs": n * es / ms / 1e6, "frac": n * es / ms / 1e6 / peak}
-    exmy.hist_mode(2)
+    exmy.hist_mode(3)
     meta = exmy.max_exponent(t)
     q = torch.empty_like(t)
     d = torch.empty_like(t)
@@ -72,9 +72,9 @@ def main():
         ms = timeit(lambda: exmy.quantize(t, f, meta, out=q))
         res[f"quantize_{f}"] = {"ms": ms, "gbs": 2 * n * es / ms / 1e6, "frac": 2 * n * es / ms / 1e6 / peak}
         buf = torch.empty(n * k // 8, dtype=torch.uint8, device=dev)
-        ms = timeit(lambda: exmy.encode(t, f, meta, axis=a.axis, out=buf))
+        ms = timeit(lambda: exmy.encode(t, f, meta, axis=a.axis, out=buf, strict=False))
         res[f"encode_{f}"] = {"ms": ms, "gbs": n * (es + k / 8) / ms / 1e6, "frac": n * (es + k / 8) / ms / 1e6 / peak}
-        p = exmy.encode(t, f, meta, axis=a.axis, out=buf)
+        p = exmy.encode(t, f, meta, axis=a.axis, out=buf, strict=False)
         ms = timeit(lambda: exmy.decode(p, out=d))
         res[f"decode_{f}"] = {"ms": ms, "gbs": n * (es + k / 8) / ms / 1e6, "frac": n * (es + k / 8) / ms / 1e6 / peak}
     if a.block:
@@ -89,14 +89,14 @@ def main():
             ms = timeit(lambda: exmy.quantize_blocked(t, f, m, (br, bc), out=q))
             res[f"bquant_{f}"] = {"ms": ms, "gbs": 2 * n * es / ms / 1e6, "frac": 2 * n * es / ms / 1e6 / peak}
             buf = torch.empty(n * k // 8, dtype=torch.uint8, device=dev)
-            ms = timeit(lambda: exmy.encode_blocked(t, f, m, (br, bc), axis=a.axis, out=buf))
+            ms = timeit(lambda: exmy.encode_blocked(t, f, m, (br, bc), axis=a.axis, out=buf, strict=False))
             res[f"bencode_{f}"] = {"ms": ms, "gbs": n * (es + k / 8) / ms / 1e6,
                                    "frac": n * (es + k / 8) / ms / 1e6 / peak}
             if (br, bc) == (1, C):
-                ms = timeit(lambda: exmy.encode_rowwise(t, f, axis=a.axis, out=buf, meta_out=m))
+                ms = timeit(lambda: exmy.encode_rowwise(t, f, axis=a.axis, out=buf, meta_out=m, strict=False))
                 res[f"rowwise_{f}"] = {"ms": ms, "gbs": n * (es + k / 8) / ms / 1e6,
                                        "frac": n * (es + k / 8) / ms / 1e6 / peak}
-            p = exmy.encode_blocked(t, f, m, (br, bc), axis=a.axis, out=buf)
+            p = exmy.encode_blocked(t, f, m, (br, bc), axis=a.axis, out=buf, strict=False)
             ms = timeit(lambda: exmy.decode(p, out=d))
             res[f"bdecode_{f}"] = {"ms": ms, "gbs": n * (es + k / 8) / ms / 1e6,
                                    "frac": n * (es + k / 8) / ms / 1e6 / peak}
@@ -106,10 +106,10 @@ def main():
                 res[f"fsmax_{f}"] = {"ms": ms, "gbs": n * es / ms / 1e6, "frac": n * es / ms / 1e6 / peak}
                 ms = timeit(lambda: exmy.quantize_fs(t, f, sc, (br, bc), out=q))
                 res[f"fsquant_{f}"] = {"ms": ms, "gbs": 2 * n * es / ms / 1e6, "frac": 2 * n * es / ms / 1e6 / peak}
-                ms = timeit(lambda: exmy.encode_fs(t, f, sc, (br, bc), axis=a.axis, out=buf))
+                ms = timeit(lambda: exmy.encode_fs(t, f, sc, (br, bc), axis=a.axis, out=buf, strict=False))
                 res[f"fsencode_{f}"] = {"ms": ms, "gbs": n * (es + k / 8) / ms / 1e6,
                                         "frac": n * (es + k / 8) / ms / 1e6 / peak}
-                pf = exmy.encode_fs(t, f, sc, (br, bc), axis=a.axis, out=buf)
+                pf = exmy.encode_fs(t, f, sc, (br, bc), axis=a.axis, out=buf, strict=False)
                 ms = timeit(lambda: exmy.decode(pf, out=d))
                 res[f"fsdecode_{f}"] = {"ms": ms, "gbs": n * (es + k / 8) / ms / 1e6,
                                         "frac": n * (es + k / 8) / ms / 1e6 / peak}
