@@ -327,9 +327,10 @@ def run_ours(args):
                 "algorithmic_bytes_per_launch": alg_bytes[dom] / launches[dom], "peak_source": peak_src}
 
     # gpu launches of OUR kernels per step: hist 1, emax 1; per format quantize 1,
-    # encode 2 (encode + specials sort), decode 2 (decode + specials scatter) or,
-    # at N > 1, one decode per received shard
-    gpu_launches = args.steps * (2 + nf * (3 + (2 if ws == 1 else ws)))
+    # encode 3 (encode, NaN/Inf fix-up pass, ordered-list compaction; the last two
+    # return at once on this data), decode 2 (decode + specials scatter) or, at N > 1,
+    # one decode per received shard
+    gpu_launches = args.steps * (2 + nf * (4 + (2 if ws == 1 else ws)))
 
     result = {
         "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": ws, "steps": args.steps,

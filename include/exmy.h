@@ -156,13 +156,15 @@ exmy_status exmy_quantize(const void *in, void *out, int dtype, int64_t n,
  *   histogram's bin 255 is that count.  The list is built after the encode
  *   kernel by ordered stream compaction (no sort): with sp_capacity > 0,
  *   sp_count must point to EXMY_SPECIALS_WORDS uint64 of device workspace
- *   (word 0 = the count, the rest per-range counts); with sp_capacity == 0
- *   one word is enough.  Without NaN/Inf (word 0 == 0) the two compaction
+ *   (word 0 = the count, then 1024 per-range counts and a fix-up flag:
+ *   the fast per-tensor kernels leave tiles holding NaN/Inf to a fix-up pass
+ *   that encodes them on the vector path with code 0 in their lanes); with
+ *   sp_capacity == 0 one word is enough.  Without NaN/Inf (word 0 == 0) the two compaction
  *   launches return at once.  sp_index/sp_bits may be NULL iff
  *   sp_capacity == 0; sp_count may be NULL only if the input is known to
  *   hold no NaN/Inf.  The same convention holds for every *_encode* call
  *   below except the grouped ones (per-entry lists of one count word). */
-#define EXMY_SPECIALS_WORDS 1025
+#define EXMY_SPECIALS_WORDS 1026
 int exmy_specials_words(void);   /* == EXMY_SPECIALS_WORDS */
 exmy_status exmy_encode(const void *in, int dtype, int64_t rows, int64_t cols, int axis,
                         int x, int y, const uint8_t *meta, uint8_t *packed,

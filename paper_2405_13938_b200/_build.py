@@ -24,7 +24,7 @@ UNITS = ["exmy_abi.cu", "exmy_tu_hist.cu", "exmy_tu_quant.cu", "exmy_tu_encode.c
          "exmy_tu_fscale.cu", "exmy_tu_push.cu", "exmy_ckpt.cpp",
          "exmy_tu_bag.cu", "exmy_tu_probe.cu"]
 HEADERS = ["exmy_device.cuh", "exmy_kernels.cuh", "exmy_fast.cuh", "exmy_blocked.cuh", "exmy_launch.cuh", "exmy_grouped.cuh",
-           "exmy_fscale.cuh", "exmy_tma.cuh"]
+           "exmy_fscale.cuh", "exmy_tma.cuh", "exmy_narrow.cuh"]
 
 
 def _sources():

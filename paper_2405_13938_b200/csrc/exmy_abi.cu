@@ -48,7 +48,7 @@ extern "C" {
 const char *exmy_version(void) { return "exmy-b200 0.2 (sm_100a)"; }
 
 int exmy_specials_words(void) {
-    static_assert(EXMY_SPECIALS_WORDS == 1 + SPECIALS_RANGES, "workspace = count + one word per range");
+    static_assert(EXMY_SPECIALS_WORDS == 2 + SPECIALS_RANGES, "workspace = count + one word per range + flag");
     return EXMY_SPECIALS_WORDS;
 }
 
@@ -200,15 +200,21 @@ exmy_status exmy_encode(const void *in, int dtype, int64_t rows, int64_t cols, i
     if (sp_capacity > 0 && (!sp_index || !sp_bits)) return EXMY_E_ARG;
     cudaStream_t st = S(stream);
     auto *spc = reinterpret_cast<unsigned long long *>(sp_count);
-    if (spc && cudaMemsetAsync(spc, 0, sizeof(unsigned long long), st) != cudaSuccess) return EXMY_E_CUDA;
+    // with a list to fill the workspace is full-size: zero it all (counts, range counts, fix-up flag)
+    const bool full_ws = spc && sp_capacity > 0;
+    if (spc && cudaMemsetAsync(spc, 0, sizeof(unsigned long long) * (full_ws ? EXMY_SPECIALS_WORDS : 1), st) !=
+                   cudaSuccess)
+        return EXMY_E_CUDA;
     if (n == 0) return EXMY_OK;
     if (!in || !packed || !meta) return EXMY_E_ARG;
-    // the kernel counts the NaN/Inf (ws[0]); the ordered list is written after it
+    // the kernels count the NaN/Inf (ws[0]; tiles holding them go to the fix-up pass, which also counts
+    // them per range); the ordered list is written after them
+    const SpecialsRanges sr = specials_ranges(rows, cols, full_ws);
     s = launch_encode(static_cast<const uint8_t *>(in), dtype == EXMY_BF16, rows, cols, axis, x, y, meta, packed,
-                      nullptr, nullptr, spc, 0, st);
+                      nullptr, nullptr, spc, 0, st, sr);
     if (s != EXMY_OK) return s;
     return launch_specials_compact(static_cast<const uint8_t *>(in), dtype == EXMY_BF16, n, 0, sp_index, sp_bits, spc,
-                                   sp_capacity, st);
+                                   sp_capacity, st, sr.len(axis, cols));
 }
 
 exmy_status exmy_decode(const uint8_t *packed, int64_t rows, int64_t cols, int axis, int x, int y,
@@ -270,7 +276,9 @@ exmy_status exmy_encode_blocked(const void *in, int dtype, int64_t rows, int64_t
     if (sp_capacity > 0 && (!sp_index || !sp_bits)) return EXMY_E_ARG;
     cudaStream_t st = S(stream);
     auto *spc = reinterpret_cast<unsigned long long *>(sp_count);
-    if (spc && cudaMemsetAsync(spc, 0, sizeof(unsigned long long), st) != cudaSuccess) return EXMY_E_CUDA;
+    if (spc && cudaMemsetAsync(spc, 0, sizeof(unsigned long long) * (sp_capacity > 0 ? EXMY_SPECIALS_WORDS : 1), st) !=
+                   cudaSuccess)
+        return EXMY_E_CUDA;
     if (n == 0) return EXMY_OK;
     if (!in || !packed || !meta) return EXMY_E_ARG;
     s = launch_encode_blocked(static_cast<const uint8_t *>(in), dtype == EXMY_BF16, rows, cols, axis, block_rows,
@@ -317,7 +325,9 @@ exmy_status exmy_encode_rowwise(const void *in, int dtype, int64_t rows, int64_t
     if (sp_capacity > 0 && (!sp_index || !sp_bits)) return EXMY_E_ARG;
     cudaStream_t st = S(stream);
     auto *spc = reinterpret_cast<unsigned long long *>(sp_count);
-    if (spc && cudaMemsetAsync(spc, 0, sizeof(unsigned long long), st) != cudaSuccess) return EXMY_E_CUDA;
+    if (spc && cudaMemsetAsync(spc, 0, sizeof(unsigned long long) * (sp_capacity > 0 ? EXMY_SPECIALS_WORDS : 1), st) !=
+                   cudaSuccess)
+        return EXMY_E_CUDA;
     if (n == 0) return EXMY_OK;
     if (!in || !packed || !meta) return EXMY_E_ARG;
     auto *pin = static_cast<const uint8_t *>(in);

@@ -407,6 +407,13 @@ __device__ __forceinline__ int mask_special_codes(const uint32_t (&w)[NW], uint3
     return bad ? -1 : n;
 }
 
+// a warp that deferred a tile raises the fix-up flag once (kernel end)
+__device__ __forceinline__ void raise_fixup_flag(unsigned long long *flag, bool deferred) {
+    const unsigned m = __activemask();
+    const unsigned b = __ballot_sync(m, deferred);
+    if (b && (threadIdx.x & 31) == __ffs(m) - 1) atomicOr(flag, 1ull);
+}
+
 // add a thread's count of specials to *spc once per warp (kernel end)
 __device__ __forceinline__ void flush_special_count(unsigned long long *spc, unsigned long long nsp) {
     const unsigned m = __activemask();
@@ -526,7 +533,8 @@ __global__ void __launch_bounds__(BF16 ? EXMY_ENC_ROWS_THREADS : 256, BF16 ? EXM
                                                        int y, const uint8_t *__restrict__ meta,
                                                        uint8_t *__restrict__ packed, SegOffsets so, int64_t *spi,
                                                        uint32_t *spb, unsigned long long *spc, int64_t cap,
-                                                       int force_generic) {
+                                                       int force_generic, unsigned long long *defer_flag) {
+    const bool defer = defer_flag != nullptr;
     using EL = Elem<BF16>;
     constexpr int NW = BF16 ? 2 : 4;   // words per 4 elements
     const Fmt F = load_fmt(x, y, meta);
@@ -549,7 +557,7 @@ __global__ void __launch_bounds__(BF16 ? EXMY_ENC_ROWS_THREADS : 256, BF16 ? EXM
     }
     // software pipeline: the next tile's 8 row chunks are in flight while
     // this tile is converted and packed
-    unsigned nsp = 0;   // NaN/Inf seen on the masked fast path
+    bool deferred = false;   // a tile with NaN/Inf (or huge values) left to k_enc_rows_fixup
     uint32_t nxt[8][NW];
     int64_t g = blockIdx.y;
     if (g < G && act) {
@@ -591,29 +599,14 @@ __global__ void __launch_bounds__(BF16 ? EXMY_ENC_ROWS_THREADS : 256, BF16 ? EXM
                 RH[0][i] = (K == 9) ? prmt(cp[i][0] >> 1, cp[i][1] >> 1, 0x6420) : 0u;
             }
             rows_fast_store<K, 1, 0>(RL, RH, packed, so, g, C, c0);
-        } else {   // NaN/Inf in the tile: masked fast codes, or the integer path for huge finite values
-            int ns = 0;
-#pragma unroll
-            for (int i = 0; i < 8 && ns >= 0; ++i) {
-                const int m = mask_special_codes<K, BF16, MODE, NW>(w[i], cp[i], P);
-                ns = m < 0 ? -1 : ns + m;
-            }
-            if (ns >= 0) {
-                nsp += (unsigned)ns;
-                uint32_t RL[1][8], RH[1][8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    RL[0][i] = prmt(cp[i][0], cp[i][1], 0x6420);
-                    RH[0][i] = (K == 9) ? prmt(cp[i][0] >> 1, cp[i][1] >> 1, 0x6420) : 0u;
-                }
-                rows_fast_store<K, 1, 0>(RL, RH, packed, so, g, C, c0);
-            } else {
-                for (int v = 0; v < 4; ++v)
-                    enc_container_generic<BF16, K>(in, C, g * C + c0 + v, 0, F, packed, so, spi, spb, spc, cap);
-            }
+        } else if (defer) {   // NaN/Inf (or huge values): k_enc_rows_fixup encodes this tile
+            deferred = true;
+        } else {   // no workspace: the integer path here (round-1 behaviour)
+            for (int v = 0; v < 4; ++v)
+                enc_container_generic<BF16, K>(in, C, g * C + c0 + v, 0, F, packed, so, spi, spb, spc, cap);
         }
     }
-    flush_special_count(spc, nsp);
+    if (defer) raise_fixup_flag(defer_flag, deferred);
 }
 
 // ---------------------------------------------------------- encode COLS
@@ -656,7 +649,9 @@ template <int K, bool BF16, int MODE>
 __global__ void __launch_bounds__(256) k_enc_cols_fast(const uint8_t *__restrict__ in, int64_t n, int x, int y,
                                                        const uint8_t *__restrict__ meta, uint8_t *__restrict__ packed,
                                                        SegOffsets so, int64_t *spi, uint32_t *spb,
-                                                       unsigned long long *spc, int64_t cap, int force_generic) {
+                                                       unsigned long long *spc, int64_t cap, int force_generic,
+                                                       unsigned long long *defer_flag) {
+    const bool defer = defer_flag != nullptr;
     using EL = Elem<BF16>;
     constexpr int NV = BF16 ? 1 : 2;   // 16-byte vectors per group of 8
     constexpr int NP = EL::V / 2;      // pairs per vector
@@ -674,7 +669,7 @@ __global__ void __launch_bounds__(256) k_enc_cols_fast(const uint8_t *__restrict
             }
         return;
     }
-    unsigned nsp = 0;   // NaN/Inf seen on the masked fast path
+    bool deferred = false;   // a warp tile with NaN/Inf (or huge values) left to k_enc_cols_fixup
     uint4 nxt[4][NV];
     int64_t base = gw * 128;
 #pragma unroll
@@ -723,49 +718,16 @@ __global__ void __launch_bounds__(256) k_enc_cols_fast(const uint8_t *__restrict
                 }
             }
             cols_fast_store<K, 0>(RL, RH, cp, packed, so, base + lane, NG);
+        } else if (defer) {   // NaN/Inf (or huge values): k_enc_cols_fixup encodes this warp tile
+            deferred = true;
         } else {
-            // NaN/Inf: masked fast codes per group, or the integer path (huge finite values)
-            int ns = 0;
-#pragma unroll
-            for (int u = 0; u < 4 && ns >= 0; ++u) {
-#pragma unroll
-                for (int t = 0; t < NV && ns >= 0; ++t) {
-                    const uint32_t ww[4] = {r[u][t].x, r[u][t].y, r[u][t].z, r[u][t].w};
-                    uint32_t c2[NP];
-#pragma unroll
-                    for (int p = 0; p < NP; ++p) c2[p] = cp[u][t * NP + p];
-                    const int m = mask_special_codes<K, BF16, MODE, 4>(ww, c2, P);
-#pragma unroll
-                    for (int p = 0; p < NP; ++p) cp[u][t * NP + p] = c2[p];
-                    ns = m < 0 ? -1 : ns + m;
-                }
-            }
-            if (ns >= 0) {
-                // groups past the end were loaded as zeros: no specials counted there
-                nsp += (unsigned)ns;
-                uint32_t RL[8], RH[8];
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const uint32_t y01 = prmt(cp[0][t], cp[1][t], 0x6420), y23 = prmt(cp[2][t], cp[3][t], 0x6420);
-                    RL[2 * t] = prmt(y01, y23, 0x6420);
-                    RL[2 * t + 1] = prmt(y01, y23, 0x7531);
-                    if (K == 9) {
-                        const uint32_t h01 = prmt(cp[0][t] >> 1, cp[1][t] >> 1, 0x6420);
-                        const uint32_t h23 = prmt(cp[2][t] >> 1, cp[3][t] >> 1, 0x6420);
-                        RH[2 * t] = prmt(h01, h23, 0x6420);
-                        RH[2 * t + 1] = prmt(h01, h23, 0x7531);
-                    }
-                }
-                cols_fast_store<K, 0>(RL, RH, cp, packed, so, base + lane, NG);
-            } else {
-                for (int u = 0; u < 4; ++u) {
-                    const int64_t q = base + 32 * u + lane;
-                    if (q < NG) enc_container_generic<BF16, K>(in, 0, q, 1, F, packed, so, spi, spb, spc, cap);
-                }
+            for (int u = 0; u < 4; ++u) {
+                const int64_t q = base + 32 * u + lane;
+                if (q < NG) enc_container_generic<BF16, K>(in, 0, q, 1, F, packed, so, spi, spb, spc, cap);
             }
         }
     }
-    flush_special_count(spc, nsp);
+    if (defer) raise_fixup_flag(defer_flag, deferred);
 }
 
 }  // namespace exmy
@@ -1138,6 +1100,204 @@ __global__ void __launch_bounds__(256) k_quant_fast(const uint8_t *__restrict__ 
             }
         }
     }
+}
+
+// ------------------------------------------------ deferred NaN/Inf tiles
+// The fast encode kernels skip every tile holding NaN/Inf (or a magnitude
+// outside the fast range) and raise a flag; this pass -- one launch that
+// returns at once while the flag is down -- re-reads the tensor, encodes
+// exactly those tiles (fast codes with the NaN/Inf lanes set to code 0, D9's
+// in-band placeholder, or the integer path for huge values), and counts the
+// NaN/Inf per compaction range, so k_specials_compact can skip its counting
+// phase.  The main kernels keep no extra registers for the rare case, and a
+// NaN-heavy tensor (a diverged gradient) stays on the vector path.
+// Workspace (include/exmy.h): ws[0] total, ws[1 + r] range r's count,
+// ws[FIXUP_FLAG_WORD] bit 0 = tiles were deferred, bit 1 = ranges counted.
+constexpr int FIXUP_FLAG_WORD = 1 + SPECIALS_RANGES;
+
+// add a per-thread count (all lanes of the calling warp in range r) to the
+// range's counter, once per warp
+__device__ __forceinline__ void fixup_flush(unsigned long long *ws, int64_t r, unsigned c) {
+    const unsigned m = __activemask();
+    const unsigned t = __reduce_add_sync(m, c);
+    if (t && (threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(ws + 1 + r, (unsigned long long)t);
+}
+
+// NaN/Inf count of NW words (bf16: 2 per word, fp32: 1)
+template <bool BF16, int NW>
+__device__ __forceinline__ int count_specials(const uint32_t (&w)[NW]) {
+    int c = 0;
+#pragma unroll
+    for (int t = 0; t < NW; ++t) {
+        if (BF16) c += __popc(((w[t] & 0x7FFF7FFFu) + 0x00800080u) & 0x80008000u);
+        else c += (w[t] & 0x7F800000u) == 0x7F800000u;
+    }
+    return c;
+}
+
+// ROWS: the main kernel's tiles; range of row group g = g >> lg_rg
+// (ranges of 8 * C * 2^lg_rg elements)
+template <int K, bool BF16, int MODE>
+__global__ void __launch_bounds__(256, 2) k_enc_rows_fixup(const uint8_t *__restrict__ in, int64_t R, int64_t C, int x,
+                                                           int y, const uint8_t *__restrict__ meta,
+                                                           uint8_t *__restrict__ packed, SegOffsets so,
+                                                           unsigned long long *ws, int lg_rg) {
+    if (ws[FIXUP_FLAG_WORD] == 0ull) return;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) atomicOr(ws + FIXUP_FLAG_WORD, 2ull);
+    using EL = Elem<BF16>;
+    constexpr int NW = BF16 ? 2 : 4;
+    const Fmt F = load_fmt(x, y, meta);
+    const FastP P = make_fast(F, BF16, 0);
+    const int64_t CV = C / 4, G = R / 8;
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool act = j < CV;
+    const int64_t c0 = (act ? j : 0) * 4;
+    const uint8_t *src = in + c0 * EL::ES;
+    const int64_t rstride = C * EL::ES;
+    int64_t cur = -1;
+    unsigned cnt = 0, total = 0;
+    uint32_t nxt[8][NW];   // software pipeline: the next tile's rows in flight (a NaN-heavy tensor is all fix-up)
+    int64_t g = blockIdx.y;
+    if (g < G && act) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) load4<BF16>(src + (8 * g + i) * rstride, nxt[i]);
+    }
+    for (; g < G; g += gridDim.y) {
+        const int64_t r = g >> lg_rg;   // the same for the whole CTA
+        if (r != cur) {
+            if (cur >= 0) fixup_flush(ws, cur, cnt);
+            cur = r;
+            cnt = 0;
+        }
+        uint32_t w[8][NW];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int q = 0; q < NW; ++q) w[i][q] = nxt[i][q];
+        const int64_t gn = g + gridDim.y;
+        if (gn < G && act) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) load4<BF16>(src + (8 * gn + i) * rstride, nxt[i]);
+        }
+        if (!act) continue;
+        int ns = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ns += count_specials<BF16, NW>(w[i]);
+        uint32_t cp[8][2];
+        bool bad = false;
+        if (ns == 32) {   // every element NaN/Inf (a diverged tensor): all codes are the placeholder 0
+#pragma unroll
+            for (int i = 0; i < 8; ++i) cp[i][0] = cp[i][1] = 0u;
+        } else {
+            uint32_t amax = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) vec_codes<K, BF16, MODE, NW>(w[i], cp[i], P, amax);
+            if (!amax_special<BF16, MODE>(amax, P)) continue;   // the main kernel stored this tile
+#pragma unroll
+            for (int i = 0; i < 8; ++i) bad = bad || mask_special_codes<K, BF16, MODE, NW>(w[i], cp[i], P) < 0;
+        }
+        cnt += (unsigned)ns;
+        total += (unsigned)ns;
+        if (bad) {   // a huge finite magnitude: the integer path (its specials are counted above)
+            for (int v = 0; v < 4; ++v)
+                enc_container_generic<BF16, K>(in, C, g * C + c0 + v, 0, F, packed, so, nullptr, nullptr, nullptr, 0);
+            continue;
+        }
+        uint32_t RL[1][8], RH[1][8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            RL[0][i] = prmt(cp[i][0], cp[i][1], 0x6420);
+            RH[0][i] = (K == 9) ? prmt(cp[i][0] >> 1, cp[i][1] >> 1, 0x6420) : 0u;
+        }
+        rows_fast_store<K, 1, 0>(RL, RH, packed, so, g, C, c0);
+    }
+    if (cur >= 0) fixup_flush(ws, cur, cnt);
+    flush_special_count(ws, total);   // the total, once per warp
+}
+
+// COLS: the main kernel's warp tiles (128 groups = 1024 elements); range of
+// warp tile `base` = (8 * base) >> lg_l (ranges of 2^lg_l >= 1024 elements)
+template <int K, bool BF16, int MODE>
+__global__ void __launch_bounds__(256) k_enc_cols_fixup(const uint8_t *__restrict__ in, int64_t n, int x, int y,
+                                                        const uint8_t *__restrict__ meta,
+                                                        uint8_t *__restrict__ packed, SegOffsets so,
+                                                        unsigned long long *ws, int lg_l) {
+    if (ws[FIXUP_FLAG_WORD] == 0ull) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(ws + FIXUP_FLAG_WORD, 2ull);
+    using EL = Elem<BF16>;
+    constexpr int NV = BF16 ? 1 : 2;
+    constexpr int NP = EL::V / 2;
+    const Fmt F = load_fmt(x, y, meta);
+    const FastP P = make_fast(F, BF16, 0);
+    const int64_t NG = n / 8;
+    const int lane = threadIdx.x & 31;
+    const int64_t step = (int64_t)gridDim.x * (blockDim.x >> 5) * 128;
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    unsigned total = 0;
+    for (int64_t base = gw * 128; base < NG; base += step) {
+        uint4 r[4][NV];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t q = base + 32 * u + lane;
+#pragma unroll
+            for (int t = 0; t < NV; ++t) r[u][t] = q < NG ? ldg_nc_v4(in + q * 8 * EL::ES + 16 * t) : make_uint4(0, 0, 0, 0);
+        }
+        uint32_t cp[4][4];
+        uint32_t amax = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+#pragma unroll
+            for (int t = 0; t < NV; ++t) {
+                uint32_t c2[NP];
+                const uint32_t ww[4] = {r[u][t].x, r[u][t].y, r[u][t].z, r[u][t].w};
+                vec_codes<K, BF16, MODE, 4>(ww, c2, P, amax);
+#pragma unroll
+                for (int p = 0; p < NP; ++p) cp[u][t * NP + p] = c2[p];
+            }
+        }
+        // the warp tile was deferred iff any lane saw a special / huge value
+        if (!__any_sync(0xFFFFFFFFu, amax_special<BF16, MODE>(amax, P))) continue;
+        int ns = 0;
+        bool bad = false;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+#pragma unroll
+            for (int t = 0; t < NV; ++t) {
+                const uint32_t ww[4] = {r[u][t].x, r[u][t].y, r[u][t].z, r[u][t].w};
+                uint32_t c2[NP];
+#pragma unroll
+                for (int p = 0; p < NP; ++p) c2[p] = cp[u][t * NP + p];
+                ns += count_specials<BF16, 4>(ww);
+                bad = bad || mask_special_codes<K, BF16, MODE, 4>(ww, c2, P) < 0;
+#pragma unroll
+                for (int p = 0; p < NP; ++p) cp[u][t * NP + p] = c2[p];
+            }
+        }
+        fixup_flush(ws, (8 * base) >> lg_l, (unsigned)ns);
+        total += (unsigned)ns;
+        if (bad) {
+            for (int u = 0; u < 4; ++u) {
+                const int64_t q = base + 32 * u + lane;
+                if (q < NG) enc_container_generic<BF16, K>(in, 0, q, 1, F, packed, so, nullptr, nullptr, nullptr, 0);
+            }
+            continue;
+        }
+        uint32_t RL[8], RH[8];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const uint32_t y01 = prmt(cp[0][t], cp[1][t], 0x6420), y23 = prmt(cp[2][t], cp[3][t], 0x6420);
+            RL[2 * t] = prmt(y01, y23, 0x6420);
+            RL[2 * t + 1] = prmt(y01, y23, 0x7531);
+            if (K == 9) {
+                const uint32_t h01 = prmt(cp[0][t] >> 1, cp[1][t] >> 1, 0x6420);
+                const uint32_t h23 = prmt(cp[2][t] >> 1, cp[3][t] >> 1, 0x6420);
+                RH[2 * t] = prmt(h01, h23, 0x6420);
+                RH[2 * t + 1] = prmt(h01, h23, 0x7531);
+            }
+        }
+        cols_fast_store<K, 0>(RL, RH, cp, packed, so, base + lane, NG);
+    }
+    flush_special_count(ws, total);
 }
 
 }  // namespace exmy

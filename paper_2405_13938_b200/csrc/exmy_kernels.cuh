@@ -931,8 +931,9 @@ __global__ void __launch_bounds__(256) k_specials_compact(const uint8_t *__restr
     const bool vec = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
     __shared__ uint32_t wsum[8];
     __shared__ unsigned long long s_prefix;
-    // ---- phase 1: ws[1 + b] := specials in range b
-    for (int b = blockIdx.x; b < nr; b += gridDim.x) {
+    // ---- phase 1: ws[1 + b] := specials in range b (already done by an encode fix-up pass: flag bit 1)
+    const bool counted = (ws[1 + SPECIALS_RANGES] & 2ull) != 0ull;
+    for (int b = counted ? nr : (int)blockIdx.x; b < nr; b += gridDim.x) {
         const int64_t e0 = (int64_t)b * L, e1 = min(n, e0 + L);
         uint32_t c = 0;
         const int64_t full = e0 + ((e1 - e0) / 8) * 8;

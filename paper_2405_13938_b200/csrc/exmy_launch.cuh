@@ -69,13 +69,24 @@ exmy_status launch_max_exponent(const uint8_t *in, bool bf16, int64_t n, uint8_t
 exmy_status launch_emax(const unsigned long long *hist, uint8_t *meta, cudaStream_t st);
 exmy_status launch_quantize(const uint8_t *in, uint8_t *out, bool bf16, int64_t n, int x, int y,
                             const uint8_t *meta, cudaStream_t st);
+// NaN/Inf range bookkeeping of a per-tensor encode (see k_enc_rows_fixup)
+struct SpecialsRanges {
+    bool defer = false;   // the workspace is full-size: fast kernels defer NaN/Inf tiles to the fix-up pass
+    int lg_rows = 0;      // ROWS: range = row group >> lg_rows
+    int lg_cols = 10;     // COLS: range = element >> lg_cols
+    int64_t len(int axis, int64_t C) const {
+        return axis == EXMY_AXIS_ROWS ? 8 * C * ((int64_t)1 << lg_rows) : ((int64_t)1 << lg_cols);
+    }
+};
+SpecialsRanges specials_ranges(int64_t R, int64_t C, bool defer);
 exmy_status launch_encode(const uint8_t *in, bool bf16, int64_t R, int64_t C, int axis, int x, int y,
                           const uint8_t *meta, uint8_t *packed, int64_t *spi, uint32_t *spb,
-                          unsigned long long *spc, int64_t cap, cudaStream_t st);
+                          unsigned long long *spc, int64_t cap, cudaStream_t st, const SpecialsRanges &sr);
 exmy_status launch_specials_sort(int64_t *spi, uint32_t *spb, const unsigned long long *spc, int64_t cap,
                                  cudaStream_t st);
 exmy_status launch_specials_compact(const uint8_t *in, bool bf16, int64_t n, int64_t elem_offset, int64_t *spi,
-                                    uint32_t *spb, unsigned long long *ws, int64_t cap, cudaStream_t st);
+                                    uint32_t *spb, unsigned long long *ws, int64_t cap, cudaStream_t st,
+                                    int64_t L = 0);
 exmy_status launch_decode(const uint8_t *packed, int64_t R, int64_t C, int axis, int x, int y,
                           const uint8_t *meta, uint8_t *out, bool obf16, cudaStream_t st);
 exmy_status launch_specials_scatter(const int64_t *spi, const uint32_t *spb, const unsigned long long *spc,

@@ -1,6 +1,7 @@
 // exmy_tu_blk_decode.cu -- decode / quantize / block max exponent with block
 // metadata launchers.
 #include "exmy_launch.cuh"
+#include "exmy_narrow.cuh"
 
 namespace exmy {
 
@@ -36,6 +37,24 @@ exmy_status launch_dec_blk_k(const uint8_t *packed, int64_t R, int64_t C, int ax
     } else if (fmt_fast) {
         bool vec = aligned(out, 16) && (M.bc % 8 == 0);
         for (int s = 0; s < p.nseg; ++s) vec = vec && aligned(packed + p.so.off[s], p.w[s]);
+        const int64_t gpr = C / 8;
+        const int lg = (gpr >= 8 && gpr <= 64 && (gpr & (gpr - 1)) == 0) ? __builtin_ctzll((unsigned long long)gpr) : -1;
+        if (vec && lg >= 0 && M.br == 1 && M.bc == C && aligned(M.meta, (size_t)(128 >> lg))) {
+            int64_t blocks = cdiv(cdiv(n / 8, 128), 256 / 32);
+            const int64_t maxb = (int64_t)num_sms() * 2;
+            if (blocks > maxb) blocks = maxb;
+#define EXMY_NARROW_DEC(LG)                                                                                          \
+    k_dec_cols_narrow<K, OBF16, LG><<<(unsigned)blocks, 256, 0, st>>>(packed, n, x, y, M.meta, p.so, out, M, C, p.nseg, \
+                                                                     widths)
+            switch (lg) {
+                case 3: EXMY_NARROW_DEC(3); break;
+                case 4: EXMY_NARROW_DEC(4); break;
+                case 5: EXMY_NARROW_DEC(5); break;
+                default: EXMY_NARROW_DEC(6); break;
+            }
+#undef EXMY_NARROW_DEC
+            return launch_status();
+        }
         if (vec) {
             const int threads = 256;
             static int occ = 0;

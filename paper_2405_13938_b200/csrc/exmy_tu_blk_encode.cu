@@ -1,5 +1,6 @@
 // exmy_tu_blk_encode.cu -- encode with block metadata launchers.
 #include "exmy_launch.cuh"
+#include "exmy_narrow.cuh"
 
 #ifndef RWS_ENABLE
 #define RWS_ENABLE 1   // TMA-staged fused per-row encode for rows <= RWS_MAX_ROW_BYTES
@@ -35,6 +36,25 @@ exmy_status launch_enc_blk_km(const uint8_t *in, int64_t R, int64_t C, int axis,
     } else {
         bool vec = aligned(in, 16) && (M.bc % 8 == 0);
         for (int s = 0; s < p.nseg; ++s) vec = vec && aligned(packed + p.so.off[s], p.w[s]);
+        // one byte per row of 64 .. 512 columns (embedding tables): the narrow-row kernel
+        const int64_t gpr = C / 8;
+        const int lg = (gpr >= 8 && gpr <= 64 && (gpr & (gpr - 1)) == 0) ? __builtin_ctzll((unsigned long long)gpr) : -1;
+        if (vec && lg >= 0 && M.br == 1 && M.bc == C && aligned(M.meta, (size_t)(128 >> lg))) {
+            int64_t blocks = cdiv(cdiv(n / 8, 128), 256 / 32);
+            const int64_t maxb = (int64_t)num_sms() * 2;
+            if (blocks > maxb) blocks = maxb;
+#define EXMY_NARROW_ENC(LG)                                                                                    \
+    k_enc_cols_narrow<K, BF16, MODE, LG><<<(unsigned)blocks, 256, 0, st>>>(in, n, x, y, M.meta, packed, p.so, spi, \
+                                                                          spb, spc, cap, M, C, g_force_generic)
+            switch (lg) {
+                case 3: EXMY_NARROW_ENC(3); break;
+                case 4: EXMY_NARROW_ENC(4); break;
+                case 5: EXMY_NARROW_ENC(5); break;
+                default: EXMY_NARROW_ENC(6); break;
+            }
+#undef EXMY_NARROW_ENC
+            return launch_status();
+        }
         if (vec) {
             const int threads = 256;
             static int occ = 0;

@@ -235,7 +235,9 @@ exmy_status exmy_encode_fs(const void *in, int dtype, int64_t rows, int64_t cols
     if (sp_capacity > 0 && (!sp_index || !sp_bits)) return EXMY_E_ARG;
     cudaStream_t st = S_(stream);
     auto *spc = reinterpret_cast<unsigned long long *>(sp_count);
-    if (spc && cudaMemsetAsync(spc, 0, sizeof(unsigned long long), st) != cudaSuccess) return EXMY_E_CUDA;
+    if (spc && cudaMemsetAsync(spc, 0, sizeof(unsigned long long) * (sp_capacity > 0 ? EXMY_SPECIALS_WORDS : 1), st) !=
+                   cudaSuccess)
+        return EXMY_E_CUDA;
     if (rows == 0 || cols == 0) return EXMY_OK;
     if (!in || !packed || !scale) return EXMY_E_ARG;
     const int k = 1 + x + y;

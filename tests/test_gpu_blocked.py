@@ -202,3 +202,29 @@ def test_encode_rowwise_config2_shape(exmy, orc):
     assert torch.equal(p.meta, m)
     p2 = exmy.encode_blocked(t, "e3m3", m, "row")
     assert torch.equal(p.data, p2.data)
+
+
+@pytest.mark.parametrize("cols", [64, 128, 256, 512])
+@pytest.mark.parametrize("fmt", [(4, 2), (3, 1), (2, 4), (6, 0), (5, 3), (0, 6), (4, 3)], ids=lambda f: f"e{f[0]}m{f[1]}")
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+def test_per_row_cols_narrow_rows(exmy, orc, cols, fmt, dt):
+    """Embedding-width tables (config 5: 128 columns) with one metadata byte per
+    row, COLS packing: the narrow-row kernels (a warp tile = 128/gpr whole rows,
+    one pipelined metadata load per tile) == the oracle, with a ragged last
+    tile, rows of wildly different scale, NaN rows and bytes forced outside the
+    fast ranges (0, 254) on some rows (integer path inside the tile)"""
+    rows = 8 * 128 // (cols // 8) * 3 + 24          # three whole tiles and a ragged fourth
+    bits = rowscaled_bits((rows, cols), cols + fmt[0], dt)
+    d = W.from_bits(bits).to(DEV)
+    meta = orc.block_max_exponent(bits, (1, cols))
+    meta[5, 0], meta[17, 0], meta[rows - 1, 0] = 0, 254, 0
+    m = torch.from_numpy(meta.copy()).to(DEV)
+    p = exmy.encode_blocked(d, fmt, m, "row", axis="cols", specials_capacity=bits.size)
+    pref, idx, sb, ns = orc.encode_blocked(bits, fmt, meta, (1, cols), orc.COLS)
+    np.testing.assert_array_equal(p.data.cpu().numpy(), pref)
+    spi, spb, cnt = p.specials()
+    assert cnt == ns and np.array_equal(spi.cpu().numpy(), idx)
+    for od in (np.uint16, np.uint32):
+        out = exmy.decode(p, torch.bfloat16 if od == np.uint16 else torch.float32)
+        ref = orc.decode_blocked(pref, bits.shape, fmt, meta, (1, cols), orc.COLS, idx, sb, out_dtype=od)
+        np.testing.assert_array_equal(W.to_bits(out), ref)
