@@ -229,8 +229,10 @@ typedef enum { EXMY_SCHEME_MAX_BEFORE = 0, EXMY_SCHEME_MAX_AFTER = 1 } exmy_sche
  * largest magnitude after rounding it RTNE to y mantissa bits in its own
  * binade (so 3.9 with y=1 gives 129, "it always rounds up to 4.0").  NaN/Inf
  * are ignored; a block with no finite non-zero element gets 0; results are
- * clamped to 254.  One warp per block: use exmy_exponent_histogram for
- * whole-tensor metadata. */
+ * clamped to 254.  Kernels: one warp per block, or for sub-row blocks of
+ * <= 32 16-byte vectors (1 x 32, per-row blocks of narrow rows) a segmented
+ * reduction over contiguous 16 KB chunks; whole-tensor metadata is
+ * exmy_max_exponent / exmy_exponent_histogram. */
 exmy_status exmy_block_max_exponent(const void *in, int dtype, int64_t rows, int64_t cols,
                                     int64_t block_rows, int64_t block_cols, int y, int scheme,
                                     uint8_t *meta, void *stream);
@@ -255,10 +257,14 @@ exmy_status exmy_decode_blocked(const uint8_t *packed, int64_t rows, int64_t col
  * P:622-627): meta[r] (device, rows bytes) := the row's
  * maximum exponent under `scheme`, then the tensor is encoded with block
  * (1, cols) -- bit-identical to exmy_block_max_exponent + exmy_encode_blocked.
- * ROWS with aligned rows of at most 16 KB runs one fused kernel (each CTA
- * reduces a row group's maxima and re-reads its rows from L2 to encode
- * them); longer rows and COLS take the two-launch path (their L2 re-read
- * misses; measured in DESIGN.md). */
+ * ROWS with aligned rows of at most 9216 bytes runs one fused kernel: a
+ * CTA stages its row group (8 rows) in shared memory with bulk
+ * asynchronous copies (cp.async.bulk on an mbarrier) and computes the 8
+ * maxima and the codes from there, so HBM is read once; rows up to 16 KB
+ * run a fused kernel that re-reads the rows from L2 (evict_last /
+ * evict_first policies); longer rows and COLS take two launches (row maxima,
+ * then the blocked encode -- COLS rows of 64..512 columns through the
+ * narrow-row kernel).  Measured in DESIGN.md §8b / §12.6. */
 exmy_status exmy_encode_rowwise(const void *in, int dtype, int64_t rows, int64_t cols, int axis,
                                 int x, int y, int scheme, uint8_t *meta, uint8_t *packed,
                                 int64_t *sp_index, uint32_t *sp_bits, uint64_t *sp_count,
@@ -295,7 +301,9 @@ exmy_status exmy_decode_rows(const uint8_t *packed, int64_t rows, int64_t cols, 
  * as exmy_encode_blocked / exmy_decode_blocked; scale is device memory,
  * (rows/block_rows) * (cols/block_cols) floats in block-row-major order. */
 
-/* scale[b] := max |finite v| over block b (fp32).  One warp per block. */
+/* scale[b] := max |finite v| over block b (fp32).  One warp per block, or
+ * for sub-row blocks of <= 32 16-byte vectors a segmented reduction (a
+ * thread per vector, the block's lanes combined by shuffles). */
 exmy_status exmy_block_float_scale(const void *in, int dtype, int64_t rows, int64_t cols,
                                    int64_t block_rows, int64_t block_cols, float *scale,
                                    void *stream);
