@@ -60,6 +60,7 @@ def _load():
         "exmy_debug_hist_mode": ([i32], i32),
         "exmy_debug_hist_blocks": ([i32], i32),
         "exmy_debug_enc_tma": ([i32], i32),
+        "exmy_debug_rowwise_cluster": ([i32], i32),
         "exmy_debug_probe": ([vp, i64, vp, i64, vp], i32),
         "exmy_exponent_histogram": ([vp, i32, i64, vp, vp], i32),
         "exmy_emax_from_histogram": ([vp, vp, vp], i32),
@@ -111,7 +112,7 @@ _lib = _load()
 LIB_PATH = _LIB_PATH
 EXPORTED = ["exmy_version", "exmy_specials_words", "exmy_status_string", "exmy_format_valid", "exmy_packed_bytes", "exmy_segments",
             "exmy_bias_from_emax", "exmy_emax_from_bias", "exmy_emax_from_histogram_host", "exmy_choose_x",
-            "exmy_debug_force_generic", "exmy_debug_hist_mode", "exmy_debug_hist_blocks", "exmy_debug_enc_tma", "exmy_debug_probe",
+            "exmy_debug_force_generic", "exmy_debug_hist_mode", "exmy_debug_hist_blocks", "exmy_debug_enc_tma", "exmy_debug_rowwise_cluster", "exmy_debug_probe",
             "exmy_exponent_histogram",
             "exmy_emax_from_histogram", "exmy_quantize", "exmy_encode", "exmy_decode", "exmy_encode_host",
             "exmy_decode_host", "exmy_block_max_exponent", "exmy_quantize_blocked", "exmy_encode_blocked",
@@ -224,6 +225,12 @@ def enc_tma(on: bool | None = None) -> int:
     """knob: ROWS encode through the TMA-staged kernel (1) or the register
     pipeline (0); returns the previous setting"""
     return _lib.exmy_debug_enc_tma(-1 if on is None else int(on))
+
+
+def rowwise_cluster(on: bool | None = None) -> int:
+    """knob: wide-row encode_rowwise on thread-block clusters (1) or the
+    two-pass paths (0); returns the previous setting"""
+    return _lib.exmy_debug_rowwise_cluster(-1 if on is None else int(on))
 
 
 def hist_blocks(blocks: int | None = None) -> int:

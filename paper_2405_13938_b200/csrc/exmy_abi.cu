@@ -12,6 +12,7 @@ int g_force_generic = 0;
 int g_hist_mode = 3;
 int g_hist_blocks = 0;
 int g_enc_tma = 0;
+int g_rowwise_cluster = 1;
 }  // namespace exmy
 
 using namespace exmy;
@@ -136,6 +137,12 @@ int exmy_debug_force_generic(int on) {
 int exmy_debug_hist_mode(int mode) {
     int prev = g_hist_mode;
     if (mode >= 0) g_hist_mode = mode;
+    return prev;
+}
+
+int exmy_debug_rowwise_cluster(int on) {
+    int prev = g_rowwise_cluster;
+    if (on >= 0) g_rowwise_cluster = on;
     return prev;
 }
 

@@ -1283,4 +1283,136 @@ __global__ void __launch_bounds__(RWS_THREADS) k_enc_rowwise_smem(const uint8_t 
                                      rws_sm, sbase, bar, phase, s_m, s_e);
 }
 
+// ------------ fused per-row metadata + encode for WIDE rows (thread-block
+// cluster, distributed shared memory).  A cluster of CL CTAs owns one row
+// group (8 rows) at a time; CTA rank r stages the column slab
+// [r C / CL, (r + 1) C / CL) of the 8 rows in its shared memory with 8 bulk
+// asynchronous copies (cp.async.bulk on an mbarrier), reduces the slab's 8
+// row maxima, and the CTAs exchange those partial maxima through distributed
+// shared memory (a cluster barrier, then loads from the peers' shared memory
+// via map_shared_rank) -- so every CTA knows the row group's 8 metadata bytes
+// and encodes its slab from its own shared memory.  HBM is read exactly once
+// for rows up to CL x 9 KB (config 2's 32 KB rows: CL = 4), where the
+// single-CTA staged kernel stops at 9 KB and the two-pass kernel re-reads
+// the rows from L2.  The partial maxima are double-buffered by row-group
+// parity: one cluster barrier per row group keeps a peer's slot stable
+// until every CTA has read it.
+template <int K, bool BF16, int MODE, int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(RWS_THREADS)
+    k_enc_rowwise_cluster(const uint8_t *__restrict__ in, int64_t R, int64_t C, int x, int y, int scheme,
+                          uint8_t *__restrict__ meta, uint8_t *__restrict__ packed, SegOffsets so, int64_t *spi,
+                          uint32_t *spb, unsigned long long *spc, int64_t cap, int force_generic) {
+    using EL = Elem<BF16>;
+    constexpr int NW = BF16 ? 2 : 4;
+    constexpr bool SIMD = (MODE == ENC_SIMD || MODE == ENC_SIMD_Y0);
+    extern __shared__ __align__(16) uint8_t rws_sm[];   // 8 rows x C / CL elements
+    __shared__ __align__(8) unsigned long long s_bar;
+    __shared__ uint32_t s_m[RWS_THREADS / 32][8];
+    __shared__ uint32_t s_part[2][8];   // this slab's 8 row maxima (fp32 magnitude bits), by row-group parity
+    __shared__ int s_e[8];
+    cooperative_groups::cluster_group cluster = cooperative_groups::this_cluster();
+    const int rank = (int)cluster.block_rank();
+    const FastP P = make_fast(fmt_of(x, y, 0), BF16, 1);
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(rws_sm);
+    const int64_t Cs = C / CL;                              // slab columns
+    const uint32_t rowb = (uint32_t)(Cs * EL::ES);          // slab row bytes (staged)
+    const int64_t growb = C * EL::ES;                       // tensor row bytes
+    const int CV16 = (int)(rowb / 16), CV4 = (int)(Cs / 4);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int64_t ncl = gridDim.x / CL, cid = blockIdx.x / CL;
+    uint32_t phase = 0;
+    int par = 0;
+    for (int64_t g = cid; g < R / 8; g += ncl, phase ^= 1u, par ^= 1) {
+        if (tid == 0) {   // this CTA's slab of the row group -> shared memory (async proxy)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(bar, 8u * rowb);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                bulk_g2s(sbase + i * rowb, in + (8 * g + i) * growb + (int64_t)rank * rowb, rowb, bar);
+        }
+        mbar_wait(bar, phase);
+        // ---- pass 1: the slab's row maxima
+        uint32_t m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int j = tid; j < CV16; j += RWS_THREADS) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const uint4 v = *reinterpret_cast<const uint4 *>(rws_sm + i * rowb + j * 16);
+                m[i] = vec_max_mag<BF16>(v, m[i]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t mm = BF16 ? max((m[i] & 0xFFFFu) << 16, m[i] & 0xFFFF0000u) : m[i];
+            const uint32_t r = __reduce_max_sync(0xFFFFFFFFu, mm);
+            if (lane == 0) s_m[warp][i] = r;
+        }
+        __syncthreads();
+        if (tid < 8) {
+            uint32_t r = 0;
+#pragma unroll
+            for (int w = 0; w < RWS_THREADS / 32; ++w) r = max(r, s_m[w][tid]);
+            s_part[par][tid] = r;
+        }
+        cluster.sync();   // every slab's partial maxima are written
+        if (tid < 8) {    // the row's maximum over the cluster's slabs (distributed shared memory)
+            uint32_t r = 0;
+#pragma unroll
+            for (int q = 0; q < CL; ++q) r = max(r, *cluster.map_shared_rank(&s_part[par][tid], q));
+            int e = scheme == 0 ? (int)(r >> 23) : exp_after_rounding(r, y);
+            e = e > 254 ? 254 : e;
+            s_e[tid] = e;
+            if (rank == 0) meta[8 * g + tid] = (uint8_t)e;
+        }
+        __syncthreads();
+        int e8[8];
+        bool ok = !force_generic;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            e8[i] = s_e[i];
+            ok = ok && make_rowp<SIMD>(e8[i], x, y).ok;
+        }
+        // ---- pass 2: encode the slab (8 x 4 tiles) from shared memory
+        for (int jj = tid; jj < CV4; jj += RWS_THREADS) {
+            const int64_t c0 = (int64_t)rank * Cs + jj * 4;   // tensor column
+            uint32_t w[8][NW];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const uint8_t *sp = rws_sm + i * rowb + jj * 4 * EL::ES;
+                if constexpr (BF16) {
+                    const uint2 t = *reinterpret_cast<const uint2 *>(sp);
+                    w[i][0] = t.x; w[i][1] = t.y;
+                } else {
+                    const uint4 t = *reinterpret_cast<const uint4 *>(sp);
+                    w[i][0] = t.x; w[i][1] = t.y; w[i][2] = t.z; w[i][3] = t.w;
+                }
+            }
+            uint32_t cp[8][2];
+            uint32_t amax = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                vec_codes_r<K, BF16, MODE, NW>(w[i], cp[i], P, make_rowp<SIMD>(e8[i], x, y), amax);
+            if (ok && !amax_special<BF16, MODE>(amax, P)) {
+                uint32_t RL[1][8], RH[1][8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    RL[0][i] = prmt(cp[i][0], cp[i][1], 0x6420);
+                    RH[0][i] = (K == 9) ? prmt(cp[i][0] >> 1, cp[i][1] >> 1, 0x6420) : 0u;
+                }
+                rows_fast_store<K, 1, 0>(RL, RH, packed, so, g, C, c0);
+            } else {
+                for (int v = 0; v < 4; ++v)
+                    enc_container_generic_rows8<BF16, K>(in, C, g, c0 + v, x, y, e8, packed, so, spi, spb, spc, cap);
+            }
+        }
+        __syncthreads();   // the staging buffer and s_e are reused by the next row group
+    }
+    cluster.sync();   // no CTA leaves while a peer may still read its partial maxima
+}
+
 }  // namespace exmy

@@ -308,6 +308,8 @@ __global__ void k_fs_decode_generic(const uint8_t *__restrict__ packed, int64_t 
 template <bool BF16, bool FAST>
 __device__ __forceinline__ uint32_t fs_quant_elem(uint32_t u, const FsE &fe, const FsD &fd, const Fmt &F,
                                                   const FastP &P, const FsMap &S, uint32_t am) {
+    (void)S;
+    (void)am;   // results below 2^-100 are redone exactly by k_fs_quant_fixup
     if (is_special_f32(u)) return u;
     const uint32_t us = fs_in(u, fe);
     uint32_t g;
@@ -317,12 +319,16 @@ __device__ __forceinline__ uint32_t fs_quant_elem(uint32_t u, const FsE &fe, con
     } else {
         g = dec_code_generic<24>(enc_code_generic(us, F), F);
     }
-    uint32_t o = fs_out(g, fd);
-    if ((o & 0x7FFFFFFFu) < 0x0D800000u || S.x8) {   // tiny results / x = 8: the definition itself
-        const uint32_t mag = enc_code_generic(us, F) & F.M;
-        if (mag != 0u) o = fs_out_exact(mag, am, F.x, F.y) | (o & 0x80000000u);
-    }
+    const uint32_t o = fs_out(g, fd);
     return BF16 ? (f32_to_bf16_bits(o) << 16) : o;
+}
+
+// the exact float-scaled emulation of one finite input pattern: the
+// e_max-127 code of the scaled value, then RN32(g amax / G) by integers
+__device__ __noinline__ uint32_t fs_quant_exact(uint32_t u, uint32_t am, float G, int x, int y) {
+    const Fmt F = fmt_of(x, y, 127);
+    const uint32_t code = enc_code_generic(fs_in(u, fs_enc(am, G)), F);
+    return fs_out_exact(code & F.M, am, x, y) | ((code >> (x + y)) << 31);
 }
 
 template <bool BF16>
@@ -565,11 +571,8 @@ __global__ void __launch_bounds__(256) k_fs_dec_rows(const uint8_t *__restrict__
 #pragma unroll
         for (int i = 0; i < 8; ++i) { RL[0][i] = 0; RH[0][i] = 0; }
         rows_unpack_raw<K, 1, 0>(raw, RL, RH);
-        // rows whose smallest non-zero result could fall below 2^-100 (or x = 8)
-        // take the checked variant: results < 2^-100 from the definition itself
-        bool chk = S.x8 != 0;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) chk = chk || hi[i] < S.tchk;
+        // (blocks whose results can fall below 2^-100, and x = 8, are redone
+        // exactly afterwards by k_fs_dec_fixup)
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             uint32_t o[4];
@@ -579,12 +582,7 @@ __global__ void __launch_bounds__(256) k_fs_dec_rows(const uint8_t *__restrict__
                 if (K == 9) code |= ((RH[0][i] >> (8 * v)) & 0xFFu) << 1;
                 const uint32_t gb = FAST ? dec_f32_fast<K, false>(code, P, y) : dec_code_generic<24>(code, F);
                 const float gf = __uint_as_float(gb & 0x7FFFFFFFu);
-                uint32_t r = __float_as_uint(__fmaf_rn(gf, hi[i], __fmul_rn(gf, lo[i])));
-                if (chk) {
-                    const uint32_t mag = code & F.M;
-                    if (mag != 0u && (S.x8 || r < 0x0D800000u))
-                        r = fs_out_exact(mag, fs_amax_at(S, 8 * g + i, c0), x, y);
-                }
+                const uint32_t r = __float_as_uint(__fmaf_rn(gf, hi[i], __fmul_rn(gf, lo[i])));
                 o[v] = r | ((code << (32 - K)) & 0x80000000u);
             }
             uint8_t *dst = out + ((8 * g + i) * C + c0) * EL::ES;
@@ -593,6 +591,74 @@ __global__ void __launch_bounds__(256) k_fs_dec_rows(const uint8_t *__restrict__
                        f32_to_bf16_bits(o[2]) | (f32_to_bf16_bits(o[3]) << 16));
             else
                 stg_v4(dst, make_uint4(o[0], o[1], o[2], o[3]));
+        }
+    }
+}
+
+// ------------------------------------------------ exact small results
+// The fast float-scale kernels decode with FMUL + FFMA, exact for results
+// >= 2^-100 (reading D23).  A block can produce smaller ones only when
+// amax * g_min / G < 2^-99 (g_min = the smallest non-zero grid value), i.e.
+// amax < tchk * G, and x = 8 codes lie below the fp32 range: those blocks are
+// redone here with the integer evaluation of the definition.  One warp per
+// block; a block that needs nothing costs one metadata load, so the pass is
+// a few microseconds on ordinary tensors (and the fast kernels keep their
+// round-1 register budgets).
+__device__ __forceinline__ bool fs_block_needs_exact(const FsMap &S, float G, int64_t b) {
+    if (S.x8) return true;
+    const float a = __uint_as_float(__float_as_uint(__ldg(S.amax + b)) & 0x7FFFFFFFu);
+    return a > 0.f && a < S.tchk * G * 1.0625f;   // conservative
+}
+
+template <bool BF16>
+__global__ void __launch_bounds__(256) k_fs_quant_fixup(const uint8_t *__restrict__ in, uint8_t *__restrict__ out,
+                                                        int64_t R, int64_t C, int x, int y, FsMap S, float G) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nb = (R / S.br) * S.nbc, warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); b < nb; b += warps) {
+        if (!fs_block_needs_exact(S, G, b)) continue;
+        const uint32_t am = __float_as_uint(__ldg(S.amax + b)) & 0x7FFFFFFFu;
+        const int64_t r0 = (b / S.nbc) * S.br, c0 = (b % S.nbc) * S.bc;
+        for (int64_t k = lane; k < S.br * S.bc; k += 32) {
+            const int64_t e = (r0 + k / S.bc) * C + c0 + k % S.bc;
+            const uint32_t u = load_elem_scalar<BF16>(in, e);
+            if (is_special_f32(u)) continue;   // passed through by the main kernel
+            const uint32_t o = fs_quant_exact(u, am, G, x, y);
+            if (BF16) {
+                const uint16_t h = (uint16_t)f32_to_bf16_bits(o);
+                memcpy(out + 2 * e, &h, 2);
+            } else {
+                memcpy(out + 4 * e, &o, 4);
+            }
+        }
+    }
+}
+
+// decode: every container (8 codes) touching a block that needs the exact
+// evaluation is decoded again by fs_dec_container (whose per-element check
+// covers all of its blocks); a container shared by two such blocks is
+// written twice with the same bytes
+template <bool OBF16>
+__global__ void __launch_bounds__(256) k_fs_dec_fixup(const uint8_t *__restrict__ packed, int64_t R, int64_t C,
+                                                      int axis, int x, int y, FsMap S, float G, SegOffsets so,
+                                                      int nseg, int4 widths, uint8_t *__restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nb = (R / S.br) * S.nbc, warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); b < nb; b += warps) {
+        if (!fs_block_needs_exact(S, G, b)) continue;
+        const int64_t r0 = (b / S.nbc) * S.br, c0 = (b % S.nbc) * S.bc;
+        if (axis == 0) {   // ROWS: container (g, c) holds rows 8g..8g+7 of column c
+            const int64_t g0 = r0 / 8, g1 = (r0 + S.br + 7) / 8, nc = g1 - g0;
+            for (int64_t k = lane; k < nc * S.bc; k += 32)
+                fs_dec_container<OBF16>(packed, C, (g0 + k / S.bc) * C + c0 + k % S.bc, 0, x, y, S, G, so, nseg,
+                                        widths, out);
+        } else {           // COLS: container q holds elements 8q .. 8q+7 of one row
+            const int64_t per_row = (c0 % 8 + S.bc + 7) / 8;
+            for (int64_t k = lane; k < S.br * per_row; k += 32) {
+                const int64_t r = r0 + k / per_row;
+                fs_dec_container<OBF16>(packed, C, (r * C + c0) / 8 + k % per_row, 1, x, y, S, G, so, nseg, widths,
+                                        out);
+            }
         }
     }
 }

@@ -14,6 +14,7 @@ extern int g_force_generic;   // exmy_debug_force_generic
 extern int g_hist_mode;       // exmy_debug_hist_mode
 extern int g_hist_blocks;     // exmy_debug_hist_blocks
 extern int g_enc_tma;         // exmy_debug_enc_tma: ROWS encode through the TMA-staged kernel
+extern int g_rowwise_cluster; // exmy_debug_rowwise_cluster: wide-row fused per-row encode on clusters
 
 inline int num_sms() {
     static int cache[64] = {0};

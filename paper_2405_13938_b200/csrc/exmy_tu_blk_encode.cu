@@ -112,6 +112,38 @@ exmy_status launch_rowwise_km(const uint8_t *in, int64_t R, int64_t C, int x, in
                               int64_t cap, cudaStream_t st) {
 #if RWS_ENABLE
     const int64_t rowb = C * Elem<BF16>::ES;
+    // wide rows: a cluster of CL CTAs stages a row group in column slabs (distributed shared memory)
+    int cl = 0;
+    for (int c : {2, 4, 8})
+        if (!cl && rowb > RWS_MAX_ROW_BYTES && rowb % (16 * c) == 0 && rowb / c <= RWS_MAX_ROW_BYTES &&
+            C % (4 * c) == 0 && g_rowwise_cluster)
+            cl = c;
+    if (cl) {
+        const size_t sm = (size_t)(8 * (rowb / cl));
+        // per (cluster size, device) configuration: the three kernels share one pointer type
+        static unsigned long long configured[9] = {0};
+        static int occ_cl[9] = {0};
+        auto launch = [&](auto kern, int CLv) -> exmy_status {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            if (dev < 0 || dev >= 64 || !(configured[CLv] & (1ull << dev))) {
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8 * RWS_MAX_ROW_BYTES));
+                occ_cl[CLv] = occupancy(kern, RWS_THREADS, 8 * RWS_MAX_ROW_BYTES);
+                if (dev >= 0 && dev < 64) configured[CLv] |= 1ull << dev;
+            }
+            const int occ_c = occ_cl[CLv];
+            int64_t blocks = (int64_t)num_sms() * (occ_c > 0 ? occ_c : 1);
+            if (blocks > (R / 8) * CLv) blocks = (R / 8) * CLv;
+            blocks = blocks / CLv * CLv;
+            if (blocks < CLv) blocks = CLv;
+            kern<<<(unsigned)blocks, RWS_THREADS, sm, st>>>(in, R, C, x, y, scheme, meta, packed, p.so, spi, spb, spc,
+                                                          cap, g_force_generic);
+            return launch_status();
+        };
+        if (cl == 2) return launch(k_enc_rowwise_cluster<K, BF16, MODE, 2>, 2);
+        if (cl == 4) return launch(k_enc_rowwise_cluster<K, BF16, MODE, 4>, 4);
+        return launch(k_enc_rowwise_cluster<K, BF16, MODE, 8>, 8);
+    }
     if (rowb % 16 == 0 && rowb <= RWS_MAX_ROW_BYTES) {   // TMA-staged: each row group read from HBM once
         const size_t sm = (size_t)(8 * rowb);
         static unsigned long long configured = 0;
@@ -193,7 +225,9 @@ exmy_status launch_encode_rowwise(const uint8_t *in, bool bf16, int64_t R, int64
     // measured (config-2 rows x 2048..16384 columns): the fused two-pass kernel
     // beats block max + blocked encode while a row group (8 rows) stays within
     // 128 KB; beyond that its second pass misses L2 and the two launches win
-    bool vec = aligned(in, 16) && (C % (bf16 ? 8 : 4) == 0) && (C * (bf16 ? 2 : 4) <= 16384);
+    // rows up to 8 x 9 KB: one HBM read (single CTA or a cluster); longer rows: the two launches
+    bool vec = aligned(in, 16) && (C % (bf16 ? 8 : 4) == 0) &&
+               (C * (bf16 ? 2 : 4) <= (g_rowwise_cluster ? 8 * RWS_MAX_ROW_BYTES : 16384));
     for (int s = 0; s < p.nseg; ++s) vec = vec && aligned(packed + p.so.off[s], p.w[s] == 8 ? 4 : 4 * p.w[s]);
     if (!vec) return EXMY_E_ALIGN;
     return bf16 ? rowwise_dispatch<true>(k, in, R, C, x, y, scheme, meta, packed, p, spi, spb, spc, cap, st)

@@ -118,6 +118,10 @@ exmy_status dec_k(const uint8_t *packed, int64_t R, int64_t C, int axis, int x, 
             if (ws) k_fs_dec_rows<K, OBF16, false, true><<<grid, threads, 0, st>>>(packed, R, C, x, y, M, G, p.so, out, lpb);
             else k_fs_dec_rows<K, OBF16, false, false><<<grid, threads, 0, st>>>(packed, R, C, x, y, M, G, p.so, out, 32);
         }
+        // blocks whose results can fall below 2^-100 (and x = 8): the exact evaluation
+        const int64_t nb = (R / M.br) * M.nbc;
+        k_fs_dec_fixup<OBF16><<<grid1(nb * 32, 8), 256, 0, st>>>(packed, R, C, axis, x, y, M, G, p.so, p.nseg,
+                                                                 make_int4(p.w[0], p.w[1], p.w[2], p.w[3]), out);
         return launch_status();
     }
     const int64_t ncont = R * C / 8;
@@ -220,6 +224,10 @@ exmy_status exmy_quantize_fs(const void *in, void *out, int dtype, int64_t rows,
         FS_QUANT(0, grid);
     }
 #undef FS_QUANT
+    // blocks whose results can fall below 2^-100 (and x = 8): the exact evaluation
+    const int64_t nb = (rows / block_rows) * (cols / block_cols);
+    if (dtype == EXMY_BF16) k_fs_quant_fixup<true><<<grid1(nb * 32, 8), 256, 0, st>>>(pi, po, rows, cols, x, y, M, G);
+    else k_fs_quant_fixup<false><<<grid1(nb * 32, 8), 256, 0, st>>>(pi, po, rows, cols, x, y, M, G);
     return launch_status();
 }
 
