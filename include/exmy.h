@@ -202,7 +202,8 @@ int exmy_debug_hist_mode(int mode);
 int exmy_debug_enc_tma(int on);
 /* exmy_encode_rowwise for rows of 9 KB .. 72 KB: 1 = the thread-block-cluster
  * kernel (row-group slabs in distributed shared memory, one HBM read), 0 =
- * the two-pass / two-launch paths; -1 queries.  Returns the previous value. */
+ * the two-pass / two-launch paths (the default: measured faster, DESIGN.md
+ * section 12); -1 queries.  Returns the previous value. */
 int exmy_debug_rowwise_cluster(int on);
 int exmy_debug_hist_blocks(int blocks);
 

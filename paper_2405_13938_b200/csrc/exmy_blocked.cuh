@@ -242,6 +242,94 @@ __global__ void __launch_bounds__(256, ENC_ROWS_BLK_MINB) k_enc_rows_blk(const u
     }
 }
 
+// ROWS encode with ONE METADATA BYTE PER ROW (the paper's recipe):
+// a CTA works on one row group at a time, so its 8 metadata bytes are one
+// uniform 8-byte load (prefetched with the tile) and each row's constants
+// (subnormal clamp, exponent offset) take 4 SIMD ops per 32 elements (PRMT
+// the byte into both 16-bit lanes, clamp, two IMADs) instead of make_rowp's
+// scalar chain per element vector (k_enc_rows_blk) or 16 shuffles per tile.
+template <int K, bool BF16, int MODE>
+__global__ void __launch_bounds__(256, (BF16 && K <= 7) ? 3 : 2)
+    k_enc_rows_rowmeta(const uint8_t *__restrict__ in, int64_t R, int64_t C, int x, int y,
+                       const uint8_t *__restrict__ meta, uint8_t *__restrict__ packed, SegOffsets so, int64_t *spi,
+                       uint32_t *spb, unsigned long long *spc, int64_t cap, int force_generic, MetaMap M) {
+    using EL = Elem<BF16>;
+    constexpr int NW = BF16 ? 2 : 4;
+    constexpr bool SIMD = (MODE == ENC_SIMD || MODE == ENC_SIMD_Y0);
+    const FastP P = make_fast(fmt_of(x, y, 0), BF16, 1);   // e_max-independent constants only
+    const int64_t CV = C / 4, G = R / 8;
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= CV) return;
+    const int64_t c0 = j * 4;
+    const uint8_t *src = in + c0 * EL::ES;
+    const int64_t rstride = C * EL::ES;
+    const uint32_t rs32 = (uint32_t)rstride;
+    // row constants from the byte e: u = o + 1 = e - (top - 1); SIMD lanes
+    // lo2 = u << 7, k3 = u << y; fp32 lo = u << 23, k3f = u << y
+    const uint32_t top1 = (uint32_t)((1 << x) - 2) * (SIMD ? 0x00010001u : 1u);
+    // fast preconditions on every byte: top <= e <= (SIMD ? 246 : 230) + y
+    const uint32_t emin4 = (uint32_t)((1 << x) - 1) * 0x01010101u;
+    const int ehi = (SIMD ? 246 : 230) + y;
+    const uint32_t emax4 = (uint32_t)(ehi > 255 ? 255 : ehi) * 0x01010101u;
+    uint32_t nw[8][NW];
+    uint2 nm = make_uint2(0u, 0u);
+    int64_t g = blockIdx.y;
+    if (g < G) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) load4<BF16>(src + (8 * g + i) * rstride, nw[i]);
+        nm = __ldg(reinterpret_cast<const uint2 *>(meta) + g);
+    }
+    for (; g < G; g += gridDim.y) {
+        uint32_t w[8][NW];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int q = 0; q < NW; ++q) w[i][q] = nw[i][q];
+        const uint2 em = nm;
+        const int64_t gn = g + gridDim.y;
+        if (gn < G) {
+            const uint8_t *pb = src + 8 * gn * rstride;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) load4<BF16>(pb + (uint32_t)i * rs32, nw[i]);
+            nm = __ldg(reinterpret_cast<const uint2 *>(meta) + gn);
+        }
+        const uint32_t mn = __vminu4(em.x, em.y), mx = __vmaxu4(em.x, em.y);
+        const bool ok = !force_generic && (__vcmpgeu4(mn, emin4) & __vcmpleu4(mx, emax4)) == 0xFFFFFFFFu;
+        uint32_t cp[8][2];
+        uint32_t amax = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t word = i < 4 ? em.x : em.y;
+            RowP Rp;
+            if (SIMD) {   // e in both 16-bit lanes
+                const uint32_t u2 = prmt(word, 0u, 0x4040u | (uint32_t)(i & 3) | ((uint32_t)(i & 3) << 8)) - top1;
+                Rp.lo2 = u2 << 7;
+                Rp.k3 = u2 << y;
+                Rp.lo = Rp.k3f = 0;
+            } else {
+                const uint32_t u = ((word >> (8 * (i & 3))) & 0xFFu) - top1;
+                Rp.lo = u << 23;
+                Rp.k3f = u << y;
+                Rp.lo2 = Rp.k3 = 0;
+            }
+            Rp.ok = true;
+            vec_codes_r<K, BF16, MODE, NW>(w[i], cp[i], P, Rp, amax);
+        }
+        if (ok && !amax_special<BF16, MODE>(amax, P)) {
+            uint32_t RL[1][8], RH[1][8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                RL[0][i] = prmt(cp[i][0], cp[i][1], 0x6420);
+                RH[0][i] = (K == 9) ? prmt(cp[i][0] >> 1, cp[i][1] >> 1, 0x6420) : 0u;
+            }
+            rows_fast_store<K, 1, 0>(RL, RH, packed, so, g, C, c0);
+        } else {
+            for (int v = 0; v < 4; ++v)
+                enc_container_generic_blk<BF16, K>(in, C, g * C + c0 + v, 0, x, y, M, packed, so, spi, spb, spc, cap);
+        }
+    }
+}
+
 // ---------------------------------------------------- encode COLS (blocked)
 // groups of 8 consecutive elements of one row; host guarantees bc % 8 == 0.
 // Row of group q: q / gpr, computed with an fp64 reciprocal and corrected.
@@ -1297,7 +1385,7 @@ __global__ void __launch_bounds__(RWS_THREADS) k_enc_rowwise_smem(const uint8_t 
 // the rows from L2.  The partial maxima are double-buffered by row-group
 // parity: one cluster barrier per row group keeps a peer's slot stable
 // until every CTA has read it.
-template <int K, bool BF16, int MODE, int CL>
+template <int K, bool BF16, int MODE, int CL, int NST>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(RWS_THREADS)
     k_enc_rowwise_cluster(const uint8_t *__restrict__ in, int64_t R, int64_t C, int x, int y, int scheme,
                           uint8_t *__restrict__ meta, uint8_t *__restrict__ packed, SegOffsets so, int64_t *spi,
@@ -1305,44 +1393,54 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(RWS_THREADS)
     using EL = Elem<BF16>;
     constexpr int NW = BF16 ? 2 : 4;
     constexpr bool SIMD = (MODE == ENC_SIMD || MODE == ENC_SIMD_Y0);
-    extern __shared__ __align__(16) uint8_t rws_sm[];   // 8 rows x C / CL elements
-    __shared__ __align__(8) unsigned long long s_bar;
+    extern __shared__ __align__(16) uint8_t rws_sm[];   // NST stages of 8 rows x C / CL elements
+    __shared__ __align__(8) unsigned long long s_bar[NST];
     __shared__ uint32_t s_m[RWS_THREADS / 32][8];
     __shared__ uint32_t s_part[2][8];   // this slab's 8 row maxima (fp32 magnitude bits), by row-group parity
     __shared__ int s_e[8];
     cooperative_groups::cluster_group cluster = cooperative_groups::this_cluster();
     const int rank = (int)cluster.block_rank();
     const FastP P = make_fast(fmt_of(x, y, 0), BF16, 1);
-    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
-    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(rws_sm);
     const int64_t Cs = C / CL;                              // slab columns
     const uint32_t rowb = (uint32_t)(Cs * EL::ES);          // slab row bytes (staged)
+    const uint32_t stb = 8u * rowb;                         // stage bytes
     const int64_t growb = C * EL::ES;                       // tensor row bytes
     const int CV16 = (int)(rowb / 16), CV4 = (int)(Cs / 4);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(rws_sm);
     if (tid == 0) {
-        mbar_init(bar, 1);
+        for (int st = 0; st < NST; ++st) mbar_init((uint32_t)__cvta_generic_to_shared(&s_bar[st]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    const int64_t ncl = gridDim.x / CL, cid = blockIdx.x / CL;
-    uint32_t phase = 0;
-    int par = 0;
-    for (int64_t g = cid; g < R / 8; g += ncl, phase ^= 1u, par ^= 1) {
-        if (tid == 0) {   // this CTA's slab of the row group -> shared memory (async proxy)
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_expect_tx(bar, 8u * rowb);
+    const int64_t ncl = gridDim.x / CL, cid = blockIdx.x / CL, G = R / 8;
+    // this CTA's slab of row group g -> stage st (async proxy; one thread)
+    auto issue = [&](int64_t g, int st) {
+        const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar[st]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(bar, stb);
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-                bulk_g2s(sbase + i * rowb, in + (8 * g + i) * growb + (int64_t)rank * rowb, rowb, bar);
-        }
-        mbar_wait(bar, phase);
+        for (int i = 0; i < 8; ++i)
+            bulk_g2s(sbase + st * stb + i * rowb, in + (8 * g + i) * growb + (int64_t)rank * rowb, rowb, bar);
+    };
+    if (tid == 0 && cid < G) issue(cid, 0);
+    uint32_t phase[NST];
+#pragma unroll
+    for (int st = 0; st < NST; ++st) phase[st] = 0;
+    int it = 0;
+    for (int64_t g = cid; g < G; g += ncl, ++it) {
+        const int st = NST == 2 ? (it & 1) : 0, par = it & 1;
+        // double-buffered: the next row group's slab is in flight during this one
+        if (NST == 2 && tid == 0 && g + ncl < G) issue(g + ncl, st ^ 1);
+        mbar_wait((uint32_t)__cvta_generic_to_shared(&s_bar[st]), phase[st]);
+        phase[st] ^= 1u;
+        const uint8_t *buf = rws_sm + st * stb;
         // ---- pass 1: the slab's row maxima
         uint32_t m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         for (int j = tid; j < CV16; j += RWS_THREADS) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const uint4 v = *reinterpret_cast<const uint4 *>(rws_sm + i * rowb + j * 16);
+                const uint4 v = *reinterpret_cast<const uint4 *>(buf + i * rowb + j * 16);
                 m[i] = vec_max_mag<BF16>(v, m[i]);
             }
         }
@@ -1383,7 +1481,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(RWS_THREADS)
             uint32_t w[8][NW];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const uint8_t *sp = rws_sm + i * rowb + jj * 4 * EL::ES;
+                const uint8_t *sp = buf + i * rowb + jj * 4 * EL::ES;
                 if constexpr (BF16) {
                     const uint2 t = *reinterpret_cast<const uint2 *>(sp);
                     w[i][0] = t.x; w[i][1] = t.y;
@@ -1410,7 +1508,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(RWS_THREADS)
                     enc_container_generic_rows8<BF16, K>(in, C, g, c0 + v, x, y, e8, packed, so, spi, spb, spc, cap);
             }
         }
-        __syncthreads();   // the staging buffer and s_e are reused by the next row group
+        __syncthreads();   // this stage and s_e are reused two (one) row groups on
+        if (NST == 1 && tid == 0 && g + ncl < G) issue(g + ncl, 0);
     }
     cluster.sync();   // no CTA leaves while a peer may still read its partial maxima
 }

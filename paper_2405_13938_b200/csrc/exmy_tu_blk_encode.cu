@@ -18,6 +18,22 @@ exmy_status launch_enc_blk_km(const uint8_t *in, int64_t R, int64_t C, int axis,
         bool vec = aligned(in, 4 * Elem<BF16>::ES) && (C % 4 == 0) && (M.bc % 4 == 0) &&
                    (M.br == 1 || M.br % 8 == 0);
         for (int s = 0; s < p.nseg; ++s) vec = vec && aligned(packed + p.so.off[s], p.w[s] == 8 ? 4 : 4 * p.w[s]);
+        if (vec && M.br == 1 && M.nbc == 1 && aligned(M.meta, 8) && 8 * C * Elem<BF16>::ES <= (int64_t)UINT32_MAX) {
+            // one byte per row: the rows' constants built once per warp (k_enc_rows_rowmeta)
+            const int threads = 256;
+            static int occ = 0;
+            if (!occ) occ = occupancy(k_enc_rows_rowmeta<K, BF16, MODE>, threads, 0);
+            const int64_t CV = C / 4, G = R / 8;
+            int64_t gx = cdiv(CV, threads);
+            int64_t gy = (int64_t)num_sms() * occ / gx;
+            if (gy < 1) gy = 1;
+            if (gy > G) gy = G;
+            if (gy > 65535) gy = 65535;
+            if (gx > INT_MAX) return EXMY_E_SHAPE;
+            k_enc_rows_rowmeta<K, BF16, MODE><<<dim3((unsigned)gx, (unsigned)gy), threads, 0, st>>>(
+                in, R, C, x, y, M.meta, packed, p.so, spi, spb, spc, cap, g_force_generic, M);
+            return launch_status();
+        }
         if (vec) {
             const int threads = 256;
             static int occ = 0;
@@ -112,26 +128,29 @@ exmy_status launch_rowwise_km(const uint8_t *in, int64_t R, int64_t C, int x, in
                               int64_t cap, cudaStream_t st) {
 #if RWS_ENABLE
     const int64_t rowb = C * Elem<BF16>::ES;
-    // wide rows: a cluster of CL CTAs stages a row group in column slabs (distributed shared memory)
+    // wide rows: a cluster of CL CTAs stages a row group in column slabs (distributed shared memory);
+    // two stages per CTA (the next row group's slab in flight) when 2 x 8 slab rows fit in 72 KB
     int cl = 0;
     for (int c : {2, 4, 8})
         if (!cl && rowb > RWS_MAX_ROW_BYTES && rowb % (16 * c) == 0 && rowb / c <= RWS_MAX_ROW_BYTES &&
             C % (4 * c) == 0 && g_rowwise_cluster)
             cl = c;
+    if (cl && rowb / 8 <= RWS_MAX_ROW_BYTES / 2 && rowb % (16 * 8) == 0 && C % 32 == 0) cl = 8;   // prefer 2 stages
     if (cl) {
-        const size_t sm = (size_t)(8 * (rowb / cl));
-        // per (cluster size, device) configuration: the three kernels share one pointer type
-        static unsigned long long configured[9] = {0};
-        static int occ_cl[9] = {0};
-        auto launch = [&](auto kern, int CLv) -> exmy_status {
+        const int nst = (2 * (rowb / cl) <= RWS_MAX_ROW_BYTES) ? 2 : 1;
+        const size_t sm = (size_t)(nst * 8 * (rowb / cl));
+        // per (kernel variant, device) configuration: the kernels share one pointer type
+        static unsigned long long configured[18] = {0};
+        static int occ_cl[18] = {0};
+        auto launch = [&](auto kern, int CLv, int slot) -> exmy_status {
             int dev = 0;
             cudaGetDevice(&dev);
-            if (dev < 0 || dev >= 64 || !(configured[CLv] & (1ull << dev))) {
+            if (dev < 0 || dev >= 64 || !(configured[slot] & (1ull << dev))) {
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8 * RWS_MAX_ROW_BYTES));
-                occ_cl[CLv] = occupancy(kern, RWS_THREADS, 8 * RWS_MAX_ROW_BYTES);
-                if (dev >= 0 && dev < 64) configured[CLv] |= 1ull << dev;
+                occ_cl[slot] = occupancy(kern, RWS_THREADS, 8 * RWS_MAX_ROW_BYTES);
+                if (dev >= 0 && dev < 64) configured[slot] |= 1ull << dev;
             }
-            const int occ_c = occ_cl[CLv];
+            const int occ_c = occ_cl[slot];
             int64_t blocks = (int64_t)num_sms() * (occ_c > 0 ? occ_c : 1);
             if (blocks > (R / 8) * CLv) blocks = (R / 8) * CLv;
             blocks = blocks / CLv * CLv;
@@ -140,9 +159,14 @@ exmy_status launch_rowwise_km(const uint8_t *in, int64_t R, int64_t C, int x, in
                                                           cap, g_force_generic);
             return launch_status();
         };
-        if (cl == 2) return launch(k_enc_rowwise_cluster<K, BF16, MODE, 2>, 2);
-        if (cl == 4) return launch(k_enc_rowwise_cluster<K, BF16, MODE, 4>, 4);
-        return launch(k_enc_rowwise_cluster<K, BF16, MODE, 8>, 8);
+        if (nst == 2) {
+            if (cl == 2) return launch(k_enc_rowwise_cluster<K, BF16, MODE, 2, 2>, 2, 0);
+            if (cl == 4) return launch(k_enc_rowwise_cluster<K, BF16, MODE, 4, 2>, 4, 1);
+            return launch(k_enc_rowwise_cluster<K, BF16, MODE, 8, 2>, 8, 2);
+        }
+        if (cl == 2) return launch(k_enc_rowwise_cluster<K, BF16, MODE, 2, 1>, 2, 3);
+        if (cl == 4) return launch(k_enc_rowwise_cluster<K, BF16, MODE, 4, 1>, 4, 4);
+        return launch(k_enc_rowwise_cluster<K, BF16, MODE, 8, 1>, 8, 5);
     }
     if (rowb % 16 == 0 && rowb <= RWS_MAX_ROW_BYTES) {   // TMA-staged: each row group read from HBM once
         const size_t sm = (size_t)(8 * rowb);

@@ -233,7 +233,7 @@ def test_per_row_cols_narrow_rows(exmy, orc, cols, fmt, dt):
 @pytest.mark.parametrize("fmt", [(3, 3), (6, 0), (2, 4), (4, 4), (1, 7)], ids=lambda f: f"e{f[0]}m{f[1]}")
 @pytest.mark.parametrize("dt", ["bf16", "f32"])
 def test_encode_rowwise_cluster_wide_rows(exmy, orc, fmt, dt):
-    """Rows of 9 KB .. 72 KB take the thread-block-cluster kernel (column slabs
+    """With the A/B knob on, rows of 9 KB .. 72 KB take the thread-block-cluster kernel (column slabs
     in distributed shared memory, CL = 2 / 4 / 8): bytes, metadata, specials
     == the oracle's per-row encode (both schemes), and == the two-pass path
     (knob off)"""
@@ -244,7 +244,11 @@ def test_encode_rowwise_cluster_wide_rows(exmy, orc, fmt, dt):
         d = W.from_bits(bits).to(DEV)
         for scheme in (0, 1):
             meta = orc.block_max_exponent(bits, (1, C), fmt[1], scheme)
-            p = exmy.encode_rowwise(d, fmt, scheme=scheme, specials_capacity=bits.size)
+            prev = exmy.rowwise_cluster(True)
+            try:
+                p = exmy.encode_rowwise(d, fmt, scheme=scheme, specials_capacity=bits.size)
+            finally:
+                exmy.rowwise_cluster(prev)
             np.testing.assert_array_equal(p.meta.cpu().numpy(), meta, err_msg=f"meta {C}")
             pref, idx, sb, ns = orc.encode_blocked(bits, fmt, meta, (1, C), orc.ROWS)
             np.testing.assert_array_equal(p.data.cpu().numpy(), pref, err_msg=f"packed {C} scheme {scheme}")
@@ -262,7 +266,11 @@ def test_encode_rowwise_cluster_config2(exmy):
     """config 2 (16384^2 bf16, 32 KB rows): the cluster kernel == block max +
     blocked encode, many row groups per cluster"""
     t = W.bf16_weights((16384, 16384), seed=1, device=DEV)
-    p = exmy.encode_rowwise(t, "e3m3", strict=False)
+    prev = exmy.rowwise_cluster(True)
+    try:
+        p = exmy.encode_rowwise(t, "e3m3", strict=False)
+    finally:
+        exmy.rowwise_cluster(prev)
     m = exmy.block_max_exponent(t, "row")
     assert torch.equal(p.meta, m)
     assert torch.equal(p.data, exmy.encode_blocked(t, "e3m3", m, "row", strict=False).data)
