@@ -188,9 +188,10 @@ exmy_status exmy_decode(const uint8_t *packed, int64_t rows, int64_t cols, int a
  * generic encode/decode paths instead of the fast paths, so both can be
  * checked against the oracle; exmy_debug_hist_mode selects the histogram
  * counter-update variant (0: lane-private read-modify-write, 1: lane-private
- * shared-memory atomics, 2 (default): the same atomics with both bf16
- * elements' counter offsets from one shift+mask and red.shared on 32-bit
- * shared addresses).
+ * shared-memory atomics, 2: the same atomics with both bf16 elements'
+ * counter offsets from one shift+mask, 3: lane-pair 16-bit counters,
+ * 4 (default): one 32-bit counter table per CTA with a column per lane,
+ * shared by all its warps -- conflict-free, constant increment).
  * exmy_debug_hist_blocks(b) caps the histogram grid at b CTAs (0: auto) so
  * tests reach the counter-overflow flushes with small inputs.  Pass -1 to
  * query.  Return the previous value. */

@@ -9,7 +9,7 @@
 
 namespace exmy {
 int g_force_generic = 0;
-int g_hist_mode = 3;
+int g_hist_mode = 4;
 int g_hist_blocks = 0;
 int g_enc_tma = 0;
 int g_rowwise_cluster = 0;   // A/B knob: measured slower than two-pass

@@ -250,6 +250,85 @@ __global__ void __launch_bounds__(HIST_THREADS) k_hist(const uint8_t *__restrict
     }
 }
 
+// MODE 4: ONE counter table per CTA, a column per lane.  Bank conflicts
+// only arise between the lanes of one instruction, so every warp of the CTA
+// can share one 256-bin x 32-lane table of 32-bit counters: lane l always
+// hits bank l (conflict-free, one wavefront per reduction; MODE 3's lane
+// pairs cost 2.3 wavefronts each and saturated the shared-memory pipe), the
+// increment is the constant 1, and a CTA's table is 32 KB however many
+// warps it runs.  The table sits on a 32 KB-aligned shared address, so an
+// element's counter address is one LOP3, (bits & 0x7F80) | lane_address,
+// for the low bf16 element (two ops for the high one / fp32).  32-bit
+// counters: the launcher keeps a CTA's share under 2^32 elements.
+constexpr int HIST4_THREADS = 256;
+constexpr int HIST4_SMEM = 64 * 1024;   // 32 KB table + its alignment slack
+
+__device__ __forceinline__ void st_shared_u32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_shared_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+
+template <bool BF16, int U>
+__global__ void __launch_bounds__(HIST4_THREADS, 3) k_hist_cta(const uint8_t *__restrict__ in, int64_t n,
+                                                               unsigned long long *__restrict__ hist) {
+    extern __shared__ uint32_t hsm[];
+    using EL = Elem<BF16>;
+    constexpr int NWARP = HIST4_THREADS / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t tab = ((uint32_t)__cvta_generic_to_shared(hsm) + 32767u) & ~32767u;
+    const uint32_t lsa = tab + 4u * (uint32_t)lane;
+    const int64_t nvec = n / EL::V;
+    const int64_t warps_total = (int64_t)gridDim.x * NWARP;
+    const int64_t gw = (int64_t)blockIdx.x * NWARP + warp;
+    const int64_t step = warps_total * 32 * U;
+    uint4 nxt[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int64_t vi = gw * 32 * U + 32 * u + lane;
+        nxt[u] = vi < nvec ? ldg_nc_v4(in + vi * 16) : make_uint4(0, 0, 0, 0);
+    }
+    // zero the table while the first loads are in flight
+    for (int i = threadIdx.x; i < 256 * 32; i += HIST4_THREADS) st_shared_u32(tab + 4u * (uint32_t)i, 0u);
+    __syncthreads();
+    for (int64_t base = gw * 32 * U; base < nvec; base += step) {
+        uint4 r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            r[u] = nxt[u];
+            const int64_t vi = base + step + 32 * u + lane;
+            nxt[u] = vi < nvec ? ldg_nc_v4(in + vi * 16) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (base + 32 * u + lane < nvec) {
+                const uint32_t w[4] = {r[u].x, r[u].y, r[u].z, r[u].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (BF16) red_shared_add((w[q] & 0x7F80u) | lsa, 1u);
+                    red_shared_add(((w[q] >> 16) & 0x7F80u) | lsa, 1u);
+                }
+            }
+        }
+    }
+    // scalar tail (n % V elements), block 0 warp 0
+    if (blockIdx.x == 0 && warp == 0) {
+        for (int64_t i = nvec * EL::V + lane; i < n; i += 32) {
+            const uint32_t u = BF16 ? ((uint32_t)((const uint16_t *)in)[i] << 16) : ((const uint32_t *)in)[i];
+            red_shared_add(((u >> 16) & 0x7F80u) | lsa, 1u);
+        }
+    }
+    __syncthreads();
+    // bin b = row b: 32 consecutive words, one warp-wide add
+    for (int b = warp; b < 256; b += NWARP) {
+        const uint32_t c = __reduce_add_sync(0xFFFFFFFFu, ld_shared_u32(tab + 128u * (uint32_t)b + 4u * (uint32_t)lane));
+        if (lane == 0 && c) atomicAdd(hist + b, (unsigned long long)c);
+    }
+}
+
 // misaligned input: plain grid-stride loop with global atomics per warp bin
 template <bool BF16>
 __global__ void k_hist_scalar(const uint8_t *__restrict__ in, int64_t n, unsigned long long *__restrict__ hist) {

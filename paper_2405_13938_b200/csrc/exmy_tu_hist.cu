@@ -26,6 +26,33 @@ exmy_status launch_hist_vec(const uint8_t *in, int64_t n, unsigned long long *hi
     return launch_status();
 }
 
+#ifndef HIST4_U
+#define HIST4_U 4   // 16-byte vectors per lane per iteration (double-buffered)
+#endif
+// MODE 4: CTA-shared lane-column counters (k_hist_cta); returns
+// EXMY_E_SHAPE when a CTA's share could overflow its 32-bit counters
+template <bool BF16>
+exmy_status launch_hist_cta(const uint8_t *in, int64_t n, unsigned long long *hist, cudaStream_t st) {
+    static unsigned long long configured = 0;
+    static int occ = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64 || !(configured & (1ull << dev))) {
+        cudaFuncSetAttribute(k_hist_cta<BF16, HIST4_U>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST4_SMEM);
+        occ = occupancy(k_hist_cta<BF16, HIST4_U>, HIST4_THREADS, HIST4_SMEM);
+        if (dev >= 0 && dev < 64) configured |= 1ull << dev;
+    }
+    const int64_t nvec = n / Elem<BF16>::V;
+    int64_t blocks = cdiv(cdiv(nvec, 32 * HIST4_U), HIST4_THREADS / 32);
+    if (blocks < 1) blocks = 1;
+    int64_t maxb = (int64_t)num_sms() * occ;
+    if (blocks > maxb) blocks = maxb;
+    if (g_hist_blocks > 0 && blocks > g_hist_blocks) blocks = g_hist_blocks;
+    if (cdiv(n, blocks) + 64 >= (int64_t)UINT32_MAX) return EXMY_E_SHAPE;
+    k_hist_cta<BF16, HIST4_U><<<(unsigned)blocks, HIST4_THREADS, HIST4_SMEM, st>>>(in, n, hist);
+    return launch_status();
+}
+
 }  // namespace
 
 exmy_status launch_histogram(const uint8_t *in, bool bf16, int64_t n, unsigned long long *hist, cudaStream_t st) {
@@ -36,7 +63,12 @@ exmy_status launch_histogram(const uint8_t *in, bool bf16, int64_t n, unsigned l
         else k_hist_scalar<false><<<(unsigned)blocks, 256, 0, st>>>(in, n, hist);
         return launch_status();
     }
+    if (g_hist_mode == 4) {
+        const exmy_status r = bf16 ? launch_hist_cta<true>(in, n, hist, st) : launch_hist_cta<false>(in, n, hist, st);
+        if (r != EXMY_E_SHAPE) return r;   // else: the 16-bit epoch kernel below
+    }
     switch (g_hist_mode) {
+        case 4:
         case 3: return bf16 ? launch_hist_vec<true, 3>(in, n, hist, st) : launch_hist_vec<false, 3>(in, n, hist, st);
         case 0: return bf16 ? launch_hist_vec<true, 0>(in, n, hist, st) : launch_hist_vec<false, 0>(in, n, hist, st);
         case 2: return bf16 ? launch_hist_vec<true, 2>(in, n, hist, st) : launch_hist_vec<false, 2>(in, n, hist, st);

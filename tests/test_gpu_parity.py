@@ -58,7 +58,7 @@ def oracle_boundary_f32(orc, fmt, e_max):
 
 
 # ----------------------------------------------------------------- K1 / K1b
-@pytest.mark.parametrize("mode", [0, 1, 2, 3])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4])
 @pytest.mark.parametrize("dt", ["bf16", "f32"])
 @pytest.mark.parametrize("n", [0, 1, 7, 8 * 1000 + 5, 1 << 20, (1 << 22) + 3])
 def test_histogram_parity(exmy, orc, dt, n, mode):
@@ -104,7 +104,7 @@ def peaked_mix(n, seed, dt="bf16"):
     return bits
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2, 3])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4])
 @pytest.mark.parametrize("blocks", [0, 1, 3])
 @pytest.mark.parametrize("n", [8 * 1000 + 5, (1 << 22) + 3, 20_000_011])
 @pytest.mark.parametrize("dt", ["bf16", "f32"])

@@ -41,7 +41,7 @@ def main():
     ap.add_argument("--cols", type=int, default=16384)
     ap.add_argument("--fmts", default="e0m6,e1m5,e2m4,e3m3,e4m2,e5m1,e6m0")
     ap.add_argument("--axis", default="rows")
-    ap.add_argument("--hist-modes", default="3")
+    ap.add_argument("--hist-modes", default="4")
     ap.add_argument("--probe", action="store_true", help="also time the roofline probe for each op's byte mix")
     ap.add_argument("--fs", action="store_true", help="with --block: also time the float-scaling scheme")
     ap.add_argument("--block", default=None, help="row | col | tensor | BRxBC: time the block-metadata path")
@@ -62,7 +62,7 @@ def main():
         exmy.hist_mode(m)
         ms = timeit(lambda: exmy.histogram(t, out=h))
         res[f"hist_mode{m}"] = {"ms": ms, "gbs": n * es / ms / 1e6, "frac": n * es / ms / 1e6 / peak}
-    exmy.hist_mode(3)
+    exmy.hist_mode(4)
     meta = exmy.max_exponent(t)
     q = torch.empty_like(t)
     d = torch.empty_like(t)

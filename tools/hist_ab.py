@@ -16,7 +16,7 @@ import workloads as W  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--modes", default="2,3")
+    ap.add_argument("--modes", default="3,4")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--only", default="")
     a = ap.parse_args()
@@ -49,7 +49,7 @@ def main():
             v = sorted(times[m])
             med = v[len(v) // 2]
             print(f"{name} mode {m}: median {med:.1f} us  min {v[0]:.1f}  ({2 * n / med / 1e3:.0f} GB/s)")
-    exmy.hist_mode(3)
+    exmy.hist_mode(4)
 
 
 if __name__ == "__main__":

@@ -21,10 +21,10 @@ def main():
     for dt in (torch.bfloat16, torch.float32):
         t = W.f32_wide((R, C), seed=1).to(dt).to(dev)
         t.view(-1)[[5, 77]] = float("nan")
-        for mode in (0, 1, 2):
+        for mode in (0, 1, 2, 3, 4):
             exmy.hist_mode(mode)
             exmy.histogram(t)
-        exmy.hist_mode(2)
+        exmy.hist_mode(4)
         m = exmy.max_exponent(t)
         for fmt in ("e3m3", "e6m0", "e4m3", "e3m5", "e8m0"):
             exmy.quantize(t, fmt, m)
