@@ -889,40 +889,143 @@ __global__ void __launch_bounds__(256) k_block_max_small(const uint8_t *__restri
     }
 }
 
-// one warp per block: max |finite| over the block, then the scheme's exponent
+// bf16: 16-bit-lane max of the magnitudes with the NaN/Inf lanes zeroed;
+// fp32: max of the finite magnitudes
+template <bool BF16>
+__device__ __forceinline__ void bmax_acc(uint32_t &am2, const uint4 &q) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        const uint32_t w = word_of(q, t);
+        if (BF16) {
+            const uint32_t a2 = w & 0x7FFF7FFFu;
+            const uint32_t sp = (a2 + 0x00800080u) & 0x80008000u;   // bit 15 of special lanes
+            am2 = vmax_u16x2(am2, a2 & ~((sp >> 15) * 0xFFFFu));
+        } else {
+            const uint32_t a = w & 0x7FFFFFFFu;
+            am2 = max(am2, a < 0x7F800000u ? a : 0u);
+        }
+    }
+}
+
+// 2-D blocks whose rows are short (br x bc, bc / V = gsz in {1..16}, e.g.
+// 32 x 32 tiles): a CTA owns a band of br rows x a chunk of 256*U vectors
+// (U = 8: 16384 bf16 columns; the launcher picks the largest U in 8,4,2
+// that still gives >= 4 work items per resident CTA, else k_block_max) and
+// streams it row by row -- one contiguous
+// 256*U*16-byte span of a row per step, the next row's span in flight while
+// this one is folded into U per-thread maxima (thread t: vectors t + 256u,
+// fixed across the band).  At the band's end the gsz lanes of each block
+// combine with xor-shuffles.  (A warp per span of 8 rows x 512 B reached
+// 69 % of copy at 32 x 32: short strided bursts.)
+template <bool BF16, int U>
+__global__ void __launch_bounds__(256) k_block_max_band(const uint8_t *__restrict__ in, int64_t R, int64_t C,
+                                                        int64_t br, int gsz, int y, int scheme,
+                                                        uint8_t *__restrict__ meta) {
+    constexpr int V = Elem<BF16>::V;
+    constexpr int64_t ES = Elem<BF16>::ES;
+    const int lane = threadIdx.x & 31;
+    const int64_t CV = C / V;
+    const int64_t nch = (CV + 256 * U - 1) / (256 * U);   // column chunks per band
+    const int64_t nbands = R / br, nwork = nbands * nch;
+    const int64_t nbc = CV / gsz;                      // blocks per block row
+    for (int64_t wk = blockIdx.x; wk < nwork; wk += gridDim.x) {
+        const int64_t band = wk / nch, v0 = (wk % nch) * 256 * U + threadIdx.x;
+        const uint8_t *base = in + (band * br * C) * ES + v0 * 16;
+        bool ok[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) ok[u] = v0 + 256 * u < CV;
+        uint32_t am[U];
+        uint4 nx[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            am[u] = 0;
+            nx[u] = ok[u] ? ldg_nc_v4(base + 256 * 16 * u) : make_uint4(0, 0, 0, 0);
+        }
+        for (int64_t i = 0; i < br; ++i) {
+            uint4 r[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) r[u] = nx[u];
+            if (i + 1 < br) {
+                const uint8_t *nb = base + (i + 1) * C * ES;
+#pragma unroll
+                for (int u = 0; u < U; ++u) nx[u] = ok[u] ? ldg_nc_v4(nb + 256 * 16 * u) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) bmax_acc<BF16>(am[u], r[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            uint32_t amax = BF16 ? max(am[u] & 0xFFFFu, am[u] >> 16) << 16 : am[u];
+            for (int o = 1; o < gsz; o <<= 1) amax = max(amax, __shfl_xor_sync(0xFFFFFFFFu, amax, o));
+            if ((lane & (gsz - 1)) == 0 && ok[u]) {
+                const int e = scheme == 0 ? (int)(amax >> 23) : exp_after_rounding(amax, y);
+                meta[band * nbc + (v0 + 256 * u) / gsz] = (uint8_t)(e > 254 ? 254 : e);
+            }
+        }
+    }
+}
+
+// one warp per block: max |finite| over the block, then the scheme's exponent.
+// 16-byte path: U independent loads per lane in flight (one per iteration
+// left the SM short of bytes in flight: 94 us for config 2's rows vs the
+// histogram's 81 us over the same bytes).  Rows of >= 32 vectors: the warp
+// walks each row; shorter block rows (e.g. 128 x 128 tiles, 16 / 32 vectors a row):
+// the lanes cover several rows at once over the block's flattened vectors
+// (a warp per row left 28 of 32 lanes idle and serialised the rows).
 template <bool BF16>
 __global__ void __launch_bounds__(256) k_block_max(const uint8_t *__restrict__ in, int64_t R, int64_t C, int64_t br,
                                                    int64_t bc, int y, int scheme, uint8_t *__restrict__ meta) {
+    constexpr int U = 8;
     const int lane = threadIdx.x & 31;
     const int64_t nbc = C / bc, nb = (R / br) * nbc;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     constexpr int V = Elem<BF16>::V;
+    constexpr int64_t ES = Elem<BF16>::ES;
     const bool vec = (bc % V == 0) && ((reinterpret_cast<uintptr_t>(in) & 15) == 0) && (C % V == 0);
+    const int64_t nv = bc / V;
+    const bool flat = vec && (nv % 32 != 0 || (br > 1 && nv < 32 * U)) && br * nv < (1ll << 31);
     for (int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); b < nb; b += warps) {
         const int64_t r0 = (b / nbc) * br, c0 = (b % nbc) * bc;
+        const uint8_t *blk = in + (r0 * C + c0) * ES;
         uint32_t amax = 0;   // max finite magnitude bits (fp32 convention)
-        for (int64_t i = 0; i < br; ++i) {
-            const uint8_t *row = in + ((r0 + i) * C + c0) * Elem<BF16>::ES;
-            if (vec) {
-                for (int64_t v = lane; v < bc / V; v += 32) {
-                    const uint4 q = ldg_nc_v4(row + v * 16);
+        if (flat) {
+            const uint32_t tot = (uint32_t)(br * nv), nv32 = (uint32_t)nv;
+            uint32_t am2 = 0;
+            for (uint32_t f0 = 0; f0 < tot; f0 += 32 * U) {
+                uint4 r[U];
 #pragma unroll
-                    for (int t = 0; t < 4; ++t) {
-                        const uint32_t w = word_of(q, t);
-                        if (BF16) {
-                            const uint32_t lo = (w << 16) & 0x7FFF0000u, hi = w & 0x7FFF0000u;
-                            if (lo < 0x7F800000u) amax = max(amax, lo);
-                            if (hi < 0x7F800000u) amax = max(amax, hi);
-                        } else {
-                            const uint32_t a = w & 0x7FFFFFFFu;
-                            if (a < 0x7F800000u) amax = max(amax, a);
-                        }
-                    }
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t f = f0 + 32 * u + lane;
+                    const uint32_t i = f / nv32;
+                    r[u] = f < tot ? ldg_nc_v4(blk + (int64_t)i * C * ES + (int64_t)(f - i * nv32) * 16)
+                                   : make_uint4(0, 0, 0, 0);
                 }
-            } else {
-                for (int64_t c = lane; c < bc; c += 32) {
-                    const uint32_t a = load_elem_scalar<BF16>(row, c) & 0x7FFFFFFFu;
-                    if (a < 0x7F800000u) amax = max(amax, a);
+#pragma unroll
+                for (int u = 0; u < U; ++u) bmax_acc<BF16>(am2, r[u]);
+            }
+            amax = BF16 ? max(am2 & 0xFFFFu, am2 >> 16) << 16 : am2;
+        } else {
+            for (int64_t i = 0; i < br; ++i) {
+                const uint8_t *row = blk + i * C * ES;
+                if (vec) {
+                    uint32_t am2 = 0;
+                    for (int64_t v0 = 0; v0 < nv; v0 += 32 * U) {
+                        uint4 r[U];
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            const int64_t v = v0 + 32 * u + lane;
+                            r[u] = v < nv ? ldg_nc_v4(row + v * 16) : make_uint4(0, 0, 0, 0);
+                        }
+#pragma unroll
+                        for (int u = 0; u < U; ++u) bmax_acc<BF16>(am2, r[u]);
+                    }
+                    if (BF16) am2 = max(am2 & 0xFFFFu, am2 >> 16) << 16;
+                    amax = max(amax, am2);
+                } else {
+                    for (int64_t c = lane; c < bc; c += 32) {
+                        const uint32_t a = load_elem_scalar<BF16>(row, c) & 0x7FFFFFFFu;
+                        if (a < 0x7F800000u) amax = max(amax, a);
+                    }
                 }
             }
         }

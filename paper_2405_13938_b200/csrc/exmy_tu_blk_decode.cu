@@ -1,5 +1,6 @@
 // exmy_tu_blk_decode.cu -- decode / quantize / block max exponent with block
 // metadata launchers.
+#include <algorithm>
 #include "exmy_launch.cuh"
 #include "exmy_narrow.cuh"
 
@@ -193,6 +194,33 @@ exmy_status launch_block_max(const uint8_t *in, bool bf16, int64_t R, int64_t C,
             else k_block_max_small<false, 1><<<(unsigned)blocks, 256, 0, st>>>(in, nvec, gsz, y, meta, nullptr);
         }
         return launch_status();
+    }
+    const int64_t gsz = bc / V;
+    // band kernel when it has >= 4 work items per resident CTA at U >= 2
+    // (tall blocks, e.g. 128 x 128, leave too few bands: warp per block below)
+    const int64_t resident = (int64_t)num_sms() * 3;   // 256 threads, <= 80 registers at U <= 4
+    int u = 8;
+    while (u > 1 && (R / br) * cdiv(C / V, (int64_t)256 * u) < 4 * resident) u >>= 1;
+    if (br > 1 && bc % V == 0 && gsz <= 16 && (gsz & (gsz - 1)) == 0 && C % (32 * V) == 0 && aligned(in, 16) &&
+        (R / br) * cdiv(C / V, (int64_t)256 * u) >= 4 * resident && u >= 2) {
+        const int64_t blocks = std::max<int64_t>(1, (R / br) * cdiv(C / V, (int64_t)256 * u));
+        if (blocks > INT_MAX) return EXMY_E_SHAPE;
+        auto go = [&](auto kern) {
+            kern<<<(unsigned)blocks, 256, 0, st>>>(in, R, C, br, (int)gsz, y, scheme, meta);
+            return launch_status();
+        };
+        if (bf16) {
+            switch (u) {
+                case 8: return go(k_block_max_band<true, 8>);
+                case 4: return go(k_block_max_band<true, 4>);
+                default: return go(k_block_max_band<true, 2>);
+            }
+        }
+        switch (u) {
+            case 8: return go(k_block_max_band<false, 8>);
+            case 4: return go(k_block_max_band<false, 4>);
+            default: return go(k_block_max_band<false, 2>);
+        }
     }
     const int64_t nb = (R / br) * (C / bc);
     int64_t blocks = cdiv(nb, 8);

@@ -65,6 +65,53 @@ def test_block_max_exponent(exmy, orc, dt, scheme):
         np.testing.assert_array_equal(got, orc.block_max_exponent(edge, (1, 1), y, scheme))
 
 
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+@pytest.mark.parametrize("scheme", [0, 1])
+def test_block_max_exponent_tiles(exmy, orc, dt, scheme):
+    """2-D blocks with short rows (k_block_max_tile: a warp reads 32 vectors
+    of each block row, covering 32 / (bc / V) blocks side by side): block
+    heights not a multiple of the 8 rows in flight, 1..16 vectors per block
+    row, NaN/Inf, zeros and subnormal rows"""
+    shape = (96, 1024)
+    bits = rowscaled_bits(shape, 7, dt)
+    rng = np.random.default_rng(11)
+    flat = bits.reshape(-1)
+    k = rng.choice(flat.size, 40, replace=False)
+    flat[k[:20]] = 0x7FC0 if dt == "bf16" else 0x7FC00000
+    flat[k[20:30]] = 0xFF80 if dt == "bf16" else 0xFF800000
+    bits[5] = 0                                             # an all-zero row
+    bits[6, :64] = 1                                        # smallest subnormals
+    d = W.from_bits(bits).to(DEV)
+    V = 8 if dt == "bf16" else 4
+    for blk in [(32, 32), (8, 16), (3, 8 * V), (12, V), (96, 2 * V), (1 * 2, 4 * V), (24, 16 * V)]:
+        if shape[0] % blk[0] or shape[1] % blk[1]:
+            continue
+        for y in (0, 2, 5):
+            got = exmy.block_max_exponent(d, blk, y, scheme).cpu().numpy()
+            ref = orc.block_max_exponent(bits, blk, y, scheme)
+            np.testing.assert_array_equal(got, ref, err_msg=f"{blk} y={y}")
+
+
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+@pytest.mark.parametrize("scheme", [0, 1])
+def test_block_max_exponent_bands(exmy, orc, dt, scheme):
+    """Shapes large enough for the band kernel (k_block_max_band: a CTA
+    streams br rows x 256*U vectors; U = 8 / 4 / 2 picked by the work count)
+    incl. a column chunk that ends mid-way (4352 columns), and tall blocks
+    that take the warp-per-block kernel's flattened path"""
+    V = 8 if dt == "bf16" else 4
+    for shape in ((4096, 4352), (2048, 8192)):
+        bits = rowscaled_bits(shape, 13, dt)
+        bits[7, :] = 0
+        d = W.from_bits(bits).to(DEV)
+        for blk in [(2, 4 * V), (4, 16 * V), (2, V), (8, 2 * V), (128, 32 * V), (64, 16 * V)]:
+            if shape[0] % blk[0] or shape[1] % blk[1]:
+                continue
+            got = exmy.block_max_exponent(d, blk, 3, scheme).cpu().numpy()
+            ref = orc.block_max_exponent(bits, blk, 3, scheme)
+            np.testing.assert_array_equal(got, ref, err_msg=f"{shape} {blk}")
+
+
 @pytest.mark.parametrize("fmt", [(3, 3), (2, 4), (4, 2), (6, 0), (1, 5), (0, 6), (2, 2), (5, 3), (2, 1), (0, 7),
                                  (1, 7), (8, 0)], ids=lambda f: f"e{f[0]}m{f[1]}")
 @pytest.mark.parametrize("dt", ["bf16", "f32"])
