@@ -55,7 +55,7 @@ __device__ __forceinline__ RowP make_rowp(int e, int x, int y) {
     return R;
 }
 
-template <int K, bool Y0>
+template <int K, bool Y0, bool SIGN = true>
 __device__ __forceinline__ uint32_t enc_pair_bf16_r(uint32_t w, const FastP &P, const RowP &R, uint32_t &amax) {
     const uint32_t a2 = w & 0x7FFF7FFFu;
     const uint32_t ev = w & 0x7F807F80u;
@@ -71,7 +71,7 @@ __device__ __forceinline__ uint32_t enc_pair_bf16_r(uint32_t w, const FastP &P, 
     const uint32_t s = hadd2_bf16(a2, c);
     uint32_t code = s - c + t - R.k3;
     code = vmin_u16x2(code, P.m2);
-    code |= (w >> (16 - K)) & ((1u << (K - 1)) * 0x00010001u);
+    if (SIGN) code |= (w >> (16 - K)) & ((1u << (K - 1)) * 0x00010001u);
     amax = vmax_u16x2(amax, a2);
     return code;
 }
@@ -91,13 +91,13 @@ __device__ __forceinline__ uint32_t enc_f32_fast_r(uint32_t u, const FastP &P, c
     return code;
 }
 
-template <int K, bool BF16, int MODE, int NW>
+template <int K, bool BF16, int MODE, int NW, bool SIGN = true>
 __device__ __forceinline__ void vec_codes_r(const uint32_t (&w)[NW], uint32_t (&cp)[BF16 ? NW : NW / 2],
                                             const FastP &P, const RowP &R, uint32_t &amax) {
     constexpr int NP = BF16 ? NW : NW / 2;
     if constexpr (MODE == ENC_SIMD || MODE == ENC_SIMD_Y0) {
 #pragma unroll
-        for (int t = 0; t < NP; ++t) cp[t] = enc_pair_bf16_r<K, MODE == ENC_SIMD_Y0>(w[t], P, R, amax);
+        for (int t = 0; t < NP; ++t) cp[t] = enc_pair_bf16_r<K, MODE == ENC_SIMD_Y0, SIGN>(w[t], P, R, amax);
     } else {
 #pragma unroll
         for (int t = 0; t < NP; ++t) {
@@ -297,6 +297,7 @@ __global__ void __launch_bounds__(256, (BF16 && K <= 7) ? 3 : 2)
         const bool ok = !force_generic && (__vcmpgeu4(mn, emin4) & __vcmpleu4(mx, emax4)) == 0xFFFFFFFFu;
         uint32_t cp[8][2];
         uint32_t amax = 0;
+        constexpr bool LATE_SIGN = SIMD && K <= 8;   // signs per row (sign_bytes), as k_enc_rows_fast
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const uint32_t word = i < 4 ? em.x : em.y;
@@ -313,13 +314,15 @@ __global__ void __launch_bounds__(256, (BF16 && K <= 7) ? 3 : 2)
                 Rp.lo2 = Rp.k3 = 0;
             }
             Rp.ok = true;
-            vec_codes_r<K, BF16, MODE, NW>(w[i], cp[i], P, Rp, amax);
+            vec_codes_r<K, BF16, MODE, NW, !LATE_SIGN>(w[i], cp[i], P, Rp, amax);
         }
         if (ok && !amax_special<BF16, MODE>(amax, P)) {
             uint32_t RL[1][8], RH[1][8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 RL[0][i] = prmt(cp[i][0], cp[i][1], 0x6420);
+                if constexpr (LATE_SIGN)
+                    RL[0][i] |= sign_bytes(w[i][0], w[i][NW - 1]) & ((1u << (K - 1)) * 0x01010101u);
                 RH[0][i] = (K == 9) ? prmt(cp[i][0] >> 1, cp[i][1] >> 1, 0x6420) : 0u;
             }
             rows_fast_store<K, 1, 0>(RL, RH, packed, so, g, C, c0);

@@ -155,7 +155,7 @@ enum EncMode { ENC_SIMD = 0, ENC_SIMD_Y0 = 1, ENC_F32 = 2, ENC_F32_Y0 = 3 };
 
 // two bf16 elements (one 32-bit word) -> two k-bit codes in 16-bit lanes;
 // amax accumulates the largest magnitude seen (NaN/Inf test at the end)
-template <int K, bool Y0>
+template <int K, bool Y0, bool SIGN = true>
 __device__ __forceinline__ uint32_t enc_pair_bf16(uint32_t w, const FastP &P, uint32_t &amax) {
     const uint32_t a2 = w & 0x7FFF7FFFu;
     const uint32_t ev = w & 0x7F807F80u;
@@ -171,9 +171,19 @@ __device__ __forceinline__ uint32_t enc_pair_bf16(uint32_t w, const FastP &P, ui
     const uint32_t s = hadd2_bf16(a2, c);
     uint32_t code = s - c + t - P.k3;
     code = vmin_u16x2(code, P.m2);
-    code |= (w >> (16 - K)) & ((1u << (K - 1)) * 0x00010001u);
+    if (SIGN) code |= (w >> (16 - K)) & ((1u << (K - 1)) * 0x00010001u);
     amax = vmax_u16x2(amax, a2);
     return code;
+}
+// The signs of the 4 bf16 elements in words w0, w1 as bytes 0x00 / 0xFF
+// (prmt's sign-replicating selectors 8 + b on the high bytes 1, 3, 5, 7), in
+// the byte order of prmt(cp0, cp1, 0x6420): the codes of a row's 4 elements
+// get their sign bits with ONE LOP3 per row instead of a shift and a LOP3
+// per pair -- the ROWS encode is bound by the ALU pipe.
+__device__ __forceinline__ uint32_t sign_bytes(uint32_t w0, uint32_t w1) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, 0xFDB9;" : "=r"(d) : "r"(w0), "r"(w1));
+    return d;
 }
 // any lane at or above the fallback threshold (NaN/Inf, or huge values)
 __device__ __forceinline__ bool amax_special_bf16(uint32_t amax, const FastP &P) {
@@ -341,14 +351,14 @@ __device__ __forceinline__ uint32_t wordvec_elem(const uint32_t (&w)[NW], int v)
     return w[v];
 }
 
-template <int K, bool BF16, int MODE, int NW>
+template <int K, bool BF16, int MODE, int NW, bool SIGN = true>
 __device__ __forceinline__ void vec_codes(const uint32_t (&w)[NW], uint32_t (&cp)[BF16 ? NW : NW / 2],
                                           const FastP &P, uint32_t &amax) {
     constexpr int NP = BF16 ? NW : NW / 2;
     if constexpr (MODE == ENC_SIMD || MODE == ENC_SIMD_Y0) {
         static_assert(BF16, "SIMD encode needs bf16 input");
 #pragma unroll
-        for (int t = 0; t < NP; ++t) cp[t] = enc_pair_bf16<K, MODE == ENC_SIMD_Y0>(w[t], P, amax);
+        for (int t = 0; t < NP; ++t) cp[t] = enc_pair_bf16<K, MODE == ENC_SIMD_Y0, SIGN>(w[t], P, amax);
     } else {
 #pragma unroll
         for (int t = 0; t < NP; ++t) {
@@ -589,13 +599,17 @@ __global__ void __launch_bounds__(BF16 ? EXMY_ENC_ROWS_THREADS : 256, BF16 ? EXM
         if (!act) continue;
         uint32_t cp[8][2];
         uint32_t amax = 0;
+        // bf16 lanes, k <= 8: codes without sign, the signs added per row below
+        constexpr bool LATE_SIGN = (MODE == ENC_SIMD || MODE == ENC_SIMD_Y0) && K <= 8;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) vec_codes<K, BF16, MODE, NW>(w[i], cp[i], P, amax);
+        for (int i = 0; i < 8; ++i) vec_codes<K, BF16, MODE, NW, !LATE_SIGN>(w[i], cp[i], P, amax);
         if (!amax_special<BF16, MODE>(amax, P)) {
             uint32_t RL[1][8], RH[1][8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 RL[0][i] = prmt(cp[i][0], cp[i][1], 0x6420);
+                if constexpr (LATE_SIGN)
+                    RL[0][i] |= sign_bytes(w[i][0], w[i][NW - 1]) & ((1u << (K - 1)) * 0x01010101u);
                 RH[0][i] = (K == 9) ? prmt(cp[i][0] >> 1, cp[i][1] >> 1, 0x6420) : 0u;
             }
             rows_fast_store<K, 1, 0>(RL, RH, packed, so, g, C, c0);
