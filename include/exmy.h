@@ -527,6 +527,31 @@ exmy_status exmy_embedding_bag(const uint8_t *packed, int64_t rows, int64_t cols
                                const int64_t *offsets, int64_t nbags, const float *weights,
                                int mode, float *out, void *stream);
 
+/* Decode fused into a matrix-vector product ("decode
+ * fused into the consumer"; serving decode is "performance critical",
+ * P:296-298; reading D26).  out[i, n] = sum_c act[i, c] * W[n, c] for the
+ * ROWS-packed weight matrix W (rows x cols, k = 1+x+y <= 8) and m fp32
+ * activation rows act (m x cols, row-major, 16-byte aligned); out is fp32
+ * (m x rows, row-major).  The decoded W never reaches HBM: each pass over
+ * <= 8 activation rows reads the packed bytes once.  meta: one device byte
+ * (per tensor) or `rows` bytes (meta_per_row = 1, the (1, cols) blocks of
+ * exmy_block_max_exponent / exmy_encode_rowwise).  Sums are fp32 in a fixed
+ * order (see exmy_gemv.cuh): not bit-identical to another summation order;
+ * the tests bound the error by the fp32 dot-product bound.  NaN/Inf weights
+ * from the encode's specials list (sp_index / sp_bits / sp_count /
+ * sp_capacity as written by exmy_encode; capacity 0: none) are applied
+ * afterwards.  Requires rows % 8 == 0, cols % 4 == 0, packed 16-byte
+ * aligned.  EXMY_E_FORMAT for k = 9. */
+/* exmy_gemv kernel choice: 1 (default) = packed bytes staged in shared
+ * memory by bulk asynchronous copies when cols % 16 == 0, 0 = the
+ * register-pipelined kernel for every shape; -1 queries.  Returns the
+ * previous value. */
+int exmy_debug_gemv_bulk(int on);
+exmy_status exmy_gemv(const uint8_t *packed, int64_t rows, int64_t cols, int x, int y,
+                      const uint8_t *meta, int meta_per_row, const int64_t *sp_index,
+                      const uint32_t *sp_bits, const unsigned long long *sp_count, int64_t sp_capacity,
+                      const float *act, int64_t m, float *out, void *stream);
+
 /* ------------------------------------------------ host-buffer conveniences */
 
 /* End-to-end encode of a HOST tensor (pinned memory recommended): H2D copy

@@ -83,6 +83,8 @@ def _load():
         "exmy_encode_push": ([vp, i32, i64, i64, i64, i64, i32, i32, vp, vp, i32, vp, vp, vp, i64, vp], i32),
         "exmy_encode_push_multicast": ([vp, i32, i64, i64, i64, i64, i32, i32, vp, vp, vp, vp, vp, i64, vp], i32),
         "exmy_embedding_bag": ([vp, i64, i64, i32, i32, vp, i32, vp, vp, i64, vp, i32, vp, vp], i32),
+        "exmy_gemv": ([vp, i64, i64, i32, i32, vp, i32, vp, vp, vp, i64, vp, i64, vp, vp], i32),
+        "exmy_debug_gemv_bulk": ([i32], i32),
         "exmy_decode_pull": ([vp, i32, i64, i64, i32, i32, vp, vp, i32, vp], i32),
         "exmy_ckpt_write": ([ctypes.c_char_p, vp, i32], i64),
         "exmy_ckpt_open": ([ctypes.c_char_p, vp], i32),
@@ -112,14 +114,14 @@ _lib = _load()
 LIB_PATH = _LIB_PATH
 EXPORTED = ["exmy_version", "exmy_specials_words", "exmy_status_string", "exmy_format_valid", "exmy_packed_bytes", "exmy_segments",
             "exmy_bias_from_emax", "exmy_emax_from_bias", "exmy_emax_from_histogram_host", "exmy_choose_x",
-            "exmy_debug_force_generic", "exmy_debug_hist_mode", "exmy_debug_hist_blocks", "exmy_debug_enc_tma", "exmy_debug_rowwise_cluster", "exmy_debug_probe",
+            "exmy_debug_force_generic", "exmy_debug_hist_mode", "exmy_debug_hist_blocks", "exmy_debug_enc_tma", "exmy_debug_rowwise_cluster", "exmy_debug_gemv_bulk", "exmy_debug_probe",
             "exmy_exponent_histogram",
             "exmy_emax_from_histogram", "exmy_quantize", "exmy_encode", "exmy_decode", "exmy_encode_host",
             "exmy_decode_host", "exmy_block_max_exponent", "exmy_quantize_blocked", "exmy_encode_blocked",
             "exmy_decode_blocked", "exmy_decode_rows", "exmy_max_exponent", "exmy_encode_rowwise",
             "exmy_group_plan_bytes", "exmy_group_plan", "exmy_group_plan_rows", "exmy_group_max_exponent", "exmy_group_encode", "exmy_group_encode_rowwise",
             "exmy_group_decode", "exmy_block_float_scale", "exmy_quantize_fs", "exmy_encode_fs", "exmy_decode_fs",
-            "exmy_encode_push", "exmy_encode_push_multicast", "exmy_decode_pull", "exmy_embedding_bag", "exmy_ckpt_write", "exmy_ckpt_open", "exmy_ckpt_count", "exmy_ckpt_info",
+            "exmy_encode_push", "exmy_encode_push_multicast", "exmy_decode_pull", "exmy_embedding_bag", "exmy_gemv", "exmy_ckpt_write", "exmy_ckpt_open", "exmy_ckpt_count", "exmy_ckpt_info",
             "exmy_ckpt_find", "exmy_ckpt_read", "exmy_ckpt_verify", "exmy_ckpt_bytes_read", "exmy_ckpt_close"]
 
 
@@ -225,6 +227,12 @@ def enc_tma(on: bool | None = None) -> int:
     """knob: ROWS encode through the TMA-staged kernel (1) or the register
     pipeline (0); returns the previous setting"""
     return _lib.exmy_debug_enc_tma(-1 if on is None else int(on))
+
+
+def gemv_bulk(on: bool | None = None) -> int:
+    """knob: gemv with bulk-staged packed bytes (1, cols % 16 == 0) or the
+    register-pipelined kernel (0); returns the previous setting"""
+    return _lib.exmy_debug_gemv_bulk(-1 if on is None else int(on))
 
 
 def rowwise_cluster(on: bool | None = None) -> int:
@@ -583,6 +591,33 @@ def decode_rows(p: Packed, row_index: torch.Tensor, dtype: torch.dtype | None = 
         per_row = 1
     _check(_lib.exmy_decode_rows(_ptr(p.data), p.rows, p.cols, p.x, p.y, _ptr(p.meta), per_row, _ptr(idx), idx.numel(),
                                  _ptr(out), _dtype_code(dtype), _stream(p.data.device)), "decode_rows")
+    return out
+
+
+def gemv(p: Packed, act: torch.Tensor, out: torch.Tensor | None = None, specials: bool = True) -> torch.Tensor:
+    """Decode fused into a matrix-vector product (reading D26): fp32
+    act (m, cols) @ W.T for the ROWS-packed W (rows, cols) -> fp32 (m, rows);
+    the decoded weights never reach HBM.  specials: apply the encode's
+    NaN/Inf list (the placeholder codes decode to 0)."""
+    if p.axis != ROWS:
+        raise ValueError("gemv needs the ROWS layout")
+    dev = p.data.device
+    a = act.to(device=dev, dtype=torch.float32)
+    if a.dim() == 1:
+        a = a.unsqueeze(0)
+    a = a.contiguous()
+    if a.dim() != 2 or a.shape[1] != p.cols:
+        raise ValueError(f"gemv: act must be (m, {p.cols})")
+    per_row = 0
+    if p.block is not None:
+        if p.block != (1, p.cols) or p.scheme == 2:
+            raise ValueError("gemv supports per-tensor or per-row exponent metadata")
+        per_row = 1
+    if out is None:
+        out = torch.empty((a.shape[0], p.rows), dtype=torch.float32, device=dev)
+    cap = p.capacity if specials else 0
+    _check(_lib.exmy_gemv(_ptr(p.data), p.rows, p.cols, p.x, p.y, _ptr(p.meta), per_row, _ptr(p.sp_index),
+                          _ptr(p.sp_bits), _ptr(p.sp_count), cap, _ptr(a), a.shape[0], _ptr(out), _stream(dev)), "gemv")
     return out
 
 

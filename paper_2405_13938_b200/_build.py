@@ -22,9 +22,9 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v
 UNITS = ["exmy_abi.cu", "exmy_tu_hist.cu", "exmy_tu_quant.cu", "exmy_tu_encode.cu", "exmy_tu_decode.cu",
          "exmy_tu_blk_encode.cu", "exmy_tu_blk_decode.cu", "exmy_tu_grouped.cu",
          "exmy_tu_fscale.cu", "exmy_tu_push.cu", "exmy_ckpt.cpp",
-         "exmy_tu_bag.cu", "exmy_tu_probe.cu"]
+         "exmy_tu_bag.cu", "exmy_tu_probe.cu", "exmy_tu_gemv.cu"]
 HEADERS = ["exmy_device.cuh", "exmy_kernels.cuh", "exmy_fast.cuh", "exmy_blocked.cuh", "exmy_launch.cuh", "exmy_grouped.cuh",
-           "exmy_fscale.cuh", "exmy_tma.cuh", "exmy_narrow.cuh"]
+           "exmy_fscale.cuh", "exmy_tma.cuh", "exmy_narrow.cuh", "exmy_gemv.cuh"]
 
 
 def _sources():
