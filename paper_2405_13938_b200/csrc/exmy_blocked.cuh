@@ -76,7 +76,7 @@ __device__ __forceinline__ uint32_t enc_pair_bf16_r(uint32_t w, const FastP &P, 
     return code;
 }
 
-template <int K, bool Y0>
+template <int K, bool Y0, bool SIGN = true>
 __device__ __forceinline__ uint32_t enc_f32_fast_r(uint32_t u, const FastP &P, const RowP &R, uint32_t &amax) {
     const uint32_t a = u & 0x7FFFFFFFu;
     const uint32_t ev = u & 0x7F800000u;
@@ -86,7 +86,7 @@ __device__ __forceinline__ uint32_t enc_f32_fast_r(uint32_t u, const FastP &P, c
     const uint32_t s = __float_as_uint(__fadd_rn(__uint_as_float(a), __uint_as_float(c)));
     uint32_t code = s - c + (ecl >> P.sh_f) - R.k3f;
     code = min(code, (1u << (K - 1)) - 1u);
-    code |= (u >> (32 - K)) & (1u << (K - 1));
+    if (SIGN) code |= (u >> (32 - K)) & (1u << (K - 1));
     amax = max(amax, a);
     return code;
 }
@@ -101,8 +101,8 @@ __device__ __forceinline__ void vec_codes_r(const uint32_t (&w)[NW], uint32_t (&
     } else {
 #pragma unroll
         for (int t = 0; t < NP; ++t) {
-            const uint32_t lo = enc_f32_fast_r<K, MODE == ENC_F32_Y0>(wordvec_elem<BF16, NW>(w, 2 * t), P, R, amax);
-            const uint32_t hi = enc_f32_fast_r<K, MODE == ENC_F32_Y0>(wordvec_elem<BF16, NW>(w, 2 * t + 1), P, R, amax);
+            const uint32_t lo = enc_f32_fast_r<K, MODE == ENC_F32_Y0, SIGN>(wordvec_elem<BF16, NW>(w, 2 * t), P, R, amax);
+            const uint32_t hi = enc_f32_fast_r<K, MODE == ENC_F32_Y0, SIGN>(wordvec_elem<BF16, NW>(w, 2 * t + 1), P, R, amax);
             cp[t] = lo | (hi << 16);
         }
     }
@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(256, (BF16 && K <= 7) ? 3 : 2)
         const bool ok = !force_generic && (__vcmpgeu4(mn, emin4) & __vcmpleu4(mx, emax4)) == 0xFFFFFFFFu;
         uint32_t cp[8][2];
         uint32_t amax = 0;
-        constexpr bool LATE_SIGN = SIMD && K <= 8;   // signs per row (sign_bytes), as k_enc_rows_fast
+        constexpr bool LATE_SIGN = BF16 ? (SIMD && K <= 8) : K <= 7;   // signs per row, as k_enc_rows_fast
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const uint32_t word = i < 4 ? em.x : em.y;
@@ -321,8 +321,12 @@ __global__ void __launch_bounds__(256, (BF16 && K <= 7) ? 3 : 2)
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 RL[0][i] = prmt(cp[i][0], cp[i][1], 0x6420);
-                if constexpr (LATE_SIGN)
-                    RL[0][i] |= sign_bytes(w[i][0], w[i][NW - 1]) & ((1u << (K - 1)) * 0x01010101u);
+                if constexpr (LATE_SIGN) {
+                    uint32_t sb;
+                    if constexpr (NW == 2) sb = sign_bytes(w[i][0], w[i][NW - 1]);
+                    else sb = sign_bytes_f32(w[i][0], w[i][1 % NW], w[i][2 % NW], w[i][3 % NW]);
+                    RL[0][i] |= sb & ((1u << (K - 1)) * 0x01010101u);
+                }
                 RH[0][i] = (K == 9) ? prmt(cp[i][0] >> 1, cp[i][1] >> 1, 0x6420) : 0u;
             }
             rows_fast_store<K, 1, 0>(RL, RH, packed, so, g, C, c0);

@@ -185,13 +185,20 @@ __device__ __forceinline__ uint32_t sign_bytes(uint32_t w0, uint32_t w1) {
     asm("prmt.b32 %0, %1, %2, 0xFDB9;" : "=r"(d) : "r"(w0), "r"(w1));
     return d;
 }
+// the same for 4 fp32 elements (sign in byte 3 of each word): 3 PRMTs
+__device__ __forceinline__ uint32_t sign_bytes_f32(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3) {
+    uint32_t a, b;
+    asm("prmt.b32 %0, %1, %2, 0x00FB;" : "=r"(a) : "r"(w0), "r"(w1));
+    asm("prmt.b32 %0, %1, %2, 0x00FB;" : "=r"(b) : "r"(w2), "r"(w3));
+    return prmt(a, b, 0x5410);
+}
 // any lane at or above the fallback threshold (NaN/Inf, or huge values)
 __device__ __forceinline__ bool amax_special_bf16(uint32_t amax, const FastP &P) {
     return ((amax + P.big2) & 0x80008000u) != 0u;
 }
 
 // one fp32 pattern -> k-bit code
-template <int K, bool Y0>
+template <int K, bool Y0, bool SIGN = true>
 __device__ __forceinline__ uint32_t enc_f32_fast(uint32_t u, const FastP &P, uint32_t &amax) {
     const uint32_t a = u & 0x7FFFFFFFu;
     const uint32_t ev = u & 0x7F800000u;
@@ -201,7 +208,7 @@ __device__ __forceinline__ uint32_t enc_f32_fast(uint32_t u, const FastP &P, uin
     const uint32_t s = __float_as_uint(__fadd_rn(__uint_as_float(a), __uint_as_float(c)));
     uint32_t code = s - c + (ecl >> P.sh_f) - P.k3f;
     code = min(code, (1u << (K - 1)) - 1u);
-    code |= (u >> (32 - K)) & (1u << (K - 1));
+    if (SIGN) code |= (u >> (32 - K)) & (1u << (K - 1));
     amax = max(amax, a);
     return code;
 }
@@ -362,8 +369,8 @@ __device__ __forceinline__ void vec_codes(const uint32_t (&w)[NW], uint32_t (&cp
     } else {
 #pragma unroll
         for (int t = 0; t < NP; ++t) {
-            uint32_t lo = enc_f32_fast<K, MODE == ENC_F32_Y0>(wordvec_elem<BF16, NW>(w, 2 * t), P, amax);
-            uint32_t hi = enc_f32_fast<K, MODE == ENC_F32_Y0>(wordvec_elem<BF16, NW>(w, 2 * t + 1), P, amax);
+            uint32_t lo = enc_f32_fast<K, MODE == ENC_F32_Y0, SIGN>(wordvec_elem<BF16, NW>(w, 2 * t), P, amax);
+            uint32_t hi = enc_f32_fast<K, MODE == ENC_F32_Y0, SIGN>(wordvec_elem<BF16, NW>(w, 2 * t + 1), P, amax);
             cp[t] = lo | (hi << 16);
         }
     }
@@ -600,7 +607,8 @@ __global__ void __launch_bounds__(BF16 ? EXMY_ENC_ROWS_THREADS : 256, BF16 ? EXM
         uint32_t cp[8][2];
         uint32_t amax = 0;
         // bf16 lanes, k <= 8: codes without sign, the signs added per row below
-        constexpr bool LATE_SIGN = (MODE == ENC_SIMD || MODE == ENC_SIMD_Y0) && K <= 8;
+        // (fp32 input: the same with 3 PRMTs per row for the 4 elements' signs)
+        constexpr bool LATE_SIGN = BF16 ? (K <= 8 && (MODE == ENC_SIMD || MODE == ENC_SIMD_Y0)) : K <= 7;
 #pragma unroll
         for (int i = 0; i < 8; ++i) vec_codes<K, BF16, MODE, NW, !LATE_SIGN>(w[i], cp[i], P, amax);
         if (!amax_special<BF16, MODE>(amax, P)) {
@@ -608,8 +616,12 @@ __global__ void __launch_bounds__(BF16 ? EXMY_ENC_ROWS_THREADS : 256, BF16 ? EXM
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 RL[0][i] = prmt(cp[i][0], cp[i][1], 0x6420);
-                if constexpr (LATE_SIGN)
-                    RL[0][i] |= sign_bytes(w[i][0], w[i][NW - 1]) & ((1u << (K - 1)) * 0x01010101u);
+                if constexpr (LATE_SIGN) {
+                    uint32_t sb;
+                    if constexpr (NW == 2) sb = sign_bytes(w[i][0], w[i][NW - 1]);
+                    else sb = sign_bytes_f32(w[i][0], w[i][1 % NW], w[i][2 % NW], w[i][3 % NW]);
+                    RL[0][i] |= sb & ((1u << (K - 1)) * 0x01010101u);
+                }
                 RH[0][i] = (K == 9) ? prmt(cp[i][0] >> 1, cp[i][1] >> 1, 0x6420) : 0u;
             }
             rows_fast_store<K, 1, 0>(RL, RH, packed, so, g, C, c0);

@@ -222,8 +222,11 @@ __device__ __forceinline__ void gemv_stage(uint32_t dst, uint32_t cw_rt, int64_t
     }
 }
 
+#ifndef GEMV_MINB
+#define GEMV_MINB 2   // CTAs per SM for m <= 4 (A/B builds)
+#endif
 template <int K, int M>
-__global__ void __launch_bounds__(GEMV_THREADS, M >= 8 ? 1 : 2)
+__global__ void __launch_bounds__(GEMV_THREADS, M >= 8 ? 1 : (M <= 2 ? GEMV_MINB : 2))
     k_gemv_rows_bulk(const uint8_t *__restrict__ packed, int64_t N, int64_t Kc, SegOffsets so, int x, int y,
                      const uint8_t *__restrict__ meta, int per_row, const float *__restrict__ act, int64_t lda,
                      float *__restrict__ out, int64_t ldo) {
