@@ -718,13 +718,15 @@ __global__ void __launch_bounds__(256) k_enc_cols_fast(const uint8_t *__restrict
         }
         uint32_t cp[4][4];   // group u, pair t (elements 2t, 2t+1)
         uint32_t amax = 0;
+        // bf16 lanes, k <= 8: signs merged per byte-lane word below (as ROWS)
+        constexpr bool LATE_SIGN = BF16 && K <= 7 && (MODE == ENC_SIMD || MODE == ENC_SIMD_Y0);   // k = 8: the 8-bit segment stores from cp
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
 #pragma unroll
             for (int t = 0; t < NV; ++t) {
                 uint32_t c2[NP];
                 const uint32_t ww[4] = {r[u][t].x, r[u][t].y, r[u][t].z, r[u][t].w};
-                vec_codes<K, BF16, MODE, 4>(ww, c2, P, amax);
+                vec_codes<K, BF16, MODE, 4, !LATE_SIGN>(ww, c2, P, amax);
 #pragma unroll
                 for (int p = 0; p < NP; ++p) cp[u][t * NP + p] = c2[p];
             }
@@ -736,6 +738,16 @@ __global__ void __launch_bounds__(256) k_enc_cols_fast(const uint8_t *__restrict
                 const uint32_t y01 = prmt(cp[0][t], cp[1][t], 0x6420), y23 = prmt(cp[2][t], cp[3][t], 0x6420);
                 RL[2 * t] = prmt(y01, y23, 0x6420);
                 RL[2 * t + 1] = prmt(y01, y23, 0x7531);
+                if constexpr (LATE_SIGN) {
+                    // sign bytes of elements 2t / 2t+1 of groups 0..3 (word t of each
+                    // group: bytes 1 and 3 hold the signs; selectors 8 + b replicate them)
+                    uint32_t s01, s23;
+                    asm("prmt.b32 %0, %1, %2, 0xFBD9;" : "=r"(s01) : "r"(word_of(r[0][0], t)), "r"(word_of(r[1][0], t)));
+                    asm("prmt.b32 %0, %1, %2, 0xFBD9;" : "=r"(s23) : "r"(word_of(r[2][0], t)), "r"(word_of(r[3][0], t)));
+                    constexpr uint32_t SM = (1u << (K - 1)) * 0x01010101u;
+                    RL[2 * t] |= prmt(s01, s23, 0x5410) & SM;
+                    RL[2 * t + 1] |= prmt(s01, s23, 0x7632) & SM;
+                }
                 if (K == 9) {
                     const uint32_t h01 = prmt(cp[0][t] >> 1, cp[1][t] >> 1, 0x6420);
                     const uint32_t h23 = prmt(cp[2][t] >> 1, cp[3][t] >> 1, 0x6420);
