@@ -141,7 +141,10 @@ constexpr int GEMV_CH = 2048;   // columns per stage
 
 // one stage (cw columns of a row group, segment spans back to back) folded
 // into the thread's 8 x M sums; CW > 0: cw == CW known at compile time
-template <int K, int M, int CW, int NT>
+// PA (k <= 7): the table has a 256-byte row per code (lane l at word l) on a
+// 64 KB-aligned shared address, so a lookup address is ONE prmt -- the code
+// byte dropped into byte 1 of the lane's address -- instead of a shift + LOP3
+template <int K, int M, int CW, int NT, bool PA = false>
 __device__ __forceinline__ void gemv_tiles(uint32_t dst, uint32_t cw, const uint32_t (&jt)[NT], int64_t c0,
                                            uint32_t lsa, const float *__restrict__ act, int64_t lda,
                                            float (&acc)[8][M]) {
@@ -187,8 +190,12 @@ __device__ __forceinline__ void gemv_tiles(uint32_t dst, uint32_t cw, const uint
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const uint32_t r = RL[t][i];
-                const uint32_t off = v == 0 ? (r << 7) : (r >> (8 * v - 7));
-                wv[i] = lds_f32((off & (TB - 128u)) | lsa);
+                if constexpr (PA) {
+                    wv[i] = lds_f32(prmt(r, lsa, 0x7604u | ((uint32_t)v << 4)));
+                } else {
+                    const uint32_t off = v == 0 ? (r << 7) : (r >> (8 * v - 7));
+                    wv[i] = lds_f32((off & (TB - 128u)) | lsa);
+                }
             }
 #pragma unroll
             for (int m = 0; m < M; ++m) {
@@ -204,7 +211,7 @@ __device__ __forceinline__ void gemv_tiles(uint32_t dst, uint32_t cw, const uint
 // into the thread's 8 x M sums; CW > 0: cw == CW known at compile time, and
 // the thread's CW / 1024 tiles are converted together (independent chains
 // of shared-memory loads and ALU work to overlap)
-template <int K, int M, int CW>
+template <int K, int M, int CW, bool PA>
 __device__ __forceinline__ void gemv_stage(uint32_t dst, uint32_t cw_rt, int64_t c0, uint32_t lsa,
                                            const float *__restrict__ act, int64_t lda, float (&acc)[8][M]) {
     if constexpr (CW > 0) {
@@ -213,13 +220,26 @@ __device__ __forceinline__ void gemv_stage(uint32_t dst, uint32_t cw_rt, int64_t
         uint32_t jt[NT];
 #pragma unroll
         for (int t = 0; t < NT; ++t) jt[t] = threadIdx.x + (uint32_t)(t * GEMV_THREADS);
-        gemv_tiles<K, M, CW, NT>(dst, (uint32_t)CW, jt, c0, lsa, act, lda, acc);
+        gemv_tiles<K, M, CW, NT, PA>(dst, (uint32_t)CW, jt, c0, lsa, act, lda, acc);
     } else {
         for (uint32_t j1 = threadIdx.x; j1 < cw_rt / 4; j1 += GEMV_THREADS) {
             const uint32_t jt[1] = {j1};
-            gemv_tiles<K, M, 0, 1>(dst, cw_rt, jt, c0, lsa, act, lda, acc);
+            gemv_tiles<K, M, 0, 1, PA>(dst, cw_rt, jt, c0, lsa, act, lda, acc);
         }
     }
+}
+
+#ifndef GEMV_PA
+#define GEMV_PA 1   // A/B builds: 0 = shift + LOP3 table addresses
+#endif
+template <int K>
+__host__ __device__ constexpr bool gemv_pa() { return GEMV_PA && K <= 7; }
+// dynamic shared memory of the bulk kernel: PA needs a 64 KB-aligned table
+// (256 B per code) -- 96 KB always holds table + stages whatever the
+// window offset of the dynamic block (< 2 KB: reserved + static)
+template <int K>
+__host__ __device__ constexpr int gemv_bulk_smem() {
+    return gemv_pa<K>() ? 98304 : 2 * (128 << K) + GEMV_NST * K * GEMV_CH;
 }
 
 #ifndef GEMV_MINB
@@ -237,12 +257,20 @@ __global__ void __launch_bounds__(GEMV_THREADS, M >= 8 ? 1 : (M <= 2 ? GEMV_MINB
     __shared__ float red[GEMV_THREADS / 32][8 * M];
     __shared__ __align__(8) unsigned long long bars[GEMV_NST];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr bool PA = gemv_pa<K>();
     const uint32_t base = (uint32_t)__cvta_generic_to_shared(gsm);
-    const uint32_t tab = (base + TB - 1u) & ~(TB - 1u);
-    const uint32_t stg0 = tab + TB;                    // the stages after the table
+    uint32_t tab, stg0;
+    if constexpr (PA) {   // table on the next 64 KB boundary, stages below it if they fit
+        tab = (base + 65535u) & ~65535u;
+        stg0 = (tab - base >= (uint32_t)GEMV_NST * STB) ? base : tab + (256u << K);
+    } else {
+        tab = (base + TB - 1u) & ~(TB - 1u);
+        stg0 = tab + TB;                               // the stages after the table
+    }
     const Fmt F = fmt_of(x, y, per_row ? 125 : min((int)meta[0], 254));
     for (int i = threadIdx.x; i < (32 << K); i += GEMV_THREADS)
-        sts_u32(tab + 4u * (uint32_t)i, dec_code_generic<24>((uint32_t)(i >> 5), F));
+        sts_u32(tab + (PA ? 256u * (uint32_t)(i >> 5) + 4u * (uint32_t)(i & 31) : 4u * (uint32_t)i),
+                dec_code_generic<24>((uint32_t)(i >> 5), F));
     const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&bars[0]);
     if (threadIdx.x == 0) {
         for (int b = 0; b < GEMV_NST; ++b) mbar_init(bar0 + 8u * b, 1);
@@ -287,8 +315,8 @@ __global__ void __launch_bounds__(GEMV_THREADS, M >= 8 ? 1 : (M <= 2 ? GEMV_MINB
         mbar_wait(bar0 + 8u * st, (uint32_t)((q / GEMV_NST) & 1));
         // full stages: the column count is the constant GEMV_CH, so every
         // segment offset in the stage is an immediate of the LDS
-        if (cw == GEMV_CH) gemv_stage<K, M, GEMV_CH>(dst, GEMV_CH, c0, lsa, act, lda, acc);
-        else gemv_stage<K, M, 0>(dst, cw, c0, lsa, act, lda, acc);
+        if (cw == GEMV_CH) gemv_stage<K, M, GEMV_CH, PA>(dst, GEMV_CH, c0, lsa, act, lda, acc);
+        else gemv_stage<K, M, 0, PA>(dst, cw, c0, lsa, act, lda, acc);
         __syncthreads();   // every thread is done with this stage
         if (threadIdx.x == 0 && q + GEMV_NST < nq) issue(q + GEMV_NST);
         if (ch == nch - 1) {   // row group done: reduce over the CTA, store, restart the sums

@@ -15,7 +15,7 @@ template <int K, int M>
 exmy_status launch_gemv_bulk(const uint8_t *packed, int64_t N, int64_t Kc, const SegOffsets &so, int x, int y,
                              const uint8_t *meta, int per_row, const float *act, int64_t lda, float *out, int64_t ldo,
                              cudaStream_t st) {
-    constexpr int smem = 2 * (128 << K) + GEMV_NST * K * GEMV_CH;   // table + alignment slack + the stages
+    constexpr int smem = gemv_bulk_smem<K>();   // table + alignment slack + the stages
     static unsigned long long configured = 0;
     static int occ = 0;
     int dev = 0;
