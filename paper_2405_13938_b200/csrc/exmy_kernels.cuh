@@ -65,9 +65,10 @@ __device__ __forceinline__ uint32_t enc_elem(uint32_t u, const Fmt &F, int64_t i
 }
 
 // ------------------------------------------------------------- K1 hist
-// Lane-private counters: warp w, lane l owns 16-bit counters for bins
-// (2*word, 2*word+1) in shared word [w][word][l] (bank = lane, no
-// conflicts, no atomics).  Counters are flushed before they can overflow.
+// Modes 0-3 (A/B; the default is MODE 4, k_hist_cta below): lane-private
+// counters -- warp w, lane l owns 16-bit counters for bins (2*word,
+// 2*word+1) in shared word [w][word][l] (bank = lane, no conflicts, no
+// atomics).  Counters are flushed before they can overflow.
 constexpr int HIST_THREADS = 128;
 constexpr int HIST_WARPS = HIST_THREADS / 32;
 constexpr int HIST_WORDS_PER_WARP = 128 * 32;                 // 128 words x 32 lanes
@@ -117,7 +118,7 @@ __device__ __forceinline__ void red_shared_add(uint32_t addr, uint32_t v) {
                     // counters per 4 warps) need ~2x12 vectors in flight per lane to cover HBM latency
                     // (config 2 bf16: U=4 114.0 us, 8 105.2, 12 103.1; fp32 200.9 -> 156.6 us)
 #endif
-// MODE 3 (default): LANE-PAIR counters.  Lanes 2j and 2j+1 share the 32-bit
+// MODE 3 (default until MODE 4, k_hist_cta, below): LANE-PAIR counters.  Lanes 2j and 2j+1 share the 32-bit
 // word [bin][j] of their warp's 16 KB (256 bins x 16 words), lane 2j counting
 // in the low half and 2j+1 in the high half, so each lane's increment is a
 // constant (1 or 0x10000) and an element costs only the bin's byte offset
